@@ -1,0 +1,231 @@
+/*
+ * kvring.h -- C ABI of libkvring: ring-shaped KV-cache replication for
+ * fault-tolerant pipeline-parallel LLM serving, B200 (sm_100a) native.
+ *
+ * Method: KevlarFlow (arXiv 2601.22438).  PAPER.md P:223-225 (§3.2):
+ *   "KevlarFlow replicates KV cache for each request to the GPU memory of
+ *    other nodes in the load balancing group ... When failure occurs ...
+ *    in-progress requests will be served continuously on the replication
+ *    target from the replicated state, avoiding retries"
+ * and P:229 (§3.2): "a block representation of KV cache ... replicate it
+ * block-by-block in the background.  A separate CUDA stream is used to
+ * overlap the communication with computation."  Ring shape: P:8 (§3.3).
+ * Readings of what the paper leaves open (R1-R16) are listed in DESIGN.md;
+ * the ones that fix behaviour visible through this ABI are cited per call.
+ *
+ * Conventions
+ *  - Every call returns KV_OK (0) or a negative kv_status_t; the message of the
+ *    last failure on the calling thread is kv_last_error().  No C++ exception
+ *    crosses this boundary.
+ *  - "device" pointers are CUDA device (or NVLink peer-mapped) addresses;
+ *    "host" pointers are CPU memory.  Streams are cudaStream_t passed as void*.
+ *  - All GPU work is enqueued asynchronously on the stream given; no call ever
+ *    waits on a peer GPU.  kv_restore is the one call that synchronises (it
+ *    must read the holder's published metadata).
+ *  - One host thread per pool handle at a time.  Pools on the same device share
+ *    an internal staging context guarded by a mutex.
+ *
+ * Memory layout (reading R4)
+ *  - 16-bit words (fp16/bf16 bit patterns, never interpreted: R13).
+ *  - block  = [layers][2 (K,V)][kv_heads][block_size][head_dim] words, so one
+ *             (layer, K/V, head, token) slice of head_dim words is contiguous
+ *             (256 B for head_dim 128) and a full block is contiguous.
+ *  - pool   = [num_blocks] blocks.  replica region = [replica_blocks] blocks,
+ *             holding the ring predecessor's blocks AT THE SAME BLOCK IDS (R5).
+ *  - dense new-token KV (kv_append source) = [sum n_new][layers][2][kv_heads][head_dim].
+ *  - replica metadata (kv_meta_bytes), written only by the predecessor's
+ *    replicate kernel, little-endian:
+ *        off 0   uint64 seq          last published step, 0 = nothing (R9)
+ *        off 8   int32  writer_node  node_id of the predecessor that wrote it
+ *        off 12  int32  max_reqs R
+ *        off 16  int32  max_blocks_per_req M
+ *        off 20  int32  magic 0x4B56524D ("KVRM")
+ *        off 24  int64  reserved
+ *        off 32  int64  req_id[2][R]  parity (step & 1) buffers, -1 = empty slot
+ *        off 32+16R     int32 len[2][R]
+ *        off 32+24R     int32 bt[R][M] block ids in the predecessor's pool
+ *                       (entries j < ceil(len/B) of a listed slot are valid)
+ *    seq is stored last with st.release.sys after a system-scope fence, so a
+ *    reader that acquires seq = t sees parity t's lengths, rows and KV slices.
+ */
+#ifndef KVRING_H
+#define KVRING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVRING_ABI_VERSION 1
+
+typedef enum {
+  KV_OK = 0,
+  KV_EINVAL = -1,      /* bad geometry / argument, unknown request, non-monotone step  */
+  KV_ENOMEM = -2,      /* pool blocks or request slots exhausted; all-or-nothing */
+  KV_ECUDA = -3,       /* a CUDA call failed or a sticky asynchronous error surfaced       */
+  KV_ESTATE = -4,      /* the pool is dead (after kv_fail_stage) or the call is not allowed  */
+  KV_ENOREPLICA = -5,  /* holder metadata invalid or nothing published (seq == 0)         */
+  KV_EPEER = -6        /* no successor bound                                                */
+} kv_status_t;
+
+typedef struct kv_pool kv_pool_t; /* opaque; one per logical node (instance, stage) */
+
+typedef struct {
+  int32_t layers;      /* L_s, layers of this pipeline stage                         */
+  int32_t kv_heads;    /* H (Llama-3.1-8B: 8)                                         */
+  int32_t head_dim;    /* d (128); head_dim * elem_bytes must be a power of 2 >= 16   */
+  int32_t block_size;  /* B tokens per block (16)                                     */
+  int32_t elem_bytes;  /* must be 2 (16-bit words)                                    */
+} kv_geom_t;
+
+typedef struct {
+  kv_geom_t g;
+  int32_t num_blocks;         /* NB of the primary pool                                 */
+  int32_t max_reqs;           /* request slots R (>= 2 x live batch: slots quarantine, R7) */
+  int32_t max_blocks_per_req; /* M                                                       */
+  int32_t device;             /* CUDA ordinal; -1 = tables only (host-logic tests: no
+                                 device memory, nothing launched, no bytes moved)        */
+  int32_t node_id;            /* logical node id, written into the successor's metadata */
+  int32_t replica_blocks;     /* blocks in this node's replica region (= pred's NB)      */
+  void *pool;                 /* device, caller-owned, num_blocks * kv_block_bytes        */
+  void *replica;              /* device, caller-owned, replica_blocks * kv_block_bytes    */
+  void *replica_meta;         /* device, caller-owned, kv_meta_bytes(R, M); initialised
+                                 by kv_pool_create (seq 0, empty slots, bt -1)            */
+} kv_pool_desc_t;
+
+/* Bytes of one block / one replica metadata region (layout above). */
+size_t kv_block_bytes(const kv_geom_t *g);
+size_t kv_meta_bytes(int32_t max_reqs, int32_t max_blocks_per_req);
+int32_t kv_abi_version(void);
+
+/* Create a pool handle over caller-owned device memory.  Validates geometry,
+ * builds the host allocator (R6 lowest-free-id, R7 one-step quarantine) and
+ * initialises replica_meta on the device (synchronously).  pool/replica bytes
+ * are left untouched (the caller fills its sentinel). */
+int kv_pool_create(const kv_pool_desc_t *desc, kv_pool_t **out);
+int kv_pool_destroy(kv_pool_t *p);
+
+/* Bind the ring link p -> successor (SPEC S:298-306 apply_plan; ring map is
+ * data, reading R1).  succ_replica / succ_meta are the successor's replica
+ * region and metadata: local device pointers or NVLink peer pointers (e.g.
+ * torch symmetric-memory buffer_ptrs).  succ_replica_blocks must be >= p's NB.
+ * NULL succ_replica disables replication.  Any (re)bind re-seeds: every live
+ * request is republished from token 0 at the next kv_replicate_step. */
+int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
+                     int32_t succ_replica_blocks, void *succ_meta);
+
+/* Step boundary: blocks and slots quarantined by the
+ * previous step become allocatable. */
+int kv_begin_step(kv_pool_t *p);
+
+/* Finish requests (§8(c) step 2): their blocks and slot go to quarantine and
+ * are not reallocated before the next kv_begin_step (R7).  Host-only. */
+int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids);
+
+/* Append new-token KV (the model's KV write; harness stand-in, §8(a) a2).
+ * Entries are processed in order: a known req_id grows by n_new[i] tokens
+ * (a new block = lowest free id whenever len % B == 0); an unknown req_id is an
+ * admission (slot = lowest free slot, then ceil(n_new/B) blocks).  src_kv is
+ * dense [sum n_new][L][2][H][d] in entry order, on the device, or on the host
+ * when flags & KV_SRC_HOST (copied by the library inside the call's stream
+ * order; pinned memory recommended).  All-or-nothing: KV_ENOMEM / KV_EINVAL
+ * leave the tables unchanged.  Launches one scatter kernel. */
+#define KV_SRC_HOST 1
+int kv_append(kv_pool_t *p, int32_t n, const int64_t *req_ids, const int32_t *n_new,
+              const void *src_kv, int32_t flags, void *stream);
+
+/* Batched form for several pools on ONE device: per pool an optional
+ * begin_step, releases, and appends -- one H2D and one kernel launch in total.
+ * Validation of every pool happens before any pool changes. */
+typedef struct {
+  kv_pool_t *pool;
+  int32_t begin_step;          /* nonzero: kv_begin_step first                 */
+  int32_t n_release;
+  const int64_t *release_ids;
+  int32_t n;                   /* appends                                      */
+  const int64_t *req_ids;
+  const int32_t *n_new;
+  const void *src_kv;          /* device (or host with KV_SRC_HOST)            */
+  int32_t flags;
+} kv_append_args_t;
+int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream);
+
+/* Publish step `step` to the successor (§8(c) step 5; R2 dirty tokens; R9).
+ * For every live slot the tokens [pub_len, len) are copied from this pool to
+ * the successor's replica region at the same block ids with 16-B stores (NVLink
+ * P2P when the successor is remote), bt entries of the touched blocks and the
+ * parity (step & 1) (req_id, len) table are written, and the last CTA stores
+ * seq = step (release, system scope).  step >= 1 and strictly increasing per
+ * pool; KV_EPEER if no successor is bound.  pub_len := len on return (the host
+ * never waits for the peer). */
+int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream);
+/* Same for several pools of ONE device in a single launch. */
+int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, void *stream);
+
+/* Fault injection: the next replicate of p executes only its first
+ * `tasks` copy tasks and never publishes -- a stage dying mid-step. -1 clears. */
+int kv_inject_abort(kv_pool_t *p, int32_t tasks);
+
+/* Simulated failure (§8(a) a7): p becomes dead; its pool, replica region and
+ * replica metadata are overwritten with 0xFF bytes on `stream`. */
+int kv_fail_stage(kv_pool_t *p, void *stream);
+
+/* Restore (§8(a) a8): rebuild the requests published in a holder's
+ * replica region into pool dst.  Reads seq = t* (acquire) and the parity-t*
+ * metadata, allocates in dst by ascending req_id then logical block j (lowest
+ * free ids, R6), copies each block's valid slots [0, min(B, len - jB)) from
+ * holder_replica (local HBM, or NVLink when it is a peer pointer) and rebuilds
+ * dst's tables.  dst may be the holder itself (promotion, R10).  Outputs
+ * (req_id, resume_len) ascending into caller arrays of capacity `cap`.
+ * Synchronous; restored requests start unpublished.  KV_ENOREPLICA if seq is 0
+ * or all-ones (poisoned) or the metadata shape differs; KV_ENOMEM all-or-nothing. */
+int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder_replica_blocks,
+               const void *holder_meta, void *stream, uint64_t *t_star,
+               int64_t *req_ids_out, int32_t *resume_len_out, int32_t cap, int32_t *n_out);
+
+/* NCCL-comparison path (§8(a) a4/a6): gather this step's dirty slices into
+ * one contiguous device buffer (header + item list + slot table + payload,
+ * see DESIGN.md "Packed format"), without touching the successor.  *bytes_out
+ * is the packed size (the 8-B count exchanged before ncclSend/Recv).  Advances
+ * pub_len like kv_replicate_step.  kv_pack_bytes gives the size without packing. */
+int kv_pack_bytes(kv_pool_t *p, size_t *bytes_out);
+int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, size_t *bytes_out,
+                 void *stream);
+/* Receiver side: scatter a packed buffer into (replica, replica_meta) and
+ * publish its step; one kernel whose grid is sized from max_items (host arg). */
+int kv_unpack(const void *packed, size_t packed_bytes, void *replica, int32_t replica_blocks,
+              void *replica_meta, const kv_geom_t *g, int32_t max_reqs,
+              int32_t max_blocks_per_req, void *stream);
+
+/* Queries (host tables; no device access). */
+int kv_query(kv_pool_t *p, int64_t req_id, int32_t *len, int32_t *blocks, int32_t cap,
+             int32_t *nblk);
+typedef struct {
+  int32_t free_blocks, quarantined_blocks, used_blocks;
+  int32_t free_slots, quarantined_slots, live_reqs;
+  int32_t dead, has_successor;
+  uint64_t last_step;
+  uint64_t bytes_replicated;   /* algorithmic payload bytes published so far */
+  uint64_t tasks_launched;     /* copy tasks issued by replicate kernels      */
+  uint64_t kernels_launched;   /* kernels issued by this pool (all kinds)     */
+  uint64_t last_step_bytes;    /* payload bytes of the latest replicate       */
+} kv_stats_t;
+int kv_stats(kv_pool_t *p, kv_stats_t *out);
+/* Per-slot tables: req_id (-1 empty), len, pub_len, nblk; arrays of max_reqs. */
+int kv_dump_slots(kv_pool_t *p, int64_t *req_id, int32_t *len, int32_t *pub_len,
+                  int32_t *nblk);
+
+/* Surface sticky asynchronous CUDA errors of p's device (synchronises it). */
+int kv_sync(kv_pool_t *p);
+const char *kv_last_error(void);
+
+/* Kernels launched by this process through libkvring, all kinds (evidence
+ * counter for bench gpu_launches). */
+uint64_t kv_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVRING_H */

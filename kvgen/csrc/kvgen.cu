@@ -1,0 +1,75 @@
+// CUDA twin of kvgen/content.py (input generator; no replication arithmetic).
+//
+//   content(seed, req, l, kv, h, pos, dim) = T[l,kv,h,dim] ^ word16(K(seed,req,pos), dim % 4)
+//   K(seed, req, pos) = sm(sm(sm(seed) ^ req) ^ pos)
+//   T[idx]            = sm(sm(seed ^ TABLE_SALT) ^ idx) & 0xFFFF,
+//                       idx = ((l*2 + kv)*H + h)*d + dim   (l = global layer)
+// with sm = splitmix64.  tests/test_kvgen_cuda.py pins it byte-for-byte to the
+// numpy generator.  Output layout: dense [n][L][2][H][d] uint16 (the layout
+// kv_append consumes).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace {
+constexpr unsigned long long kGolden = 0x9E3779B97F4A7C15ull;
+constexpr unsigned long long kTableSalt = 0x4B565441424C45ull;
+
+__host__ __device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
+  unsigned long long z = x + kGolden;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// One thread = 8 consecutive words (16 B) of one token's dense row.
+__global__ void content_kernel(unsigned long long seed_mix, unsigned long long salt_mix,
+                               const int64_t *__restrict__ req, const int32_t *__restrict__ pos,
+                               long long n, int layer0, int L, int H, int d,
+                               uint16_t *__restrict__ out) {
+  const long long words_per_tok = (long long)L * 2 * H * d;
+  const long long chunks = n * (words_per_tok / 8);
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < chunks;
+       c += (long long)gridDim.x * blockDim.x) {
+    const long long w0 = c * 8;
+    const long long tok = w0 / words_per_tok;
+    const long long within = w0 - tok * words_per_tok;  // index in [L][2][H][d]
+    const unsigned long long key =
+        sm64(sm64(seed_mix ^ (unsigned long long)req[tok]) ^ (unsigned long long)(long long)pos[tok]);
+    const long long lkvh = within / d;
+    const int dim0 = (int)(within - lkvh * d);
+    const long long l_local = lkvh / (2 * H);
+    const long long rest = lkvh - l_local * 2 * H;  // kv*H + h
+    const unsigned long long base =
+        ((unsigned long long)((layer0 + l_local) * 2 * H + rest)) * (unsigned long long)d;
+    uint16_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int dim = dim0 + k;
+      const uint16_t t = (uint16_t)(sm64(salt_mix ^ (base + dim)) & 0xFFFFull);
+      const uint16_t wd = (uint16_t)((key >> (16 * (dim & 3))) & 0xFFFFull);
+      v[k] = t ^ wd;
+    }
+    uint4 pk;
+    pk.x = v[0] | ((uint32_t)v[1] << 16);
+    pk.y = v[2] | ((uint32_t)v[3] << 16);
+    pk.z = v[4] | ((uint32_t)v[5] << 16);
+    pk.w = v[6] | ((uint32_t)v[7] << 16);
+    *reinterpret_cast<uint4 *>(out + w0) = pk;
+  }
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int kvgen_content(
+    unsigned long long seed, const int64_t *req_dev, const int32_t *pos_dev, long long n,
+    int layer0, int L, int H, int d, uint16_t *out_dev, void *stream) {
+  if (n <= 0) return 0;
+  if (d % 8 != 0) return -1;
+  const unsigned long long seed_mix = sm64(seed);
+  const unsigned long long salt_mix = sm64(seed ^ kTableSalt);
+  const long long chunks = n * ((long long)L * 2 * H * d / 8);
+  long long grid = (chunks + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  content_kernel<<<(int)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      seed_mix, salt_mix, req_dev, pos_dev, n, layer0, L, H, d, out_dev);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}

@@ -1,0 +1,1041 @@
+// libkvring host core: C ABI (include/kvring.h), allocator and block tables
+// (N2), ring link state, work-list / task builder (N4), staging of the
+// per-step descriptors (one H2D per call) and kernel launches.
+//
+// Paper: KevlarFlow (arXiv 2601.22438) P:223-229 §3.2 (background replication
+// of each request's KV, block representation, separate stream, promotion on
+// the replication target).  Readings R1-R16: DESIGN.md.  The allocator and
+// the step protocol follow SURVEY §8(c) steps 1-7 exactly; the CPU oracle
+// (oracle/) implements the same rules independently and the tests compare the
+// two byte for byte.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime_api.h>
+
+#include "kvring.h"
+#include "kvring_internal.h"
+
+#define KV_API extern "C" __attribute__((visibility("default")))
+
+using namespace kvring;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(KV_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                               \
+  } while (0)
+
+// RAII current-device switch (restores the caller's device).
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Lowest-free-id set over [0, n) (reading R6): 64-bit words + first-nonzero hint.
+class IdSet {
+ public:
+  void init(int n, bool full) {
+    n_ = n;
+    words_.assign((n + 63) / 64, 0ull);
+    count_ = 0;
+    hint_ = 0;
+    if (full)
+      for (int i = 0; i < n; ++i) insert(i);
+  }
+  bool contains(int i) const { return (words_[i >> 6] >> (i & 63)) & 1ull; }
+  void insert(int i) {
+    words_[i >> 6] |= 1ull << (i & 63);
+    ++count_;
+    if ((i >> 6) < hint_) hint_ = i >> 6;
+  }
+  int take_min() {  // precondition: count_ > 0
+    while (words_[hint_] == 0ull) ++hint_;
+    const int b = __builtin_ctzll(words_[hint_]);
+    words_[hint_] &= words_[hint_] - 1ull;
+    --count_;
+    return hint_ * 64 + b;
+  }
+  int size() const { return count_; }
+
+ private:
+  int n_ = 0, count_ = 0, hint_ = 0;
+  std::vector<unsigned long long> words_;
+};
+
+// Pinned-host + device staging buffer ring, per device (shared by its pools).
+struct StageBuf {
+  char *host = nullptr;
+  char *dev = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+
+struct DeviceCtx {
+  int device = 0;
+  std::mutex mu;
+  static constexpr int kRing = 8;
+  StageBuf ring[kRing];
+  int next = 0;
+  StageBuf src[kRing];  // device copies of host-resident append sources (KV_SRC_HOST)
+  int next_src = 0;
+  unsigned long long *unpack_counter = nullptr;
+  size_t cap_hint = 1 << 16;
+
+  // Returns a buffer of >= bytes whose previous use has completed.
+  int acquire(StageBuf *ringv, int &nxt, size_t bytes, bool want_host, StageBuf **out) {
+    StageBuf &b = ringv[nxt];
+    nxt = (nxt + 1) % kRing;
+    if (b.pending) {
+      CU(cudaEventSynchronize(b.ev));
+      b.pending = false;
+    }
+    if (b.cap < bytes) {
+      size_t cap = std::max(bytes, b.cap * 2);
+      cap = std::max(cap, cap_hint);
+      cap = (cap + 4095) & ~(size_t)4095;
+      if (b.host) cudaFreeHost(b.host);
+      if (b.dev) cudaFree(b.dev);
+      b.host = nullptr;
+      b.dev = nullptr;
+      b.cap = 0;
+      if (want_host) CU(cudaHostAlloc(reinterpret_cast<void **>(&b.host), cap, cudaHostAllocDefault));
+      CU(cudaMalloc(reinterpret_cast<void **>(&b.dev), cap));
+      b.cap = cap;
+    }
+    if (!b.ev) CU(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+    *out = &b;
+    return KV_OK;
+  }
+  int done(StageBuf *b, cudaStream_t s) {
+    CU(cudaEventRecord(b->ev, s));
+    b->pending = true;
+    return KV_OK;
+  }
+};
+
+std::mutex g_ctx_mu;
+std::map<int, std::unique_ptr<DeviceCtx>> g_ctx;
+
+DeviceCtx *ctx_for(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  auto &p = g_ctx[device];
+  if (!p) {
+    p.reset(new DeviceCtx());
+    p->device = device;
+  }
+  return p.get();
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace
+
+struct kv_pool {
+  kv_geom_t g{};
+  int NB = 0, R = 0, M = 0, device = -1, node_id = 0, replica_blocks = 0;
+  char *pool = nullptr, *replica = nullptr, *meta = nullptr;
+  // geometry derived
+  long long block_bytes = 0;
+  int token_bytes = 0, seg_bytes = 0, combos = 0, task_segs = 0, cps_shift = 0;
+  // ring link
+  bool has_succ = false;
+  int succ_node = -1, succ_replica_blocks = 0;
+  char *succ_replica = nullptr, *succ_meta = nullptr;
+  // allocator (R6, R7)
+  IdSet free_blocks, free_slots;
+  std::vector<int> q_blocks, q_slots;
+  std::vector<int64_t> slot_req;
+  std::vector<int32_t> slot_len, pub_len;
+  std::vector<std::vector<int32_t>> slot_bt;
+  std::unordered_map<int64_t, int> slot_of;
+  // state
+  bool dead = false;
+  uint64_t last_step = 0;
+  int abort_after = -1;
+  unsigned long long *counter = nullptr;  // device, monotone
+  unsigned long long issued = 0;          // host mirror of the counter target
+  uint64_t bytes_replicated = 0, tasks_launched = 0, kernels = 0, last_step_bytes = 0;
+
+  KvGeomDev geom_dev() const {
+    KvGeomDev d;
+    d.block_bytes = block_bytes;
+    d.token_bytes = token_bytes;
+    d.seg_bytes = seg_bytes;
+    d.block_size = g.block_size;
+    d.cps_shift = cps_shift;
+    return d;
+  }
+  bool same_geom(const kv_pool &o) const {
+    return g.layers == o.g.layers && g.kv_heads == o.g.kv_heads && g.head_dim == o.g.head_dim &&
+           g.block_size == o.g.block_size && g.elem_bytes == o.g.elem_bytes;
+  }
+};
+
+namespace {
+
+int validate_geom(const kv_geom_t *g) {
+  if (!g) return fail(KV_EINVAL, "null geometry");
+  if (g->layers <= 0 || g->kv_heads <= 0 || g->head_dim <= 0 || g->block_size <= 0 ||
+      g->block_size > 4096)
+    return fail(KV_EINVAL, "geometry fields must be positive (block_size <= 4096)");
+  if (g->elem_bytes != 2) return fail(KV_EINVAL, "elem_bytes must be 2 (16-bit words)");
+  const int seg = g->head_dim * g->elem_bytes;
+  if (seg < 16 || (seg & (seg - 1)) != 0)
+    return fail(KV_EINVAL, "head_dim * elem_bytes = %d must be a power of two >= 16", seg);
+  return KV_OK;
+}
+
+// Appends the tasks of one item (n_tok tokens x combos slices) split into
+// tasks of <= task_segs slices.
+inline void push_item(std::vector<KvTask> &out, int16_t pool, int src_unit, int dst_unit, int slot,
+                      int j, int tok_lo, int n_tok, int combos, int task_segs) {
+  const int nseg = n_tok * combos;
+  for (int b = 0; b < nseg; b += task_segs) {
+    KvTask t;
+    t.src_unit = src_unit;
+    t.dst_unit = dst_unit;
+    t.pool = pool;
+    t.slot = (int16_t)slot;
+    t.j = (int16_t)j;
+    t.tok_lo = (int16_t)tok_lo;
+    t.n_tok = (int16_t)n_tok;
+    t.flags = b == 0 ? kFirst : 0;
+    t.seg_begin = b;
+    t.seg_count = std::min(task_segs, nseg - b);
+    t.pad = 0;
+    out.push_back(t);
+  }
+}
+
+inline void push_publish_only(std::vector<KvTask> &out, int16_t pool) {
+  KvTask t{};
+  t.pool = pool;
+  t.slot = -1;
+  t.n_tok = 1;
+  t.seg_count = 0;
+  out.push_back(t);
+}
+
+// ---- append ---------------------------------------------------------------
+int append_validate(kv_pool *p, const kv_append_args_t &a) {
+  if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+  if (a.n < 0 || a.n_release < 0) return fail(KV_EINVAL, "negative count");
+  if ((a.n > 0 && (!a.req_ids || !a.n_new)) || (a.n_release > 0 && !a.release_ids))
+    return fail(KV_EINVAL, "null array");
+  // releases first (their blocks only reach the free list at the next begin_step)
+  std::unordered_map<int64_t, int> seen;
+  for (int i = 0; i < a.n_release; ++i) {
+    if (!p->slot_of.count(a.release_ids[i]))
+      return fail(KV_EINVAL, "release of unknown request %lld", (long long)a.release_ids[i]);
+    if (seen[a.release_ids[i]]++) return fail(KV_EINVAL, "request released twice");
+  }
+  const int B = p->g.block_size;
+  long long need_blocks = 0, need_slots = 0, tokens = 0;
+  std::unordered_map<int64_t, int> in_call;
+  for (int i = 0; i < a.n; ++i) {
+    const int64_t r = a.req_ids[i];
+    const int n = a.n_new[i];
+    if (n < 0) return fail(KV_EINVAL, "negative n_new");
+    if (in_call[r]++) return fail(KV_EINVAL, "request %lld twice in one append", (long long)r);
+    if (seen.count(r)) return fail(KV_EINVAL, "request %lld released and appended", (long long)r);
+    long long cur = 0;
+    auto it = p->slot_of.find(r);
+    if (it != p->slot_of.end()) {
+      cur = p->slot_len[it->second];
+    } else {
+      if (n <= 0) return fail(KV_EINVAL, "admission of %lld with no tokens", (long long)r);
+      ++need_slots;
+    }
+    const long long tot = (cur + n + B - 1) / B;
+    if (tot > p->M) return fail(KV_ENOMEM, "request %lld exceeds max_blocks_per_req", (long long)r);
+    need_blocks += tot - (cur + B - 1) / B;
+    tokens += n;
+  }
+  if (need_slots > p->free_slots.size() || need_blocks > p->free_blocks.size())
+    return fail(KV_ENOMEM, "pool %d exhausted (need %lld blocks / %lld slots, free %d / %d)",
+                p->node_id, need_blocks, need_slots, p->free_blocks.size(), p->free_slots.size());
+  if (tokens > 0x7fffffffLL) return fail(KV_EINVAL, "too many tokens in one append");
+  return KV_OK;
+}
+
+void do_begin_step(kv_pool *p) {
+  for (int b : p->q_blocks) p->free_blocks.insert(b);
+  for (int s : p->q_slots) p->free_slots.insert(s);
+  p->q_blocks.clear();
+  p->q_slots.clear();
+}
+
+void do_release(kv_pool *p, int n, const int64_t *ids) {
+  for (int i = 0; i < n; ++i) {
+    auto it = p->slot_of.find(ids[i]);
+    const int s = it->second;
+    p->slot_of.erase(it);
+    for (int b : p->slot_bt[s]) p->q_blocks.push_back(b);
+    p->slot_bt[s].clear();
+    p->q_slots.push_back(s);
+    p->slot_req[s] = -1;
+    p->slot_len[s] = 0;
+    p->pub_len[s] = 0;
+  }
+}
+
+// Applies the appends to the tables and emits the scatter tasks (src rows are
+// token rows of the dense source, `row_base` added).
+void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<KvTask> &tasks) {
+  const int B = p->g.block_size;
+  int row = 0;
+  for (int i = 0; i < a.n; ++i) {
+    const int64_t r = a.req_ids[i];
+    int s;
+    auto it = p->slot_of.find(r);
+    if (it == p->slot_of.end()) {
+      s = p->free_slots.take_min();
+      p->slot_of[r] = s;
+      p->slot_req[s] = r;
+      p->slot_len[s] = 0;
+      p->pub_len[s] = 0;
+      p->slot_bt[s].clear();
+    } else {
+      s = it->second;
+    }
+    int len = p->slot_len[s];
+    int left = a.n_new[i];
+    while (left > 0) {
+      if (len % B == 0) p->slot_bt[s].push_back(p->free_blocks.take_min());
+      const int j = len / B, lo = len % B;
+      const int n = std::min(B - lo, left);
+      if (p->device >= 0)
+        push_item(tasks, pidx, row, p->slot_bt[s][j], -1, j, lo, n, p->combos, p->task_segs);
+      row += n;
+      len += n;
+      left -= n;
+    }
+    p->slot_len[s] = len;
+  }
+}
+
+// ---- replicate --------------------------------------------------------------
+// Dirty ranges [pub_len, len) of every live slot split at block boundaries
+// (§8(a) a3); returns payload bytes.
+uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks, bool packed,
+                           int32_t *packed_unit) {
+  const int B = p->g.block_size;
+  uint64_t bytes = 0;
+  for (int s = 0; s < p->R; ++s) {
+    if (p->slot_req[s] < 0) continue;
+    int pos = p->pub_len[s];
+    const int len = p->slot_len[s];
+    while (pos < len) {
+      const int j = pos / B, lo = pos % B;
+      const int n = std::min(B - lo, len - pos);
+      const int blk = p->slot_bt[s][j];
+      if (packed) {
+        push_item(tasks, pidx, blk, *packed_unit, s, j, lo, n, p->combos, p->task_segs);
+        *packed_unit += n * p->combos;
+      } else {
+        push_item(tasks, pidx, blk, blk, s, j, lo, n, p->combos, p->task_segs);
+      }
+      bytes += (uint64_t)n * p->token_bytes;
+      pos += n;
+    }
+  }
+  return bytes;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+KV_API int32_t kv_abi_version(void) { return KVRING_ABI_VERSION; }
+
+KV_API const char *kv_last_error(void) { return g_err.c_str(); }
+
+KV_API uint64_t kv_kernel_launch_count(void) { return g_launches.load(); }
+
+KV_API size_t kv_block_bytes(const kv_geom_t *g) {
+  if (!g || validate_geom(g) != KV_OK) return 0;
+  return (size_t)g->layers * 2 * g->kv_heads * g->block_size * g->head_dim * g->elem_bytes;
+}
+
+KV_API size_t kv_meta_bytes(int32_t max_reqs, int32_t max_blocks_per_req) {
+  if (max_reqs <= 0 || max_blocks_per_req <= 0) return 0;
+  return meta_bytes(max_reqs, max_blocks_per_req);
+}
+
+KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
+  if (!d || !out) return fail(KV_EINVAL, "null argument");
+  *out = nullptr;
+  int rc = validate_geom(&d->g);
+  if (rc) return rc;
+  if (d->num_blocks <= 0 || d->max_reqs <= 0 || d->max_blocks_per_req <= 0)
+    return fail(KV_EINVAL, "num_blocks, max_reqs, max_blocks_per_req must be positive");
+  if (d->max_reqs > 32767 || d->max_blocks_per_req > 32767)
+    return fail(KV_EINVAL, "max_reqs and max_blocks_per_req must be < 32768");
+  if (d->device >= 0 && (!d->pool || !d->replica || !d->replica_meta))
+    return fail(KV_EINVAL, "pool, replica and replica_meta must be device pointers");
+  std::unique_ptr<kv_pool> p(new kv_pool());
+  p->g = d->g;
+  p->NB = d->num_blocks;
+  p->R = d->max_reqs;
+  p->M = d->max_blocks_per_req;
+  p->device = d->device;
+  p->node_id = d->node_id;
+  p->replica_blocks = d->replica_blocks > 0 ? d->replica_blocks : d->num_blocks;
+  p->pool = static_cast<char *>(d->pool);
+  p->replica = static_cast<char *>(d->replica);
+  p->meta = static_cast<char *>(d->replica_meta);
+  p->seg_bytes = d->g.head_dim * d->g.elem_bytes;
+  p->combos = d->g.layers * 2 * d->g.kv_heads;
+  p->token_bytes = p->combos * p->seg_bytes;
+  p->block_bytes = (long long)p->token_bytes * d->g.block_size;
+  p->task_segs = std::max(1, 32768 / p->seg_bytes);
+  p->cps_shift = __builtin_ctz(p->seg_bytes / 16);
+  p->free_blocks.init(p->NB, true);
+  p->free_slots.init(p->R, true);
+  p->slot_req.assign(p->R, -1);
+  p->slot_len.assign(p->R, 0);
+  p->pub_len.assign(p->R, 0);
+  p->slot_bt.assign(p->R, {});
+  for (auto &v : p->slot_bt) v.reserve(8);
+  if (p->device >= 0) {
+    DeviceGuard dg(p->device);
+    if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", p->device);
+    CU(cudaMalloc(reinterpret_cast<void **>(&p->counter), sizeof(unsigned long long)));
+    CU(cudaMemset(p->counter, 0, sizeof(unsigned long long)));
+    CU(launch_meta_init(p->meta, p->R, p->M, 0));
+    g_launches++;
+    p->kernels++;
+    CU(cudaDeviceSynchronize());
+    ctx_for(p->device);
+  }
+  *out = p.release();
+  return KV_OK;
+}
+
+KV_API int kv_pool_destroy(kv_pool_t *p) {
+  if (!p) return KV_OK;
+  if (p->counter) {
+    DeviceGuard dg(p->device);
+    cudaDeviceSynchronize();
+    cudaFree(p->counter);
+  }
+  delete p;
+  return KV_OK;
+}
+
+KV_API int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
+                            int32_t succ_replica_blocks, void *succ_meta) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+  if (succ_replica == nullptr) {
+    p->has_succ = false;
+    p->succ_replica = nullptr;
+    p->succ_meta = nullptr;
+    p->succ_node = -1;
+  } else {
+    if (!succ_meta) return fail(KV_EINVAL, "successor metadata pointer is null");
+    if (succ_replica_blocks < p->NB)
+      return fail(KV_EINVAL, "successor replica region (%d blocks) smaller than pool (%d)",
+                  succ_replica_blocks, p->NB);
+    p->has_succ = true;
+    p->succ_node = succ_node;
+    p->succ_replica = static_cast<char *>(succ_replica);
+    p->succ_replica_blocks = succ_replica_blocks;
+    p->succ_meta = static_cast<char *>(succ_meta);
+  }
+  std::fill(p->pub_len.begin(), p->pub_len.end(), 0);  // re-seed the new link
+  return KV_OK;
+}
+
+KV_API int kv_begin_step(kv_pool_t *p) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+  do_begin_step(p);
+  return KV_OK;
+}
+
+KV_API int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  kv_append_args_t a{};
+  a.pool = p;
+  a.n_release = n;
+  a.release_ids = req_ids;
+  int rc = append_validate(p, a);
+  if (rc) return rc;
+  do_release(p, n, req_ids);
+  return KV_OK;
+}
+
+KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream) {
+  if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
+  kv_pool *p0 = args[0].pool;
+  if (!p0) return fail(KV_EINVAL, "null pool");
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = args[k].pool;
+    if (!p) return fail(KV_EINVAL, "null pool");
+    if (p->device != p0->device || !p->same_geom(*p0))
+      return fail(KV_EINVAL, "kv_append_multi pools must share device and geometry");
+    for (int k2 = 0; k2 < k; ++k2)
+      if (args[k2].pool == p) return fail(KV_EINVAL, "pool listed twice");
+  }
+  // Phase 1: validate every pool against its state after begin_step + releases.
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = args[k].pool;
+    if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+    // validation must see the quarantine released when begin_step is requested
+    if (args[k].begin_step) {
+      IdSet fb = p->free_blocks, fs = p->free_slots;
+      const std::vector<int> qb = p->q_blocks, qs = p->q_slots;
+      do_begin_step(p);
+      int rc = append_validate(p, args[k]);
+      p->free_blocks = fb;
+      p->free_slots = fs;
+      p->q_blocks = qb;
+      p->q_slots = qs;
+      if (rc) return rc;
+    } else {
+      int rc = append_validate(p, args[k]);
+      if (rc) return rc;
+    }
+    if (p->device >= 0) {
+      for (int i = 0; i < args[k].n; ++i)
+        if (args[k].n_new[i] > 0 && !args[k].src_kv)
+          return fail(KV_EINVAL, "null src_kv with tokens to append");
+    }
+  }
+  // Phase 2: apply and build tasks.
+  std::vector<KvTask> tasks;
+  std::vector<long long> rows(n_pools, 0);
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = args[k].pool;
+    if (args[k].begin_step) do_begin_step(p);
+    do_release(p, args[k].n_release, args[k].release_ids);
+    do_append(p, args[k], (int16_t)k, tasks);
+    for (int i = 0; i < args[k].n; ++i) rows[k] += args[k].n_new[i];
+  }
+  if (p0->device < 0 || tasks.empty()) return KV_OK;
+  // Phase 3: stage params + tasks, copy host sources if needed, launch.
+  DeviceGuard dg(p0->device);
+  if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DeviceCtx *ctx = ctx_for(p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::vector<KvPoolParams> params(n_pools);
+  // host-resident sources (KV_SRC_HOST) are copied into ONE device staging buffer
+  size_t host_src_bytes = 0;
+  for (int k = 0; k < n_pools; ++k)
+    if (args[k].flags & KV_SRC_HOST) host_src_bytes += (size_t)rows[k] * args[k].pool->token_bytes;
+  StageBuf *sb = nullptr;
+  if (host_src_bytes > 0) {
+    int rc = ctx->acquire(ctx->src, ctx->next_src, host_src_bytes, false, &sb);
+    if (rc) return rc;
+  }
+  size_t src_off = 0;
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = args[k].pool;
+    KvPoolParams &pp = params[k];
+    std::memset(&pp, 0, sizeof pp);
+    const char *src = static_cast<const char *>(args[k].src_kv);
+    if ((args[k].flags & KV_SRC_HOST) && rows[k] > 0) {
+      const size_t bytes = (size_t)rows[k] * p->token_bytes;
+      CU(cudaMemcpyAsync(sb->dev + src_off, src, bytes, cudaMemcpyHostToDevice, st));
+      src = sb->dev + src_off;
+      src_off += bytes;
+    }
+    pp.src = src;
+    pp.dst = p->pool;
+    pp.publish = 0;
+  }
+  const size_t pbytes = sizeof(KvPoolParams) * n_pools;
+  const size_t tbytes = sizeof(KvTask) * tasks.size();
+  StageBuf *b = nullptr;
+  int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + tbytes, true, &b);
+  if (rc) return rc;
+  std::memcpy(b->host, params.data(), pbytes);
+  std::memcpy(b->host + pbytes, tasks.data(), tbytes);
+  CU(cudaMemcpyAsync(b->dev, b->host, pbytes + tbytes, cudaMemcpyHostToDevice, st));
+  const int grid = copy_grid(p0->device, (int)tasks.size());
+  CU(launch_copy(kTokMajor, kPaged, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                 (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+                 p0->geom_dev(), grid, st));
+  g_launches++;
+  p0->kernels++;
+  if (sb) {
+    int rc2 = ctx->done(sb, st);  // the staged source outlives the kernel
+    if (rc2) return rc2;
+  }
+  return ctx->done(b, st);
+}
+
+KV_API int kv_append(kv_pool_t *p, int32_t n, const int64_t *req_ids, const int32_t *n_new,
+                     const void *src_kv, int32_t flags, void *stream) {
+  kv_append_args_t a{};
+  a.pool = p;
+  a.n = n;
+  a.req_ids = req_ids;
+  a.n_new = n_new;
+  a.src_kv = src_kv;
+  a.flags = flags;
+  return kv_append_multi(1, &a, stream);
+}
+
+namespace {
+
+int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st) {
+  if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
+  kv_pool *p0 = pools[0];
+  if (!p0) return fail(KV_EINVAL, "null pool");
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    if (!p) return fail(KV_EINVAL, "null pool");
+    if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+    if (!p->has_succ) return fail(KV_EPEER, "pool %d has no successor", p->node_id);
+    if (step == 0 || step <= p->last_step)
+      return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
+                  (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
+    if (p->device != p0->device || !p->same_geom(*p0))
+      return fail(KV_EINVAL, "pools of one launch must share device and geometry");
+    for (int k2 = 0; k2 < k; ++k2)
+      if (pools[k2] == p) return fail(KV_EINVAL, "pool listed twice");
+  }
+  std::vector<KvTask> tasks;
+  std::vector<KvPoolParams> params(n_pools);
+  std::vector<int> ntask(n_pools);
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    const size_t before = tasks.size();
+    const uint64_t bytes = build_dirty_tasks(p, (int16_t)k, tasks, false, nullptr);
+    if (tasks.size() == before) push_publish_only(tasks, (int16_t)k);
+    ntask[k] = (int)(tasks.size() - before);
+    if (p->abort_after >= 0 && p->abort_after < ntask[k]) {
+      tasks.resize(before + p->abort_after);  // fault injection: partial step, no publish
+      ntask[k] = p->abort_after;
+    }
+    p->last_step_bytes = bytes;
+  }
+  if (p0->device < 0) {  // tables only
+    for (int k = 0; k < n_pools; ++k) {
+      kv_pool *p = pools[k];
+      p->bytes_replicated += p->last_step_bytes;
+      p->pub_len = p->slot_len;
+      p->last_step = step;
+      p->tasks_launched += ntask[k];
+    }
+    return KV_OK;
+  }
+  DeviceGuard dg(p0->device);
+  if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
+  DeviceCtx *ctx = ctx_for(p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const size_t pbytes = sizeof(KvPoolParams) * n_pools;
+  size_t sbytes = 0;
+  for (int k = 0; k < n_pools; ++k) sbytes += 12 * (size_t)pools[k]->R;
+  sbytes = (sbytes + 15) & ~(size_t)15;
+  const size_t tbytes = sizeof(KvTask) * tasks.size();
+  StageBuf *b = nullptr;
+  int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + sbytes + tbytes, true, &b);
+  if (rc) return rc;
+  char *h = b->host;
+  size_t off = pbytes;
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    KvPoolParams &pp = params[k];
+    std::memset(&pp, 0, sizeof pp);
+    pp.src = p->pool;
+    pp.dst = p->succ_replica;
+    pp.meta = p->succ_meta;
+    std::memcpy(h + off, p->slot_req.data(), 8 * (size_t)p->R);
+    pp.slot_req = reinterpret_cast<const int64_t *>(b->dev + off);
+    off += 8 * (size_t)p->R;
+    std::memcpy(h + off, p->slot_len.data(), 4 * (size_t)p->R);
+    pp.slot_len = reinterpret_cast<const int32_t *>(b->dev + off);
+    off += 4 * (size_t)p->R;
+    pp.counter = p->counter;
+    const bool aborting = p->abort_after >= 0;
+    p->issued += (unsigned long long)ntask[k];
+    pp.target = aborting ? ~0ull : p->issued;
+    pp.step = step;
+    pp.max_reqs = p->R;
+    pp.max_blk = p->M;
+    pp.writer_node = p->node_id;
+    pp.publish = 1;
+  }
+  std::memcpy(h, params.data(), pbytes);
+  std::memcpy(h + pbytes + sbytes, tasks.data(), tbytes);
+  CU(cudaMemcpyAsync(b->dev, h, pbytes + sbytes + tbytes, cudaMemcpyHostToDevice, st));
+  if (!tasks.empty()) {
+    const int grid = copy_grid(p0->device, (int)tasks.size());
+    CU(launch_copy(kPaged, kPaged, reinterpret_cast<const KvTask *>(b->dev + pbytes + sbytes),
+                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+                   p0->geom_dev(), grid, st));
+    g_launches++;
+    p0->kernels++;
+  }
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    p->bytes_replicated += p->last_step_bytes;
+    p->tasks_launched += ntask[k];
+    p->pub_len = p->slot_len;
+    p->last_step = step;
+    p->abort_after = -1;
+  }
+  return ctx->done(b, st);
+}
+
+}  // namespace
+
+KV_API int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream) {
+  return replicate_impl(1, &p, step, static_cast<cudaStream_t>(stream));
+}
+
+KV_API int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step,
+                                   void *stream) {
+  return replicate_impl(n_pools, pools, step, static_cast<cudaStream_t>(stream));
+}
+
+KV_API int kv_inject_abort(kv_pool_t *p, int32_t tasks) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  p->abort_after = tasks < 0 ? -1 : tasks;
+  return KV_OK;
+}
+
+KV_API int kv_fail_stage(kv_pool_t *p, void *stream) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  if (p->dead) return fail(KV_ESTATE, "pool %d already dead", p->node_id);
+  p->dead = true;
+  p->has_succ = false;
+  if (p->device < 0) return KV_OK;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CU(cudaMemsetAsync(p->pool, 0xFF, (size_t)p->NB * p->block_bytes, st));
+  CU(cudaMemsetAsync(p->replica, 0xFF, (size_t)p->replica_blocks * p->block_bytes, st));
+  CU(cudaMemsetAsync(p->meta, 0xFF, meta_bytes(p->R, p->M), st));
+  return KV_OK;
+}
+
+KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder_replica_blocks,
+                      const void *holder_meta, void *stream, uint64_t *t_star,
+                      int64_t *req_ids_out, int32_t *resume_len_out, int32_t cap,
+                      int32_t *n_out) {
+  if (!dst || !holder_replica || !holder_meta) return fail(KV_EINVAL, "null argument");
+  if (dst->dead) return fail(KV_ESTATE, "restore target %d is dead", dst->node_id);
+  if (dst->device < 0) return fail(KV_ESTATE, "restore needs a device pool");
+  DeviceGuard dg(dst->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int R = dst->R, M = dst->M, B = dst->g.block_size;
+  // 1. acquire the holder's seq and the parity metadata (synchronous read).
+  std::vector<char> meta(meta_bytes(R, M));
+  CU(cudaStreamSynchronize(st));
+  CU(cudaMemcpy(meta.data(), holder_meta, 32, cudaMemcpyDefault));
+  uint64_t seq;
+  int32_t hdr[4];
+  std::memcpy(&seq, meta.data(), 8);
+  std::memcpy(hdr, meta.data() + 8, 16);
+  if (hdr[3] != kMetaMagic || hdr[1] != R || hdr[2] != M)
+    return fail(KV_ENOREPLICA, "holder metadata invalid (magic %x, R %d, M %d)", hdr[3], hdr[1],
+                hdr[2]);
+  if (seq == 0 || seq == ~0ull) return fail(KV_ENOREPLICA, "holder published nothing (seq %llu)",
+                                            (unsigned long long)seq);
+  CU(cudaMemcpy(meta.data(), holder_meta, meta.size(), cudaMemcpyDefault));
+  std::memcpy(&seq, meta.data(), 8);
+  const int par = (int)(seq & 1);
+  const int64_t *mreq = reinterpret_cast<const int64_t *>(meta.data() + 32) + (size_t)par * R;
+  const int32_t *mlen =
+      reinterpret_cast<const int32_t *>(meta.data() + meta_off_len(R)) + (size_t)par * R;
+  const int32_t *mbt = reinterpret_cast<const int32_t *>(meta.data() + meta_off_bt(R));
+  struct Ent {
+    int64_t req;
+    int len, slot;
+  };
+  std::vector<Ent> ents;
+  long long need_blocks = 0;
+  for (int s = 0; s < R; ++s)
+    if (mreq[s] >= 0) {
+      if (mlen[s] < 0 || ceil_div(mlen[s], B) > M)
+        return fail(KV_ENOREPLICA, "holder metadata slot %d corrupt", s);
+      ents.push_back({mreq[s], mlen[s], s});
+      need_blocks += ceil_div(mlen[s], B);
+    }
+  std::sort(ents.begin(), ents.end(), [](const Ent &a, const Ent &b) { return a.req < b.req; });
+  if ((int)ents.size() > cap) return fail(KV_EINVAL, "output capacity %d < %zu", cap, ents.size());
+  if ((long long)ents.size() > dst->free_slots.size() || need_blocks > dst->free_blocks.size())
+    return fail(KV_ENOMEM, "restore target too small");
+  for (auto &e : ents) {
+    if (dst->slot_of.count(e.req))
+      return fail(KV_EINVAL, "request %lld already in restore target", (long long)e.req);
+    for (int j = 0; j < ceil_div(e.len, B); ++j) {
+      const int b = mbt[(size_t)e.slot * M + j];
+      if (b < 0 || b >= holder_replica_blocks)
+        return fail(KV_ENOREPLICA, "holder bt entry out of range");
+    }
+  }
+  // 2. allocate (req_id asc, j asc, lowest free ids) and build the remap tasks.
+  std::vector<KvTask> tasks;
+  for (auto &e : ents) {
+    const int s = dst->free_slots.take_min();
+    dst->slot_of[e.req] = s;
+    dst->slot_req[s] = e.req;
+    dst->slot_len[s] = e.len;
+    dst->pub_len[s] = 0;
+    dst->slot_bt[s].clear();
+    for (int j = 0; j < ceil_div(e.len, B); ++j) {
+      const int nb = dst->free_blocks.take_min();
+      dst->slot_bt[s].push_back(nb);
+      const int valid = std::min(B, e.len - j * B);
+      push_item(tasks, 0, mbt[(size_t)e.slot * M + j], nb, -1, j, 0, valid, dst->combos,
+                dst->task_segs);
+    }
+  }
+  // 3. copy valid slots (local HBM, or NVLink reads when the holder is remote).
+  if (!tasks.empty()) {
+    DeviceCtx *ctx = ctx_for(dst->device);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    KvPoolParams pp;
+    std::memset(&pp, 0, sizeof pp);
+    pp.src = static_cast<const char *>(holder_replica);
+    pp.dst = dst->pool;
+    const size_t pbytes = sizeof pp, tbytes = sizeof(KvTask) * tasks.size();
+    StageBuf *b = nullptr;
+    int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + tbytes, true, &b);
+    if (rc) return rc;
+    std::memcpy(b->host, &pp, pbytes);
+    std::memcpy(b->host + pbytes, tasks.data(), tbytes);
+    CU(cudaMemcpyAsync(b->dev, b->host, pbytes + tbytes, cudaMemcpyHostToDevice, st));
+    CU(launch_copy(kPaged, kPaged, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+                   dst->geom_dev(), copy_grid(dst->device, (int)tasks.size()), st));
+    g_launches++;
+    dst->kernels++;
+    rc = ctx->done(b, st);
+    if (rc) return rc;
+  }
+  // 4. outputs
+  if (t_star) *t_star = seq;
+  for (size_t i = 0; i < ents.size(); ++i) {
+    if (req_ids_out) req_ids_out[i] = ents[i].req;
+    if (resume_len_out) resume_len_out[i] = ents[i].len;
+  }
+  if (n_out) *n_out = (int32_t)ents.size();
+  return KV_OK;
+}
+
+// ---- NCCL-comparison pack / unpack -------------------------------------------
+namespace {
+size_t packed_layout(kv_pool *p, size_t n_tasks, uint64_t payload_bytes, KvPackedHeader *h) {
+  size_t off = sizeof(KvPackedHeader);
+  off = (off + 31) & ~(size_t)31;
+  h->task_off = off;
+  off += sizeof(KvTask) * n_tasks;
+  off = (off + 15) & ~(size_t)15;
+  h->slot_off = off;
+  off += 12 * (size_t)p->R;
+  off = (off + 255) & ~(size_t)255;
+  h->payload_off = off;
+  h->payload_bytes = payload_bytes;
+  off += payload_bytes;
+  h->total_bytes = off;
+  return off;
+}
+}  // namespace
+
+KV_API int kv_pack_bytes(kv_pool_t *p, size_t *bytes_out) {
+  if (!p || !bytes_out) return fail(KV_EINVAL, "null argument");
+  std::vector<KvTask> tasks;
+  int32_t unit = 0;
+  const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit);
+  if (tasks.empty()) push_publish_only(tasks, 0);
+  KvPackedHeader h{};
+  *bytes_out = packed_layout(p, tasks.size(), bytes, &h);
+  return KV_OK;
+}
+
+KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, size_t *bytes_out,
+                        void *stream) {
+  if (!p || !packed) return fail(KV_EINVAL, "null argument");
+  if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+  if (p->device < 0) return fail(KV_ESTATE, "pack needs a device pool");
+  if (step == 0 || step <= p->last_step) return fail(KV_EINVAL, "step not increasing");
+  std::vector<KvTask> tasks;
+  int32_t unit = 0;
+  const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit);
+  if (tasks.empty()) push_publish_only(tasks, 0);
+  KvPackedHeader h{};
+  const size_t total = packed_layout(p, tasks.size(), bytes, &h);
+  if (total > cap) return fail(KV_ENOMEM, "packed buffer too small (%zu > %zu)", total, cap);
+  h.magic = kPackedMagic;
+  h.n_tasks = (int32_t)tasks.size();
+  h.max_reqs = p->R;
+  h.max_blk = p->M;
+  h.writer_node = p->node_id;
+  h.seg_bytes = p->seg_bytes;
+  h.step = step;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DeviceCtx *ctx = ctx_for(p->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  // head of the packed buffer: header + receiver-form tasks + slot table
+  const size_t head = h.payload_off;
+  KvPoolParams pp;
+  std::memset(&pp, 0, sizeof pp);
+  StageBuf *b = nullptr;
+  const size_t pbytes = sizeof pp, tbytes = sizeof(KvTask) * tasks.size();
+  int rc = ctx->acquire(ctx->ring, ctx->next, head + pbytes + tbytes, true, &b);
+  if (rc) return rc;
+  char *hb = b->host;
+  std::memset(hb, 0, head);
+  std::memcpy(hb, &h, sizeof h);
+  KvTask *rt = reinterpret_cast<KvTask *>(hb + h.task_off);
+  for (size_t i = 0; i < tasks.size(); ++i) {  // receiver: packed -> paged at the same ids
+    rt[i] = tasks[i];
+    rt[i].src_unit = tasks[i].dst_unit;
+    rt[i].dst_unit = tasks[i].src_unit;
+  }
+  std::memcpy(hb + h.slot_off, p->slot_req.data(), 8 * (size_t)p->R);
+  std::memcpy(hb + h.slot_off + 8 * (size_t)p->R, p->slot_len.data(), 4 * (size_t)p->R);
+  pp.src = p->pool;
+  pp.dst = static_cast<char *>(packed) + h.payload_off;
+  std::memcpy(hb + head, &pp, pbytes);
+  std::memcpy(hb + head + pbytes, tasks.data(), tbytes);
+  CU(cudaMemcpyAsync(packed, hb, head, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(b->dev, hb + head, pbytes + tbytes, cudaMemcpyHostToDevice, st));
+  int real = 0;
+  for (auto &t : tasks) real += t.seg_count > 0;
+  if (real > 0) {
+    CU(launch_copy(kPaged, kPacked, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+                   p->geom_dev(), copy_grid(p->device, (int)tasks.size()), st));
+    g_launches++;
+    p->kernels++;
+  }
+  rc = ctx->done(b, st);
+  if (rc) return rc;
+  p->last_step_bytes = bytes;
+  p->bytes_replicated += bytes;
+  p->pub_len = p->slot_len;
+  p->last_step = step;
+  if (bytes_out) *bytes_out = total;
+  return KV_OK;
+}
+
+KV_API int kv_unpack(const void *packed, size_t packed_bytes, void *replica,
+                     int32_t replica_blocks, void *replica_meta, const kv_geom_t *g,
+                     int32_t max_reqs, int32_t max_blocks_per_req, void *stream) {
+  if (!packed || !replica || !replica_meta || !g) return fail(KV_EINVAL, "null argument");
+  int rc = validate_geom(g);
+  if (rc) return rc;
+  if (packed_bytes < sizeof(KvPackedHeader)) return fail(KV_EINVAL, "packed buffer too small");
+  (void)replica_blocks;
+  (void)max_reqs;
+  (void)max_blocks_per_req;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  DeviceCtx *ctx = ctx_for(dev);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!ctx->unpack_counter) {
+    CU(cudaMalloc(reinterpret_cast<void **>(&ctx->unpack_counter), sizeof(unsigned long long)));
+    CU(cudaMemset(ctx->unpack_counter, 0, sizeof(unsigned long long)));
+  }
+  KvGeomDev gd;
+  const int seg = g->head_dim * g->elem_bytes;
+  gd.seg_bytes = seg;
+  gd.token_bytes = g->layers * 2 * g->kv_heads * seg;
+  gd.block_bytes = (long long)gd.token_bytes * g->block_size;
+  gd.block_size = g->block_size;
+  gd.cps_shift = __builtin_ctz(seg / 16);
+  const int grid = copy_grid(dev, (int)std::max<size_t>(1, packed_bytes / 32768 + 1));
+  CU(launch_unpack(static_cast<const char *>(packed), static_cast<char *>(replica),
+                   static_cast<char *>(replica_meta), ctx->unpack_counter, gd, grid,
+                   static_cast<cudaStream_t>(stream)));
+  g_launches++;
+  return KV_OK;
+}
+
+KV_API int kv_query(kv_pool_t *p, int64_t req_id, int32_t *len, int32_t *blocks, int32_t cap,
+                    int32_t *nblk) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  auto it = p->slot_of.find(req_id);
+  if (it == p->slot_of.end()) return fail(KV_EINVAL, "unknown request %lld", (long long)req_id);
+  const int s = it->second;
+  if (len) *len = p->slot_len[s];
+  const int n = (int)p->slot_bt[s].size();
+  if (nblk) *nblk = n;
+  if (blocks)
+    for (int j = 0; j < std::min(n, cap); ++j) blocks[j] = p->slot_bt[s][j];
+  return KV_OK;
+}
+
+KV_API int kv_stats(kv_pool_t *p, kv_stats_t *o) {
+  if (!p || !o) return fail(KV_EINVAL, "null argument");
+  o->free_blocks = p->free_blocks.size();
+  o->quarantined_blocks = (int32_t)p->q_blocks.size();
+  o->used_blocks = p->NB - o->free_blocks - o->quarantined_blocks;
+  o->free_slots = p->free_slots.size();
+  o->quarantined_slots = (int32_t)p->q_slots.size();
+  o->live_reqs = (int32_t)p->slot_of.size();
+  o->dead = p->dead;
+  o->has_successor = p->has_succ;
+  o->last_step = p->last_step;
+  o->bytes_replicated = p->bytes_replicated;
+  o->tasks_launched = p->tasks_launched;
+  o->kernels_launched = p->kernels;
+  o->last_step_bytes = p->last_step_bytes;
+  return KV_OK;
+}
+
+KV_API int kv_dump_slots(kv_pool_t *p, int64_t *req_id, int32_t *len, int32_t *pub_len,
+                         int32_t *nblk) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  for (int s = 0; s < p->R; ++s) {
+    if (req_id) req_id[s] = p->slot_req[s];
+    if (len) len[s] = p->slot_len[s];
+    if (pub_len) pub_len[s] = p->pub_len[s];
+    if (nblk) nblk[s] = (int32_t)p->slot_bt[s].size();
+  }
+  return KV_OK;
+}
+
+KV_API int kv_sync(kv_pool_t *p) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  if (p->device < 0) return KV_OK;
+  DeviceGuard dg(p->device);
+  CU(cudaDeviceSynchronize());
+  CU(cudaGetLastError());
+  return KV_OK;
+}

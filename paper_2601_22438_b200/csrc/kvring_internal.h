@@ -1,0 +1,90 @@
+// Internal types shared by the host core (kvring_host.cpp) and the sm_100a
+// kernels (kvring_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime_api.h>
+
+namespace kvring {
+
+// Address modes of the one copy engine.  A copy task
+// moves `seg_count` (layer, K/V, head, token) slices of seg_bytes each; the
+// slice s of an item with n_tok tokens is combo = s / n_tok, tok = s % n_tok.
+enum AddrMode : int {
+  kPaged = 0,     // base + unit*block_bytes + (combo*B + tok_lo + tok)*seg   (pool / replica)
+  kTokMajor = 1,  // base + (unit + tok)*token_bytes + combo*seg              (dense model KV)
+  kPacked = 2,    // base + (unit + s)*seg                                     (packed send buffer)
+};
+
+// 32-byte copy task (host-built, H2D-staged every step).
+struct alignas(16) KvTask {
+  int32_t src_unit;   // block id / token row / packed segment offset of the item
+  int32_t dst_unit;
+  int16_t pool;       // index into the launch's KvPoolParams
+  int16_t slot;       // request slot of the item (bt publication), -1 = none
+  int16_t j;          // logical block index of the item
+  int16_t tok_lo;     // first token slot inside the block
+  int16_t n_tok;      // tokens in the item (1..B)
+  int16_t flags;      // kFirst: this task writes the item's bt entry
+  int32_t seg_begin;  // first slice (item-relative) of this task
+  int32_t seg_count;  // slices in this task (0 = publish-only task)
+  int32_t pad;
+};
+static_assert(sizeof(KvTask) == 32, "KvTask must be 32 B");
+enum : int16_t { kFirst = 1 };
+
+// Per-pool launch parameters (device copy staged with the tasks).
+struct alignas(16) KvPoolParams {
+  const char *src;             // source base
+  char *dst;                   // destination base
+  char *meta;                  // destination metadata (publish), or nullptr
+  const int64_t *slot_req;     // staged [R] req ids (publish)
+  const int32_t *slot_len;     // staged [R] lengths (publish)
+  unsigned long long *counter; // monotone completed-task counter (publish)
+  unsigned long long target;   // counter value after the last task of this launch
+  unsigned long long step;     // seq to publish
+  int32_t max_reqs, max_blk, writer_node, publish;
+  int32_t src_mode_unused, pad0, pad1, pad2;
+};
+
+struct KvGeomDev {
+  long long block_bytes;
+  int token_bytes;
+  int seg_bytes;
+  int block_size;
+  int cps_shift;    // log2(seg_bytes / 16): 16-B chunks per slice
+};
+
+// Metadata region layout (include/kvring.h).
+constexpr int kMetaMagic = 0x4B56524D;
+inline size_t meta_off_req(int) { return 32; }
+inline size_t meta_off_len(int R) { return 32 + 16 * (size_t)R; }
+inline size_t meta_off_bt(int R) { return 32 + 24 * (size_t)R; }
+inline size_t meta_bytes(int R, int M) {
+  size_t b = 32 + 24 * (size_t)R + 4 * (size_t)R * (size_t)M;
+  return (b + 255) & ~(size_t)255;
+}
+
+// Packed (NCCL-variant) buffer header.
+struct alignas(16) KvPackedHeader {
+  int32_t magic;        // 0x4B565042 "KVPB"
+  int32_t n_tasks;
+  int32_t max_reqs, max_blk;
+  int32_t writer_node, seg_bytes;
+  unsigned long long step;
+  unsigned long long task_off, slot_off, payload_off, payload_bytes, total_bytes;
+};
+constexpr int kPackedMagic = 0x4B565042;
+
+// Launch wrappers (kvring_kernels.cu).  All return the cudaError_t of the launch.
+cudaError_t launch_copy(int src_mode, int dst_mode, const KvTask *tasks, int n_tasks,
+                        const KvPoolParams *params, const KvGeomDev &g, int grid,
+                        cudaStream_t stream);
+cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
+                          unsigned long long *counter, const KvGeomDev &g, int grid,
+                          cudaStream_t stream);
+cudaError_t launch_meta_init(char *meta, int R, int M, cudaStream_t stream);
+int copy_grid(int device, int n_tasks);
+
+}  // namespace kvring

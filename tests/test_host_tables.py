@@ -1,0 +1,144 @@
+"""CPU tests of libkvring's host logic (no GPU): the library loads and exports
+every symbol include/kvring.h declares, and the C++ allocator / step protocol
+(tables-only pools, device = -1: nothing is launched, no KV byte moves) matches
+the CPU oracle's tables step by step -- at full C2 / C4 geometry."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from kvgen import configs
+from oracle import OracleNode
+from oracle.simulate import OracleRing
+from paper_2601_22438_b200 import kvring as K
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAKE_PTR = 0x1000   # never dereferenced by a tables-only pool
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "kvring.h")).read()
+    declared = set(re.findall(r"\b(kv_[a-z_]+)\s*\(", hdr))
+    lib = K.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(K.EXPORTED)
+    assert K.kv_abi_version() == 1
+    g = K.geom(8)
+    assert K.kv_block_bytes(g) == 512 * 1024
+    assert K.kv_meta_bytes(64, 192) % 256 == 0
+    assert K.kv_meta_bytes(64, 192) >= 32 + 24 * 64 + 4 * 64 * 192
+
+
+def _pool(cfg, node_id, device=-1):
+    g = cfg.geom
+    d = K.kv_pool_desc_t(K.geom(g.layers, g.kv_heads, g.head_dim, g.block_size, g.elem_bytes),
+                         cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, device, node_id,
+                         cfg.num_blocks, None, None, None)
+    return K.kv_pool_create(d)
+
+
+def _tables(h, R):
+    req, ln, pub, nb = K.kv_dump_slots(h, R)
+    out = {}
+    for s in range(R):
+        if req[s] >= 0:
+            out[int(req[s])] = (s, int(ln[s]), K.kv_query(h, int(req[s]))[1])
+    return out
+
+
+@pytest.mark.parametrize("name,steps", [("c1_tiny", 9), ("c2_pp4_b64", 260), ("c4_failover_16", 60)])
+def test_tables_match_oracle(name, steps):
+    """Slots, lengths, block ids and per-step payload bytes == oracle (metadata mode)."""
+    cfg = configs.ALL[name]
+    cfg = configs.scaled(cfg, fail_step=None, fail_node=None)
+    ring = OracleRing(cfg, content=False)
+    sched = ring.sched
+    coords = ring.coords
+    hs = {c: _pool(cfg, k) for k, c in enumerate(coords)}
+    for c in coords:
+        K.kv_set_successor(hs[c], 0, FAKE_PTR, cfg.num_blocks, FAKE_PTR)
+    try:
+        for t in range(steps):
+            ring.appends(t)
+            entries = []
+            for c in coords:
+                p = c[0]
+                ev = sched[p].steps[t]
+                ids, n_new = ev.appends()
+                entries.append(dict(pool=hs[c], begin_step=1, release=ev.retire,
+                                    req_ids=sorted(ev.decode) + [r for r, _ in ev.admit],
+                                    n_new=[1] * len(ev.decode) + [pp for _, pp in ev.admit], src=None))
+            K.kv_append_multi(entries)
+            if t >= 1:
+                before = {c: ring.nodes[c].pub_len.copy() for c in coords}
+                moved0 = ring.moved
+                ring.replicate(t)
+                K.kv_replicate_step_multi([hs[c] for c in coords], t)
+                total = sum(K.kv_stats(hs[c])["last_step_bytes"] for c in coords)
+                assert total == ring.moved - moved0
+            for c in coords:
+                assert _tables(hs[c], cfg.max_reqs) == ring.nodes[c].live(), (t, c)
+                st = K.kv_stats(hs[c])
+                n = ring.nodes[c]
+                assert st["free_blocks"] == len(n.free_blocks)
+                assert st["quarantined_blocks"] == len(n.q_blocks)
+    finally:
+        for h in hs.values():
+            K.kv_pool_destroy(h)
+
+
+def test_errors_and_all_or_nothing():
+    cfg = configs.scaled(configs.C1, num_blocks=4, max_reqs=2, max_blocks_per_req=4)
+    h = _pool(cfg, 0)
+    try:
+        K.kv_append(h, [1], [40], None)                         # 3 blocks
+        before = _tables(h, 2)
+        with pytest.raises(K.KvError) as e:
+            K.kv_append(h, [1, 2], [9, 20], None)               # needs 3 more, 1 free
+        assert e.value.code == K.KV_ENOMEM
+        assert _tables(h, 2) == before
+        with pytest.raises(K.KvError) as e:
+            K.kv_append(h, [5], [0], None)
+        assert e.value.code == K.KV_EINVAL                       # empty admission
+        with pytest.raises(K.KvError) as e:
+            K.kv_append(h, [7, 7], [1, 1], None)
+        assert e.value.code == K.KV_EINVAL
+        with pytest.raises(K.KvError) as e:
+            K.kv_release(h, [99])
+        assert e.value.code == K.KV_EINVAL
+        with pytest.raises(K.KvError) as e:
+            K.kv_replicate_step(h, 1)
+        assert e.value.code == K.KV_EPEER
+        K.kv_set_successor(h, 1, FAKE_PTR, 4, FAKE_PTR)
+        with pytest.raises(K.KvError) as e:
+            K.kv_replicate_step(h, 0)
+        assert e.value.code == K.KV_EINVAL                       # steps start at 1
+        K.kv_replicate_step(h, 3)
+        with pytest.raises(K.KvError) as e:
+            K.kv_replicate_step(h, 3)
+        assert e.value.code == K.KV_EINVAL                       # strictly increasing
+        with pytest.raises(K.KvError):
+            K.kv_set_successor(h, 1, FAKE_PTR, 3, FAKE_PTR)      # replica region too small
+        # release -> quarantine: not reusable before begin_step (R7)
+        K.kv_release(h, [1])
+        assert K.kv_stats(h)["quarantined_blocks"] == 3
+        with pytest.raises(K.KvError) as e:
+            K.kv_append(h, [2], [20], None)
+        assert e.value.code == K.KV_ENOMEM
+        K.kv_begin_step(h)
+        K.kv_append(h, [2], [20], None)
+        assert K.kv_query(h, 2) == (20, [0, 1])
+    finally:
+        K.kv_pool_destroy(h)
+
+
+def test_bad_geometry_rejected():
+    for kw in (dict(layers=0), dict(head_dim=100), dict(elem_bytes=4), dict(block_size=0)):
+        g = dict(layers=2, kv_heads=8, head_dim=128, block_size=16, elem_bytes=2)
+        g.update(kw)
+        d = K.kv_pool_desc_t(K.geom(**g), 8, 2, 4, -1, 0, 8, None, None, None)
+        with pytest.raises(K.KvError) as e:
+            K.kv_pool_create(d)
+        assert e.value.code == K.KV_EINVAL
