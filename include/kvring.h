@@ -164,6 +164,24 @@ int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream);
 /* Same for several pools of ONE device in a single launch. */
 int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, void *stream);
 
+/* Decode-loop driver: for each step, kv_append_multi(append) on append_stream,
+ * then -- ordered after it by an event when the streams differ -- the
+ * publication kv_replicate_step_multi(repl_pools, step) on repl_stream: the
+ * paper's "separate CUDA stream ... to overlap the communication with
+ * computation" (§3.2).  Optional cudaEvent_t handles are recorded on
+ * repl_stream before the publication's H2D (ev_call), around its kernel
+ * (ev_kernel_start / ev_kernel_end) and after it (ev_done).  Stops at the
+ * first error (steps before it stay applied). */
+typedef struct {
+  int32_t n_append;
+  const kv_append_args_t *append;
+  int32_t n_repl;              /* 0: no publication this step (e.g. step 0) */
+  kv_pool_t *const *repl_pools;
+  uint64_t step;
+  void *ev_call, *ev_kernel_start, *ev_kernel_end, *ev_done;
+} kv_step_t;
+int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream, void *repl_stream);
+
 /* Fault injection: the next replicate of p executes only its first
  * `tasks` copy tasks and never publishes -- a stage dying mid-step. -1 clears. */
 int kv_inject_abort(kv_pool_t *p, int32_t tasks);
@@ -224,6 +242,12 @@ const char *kv_last_error(void);
 /* Kernels launched by this process through libkvring, all kinds (evidence
  * counter for bench gpu_launches). */
 uint64_t kv_kernel_launch_count(void);
+
+/* Profiling hook: record the given cudaEvent_t handles (either may be NULL)
+ * on the launch stream immediately before / after the NEXT kernel this thread
+ * launches through libkvring (the descriptor H2D that precedes it is excluded).
+ * Used by bench.py to time the ring-put kernel live. */
+int kv_time_next_launch(void *ev_before, void *ev_after);
 
 #ifdef __cplusplus
 }

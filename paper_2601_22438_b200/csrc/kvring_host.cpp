@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -164,6 +165,25 @@ DeviceCtx *ctx_for(int device) {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Optional CUDA events recorded right around the next kernel this thread
+// launches through libkvring (kv_time_next_launch): kernel-only timing for the
+// bench's live roofline, excluding the descriptor H2D that precedes it.
+thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+
+cudaError_t timed_launch(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
+                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t st) {
+  cudaEvent_t b = g_ev_before, a = g_ev_after;
+  g_ev_before = g_ev_after = nullptr;
+  if (b) {
+    cudaError_t e = cudaEventRecord(b, st);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st);
+  if (e != cudaSuccess) return e;
+  if (a) return cudaEventRecord(a, st);
+  return cudaSuccess;
+}
+
 }  // namespace
 
 struct kv_pool {
@@ -175,6 +195,7 @@ struct kv_pool {
   int token_bytes = 0, seg_bytes = 0, combos = 0, task_segs = 0, cps_shift = 0;
   // ring link
   bool has_succ = false;
+  bool succ_sys = true;  // successor memory is not this GPU's HBM (NVLink peer)
   int succ_node = -1, succ_replica_blocks = 0;
   char *succ_replica = nullptr, *succ_meta = nullptr;
   // allocator (R6, R7)
@@ -184,6 +205,10 @@ struct kv_pool {
   std::vector<int32_t> slot_len, pub_len;
   std::vector<std::vector<int32_t>> slot_bt;
   std::unordered_map<int64_t, int> slot_of;
+  std::vector<uint32_t> rel_stamp, app_stamp;  // per-slot call stamps (validation)
+  uint32_t call_id = 0;
+  std::vector<int64_t> scratch_ids;
+  std::vector<KvTask> scratch_tasks;
   // state
   bool dead = false;
   uint64_t last_step = 0;
@@ -253,33 +278,42 @@ inline void push_publish_only(std::vector<KvTask> &out, int16_t pool) {
 }
 
 // ---- append ---------------------------------------------------------------
-int append_validate(kv_pool *p, const kv_append_args_t &a) {
+// Validates one pool's releases + appends against `free_b` / `free_s` free
+// blocks / slots (the counts after the optional begin_step).  No allocation
+// on the hot path: duplicate detection uses per-slot call stamps.
+int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, long long free_s) {
   if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
   if (a.n < 0 || a.n_release < 0) return fail(KV_EINVAL, "negative count");
   if ((a.n > 0 && (!a.req_ids || !a.n_new)) || (a.n_release > 0 && !a.release_ids))
     return fail(KV_EINVAL, "null array");
-  // releases first (their blocks only reach the free list at the next begin_step)
-  std::unordered_map<int64_t, int> seen;
+  const uint32_t cid = ++p->call_id;
   for (int i = 0; i < a.n_release; ++i) {
-    if (!p->slot_of.count(a.release_ids[i]))
+    auto it = p->slot_of.find(a.release_ids[i]);
+    if (it == p->slot_of.end())
       return fail(KV_EINVAL, "release of unknown request %lld", (long long)a.release_ids[i]);
-    if (seen[a.release_ids[i]]++) return fail(KV_EINVAL, "request released twice");
+    if (p->rel_stamp[it->second] == cid) return fail(KV_EINVAL, "request released twice");
+    p->rel_stamp[it->second] = cid;
   }
   const int B = p->g.block_size;
   long long need_blocks = 0, need_slots = 0, tokens = 0;
-  std::unordered_map<int64_t, int> in_call;
+  p->scratch_ids.clear();
   for (int i = 0; i < a.n; ++i) {
     const int64_t r = a.req_ids[i];
     const int n = a.n_new[i];
     if (n < 0) return fail(KV_EINVAL, "negative n_new");
-    if (in_call[r]++) return fail(KV_EINVAL, "request %lld twice in one append", (long long)r);
-    if (seen.count(r)) return fail(KV_EINVAL, "request %lld released and appended", (long long)r);
     long long cur = 0;
     auto it = p->slot_of.find(r);
     if (it != p->slot_of.end()) {
-      cur = p->slot_len[it->second];
+      const int s = it->second;
+      if (p->app_stamp[s] == cid)
+        return fail(KV_EINVAL, "request %lld twice in one append", (long long)r);
+      if (p->rel_stamp[s] == cid)
+        return fail(KV_EINVAL, "request %lld released and appended", (long long)r);
+      p->app_stamp[s] = cid;
+      cur = p->slot_len[s];
     } else {
       if (n <= 0) return fail(KV_EINVAL, "admission of %lld with no tokens", (long long)r);
+      p->scratch_ids.push_back(r);
       ++need_slots;
     }
     const long long tot = (cur + n + B - 1) / B;
@@ -287,9 +321,15 @@ int append_validate(kv_pool *p, const kv_append_args_t &a) {
     need_blocks += tot - (cur + B - 1) / B;
     tokens += n;
   }
-  if (need_slots > p->free_slots.size() || need_blocks > p->free_blocks.size())
-    return fail(KV_ENOMEM, "pool %d exhausted (need %lld blocks / %lld slots, free %d / %d)",
-                p->node_id, need_blocks, need_slots, p->free_blocks.size(), p->free_slots.size());
+  if (p->scratch_ids.size() > 1) {
+    std::sort(p->scratch_ids.begin(), p->scratch_ids.end());
+    for (size_t i = 1; i < p->scratch_ids.size(); ++i)
+      if (p->scratch_ids[i] == p->scratch_ids[i - 1])
+        return fail(KV_EINVAL, "request %lld twice in one append", (long long)p->scratch_ids[i]);
+  }
+  if (need_slots > free_s || need_blocks > free_b)
+    return fail(KV_ENOMEM, "pool %d exhausted (need %lld blocks / %lld slots, free %lld / %lld)",
+                p->node_id, need_blocks, need_slots, free_b, free_s);
   if (tokens > 0x7fffffffLL) return fail(KV_EINVAL, "too many tokens in one append");
   return KV_OK;
 }
@@ -389,6 +429,12 @@ KV_API const char *kv_last_error(void) { return g_err.c_str(); }
 
 KV_API uint64_t kv_kernel_launch_count(void) { return g_launches.load(); }
 
+KV_API int kv_time_next_launch(void *ev_before, void *ev_after) {
+  g_ev_before = static_cast<cudaEvent_t>(ev_before);
+  g_ev_after = static_cast<cudaEvent_t>(ev_after);
+  return KV_OK;
+}
+
 KV_API size_t kv_block_bytes(const kv_geom_t *g) {
   if (!g || validate_geom(g) != KV_OK) return 0;
   return (size_t)g->layers * 2 * g->kv_heads * g->block_size * g->head_dim * g->elem_bytes;
@@ -433,6 +479,9 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
   p->slot_len.assign(p->R, 0);
   p->pub_len.assign(p->R, 0);
   p->slot_bt.assign(p->R, {});
+  p->rel_stamp.assign(p->R, 0);
+  p->app_stamp.assign(p->R, 0);
+  p->slot_of.reserve(2 * (size_t)p->R);
   for (auto &v : p->slot_bt) v.reserve(8);
   if (p->device >= 0) {
     DeviceGuard dg(p->device);
@@ -475,6 +524,14 @@ KV_API int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
       return fail(KV_EINVAL, "successor replica region (%d blocks) smaller than pool (%d)",
                   succ_replica_blocks, p->NB);
     p->has_succ = true;
+    p->succ_sys = true;
+    if (p->device >= 0) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, succ_replica) == cudaSuccess &&
+          at.type == cudaMemoryTypeDevice && at.device == p->device)
+        p->succ_sys = false;
+      cudaGetLastError();
+    }
     p->succ_node = succ_node;
     p->succ_replica = static_cast<char *>(succ_replica);
     p->succ_replica_blocks = succ_replica_blocks;
@@ -497,7 +554,7 @@ KV_API int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids) {
   a.pool = p;
   a.n_release = n;
   a.release_ids = req_ids;
-  int rc = append_validate(p, a);
+  int rc = append_validate(p, a, p->free_blocks.size(), p->free_slots.size());
   if (rc) return rc;
   do_release(p, n, req_ids);
   return KV_OK;
@@ -505,6 +562,8 @@ KV_API int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids) {
 
 KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream) {
   if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
+  if (n_pools > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "at most %d pools per launch",
+                                                    kMaxPoolsPerLaunchHost);
   kv_pool *p0 = args[0].pool;
   if (!p0) return fail(KV_EINVAL, "null pool");
   for (int k = 0; k < n_pools; ++k) {
@@ -519,21 +578,12 @@ KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = args[k].pool;
     if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
-    // validation must see the quarantine released when begin_step is requested
-    if (args[k].begin_step) {
-      IdSet fb = p->free_blocks, fs = p->free_slots;
-      const std::vector<int> qb = p->q_blocks, qs = p->q_slots;
-      do_begin_step(p);
-      int rc = append_validate(p, args[k]);
-      p->free_blocks = fb;
-      p->free_slots = fs;
-      p->q_blocks = qb;
-      p->q_slots = qs;
-      if (rc) return rc;
-    } else {
-      int rc = append_validate(p, args[k]);
-      if (rc) return rc;
-    }
+    // validation sees the quarantine released when begin_step is requested
+    const bool bs = args[k].begin_step != 0;
+    int rc = append_validate(p, args[k],
+                             p->free_blocks.size() + (bs ? (long long)p->q_blocks.size() : 0),
+                             p->free_slots.size() + (bs ? (long long)p->q_slots.size() : 0));
+    if (rc) return rc;
     if (p->device >= 0) {
       for (int i = 0; i < args[k].n; ++i)
         if (args[k].n_new[i] > 0 && !args[k].src_kv)
@@ -541,7 +591,8 @@ KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *
     }
   }
   // Phase 2: apply and build tasks.
-  std::vector<KvTask> tasks;
+  thread_local std::vector<KvTask> tasks;
+  tasks.clear();
   std::vector<long long> rows(n_pools, 0);
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = args[k].pool;
@@ -592,8 +643,8 @@ KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *
   std::memcpy(b->host + pbytes, tasks.data(), tbytes);
   CU(cudaMemcpyAsync(b->dev, b->host, pbytes + tbytes, cudaMemcpyHostToDevice, st));
   const int grid = copy_grid(p0->device, (int)tasks.size());
-  CU(launch_copy(kTokMajor, kPaged, reinterpret_cast<const KvTask *>(b->dev + pbytes),
-                 (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+  CU(timed_launch(kKindAppend, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                 (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), n_pools,
                  p0->geom_dev(), grid, st));
   g_launches++;
   p0->kernels++;
@@ -620,6 +671,8 @@ namespace {
 
 int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st) {
   if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
+  if (n_pools > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "at most %d pools per launch",
+                                                    kMaxPoolsPerLaunchHost);
   kv_pool *p0 = pools[0];
   if (!p0) return fail(KV_EINVAL, "null pool");
   for (int k = 0; k < n_pools; ++k) {
@@ -635,7 +688,8 @@ int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream
     for (int k2 = 0; k2 < k; ++k2)
       if (pools[k2] == p) return fail(KV_EINVAL, "pool listed twice");
   }
-  std::vector<KvTask> tasks;
+  thread_local std::vector<KvTask> tasks;
+  tasks.clear();
   std::vector<KvPoolParams> params(n_pools);
   std::vector<int> ntask(n_pools);
   for (int k = 0; k < n_pools; ++k) {
@@ -643,6 +697,7 @@ int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream
     const size_t before = tasks.size();
     const uint64_t bytes = build_dirty_tasks(p, (int16_t)k, tasks, false, nullptr);
     if (tasks.size() == before) push_publish_only(tasks, (int16_t)k);
+    tasks[before].flags |= kPoolFirst;
     ntask[k] = (int)(tasks.size() - before);
     if (p->abort_after >= 0 && p->abort_after < ntask[k]) {
       tasks.resize(before + p->abort_after);  // fault injection: partial step, no publish
@@ -696,14 +751,17 @@ int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream
     pp.max_blk = p->M;
     pp.writer_node = p->node_id;
     pp.publish = 1;
+    pp.sys_scope = p->succ_sys ? 1 : 0;
   }
   std::memcpy(h, params.data(), pbytes);
   std::memcpy(h + pbytes + sbytes, tasks.data(), tbytes);
   CU(cudaMemcpyAsync(b->dev, h, pbytes + sbytes + tbytes, cudaMemcpyHostToDevice, st));
   if (!tasks.empty()) {
     const int grid = copy_grid(p0->device, (int)tasks.size());
-    CU(launch_copy(kPaged, kPaged, reinterpret_cast<const KvTask *>(b->dev + pbytes + sbytes),
-                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+    static const bool dbg_nopub = getenv("KVRING_DEBUG_RINGPUT_NOPUB") != nullptr;
+    CU(timed_launch(dbg_nopub ? kKindRestore : kKindRingPut,
+                   reinterpret_cast<const KvTask *>(b->dev + pbytes + sbytes),
+                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), n_pools,
                    p0->geom_dev(), grid, st));
     g_launches++;
     p0->kernels++;
@@ -838,8 +896,8 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
     std::memcpy(b->host, &pp, pbytes);
     std::memcpy(b->host + pbytes, tasks.data(), tbytes);
     CU(cudaMemcpyAsync(b->dev, b->host, pbytes + tbytes, cudaMemcpyHostToDevice, st));
-    CU(launch_copy(kPaged, kPaged, reinterpret_cast<const KvTask *>(b->dev + pbytes),
-                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+    CU(timed_launch(kKindRestore, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), 1,
                    dst->geom_dev(), copy_grid(dst->device, (int)tasks.size()), st));
     g_launches++;
     dst->kernels++;
@@ -896,6 +954,7 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
   int32_t unit = 0;
   const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit);
   if (tasks.empty()) push_publish_only(tasks, 0);
+  tasks[0].flags |= kPoolFirst;
   KvPackedHeader h{};
   const size_t total = packed_layout(p, tasks.size(), bytes, &h);
   if (total > cap) return fail(KV_ENOMEM, "packed buffer too small (%zu > %zu)", total, cap);
@@ -938,8 +997,8 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
   int real = 0;
   for (auto &t : tasks) real += t.seg_count > 0;
   if (real > 0) {
-    CU(launch_copy(kPaged, kPacked, reinterpret_cast<const KvTask *>(b->dev + pbytes),
-                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev),
+    CU(timed_launch(kKindPack, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), 1,
                    p->geom_dev(), copy_grid(p->device, (int)tasks.size()), st));
     g_launches++;
     p->kernels++;
@@ -1037,5 +1096,52 @@ KV_API int kv_sync(kv_pool_t *p) {
   DeviceGuard dg(p->device);
   CU(cudaDeviceSynchronize());
   CU(cudaGetLastError());
+  return KV_OK;
+}
+
+// ---- decode-loop driver -------------------------------------------------------
+// For each step: appends on the compute stream, then (after an event) the
+// publication on the replication stream -- the paper's "separate CUDA stream
+// ... to overlap the communication with computation" (§3.2).
+KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream,
+                        void *repl_stream) {
+  if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
+  cudaStream_t sa = static_cast<cudaStream_t>(append_stream);
+  cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
+  thread_local cudaEvent_t ready = nullptr;
+  thread_local int ready_dev = -1;
+  for (int k = 0; k < n_steps; ++k) {
+    const kv_step_t &st = steps[k];
+    int dev = -1;
+    if (st.n_append > 0) {
+      int rc = kv_append_multi(st.n_append, st.append, append_stream);
+      if (rc) return rc;
+      dev = st.append[0].pool->device;
+    }
+    if (st.n_repl <= 0) continue;
+    if (dev < 0) dev = st.repl_pools[0]->device;
+    if (dev < 0) {  // tables-only pools: no streams involved
+      int rc = replicate_impl(st.n_repl, st.repl_pools, st.step, sr);
+      if (rc) return rc;
+      continue;
+    }
+    DeviceGuard dg(dev);
+    if (sa != sr) {
+      if (!ready || ready_dev != dev) {
+        if (ready) cudaEventDestroy(ready);
+        CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        ready_dev = dev;
+      }
+      CU(cudaEventRecord(ready, sa));
+      CU(cudaStreamWaitEvent(sr, ready, 0));
+    }
+    if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
+    g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
+    g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
+    int rc = replicate_impl(st.n_repl, st.repl_pools, st.step, sr);
+    g_ev_before = g_ev_after = nullptr;
+    if (rc) return rc;
+    if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
+  }
   return KV_OK;
 }

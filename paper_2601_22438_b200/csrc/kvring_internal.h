@@ -32,7 +32,7 @@ struct alignas(16) KvTask {
   int32_t pad;
 };
 static_assert(sizeof(KvTask) == 32, "KvTask must be 32 B");
-enum : int16_t { kFirst = 1 };
+enum : int16_t { kFirst = 1, kPoolFirst = 2 };  // kPoolFirst: writes the pool's parity table
 
 // Per-pool launch parameters (device copy staged with the tasks).
 struct alignas(16) KvPoolParams {
@@ -45,7 +45,8 @@ struct alignas(16) KvPoolParams {
   unsigned long long target;   // counter value after the last task of this launch
   unsigned long long step;     // seq to publish
   int32_t max_reqs, max_blk, writer_node, publish;
-  int32_t src_mode_unused, pad0, pad1, pad2;
+  int32_t sys_scope;           // successor is an NVLink peer: system-scope fences / release
+  int32_t pad0, pad1, pad2;
 };
 
 struct KvGeomDev {
@@ -78,9 +79,10 @@ struct alignas(16) KvPackedHeader {
 constexpr int kPackedMagic = 0x4B565042;
 
 // Launch wrappers (kvring_kernels.cu).  All return the cudaError_t of the launch.
-cudaError_t launch_copy(int src_mode, int dst_mode, const KvTask *tasks, int n_tasks,
-                        const KvPoolParams *params, const KvGeomDev &g, int grid,
-                        cudaStream_t stream);
+enum KernelKind : int { kKindAppend = 0, kKindRingPut = 1, kKindRestore = 2, kKindPack = 3 };
+constexpr int kMaxPoolsPerLaunchHost = 64;
+cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
+                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream);
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           unsigned long long *counter, const KvGeomDev &g, int grid,
                           cudaStream_t stream);

@@ -14,6 +14,8 @@
 // completes a pool's last task writes the parity metadata and then the seq
 // flag with st.release.sys (reading R9: a reader that acquires seq = t sees
 // everything of step t).
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "kvring_internal.h"
@@ -39,55 +41,76 @@ __device__ __forceinline__ void st_stream(void *p, const uint4 &v) {
                : "memory");
 }
 
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long *p,
-                                                   unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Byte offset of a task's item base (64-bit) and of slice s inside the item
+// (32-bit: an item never spans more than one block / B token rows).
+template <int MODE>
+__device__ __forceinline__ long long item_base(const KvGeomDev &g, int unit, int tok_lo) {
+  if (MODE == kPacked) return (long long)unit * g.seg_bytes;
+  if (MODE == kPaged) return (long long)unit * g.block_bytes + (long long)tok_lo * g.seg_bytes;
+  return (long long)unit * g.token_bytes;  // kTokMajor
 }
 
 template <int MODE>
-__device__ __forceinline__ long long slice_offset(const KvGeomDev &g, int unit, int s,
-                                                  int n_tok, int tok_lo) {
-  if (MODE == kPacked) return ((long long)unit + s) * g.seg_bytes;
+__device__ __forceinline__ unsigned slice_off(const KvGeomDev &g, int s, int n_tok) {
+  if (MODE == kPacked) return (unsigned)s * (unsigned)g.seg_bytes;
   const int combo = s / n_tok;
   const int tok = s - combo * n_tok;
-  if (MODE == kPaged)
-    return (long long)unit * g.block_bytes +
-           (long long)(combo * g.block_size + tok_lo + tok) * g.seg_bytes;
-  // kTokMajor
-  return ((long long)unit + tok) * g.token_bytes + (long long)combo * g.seg_bytes;
+  if (MODE == kPaged) return (unsigned)(combo * g.block_size + tok) * (unsigned)g.seg_bytes;
+  return (unsigned)tok * (unsigned)g.token_bytes + (unsigned)combo * (unsigned)g.seg_bytes;
 }
 
 // Copy one task's slices: thread t handles 16-B chunks t, t+256, ... of the
-// task; 16 consecutive lanes cover one 256-B slice (coalesced).
+// task; 16 consecutive lanes cover one 256-B slice (coalesced).  All loads of
+// a round are issued before its stores (8 x 16 B in flight per thread).
 template <int SRC, int DST>
 __device__ __forceinline__ void copy_task(const KvTask &tk, const char *__restrict__ src,
                                           char *__restrict__ dst, const KvGeomDev &g) {
+  const char *sb = src + item_base<SRC>(g, tk.src_unit, tk.tok_lo);
+  char *db = dst + item_base<DST>(g, tk.dst_unit, tk.tok_lo);
   const int nchunks = tk.seg_count << g.cps_shift;
   const int cmask = (1 << g.cps_shift) - 1;
   for (int base = 0; base < nchunks; base += kThreads * kUnroll) {
     uint4 v[kUnroll];
-    long long doff[kUnroll];
+    unsigned doff[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int c = base + u * kThreads + (int)threadIdx.x;
       if (c < nchunks) {
         const int s = tk.seg_begin + (c >> g.cps_shift);
-        const int lc = (c & cmask) << 4;
-        const long long so = slice_offset<SRC>(g, tk.src_unit, s, tk.n_tok, tk.tok_lo) + lc;
-        doff[u] = slice_offset<DST>(g, tk.dst_unit, s, tk.n_tok, tk.tok_lo) + lc;
-        v[u] = ld_stream(src + so);
+        const unsigned lc = (unsigned)(c & cmask) << 4;
+        doff[u] = slice_off<DST>(g, s, tk.n_tok) + lc;
+        v[u] = ld_stream(sb + slice_off<SRC>(g, s, tk.n_tok) + lc);
       }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int c = base + u * kThreads + (int)threadIdx.x;
-      if (c < nchunks) st_stream(dst + doff[u], v[u]);
+      if (c < nchunks) st_stream(db + doff[u], v[u]);
     }
   }
 }
 
-// Publication of one pool's step by the CTA that completed its last task.
-__device__ void publish(const KvPoolParams &pp) {
+__device__ __forceinline__ unsigned long long atom_add_release(unsigned long long *p,
+                                                               unsigned long long v, bool sys) {
+  unsigned long long old;
+  if (sys)
+    asm volatile("atom.add.acq_rel.sys.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  else
+    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v, bool sys) {
+  if (sys)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Parity-`step` (req_id, len) table of one pool (reading R9).  Written by the
+// CTA that owns the pool's first task, BEFORE that CTA's release: a reader
+// only trusts parity t once it acquires seq = t, so writing it early is safe.
+__device__ void write_parity_table(const KvPoolParams &pp) {
   char *meta = pp.meta;
   const int R = pp.max_reqs;
   const int par = (int)(pp.step & 1ull);
@@ -97,55 +120,79 @@ __device__ void publish(const KvPoolParams &pp) {
     mreq[s] = pp.slot_req[s];
     mlen[s] = pp.slot_len[s];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *reinterpret_cast<int32_t *>(meta + 8) = pp.writer_node;
-    __threadfence_system();
-    st_release_sys_u64(reinterpret_cast<unsigned long long *>(meta), pp.step);
-  }
+  if (threadIdx.x == 0) *reinterpret_cast<int32_t *>(meta + 8) = pp.writer_node;
 }
 
-// Called by all threads after a task's data stores: bt entry, fence, count, maybe publish.
-__device__ __forceinline__ void finish_task(const KvTask &tk, const KvPoolParams &pp,
-                                            int *s_last) {
-  if (!pp.publish) return;
-  if (threadIdx.x == 0 && (tk.flags & kFirst) && tk.slot >= 0) {
-    int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
-    bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
-  }
-  __syncthreads();  // every thread's stores of this task precede thread 0's fence
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    const unsigned long long old = atomicAdd(pp.counter, 1ull);
-    *s_last = (old + 1ull == pp.target);
-  }
-  __syncthreads();
-  if (*s_last) publish(pp);
-}
+constexpr int kMaxPoolsPerLaunch = 64;
 
-template <int SRC, int DST>
-__global__ void __launch_bounds__(kThreads) copy_kernel(const KvTask *__restrict__ tasks,
-                                                        int n_tasks,
-                                                        const KvPoolParams *__restrict__ params,
-                                                        KvGeomDev g) {
-  __shared__ int s_last;
+// Grid-stride over tasks.  A CTA counts the tasks it finished per pool in
+// shared memory.  After its loop: __syncthreads(), then ONE thread adds the
+// counts with acquire-release RMWs (GPU scope, or system scope when the
+// successor is an NVLink peer) -- the bar.sync + single-release pattern of
+// CUTLASS's semaphore, so no per-thread fences.  The CTA whose RMW completes a
+// pool's count stores that pool's seq with a release store (last-CTA
+// pattern): readers that acquire seq = t see all of step t.
+template <int SRC, int DST, bool PUB>
+__device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
+                                          const KvPoolParams *__restrict__ params,
+                                          const KvGeomDev &g, int n_pools) {
+  __shared__ int s_cnt[kMaxPoolsPerLaunch];
+  if (PUB) {
+    for (int i = threadIdx.x; i < n_pools; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+  }
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
     const KvPoolParams &pp = params[tk.pool];
     copy_task<SRC, DST>(tk, pp.src, pp.dst, g);
-    finish_task(tk, pp, &s_last);
+    if (PUB) {
+      if (tk.flags & kPoolFirst) write_parity_table(pp);
+      if (threadIdx.x == 0) {
+        if ((tk.flags & kFirst) && tk.slot >= 0) {
+          int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
+          bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
+        }
+        s_cnt[tk.pool] += 1;
+      }
+    }
+  }
+  if (!PUB) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n_pools; ++i) {
+      if (s_cnt[i] == 0) continue;
+      const KvPoolParams &pp = params[i];
+      const bool sys = pp.sys_scope != 0;
+      const unsigned long long old =
+          atom_add_release(pp.counter, (unsigned long long)s_cnt[i], sys);
+      if (old + (unsigned long long)s_cnt[i] == pp.target)
+        st_release(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
+    }
   }
 }
 
+// One named kernel per role (ncu / launch lists show what ran).
+#define KV_KERNEL(NAME, SRC, DST, PUB)                                                   \
+  __global__ void __launch_bounds__(kThreads, 4)                                         \
+      NAME(const KvTask *__restrict__ tasks, int n_tasks,                                \
+           const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {          \
+    run_tasks<SRC, DST, PUB>(tasks, n_tasks, params, g, n_pools);                        \
+  }
+KV_KERNEL(kv_append_scatter_kernel, kTokMajor, kPaged, false)  // a2: model KV write stand-in
+KV_KERNEL(kv_ring_put_kernel, kPaged, kPaged, true)            // a4+a5: gather + ring hop + publish
+KV_KERNEL(kv_restore_remap_kernel, kPaged, kPaged, false)      // a8: replica -> new block ids
+KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false)       // a4: NCCL-variant sender
+#undef KV_KERNEL
+
 // Receiver of the NCCL comparison: parameters come from the packed header on
-// the device, so the receiving host never reads the buffer.
-__global__ void __launch_bounds__(kThreads) unpack_kernel(const char *__restrict__ packed,
-                                                          char *replica, char *meta,
-                                                          unsigned long long *counter,
-                                                          KvGeomDev g) {
+// the device, so the receiving host never reads the buffer.  The counter is
+// per call (reset by the publishing CTA), not monotone.
+__global__ void __launch_bounds__(kThreads) kv_unpack_kernel(const char *__restrict__ packed,
+                                                             char *replica, char *meta,
+                                                             unsigned long long *counter,
+                                                             KvGeomDev g) {
   __shared__ KvPoolParams pp;
-  __shared__ int s_last;
-  __shared__ int n_tasks;
+  __shared__ int s_cnt, n_tasks;
   const KvPackedHeader *h = reinterpret_cast<const KvPackedHeader *>(packed);
   if (threadIdx.x == 0) {
     n_tasks = h->n_tasks;
@@ -161,18 +208,34 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const char *__restrict
     pp.max_blk = h->max_blk;
     pp.writer_node = h->writer_node;
     pp.publish = 1;
+    pp.sys_scope = 1;
+    s_cnt = 0;
   }
   __syncthreads();
   const KvTask *tasks = reinterpret_cast<const KvTask *>(packed + h->task_off);
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
     copy_task<kPacked, kPaged>(tk, pp.src, pp.dst, g);
-    finish_task(tk, pp, &s_last);
-    if (s_last && threadIdx.x == 0) *counter = 0ull;  // counter is per call, not monotone
+    if (tk.flags & kPoolFirst) write_parity_table(pp);
+    if (threadIdx.x == 0) {
+      if ((tk.flags & kFirst) && tk.slot >= 0) {
+        int32_t *bt = reinterpret_cast<int32_t *>(meta + 32 + 24 * (size_t)pp.max_reqs);
+        bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
+      }
+      s_cnt += 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt > 0) {
+    const unsigned long long old = atom_add_release(counter, (unsigned long long)s_cnt, true);
+    if (old + (unsigned long long)s_cnt == pp.target) {
+      st_release(reinterpret_cast<unsigned long long *>(meta), pp.step, true);
+      *counter = 0ull;  // per-call counter: the next unpack is stream-ordered after this one
+    }
   }
 }
 
-__global__ void meta_init_kernel(char *meta, int R, int M) {
+__global__ void kv_meta_init_kernel(char *meta, int R, int M) {
   const size_t n_req = 2 * (size_t)R, n_bt = (size_t)R * M;
   const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -206,31 +269,42 @@ int copy_grid(int device, int n_tasks) {
       v = 148;
     sms[d] = v;
   }
-  const int cap = sms[d] * 8;  // 8 resident 256-thread CTAs per SM
+  static int per_sm = 0;
+  if (per_sm == 0) {  // debug knob for experiments: KVRING_CTAS_PER_SM
+    const char *e = getenv("KVRING_CTAS_PER_SM");
+    per_sm = (e && atoi(e) > 0) ? atoi(e) : 8;
+  }
+  const int cap = sms[d] * per_sm;  // grid-stride beyond this
   return n_tasks < cap ? (n_tasks > 0 ? n_tasks : 1) : cap;
 }
 
-cudaError_t launch_copy(int src_mode, int dst_mode, const KvTask *tasks, int n_tasks,
-                        const KvPoolParams *params, const KvGeomDev &g, int grid,
-                        cudaStream_t stream) {
+cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
+                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream) {
   if (n_tasks <= 0) return cudaSuccess;
-#define KV_LAUNCH(S, D)                                                              \
-  if (src_mode == S && dst_mode == D) {                                              \
-    copy_kernel<S, D><<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g);     \
-    return cudaGetLastError();                                                       \
+  if (n_pools > kMaxPoolsPerLaunch) return cudaErrorInvalidValue;
+  switch (kind) {
+    case kKindAppend:
+      kv_append_scatter_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
+      break;
+    case kKindRingPut:
+      kv_ring_put_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
+      break;
+    case kKindRestore:
+      kv_restore_remap_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
+      break;
+    case kKindPack:
+      kv_gather_pack_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
+      break;
+    default:
+      return cudaErrorInvalidValue;
   }
-  KV_LAUNCH(kTokMajor, kPaged)  // append-scatter
-  KV_LAUNCH(kPaged, kPaged)     // ring-put, restore-remap
-  KV_LAUNCH(kPaged, kPacked)    // gather-pack
-  KV_LAUNCH(kPacked, kPaged)    // (host-driven unpack; tests)
-#undef KV_LAUNCH
-  return cudaErrorInvalidValue;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           unsigned long long *counter, const KvGeomDev &g, int grid,
                           cudaStream_t stream) {
-  unpack_kernel<<<grid, kThreads, 0, stream>>>(packed, replica, meta, counter, g);
+  kv_unpack_kernel<<<grid, kThreads, 0, stream>>>(packed, replica, meta, counter, g);
   return cudaGetLastError();
 }
 
@@ -239,7 +313,7 @@ cudaError_t launch_meta_init(char *meta, int R, int M, cudaStream_t stream) {
   int grid = (int)((n + 255) / 256);
   if (grid > 1024) grid = 1024;
   if (grid < 1) grid = 1;
-  meta_init_kernel<<<grid, 256, 0, stream>>>(meta, R, M);
+  kv_meta_init_kernel<<<grid, 256, 0, stream>>>(meta, R, M);
   return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_last_error", "kv_meta_bytes", "kv_pack_bytes", "kv_pack_step", "kv_pool_create",
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
-            "kv_unpack"]
+            "kv_unpack", "kv_time_next_launch", "kv_run_steps"]
 
 
 class KvError(RuntimeError):
@@ -54,6 +54,14 @@ class kv_append_args_t(ctypes.Structure):
                 ("n_release", ctypes.c_int32), ("release_ids", ctypes.c_void_p),
                 ("n", ctypes.c_int32), ("req_ids", ctypes.c_void_p), ("n_new", ctypes.c_void_p),
                 ("src_kv", ctypes.c_void_p), ("flags", ctypes.c_int32)]
+
+
+class kv_step_t(ctypes.Structure):
+    _fields_ = [("n_append", ctypes.c_int32), ("append", ctypes.c_void_p),
+                ("n_repl", ctypes.c_int32), ("repl_pools", ctypes.c_void_p),
+                ("step", ctypes.c_uint64), ("ev_call", ctypes.c_void_p),
+                ("ev_kernel_start", ctypes.c_void_p), ("ev_kernel_end", ctypes.c_void_p),
+                ("ev_done", ctypes.c_void_p)]
 
 
 class kv_stats_t(ctypes.Structure):
@@ -109,6 +117,8 @@ def lib() -> ctypes.CDLL:
             "kv_stats": (ctypes.c_int, [_P, ctypes.POINTER(kv_stats_t)]),
             "kv_dump_slots": (ctypes.c_int, [_P, _P, _P, _P, _P]),
             "kv_sync": (ctypes.c_int, [_P]),
+            "kv_time_next_launch": (ctypes.c_int, [_P, _P]),
+            "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -192,17 +202,58 @@ def kv_append(p: int, req_ids, n_new, src_kv, flags: int = 0, stream: int = 0) -
 
 def kv_append_multi(entries, stream: int = 0) -> None:
     """entries: list of dicts {pool, begin_step, release, req_ids, n_new, src, flags}."""
+    arr, keep = _append_array(entries)
+    _check(lib().kv_append_multi(len(entries), ctypes.addressof(arr), stream))
+
+
+def _append_array(entries):
     keep = []
-    arr = (kv_append_args_t * len(entries))()
+    arr = (kv_append_args_t * max(1, len(entries)))()
     for k, e in enumerate(entries):
         rel = _i64(e.get("release", []))
         ids = _i64(e.get("req_ids", []))
         nn = _i32(e.get("n_new", []))
-        keep.extend([rel, ids, nn])
+        keep.extend([rel, ids, nn, e.get("src")])
         arr[k] = kv_append_args_t(e["pool"], int(e.get("begin_step", 0)), rel.size, _ptr(rel),
                                   ids.size, _ptr(ids), _ptr(nn), _ptr(e.get("src")),
                                   int(e.get("flags", 0)))
-    _check(lib().kv_append_multi(len(entries), ctypes.addressof(arr), stream))
+    return arr, keep
+
+
+class PreparedSteps:
+    """Marshalled arguments of a run of decode steps for kv_run_steps (built ahead
+    of time: per step the append entries, the pools to publish and optional
+    timing events)."""
+
+    def __init__(self, steps):
+        self.keep = []
+        self.arr = (kv_step_t * len(steps))()
+        for k, st in enumerate(steps):
+            app, keep = _append_array(st.get("append", []))
+            pools = st.get("repl_pools", [])
+            parr = (_P * max(1, len(pools)))(*pools)
+            self.keep.extend([app, keep, parr])
+            ev = [st.get(x) for x in ("ev_call", "ev_kernel_start", "ev_kernel_end", "ev_done")]
+            self.keep.append(ev)
+            self.arr[k] = kv_step_t(len(st.get("append", [])), ctypes.addressof(app), len(pools),
+                                    ctypes.addressof(parr), int(st.get("step", 0)),
+                                    *[_event_handle(e) for e in ev])
+        self.n = len(steps)
+
+
+def _event_handle(e):
+    if e is None:
+        return None
+    if isinstance(e, int):
+        return e
+    if e.cuda_event == 0:   # torch creates events lazily
+        e.record()
+    return e.cuda_event
+
+
+def kv_run_steps(prepared: "PreparedSteps", append_stream: int = 0, repl_stream: int = 0) -> None:
+    _check(lib().kv_run_steps(prepared.n, ctypes.addressof(prepared.arr), append_stream,
+                              repl_stream))
 
 
 def kv_replicate_step(p: int, step: int, stream: int = 0) -> None:
@@ -273,6 +324,11 @@ def kv_dump_slots(p: int, max_reqs: int):
     nb = np.zeros(max_reqs, dtype=np.int32)
     _check(lib().kv_dump_slots(p, _ptr(req), _ptr(ln), _ptr(pub), _ptr(nb)))
     return req, ln, pub, nb
+
+
+def kv_time_next_launch(ev_before, ev_after) -> None:
+    """ev_*: torch.cuda.Event (recorded by libkvring around its next kernel) or None."""
+    _check(lib().kv_time_next_launch(_event_handle(ev_before), _event_handle(ev_after)))
 
 
 def kv_sync(p: int) -> None:

@@ -278,9 +278,10 @@ class ScheduleDriver:
             pos.extend(range(p0, p0 + n))
         return ids, pos
 
-    def append_step(self, t: int, stream=None, sources: dict | None = None) -> None:
+    def append_step(self, t: int, stream=None, sources: dict | None = None,
+                    plan: dict | None = None) -> None:
         entries = []
-        for node, e in self.plan(t).items():
+        for node, e in (self.plan(t) if plan is None else plan).items():
             if node not in self.rt.local:
                 continue
             if sources is not None and node in sources:

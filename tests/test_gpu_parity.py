@@ -237,3 +237,39 @@ def test_c2_full_size_sampled():
             assert np.array_equal(rep, want)
     finally:
         rt.destroy()
+
+
+def test_run_steps_two_streams_bit_exact():
+    """kv_run_steps (the native decode loop the bench times: append on one stream,
+    publish on a second stream after an event) == oracle, whole arrays."""
+    from paper_2601_22438_b200 import kvring as K
+    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=6, n_requests=60, n_steps=30, fixed_prompt=None,
+                         fail_node=None, fail_step=None)
+    sched = _churn_sched(cfg, 21)
+    rt, drv = make_gpu(cfg, schedules=sched)
+    oring = OracleRing(cfg, schedules=sched)
+    try:
+        comp = torch.cuda.current_stream()
+        repl = torch.cuda.Stream()
+        steps, keep = [], []
+        for t in range(cfg.n_steps):
+            app = []
+            for node, e in drv.plan(t).items():
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = drv.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+            pools = [rt.handle(n) for n in rt.alive_local()] if t >= 1 else []
+            steps.append(dict(append=app, repl_pools=pools, step=t))
+            oring.appends(t)
+            if t >= 1:
+                oring.replicate(t)
+        prep = K.PreparedSteps(steps)
+        torch.cuda.synchronize()
+        K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
+        torch.cuda.synchronize()
+        compare_state(rt, drv, oring, tag="run_steps")
+    finally:
+        rt.destroy()
