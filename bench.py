@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-restore", action="store_true")
+    ap.add_argument("--bulk-reps", type=int, default=5, help="C5 bulk re-seed reps (0: skip)")
+    ap.add_argument("--nccl-steps", type=int, default=100,
+                    help="steps replicated through the NCCL send/recv comparison (0: skip)")
     ap.add_argument("--single-stream", action="store_true",
                     help="append and replicate on one stream (default: replication stream)")
     return ap.parse_args()
@@ -147,7 +150,7 @@ def run_kvring(args):
     coords = {(p, s): p * S + s for p in range(N) for s in range(S)}
     placement = {coords[(p, s)]: (p + s) % N for (p, s) in coords}
     succ = {coords[(p, s)]: coords[(p, (s + 1) % S)] for (p, s) in coords}
-    n_total = args.prelude + args.warmup + args.steps + args.e2e_steps + 2
+    n_total = args.prelude + args.warmup + args.steps + args.e2e_steps + args.nccl_steps + 2
     scheds = configs.build_schedules(cfg, n_steps=n_total)
     rt = RingRuntime(g, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement, succ,
                      rank=rank, world=world, device=local_rank, spares=1, group=group,
@@ -255,10 +258,23 @@ def run_kvring(args):
         e2e = run_e2e(args, drv, rt, t, comp, repl, content, dev, world)
         t += args.e2e_steps
 
+    # ---- NCCL comparison (a6): same workload, pack -> count -> send/recv -> unpack ---
+    nccl = None
+    if args.nccl_steps > 0:
+        nccl = run_nccl(args, drv, rt, t, comp, content, dev, world)
+        t += args.nccl_steps
+
     # ---- restore: fail stage 2 of pipeline 0, restore into a fresh pool ---------
     restore = None
     if not args.no_restore and world == 1:
         restore = run_restore(drv, rt, t, dev, comp)
+
+    # ---- bulk leg (C5: 32k-token prefill per stage, full-block re-seed) -----------
+    pool_gib = rt.n_slots * 2 * rt.replica_bytes / 2**30
+    rt.destroy()
+    del rt, drv
+    torch.cuda.empty_cache()
+    bulk = run_bulk(args, rank, world, local_rank, dev, group) if args.bulk_reps > 0 else None
 
     # ---- reduce over ranks --------------------------------------------------------
     vec = torch.tensor([ms, my_bytes, float(launches), wall], dtype=torch.float64, device=dev)
@@ -304,7 +320,7 @@ def run_kvring(args):
                    "streams": "single" if args.single_stream else "compute+replication",
                    "l2": "inputs > L2 (pre-generated sources %.1f GiB, pools %.1f GiB/GPU); the "
                          "replicated slices were just written by append, as in serving"
-                         % (src_bytes / 2**30, rt.n_slots * 2 * rt.replica_bytes / 2**30)},
+                         % (src_bytes / 2**30, pool_gib)},
         "gb_s_per_gpu": round(value / N, 2),
         "replicated_bytes": int(tot_bytes),
         "step_overhead_us": {"median": round(statistics.median(rep_us), 2),
@@ -322,14 +338,148 @@ def run_kvring(args):
         line["e2e"] = e2e
     if restore is not None:
         line["restore"] = restore
+    if bulk is not None:
+        line["bulk"] = bulk
+    if nccl is not None:
+        line["nccl_compare"] = nccl
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, t_timed0, min(args.steps, 60))
     if rank == 0:
         print(json.dumps(line), flush=True)
-    rt.destroy()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_bulk(args, rank, world, local_rank, dev, group):
+    """C5 (BASELINE configs[4]): 8 stages x 4 layers, one P = 32,768 request per stage
+    (2,048 full blocks of 256 KiB = 512 MiB), stage s on GPU s mod N, all links
+    replicating at once.  Each rep re-binds every link (pub_len = 0, full re-seed)
+    and publishes one step: the full-block bulk copy, HBM loopback at N = 1, NVLink
+    at N > 1.  Kernel time by CUDA events around each ring-put launch."""
+    import torch
+    import torch.distributed as dist
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED
+    from kvgen.cuda import content_tokens_cuda
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import RingRuntime
+    cfg = configs.C5
+    g = cfg.geom
+    S = cfg.stages
+    placement = {s: s % world for s in range(S)}
+    succ = {s: (s + 1) % S for s in range(S)}
+    rt = RingRuntime(g, cfg.num_blocks, 2, cfg.max_blocks_per_req, placement, succ, rank=rank,
+                     world=world, device=local_rank, spares=0, group=group, sentinel=None)
+    P = cfg.fixed_prompt
+    comp = torch.cuda.current_stream(dev)
+    for s in rt.alive_local():
+        src = content_tokens_cuda(CONTENT_SEED, [s] * P, range(P), s * g.layers, g.layers,
+                                  g.kv_heads, g.head_dim, device=local_rank)
+        K.kv_append(rt.handle(s), [s], [P], src, 0, comp.cuda_stream)
+        torch.cuda.synchronize(dev)
+        del src
+    nodes = rt.alive_local()
+    handles = [rt.handle(n) for n in nodes]
+    D = P * g.token_bytes * len(nodes)
+    times = []
+    for rep in range(args.bulk_reps + 1):
+        for n in nodes:
+            rt.set_succ(n, succ[n])          # re-bind: the next publish re-seeds everything
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        K.kv_time_next_launch(a, b)
+        K.kv_replicate_step_multi(handles, rep + 1, comp.cuda_stream)
+        torch.cuda.synchronize(dev)
+        if rep > 0:                          # rep 0 is the warm-up
+            times.append(a.elapsed_time(b))
+    ms = statistics.median(times)
+    vec = torch.tensor([ms, float(D)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, tot = float(mx[0]), float(sm[1])
+    else:
+        ms_max, tot = ms, float(D)
+    # sampled check: the last published seq on this GPU's replica metadata
+    seq_ok = all(int(rt.read_meta(n)["seq"]) == args.bulk_reps + 1 for n in nodes)
+    rt.destroy()
+    hbm_peak, src_peak = peaks()
+    per_gpu = D / (ms * 1e-3) / 1e9
+    if world == 1:
+        ach = 2 * D / (ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "peak_source": src_peak,
+                "algorithmic_bytes_per_launch": int(2 * D)}
+    else:
+        roof = {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": NVLINK_PEAK_GBS,
+                "unit": "GB/s", "frac": round(per_gpu / NVLINK_PEAK_GBS, 4),
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
+                "algorithmic_bytes_per_launch": int(D)}
+    return {"workload": "c5_bulk_32k", "stages": S, "stages_per_gpu": len(nodes),
+            "bytes_per_link": int(P * g.token_bytes), "kernel_ms_median": round(ms, 4),
+            "kernel_ms_max_over_ranks": round(ms_max, 4),
+            "replicated_gb_s_total": round(tot / (ms_max * 1e-3) / 1e9, 1),
+            "roofline": roof, "reps": args.bulk_reps, "seq_ok": seq_ok}
+
+
+def run_nccl(args, drv, rt, t0, comp, content, dev, world):
+    """The paper's transport (NCCL send/recv, P:8 §3.3) on the same workload, as the
+    measured comparison: per step append, then gather-pack, 8-B count exchange,
+    grouped send/recv, unpack + publish.  One stream; per-step transport time by
+    CUDA events around pack..unpack."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.nccl_compare import NcclRing
+    n = args.nccl_steps
+    ring = NcclRing(rt, 256 << 20)
+    srcs, plans = {}, {}
+    for tt in range(t0, t0 + n):
+        plans[tt] = drv.plan(tt)
+        srcs[tt] = {}
+        for node, e in plans[tt].items():
+            if node in rt.local:
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                srcs[tt][node] = content(e["stage"], ids, pos) if ids else None
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n)]
+    b0 = {nd: K.kv_stats(rt.handle(nd))["bytes_replicated"] for nd in rt.alive_local()}
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    st.record(comp)
+    for k in range(n):
+        tt = t0 + k
+        drv.append_step(tt, stream=comp, sources=srcs[tt], plan=plans[tt])
+        evs[k][0].record(comp)
+        ring.step(tt, comp)
+        evs[k][1].record(comp)
+    en.record(comp)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - w0
+    ms = st.elapsed_time(en)
+    by = sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in rt.alive_local())
+    us = [a.elapsed_time(b) * 1e3 for a, b in evs]
+    vec = torch.tensor([ms, float(by), wall], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, by, wall = float(mx[0]), float(sm[1]), float(mx[2])
+    return {"transport": "nccl send/recv (pack, count exchange, send/recv, unpack)" if world > 1
+            else "loopback pack -> unpack (no NCCL at N=1)",
+            "value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "steps": n,
+            "ms_per_step": round(ms / n, 4), "wall_ms_per_step": round(wall / n * 1e3, 4),
+            "transport_us_per_step": {"median": round(statistics.median(us), 2),
+                                      "p99": round(float(np.percentile(us, 99)), 2)}}
 
 
 def _append_host(drv, t, host_sources, stream):
@@ -368,7 +518,9 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
                     h2d += d.numel() * 2
     torch.cuda.synchronize(dev)
     nodes = rt.alive_local()
-    seq_dev = [rt.local[rt.succ[nd]].meta[:8] if rt.succ[nd] in rt.local else None for nd in nodes]
+    # the step's result on this GPU: the seq flags its nodes' predecessors published into
+    # this GPU's replica metadata (local memory whatever the ring placement)
+    seq_dev = [rt.local[nd].meta[:8] for nd in nodes]
     seq_host = torch.empty((n, len(nodes), 8), dtype=torch.uint8, pin_memory=True)
     d2h = 0
     b0 = {nd: K.kv_stats(rt.handle(nd))["bytes_replicated"] for nd in nodes}
@@ -405,8 +557,14 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
         sm = vec.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         ms, by = float(mx[0]), float(sm[1])
-    seqs = seq_host[-1].numpy().view(np.uint64).reshape(-1)
-    ok = bool(all(int(x) == t0 + n - 1 for i, x in enumerate(seqs) if seq_dev[i] is not None))
+    # per-step read-backs are not synchronised with the remote writers (one-sided
+    # publication); after a barrier every local replica must hold the last step
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ok = bool(all(int(sd.cpu().numpy().view(np.uint64)[0]) == t0 + n - 1 for sd in seq_dev))
+    if world > 1:
+        dist.barrier()
     return {"value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d // n), "d2h_bytes_per_step": int(d2h // n),
             "steps": n, "ms_per_step": round(ms / n, 4), "wall_s": round(wall, 3),

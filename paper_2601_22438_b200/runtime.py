@@ -358,3 +358,75 @@ class ScheduleDriver:
             if on_step is not None:
                 on_step(self, t)
         return self
+
+
+class TablesRuntime:
+    """RingRuntime's interface over tables-only pools (kv_pool_desc_t.device = -1):
+    the C++ allocator, quarantine and work-list builder run, nothing is launched
+    and no KV byte moves.  Used by the CPU tests of the multi-rank host logic."""
+
+    FAKE = 0x1000
+
+    def __init__(self, geom, num_blocks, max_reqs, max_blocks_per_req, placement, succ,
+                 rank=0, world=1):
+        self.g = geom
+        self.NB, self.R, self.M = num_blocks, max_reqs, max_blocks_per_req
+        self.placement, self.succ = dict(placement), dict(succ)
+        self.rank, self.world = rank, world
+        self.kg = K.geom(geom.layers, geom.kv_heads, geom.head_dim, geom.block_size,
+                         geom.elem_bytes)
+        self.dead: set[int] = set()
+        self.handles: dict[int, int] = {}
+        self.local = self.handles
+        for n in sorted(placement):
+            if placement[n] == rank:
+                self._create(n)
+        for n in sorted(self.handles):
+            self._link(n)
+
+    def _create(self, node):
+        d = K.kv_pool_desc_t(self.kg, self.NB, self.R, self.M, -1, node, self.NB, None, None, None)
+        self.handles[node] = K.kv_pool_create(d)
+
+    def _link(self, node):
+        m = self.succ.get(node)
+        if m is None or m in self.dead:
+            K.kv_set_successor(self.handles[node], -1, None, 0, None)
+        else:
+            K.kv_set_successor(self.handles[node], m, self.FAKE + m, self.NB, self.FAKE + m)
+
+    def handle(self, node):
+        return self.handles[node]
+
+    def alive_local(self):
+        return [n for n in sorted(self.handles) if n not in self.dead]
+
+    def append_all(self, entries, stream=None):
+        if entries:
+            K.kv_append_multi([dict(e, pool=self.handle(e["node"]), src=None) for e in entries])
+
+    def replicate_all(self, step, nodes=None, stream=None):
+        nodes = [n for n in (self.alive_local() if nodes is None else nodes)
+                 if self.succ.get(n) is not None]
+        if nodes:
+            K.kv_replicate_step_multi([self.handle(n) for n in nodes], step)
+
+    def fail(self, node, stream=None):
+        self.dead.add(node)
+        if node in self.handles:
+            K.kv_fail_stage(self.handles[node])
+        for n, m in list(self.succ.items()):
+            if m == node:
+                self.succ[n] = None
+                if n in self.handles and n not in self.dead:
+                    self._link(n)
+
+    def set_succ(self, node, succ):
+        self.succ[node] = succ
+        if node in self.handles and node not in self.dead:
+            self._link(node)
+
+    def destroy(self):
+        for h in self.handles.values():
+            K.kv_pool_destroy(h)
+        self.handles.clear()

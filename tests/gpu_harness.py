@@ -45,10 +45,13 @@ def node_map(rt, drv, oring: OracleRing) -> dict:
     return m
 
 
-def compare_state(rt, drv, oring: OracleRing, content: bool = True, tag="") -> None:
+def compare_state(rt, drv, oring: OracleRing, content: bool = True, tag="", only=None) -> None:
+    """Byte-for-byte comparison of every local node (or the node ids in ``only``)."""
     torch.cuda.synchronize()
     from paper_2601_22438_b200 import kvring as K
     for gid, on in node_map(rt, drv, oring).items():
+        if gid not in rt.local or (only is not None and gid not in only):
+            continue
         slot = rt.local[gid]
         if content:
             prim = slot.pool.cpu().numpy().view(np.uint16)

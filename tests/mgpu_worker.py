@@ -1,0 +1,123 @@
+"""Multi-GPU parity worker (launched by tests/test_multigpu.py under torchrun).
+
+N pipelines x 4 stages, node (p, s) on rank (p + s) mod N, stage ring inside each
+pipeline: every ring hop is a one-sided NVLink store into the successor GPU's
+symmetric-memory replica region.  Every rank runs the CPU oracle on the same
+inputs (tiny config) and compares its own nodes byte for byte, every few steps;
+a stage fails mid-run and is restored into a fresh pool on its holder's GPU,
+and a second failure is restored REMOTELY (dst on another GPU, replica read over
+NVLink).  Exit code 0 = parity on every rank.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED
+    from kvgen.cuda import content_tokens_cuda
+    from kvgen.schedule import closed_loop_schedule
+    from oracle.simulate import OracleRing
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    from gpu_harness import compare_state
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    lr = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(lr)
+    dev = torch.device("cuda", lr)
+    from datetime import timedelta
+    dist.init_process_group("nccl", device_id=dev, timeout=timedelta(seconds=120))
+    N, S = world, 4
+    cfg = configs.scaled(configs.C1, pipelines=N, num_blocks=96, max_reqs=12,
+                         max_blocks_per_req=12, batch_cap=6, n_requests=60, n_steps=30,
+                         fixed_prompt=None, fail_node=(0, 1), fail_step=13)
+    rng = np.random.default_rng(77)
+    scheds = [closed_loop_schedule(rng.integers(1, 70, size=60), rng.integers(1, 30, size=60),
+                                   cfg.n_steps, cfg.batch_cap, pipeline=p) for p in range(N)]
+    coords = {(p, s): p * S + s for p in range(N) for s in range(S)}
+    placement = {coords[(p, s)]: (p + s) % N for (p, s) in coords}
+    succ = {coords[(p, s)]: coords[(p, (s + 1) % S)] for (p, s) in coords}
+    rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement,
+                     succ, rank=rank, world=world, device=lr, spares=2, group=dist.group.WORLD)
+    g = cfg.geom
+
+    def content(stage, ids, pos):
+        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim, device=lr)
+
+    drv = ScheduleDriver(rt, scheds, coords, content)
+    oring = OracleRing(cfg, schedules=scheds)
+    transport = os.environ.get("KV_TRANSPORT", "p2p")
+    nccl = None
+    if transport == "nccl":
+        from paper_2601_22438_b200.nccl_compare import NcclRing
+        nccl = NcclRing(rt, 64 << 20)
+    for t in range(cfg.n_steps):
+        drv.append_step(t)
+        oring.appends(t)
+        if t == cfg.fail_step:
+            drv.fail_and_restore(t, cfg.fail_node)
+            oring.fail_and_restore(t, cfg.fail_node)
+        if t >= 1:
+            if nccl is None:
+                rt.replicate_all(t)
+            else:
+                nccl.step(t)
+            oring.replicate(t)
+        torch.cuda.synchronize(dev)
+        dist.barrier()           # every rank's stores into peers are complete
+        if t % 4 == 0 or t == cfg.n_steps - 1:
+            compare_state(rt, drv, oring, tag=f"rank {rank} step {t}")
+        dist.barrier()
+    # remote restore: a fresh pool on rank (holder_rank + 1) % N reads the holder's
+    # replica region over NVLink.  Fail stage 2 of pipeline 0 after the last step.
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    f = drv.serving[(0, 2)]
+    holder = rt.succ[f]
+    rt.fail(f)
+    dst_rank = (rt.placement[holder] + 1) % N
+    dst = drv.next_node
+    drv.next_node += 1
+    rt.new_node(dst, dst_rank)
+    ok = 1
+    if rank == dst_rank:
+        t_star, restored = rt.restore(dst, holder)
+        torch.cuda.synchronize(dev)
+        # expected: the oracle's published state of f at its holder
+        hold_o = oring.serving[(0, 2)].succ
+        exp = sorted((r, ln) for r, (s, ln, bt) in hold_o.published().items())
+        if restored != exp or t_star != cfg.n_steps - 1:
+            print(f"rank {rank}: remote restore mismatch {restored} vs {exp}", flush=True)
+            ok = 0
+        from kvgen.content import content_tokens
+        pool = rt.local[dst].pool.cpu().numpy().view(np.uint16)
+        for r, ln in restored:
+            _, bt = K.kv_query(rt.handle(dst), r)
+            want = content_tokens(CONTENT_SEED, [r] * ln, range(ln), 2 * g.layers, g.layers,
+                                  g.kv_heads, g.head_dim)
+            got = np.stack([pool[bt[p // 16], :, :, :, p % 16] for p in range(ln)])
+            if not np.array_equal(got, want):
+                print(f"rank {rank}: remote restore content mismatch for {r}", flush=True)
+                ok = 0
+    okt = torch.tensor([ok], device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    rt.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_PARITY_OK" if int(okt) == 1 else "MGPU_PARITY_FAIL", flush=True)
+    sys.exit(0 if int(okt) == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -273,3 +273,28 @@ def test_run_steps_two_streams_bit_exact():
         compare_state(rt, drv, oring, tag="run_steps")
     finally:
         rt.destroy()
+
+
+def test_nccl_loopback_transport_bit_exact():
+    """The comparison transport at world size 1 (pack -> unpack into the local
+    successor) keeps every replica == oracle, whole arrays."""
+    from paper_2601_22438_b200.nccl_compare import NcclRing
+    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=6, n_requests=60, n_steps=25, fixed_prompt=None,
+                         fail_node=None, fail_step=None)
+    sched = _churn_sched(cfg, 9)
+    rt, drv = make_gpu(cfg, schedules=sched)
+    oring = OracleRing(cfg, schedules=sched)
+    ring = NcclRing(rt, 32 << 20)
+    try:
+        for t in range(cfg.n_steps):
+            drv.append_step(t)
+            oring.appends(t)
+            if t >= 1:
+                ring.step(t)
+                oring.replicate(t)
+            if t % 6 == 0:
+                compare_state(rt, drv, oring, tag=f"nccl-loopback {t}")
+        compare_state(rt, drv, oring, tag="nccl-loopback end")
+    finally:
+        rt.destroy()
