@@ -39,6 +39,7 @@ METRIC = "replicated KV GB/s (ring KV-cache replication, per-decode-step, C2)"
 UNIT = "GB/s"
 PRELUDE = 200
 CFG_NAME = "c2_pp4_b64"
+TIME_EVERY = 4
 
 
 def parse():
@@ -199,6 +200,8 @@ def run_kvring(args):
     # (kv_run_steps: the native decode loop, append on the compute stream, publish
     # on the replication stream).
     def prepare(t0, n, timing):
+        # kernel-timing events on every TIME_EVERY-th step (each record is a host API
+        # call inside the timed region; sampling keeps the host loop lean)
         steps, evs = [], []
         for tt in range(t0, t0 + n):
             plan = drv.plan(tt)
@@ -207,7 +210,7 @@ def run_kvring(args):
                    for node, e in plan.items() if node in rt.local]
             pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
             st = dict(append=app, repl_pools=pools if tt >= 1 else [], step=tt)
-            if timing:
+            if timing and (tt - t0) % TIME_EVERY == 0:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
                 evs.append(ev)
@@ -326,9 +329,12 @@ def run_kvring(args):
         "step_overhead_us": {"median": round(statistics.median(rep_us), 2),
                              "p99": round(float(np.percentile(rep_us, 99)), 2),
                              "budget_us": 400.0, "tpot_ms": 20.0,
-                             "what": "replication-stream device time per step: work-list H2D + "
-                                     "ring-put kernel (CUDA events recorded by kv_run_steps)"},
-        "ring_put_kernel_us": {"median": round(med_kern, 2), "avg": round(avg_kern, 2)},
+                             "what": "replication-stream device time per step (ring-put kernel incl. "
+                                     "its launch; the step's descriptors are staged with one H2D before "
+                                     "the append), CUDA events by kv_run_steps on every %d-th timed "
+                                     "step" % TIME_EVERY},
+        "ring_put_kernel_us": {"median": round(med_kern, 2), "avg": round(avg_kern, 2),
+                               "sampled_launches": len(kern_us)},
         "roofline": roof,
         "gpu_launches": int(tot_launch),
         "wall_s_timed": round(wall, 3),

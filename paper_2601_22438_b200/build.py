@@ -52,6 +52,9 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
                    "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
+            extra = os.environ.get("KVRING_NVCC_DEFS", "")   # experiments: e.g. -DKV_UNROLL=4
+            if extra:
+                cmd[1:1] = extra.split()
             _run(cmd)
         objs.append(o)
     for src in SOURCES_CPP:

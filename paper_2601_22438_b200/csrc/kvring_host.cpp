@@ -28,6 +28,23 @@
 
 #define KV_API extern "C" __attribute__((visibility("default")))
 
+#ifdef KV_HOST_PROFILE  // diagnostic build only: per-phase host time
+#include <chrono>
+static double g_prof[8];
+struct ProfScope {
+  int i;
+  std::chrono::steady_clock::time_point t0;
+  explicit ProfScope(int i_) : i(i_), t0(std::chrono::steady_clock::now()) {}
+  ~ProfScope() {
+    g_prof[i] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+#define KV_PROF(i) ProfScope kv_prof_##i(i)
+extern "C" __attribute__((visibility("default"))) double kv_prof_get(int i) { return g_prof[i]; }
+#else
+#define KV_PROF(i)
+#endif
+
 using namespace kvring;
 
 namespace {
@@ -96,6 +113,64 @@ class IdSet {
  private:
   int n_ = 0, count_ = 0, hint_ = 0;
   std::vector<unsigned long long> words_;
+};
+
+// req_id -> slot map: open addressing, linear probing, backward-shift erase
+// (no tombstones).  Capacity is a power of two >= 4 x max_reqs, so probes stay short.
+class SlotMap {
+ public:
+  void init(int max_entries) {
+    size_t cap = 16;
+    while (cap < 4 * (size_t)max_entries) cap <<= 1;
+    keys_.assign(cap, kEmpty);
+    vals_.assign(cap, -1);
+    mask_ = cap - 1;
+    size_ = 0;
+  }
+  int find(int64_t k) const {
+    for (size_t i = hash(k);; i = (i + 1) & mask_) {
+      if (keys_[i] == k) return vals_[i];
+      if (keys_[i] == kEmpty) return -1;
+    }
+  }
+  void insert(int64_t k, int v) {  // k not present
+    size_t i = hash(k);
+    while (keys_[i] != kEmpty) i = (i + 1) & mask_;
+    keys_[i] = k;
+    vals_[i] = v;
+    ++size_;
+  }
+  void erase(int64_t k) {
+    size_t i = hash(k);
+    while (keys_[i] != k) {
+      if (keys_[i] == kEmpty) return;
+      i = (i + 1) & mask_;
+    }
+    for (size_t j = (i + 1) & mask_;; j = (j + 1) & mask_) {  // backward shift
+      if (keys_[j] == kEmpty) break;
+      const size_t h = hash(keys_[j]);
+      const bool move = (j > i) ? (h <= i || h > j) : (h <= i && h > j);
+      if (move) {
+        keys_[i] = keys_[j];
+        vals_[i] = vals_[j];
+        i = j;
+      }
+    }
+    keys_[i] = kEmpty;
+    vals_[i] = -1;
+    --size_;
+  }
+  size_t size() const { return size_; }
+
+ private:
+  static constexpr int64_t kEmpty = INT64_MIN;
+  size_t hash(int64_t k) const {
+    uint64_t x = (uint64_t)k * 0x9E3779B97F4A7C15ull;
+    return (size_t)(x >> 32) & mask_;
+  }
+  std::vector<int64_t> keys_;
+  std::vector<int> vals_;
+  size_t mask_ = 0, size_ = 0;
 };
 
 // Pinned-host + device staging buffer ring, per device (shared by its pools).
@@ -204,7 +279,7 @@ struct kv_pool {
   std::vector<int64_t> slot_req;
   std::vector<int32_t> slot_len, pub_len;
   std::vector<std::vector<int32_t>> slot_bt;
-  std::unordered_map<int64_t, int> slot_of;
+  SlotMap slot_of;
   std::vector<uint32_t> rel_stamp, app_stamp;  // per-slot call stamps (validation)
   uint32_t call_id = 0;
   std::vector<int64_t> scratch_ids;
@@ -288,11 +363,11 @@ int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, lon
     return fail(KV_EINVAL, "null array");
   const uint32_t cid = ++p->call_id;
   for (int i = 0; i < a.n_release; ++i) {
-    auto it = p->slot_of.find(a.release_ids[i]);
-    if (it == p->slot_of.end())
+    const int rs = p->slot_of.find(a.release_ids[i]);
+    if (rs < 0)
       return fail(KV_EINVAL, "release of unknown request %lld", (long long)a.release_ids[i]);
-    if (p->rel_stamp[it->second] == cid) return fail(KV_EINVAL, "request released twice");
-    p->rel_stamp[it->second] = cid;
+    if (p->rel_stamp[rs] == cid) return fail(KV_EINVAL, "request released twice");
+    p->rel_stamp[rs] = cid;
   }
   const int B = p->g.block_size;
   long long need_blocks = 0, need_slots = 0, tokens = 0;
@@ -302,9 +377,8 @@ int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, lon
     const int n = a.n_new[i];
     if (n < 0) return fail(KV_EINVAL, "negative n_new");
     long long cur = 0;
-    auto it = p->slot_of.find(r);
-    if (it != p->slot_of.end()) {
-      const int s = it->second;
+    const int s = p->slot_of.find(r);
+    if (s >= 0) {
       if (p->app_stamp[s] == cid)
         return fail(KV_EINVAL, "request %lld twice in one append", (long long)r);
       if (p->rel_stamp[s] == cid)
@@ -312,6 +386,7 @@ int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, lon
       p->app_stamp[s] = cid;
       cur = p->slot_len[s];
     } else {
+      if (r < 0) return fail(KV_EINVAL, "request ids must be >= 0 (-1 marks an empty slot)");
       if (n <= 0) return fail(KV_EINVAL, "admission of %lld with no tokens", (long long)r);
       p->scratch_ids.push_back(r);
       ++need_slots;
@@ -343,9 +418,8 @@ void do_begin_step(kv_pool *p) {
 
 void do_release(kv_pool *p, int n, const int64_t *ids) {
   for (int i = 0; i < n; ++i) {
-    auto it = p->slot_of.find(ids[i]);
-    const int s = it->second;
-    p->slot_of.erase(it);
+    const int s = p->slot_of.find(ids[i]);
+    p->slot_of.erase(ids[i]);
     for (int b : p->slot_bt[s]) p->q_blocks.push_back(b);
     p->slot_bt[s].clear();
     p->q_slots.push_back(s);
@@ -357,22 +431,20 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
 
 // Applies the appends to the tables and emits the scatter tasks (src rows are
 // token rows of the dense source, `row_base` added).
-void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<KvTask> &tasks) {
+void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<KvTask> &tasks,
+               int task_segs) {
   const int B = p->g.block_size;
   int row = 0;
   for (int i = 0; i < a.n; ++i) {
     const int64_t r = a.req_ids[i];
-    int s;
-    auto it = p->slot_of.find(r);
-    if (it == p->slot_of.end()) {
+    int s = p->slot_of.find(r);
+    if (s < 0) {
       s = p->free_slots.take_min();
-      p->slot_of[r] = s;
+      p->slot_of.insert(r, s);
       p->slot_req[s] = r;
       p->slot_len[s] = 0;
       p->pub_len[s] = 0;
       p->slot_bt[s].clear();
-    } else {
-      s = it->second;
     }
     int len = p->slot_len[s];
     int left = a.n_new[i];
@@ -381,7 +453,7 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<
       const int j = len / B, lo = len % B;
       const int n = std::min(B - lo, left);
       if (p->device >= 0)
-        push_item(tasks, pidx, row, p->slot_bt[s][j], -1, j, lo, n, p->combos, p->task_segs);
+        push_item(tasks, pidx, row, p->slot_bt[s][j], -1, j, lo, n, p->combos, task_segs);
       row += n;
       len += n;
       left -= n;
@@ -394,7 +466,7 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<
 // Dirty ranges [pub_len, len) of every live slot split at block boundaries
 // (§8(a) a3); returns payload bytes.
 uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks, bool packed,
-                           int32_t *packed_unit) {
+                           int32_t *packed_unit, int task_segs) {
   const int B = p->g.block_size;
   uint64_t bytes = 0;
   for (int s = 0; s < p->R; ++s) {
@@ -406,10 +478,10 @@ uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks,
       const int n = std::min(B - lo, len - pos);
       const int blk = p->slot_bt[s][j];
       if (packed) {
-        push_item(tasks, pidx, blk, *packed_unit, s, j, lo, n, p->combos, p->task_segs);
+        push_item(tasks, pidx, blk, *packed_unit, s, j, lo, n, p->combos, task_segs);
         *packed_unit += n * p->combos;
       } else {
-        push_item(tasks, pidx, blk, blk, s, j, lo, n, p->combos, p->task_segs);
+        push_item(tasks, pidx, blk, blk, s, j, lo, n, p->combos, task_segs);
       }
       bytes += (uint64_t)n * p->token_bytes;
       pos += n;
@@ -481,7 +553,7 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
   p->slot_bt.assign(p->R, {});
   p->rel_stamp.assign(p->R, 0);
   p->app_stamp.assign(p->R, 0);
-  p->slot_of.reserve(2 * (size_t)p->R);
+  p->slot_of.init(p->R);
   for (auto &v : p->slot_bt) v.reserve(8);
   if (p->device >= 0) {
     DeviceGuard dg(p->device);
@@ -560,98 +632,312 @@ KV_API int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids) {
   return KV_OK;
 }
 
-KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream) {
-  if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
-  if (n_pools > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "at most %d pools per launch",
-                                                    kMaxPoolsPerLaunchHost);
-  kv_pool *p0 = args[0].pool;
-  if (!p0) return fail(KV_EINVAL, "null pool");
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = args[k].pool;
+namespace {
+
+// ---- launches: prepare on the host, stage descriptors with ONE H2D, enqueue ----
+inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// One kernel launch prepared on the host.
+struct Launch {
+  int kind = kKindAppend;
+  int n_pools = 0;
+  kv_pool *p0 = nullptr;
+  std::vector<KvPoolParams> params;
+  std::vector<char> tables;        // replicate: per pool slot_req[R] (8R B) then slot_len[R] (4R B)
+  std::vector<size_t> table_off;   // per pool offset into `tables`
+  std::vector<KvTask> tasks;
+  std::vector<int> ntask;          // replicate: tasks per pool
+  std::vector<uint64_t> bytes;     // replicate: payload bytes per pool
+  std::vector<const void *> host_src;  // append: host sources (KV_SRC_HOST), per pool
+  std::vector<size_t> host_src_bytes;
+  // filled by stage()
+  const KvPoolParams *params_dev = nullptr;
+  const KvTask *tasks_dev = nullptr;
+  void reset(int kind_, int n) {
+    kind = kind_;
+    n_pools = n;
+    params.assign(n, KvPoolParams{});
+    tables.clear();
+    table_off.assign(n, 0);
+    tasks.clear();
+    ntask.assign(n, 0);
+    bytes.assign(n, 0);
+    host_src.assign(n, nullptr);
+    host_src_bytes.assign(n, 0);
+    params_dev = nullptr;
+    tasks_dev = nullptr;
+  }
+  size_t staged_bytes() const {
+    return align16(sizeof(KvPoolParams) * n_pools) + align16(tables.size()) +
+           sizeof(KvTask) * tasks.size();
+  }
+};
+
+// Task size for one launch: spread the launch's slices over every resident CTA
+// (SMs x 4) so a decode-sized step runs in one wave, capped at 32 KiB per task.
+int choose_task_segs(const kv_pool *p, long long total_segs) {
+  const int maxs = std::max(1, 32768 / p->seg_bytes);
+  const long long slots = (long long)resident_ctas(p->device < 0 ? 0 : p->device);
+  long long t = (total_segs + slots - 1) / std::max(1LL, slots);
+  t = (t + 15) & ~15LL;
+  t = std::max<long long>(std::min(maxs, 16), t);
+  return (int)std::min<long long>(maxs, t);
+}
+
+int check_same_device(int n, kv_pool *const *pools) {
+  kv_pool *p0 = pools[0];
+  for (int k = 0; k < n; ++k) {
+    kv_pool *p = pools[k];
     if (!p) return fail(KV_EINVAL, "null pool");
     if (p->device != p0->device || !p->same_geom(*p0))
-      return fail(KV_EINVAL, "kv_append_multi pools must share device and geometry");
+      return fail(KV_EINVAL, "pools of one launch must share device and geometry");
     for (int k2 = 0; k2 < k; ++k2)
-      if (args[k2].pool == p) return fail(KV_EINVAL, "pool listed twice");
+      if (pools[k2] == p) return fail(KV_EINVAL, "pool listed twice");
   }
-  // Phase 1: validate every pool against its state after begin_step + releases.
+  return KV_OK;
+}
+
+// Validates every pool (all-or-nothing), applies begin_step / releases / appends
+// to the host tables and builds the scatter tasks.
+int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
+  if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
+  if (n_pools > kMaxPoolsPerLaunchHost)
+    return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
+  kv_pool *pools[kMaxPoolsPerLaunchHost];
+  for (int k = 0; k < n_pools; ++k) pools[k] = args[k].pool;
+  if (!pools[0]) return fail(KV_EINVAL, "null pool");
+  int rc = check_same_device(n_pools, pools);
+  if (rc) return rc;
+  long long tokens = 0;
+  {
+  KV_PROF(0);
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = args[k].pool;
     if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
-    // validation sees the quarantine released when begin_step is requested
-    const bool bs = args[k].begin_step != 0;
-    int rc = append_validate(p, args[k],
-                             p->free_blocks.size() + (bs ? (long long)p->q_blocks.size() : 0),
-                             p->free_slots.size() + (bs ? (long long)p->q_slots.size() : 0));
+    const bool bs = args[k].begin_step != 0;  // validation sees the released quarantine
+    rc = append_validate(p, args[k],
+                         p->free_blocks.size() + (bs ? (long long)p->q_blocks.size() : 0),
+                         p->free_slots.size() + (bs ? (long long)p->q_slots.size() : 0));
     if (rc) return rc;
-    if (p->device >= 0) {
-      for (int i = 0; i < args[k].n; ++i)
-        if (args[k].n_new[i] > 0 && !args[k].src_kv)
-          return fail(KV_EINVAL, "null src_kv with tokens to append");
-    }
+    long long rows = 0;
+    for (int i = 0; i < args[k].n; ++i) rows += args[k].n_new[i];
+    if (p->device >= 0 && rows > 0 && !args[k].src_kv)
+      return fail(KV_EINVAL, "null src_kv with tokens to append");
+    tokens += rows;
   }
-  // Phase 2: apply and build tasks.
-  thread_local std::vector<KvTask> tasks;
-  tasks.clear();
-  std::vector<long long> rows(n_pools, 0);
+  }
+  KV_PROF(1);
+  L.reset(kKindAppend, n_pools);
+  L.p0 = pools[0];
+  const int task_segs = choose_task_segs(L.p0, tokens * L.p0->combos);
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = args[k].pool;
     if (args[k].begin_step) do_begin_step(p);
     do_release(p, args[k].n_release, args[k].release_ids);
-    do_append(p, args[k], (int16_t)k, tasks);
-    for (int i = 0; i < args[k].n; ++i) rows[k] += args[k].n_new[i];
+    const size_t before = L.tasks.size();
+    do_append(p, args[k], (int16_t)k, L.tasks, task_segs);
+    L.ntask[k] = (int)(L.tasks.size() - before);
+    long long rows = 0;
+    for (int i = 0; i < args[k].n; ++i) rows += args[k].n_new[i];
+    KvPoolParams &pp = L.params[k];
+    pp.src = static_cast<const char *>(args[k].src_kv);
+    pp.dst = p->pool;
+    if ((args[k].flags & KV_SRC_HOST) && rows > 0) {
+      L.host_src[k] = args[k].src_kv;
+      L.host_src_bytes[k] = (size_t)rows * p->token_bytes;
+    }
   }
-  if (p0->device < 0 || tasks.empty()) return KV_OK;
-  // Phase 3: stage params + tasks, copy host sources if needed, launch.
-  DeviceGuard dg(p0->device);
+  return KV_OK;
+}
+
+// Validates the pools and builds the dirty work list (§8(a) a3); state is
+// committed by commit_replicate once the launch is enqueued.
+int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch &L) {
+  if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
+  if (n_pools > kMaxPoolsPerLaunchHost)
+    return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
+  if (!pools[0]) return fail(KV_EINVAL, "null pool");
+  int rc = check_same_device(n_pools, pools);
+  if (rc) return rc;
+  long long dirty = 0;
+  KV_PROF(2);
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+    if (!p->has_succ) return fail(KV_EPEER, "pool %d has no successor", p->node_id);
+    if (step == 0 || step <= p->last_step)
+      return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
+                  (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
+    for (int s = 0; s < p->R; ++s)
+      if (p->slot_req[s] >= 0) dirty += p->slot_len[s] - p->pub_len[s];
+  }
+  L.reset(kKindRingPut, n_pools);
+  L.p0 = pools[0];
+  const int task_segs = choose_task_segs(L.p0, dirty * L.p0->combos);
+  size_t toff = 0;
+  for (int k = 0; k < n_pools; ++k) toff += 12 * (size_t)pools[k]->R;
+  L.tables.resize(toff);
+  toff = 0;
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    const size_t before = L.tasks.size();
+    L.bytes[k] = build_dirty_tasks(p, (int16_t)k, L.tasks, false, nullptr, task_segs);
+    if (L.tasks.size() == before) push_publish_only(L.tasks, (int16_t)k);
+    L.tasks[before].flags |= kPoolFirst;
+    L.ntask[k] = (int)(L.tasks.size() - before);
+    const bool aborting = p->abort_after >= 0 && p->abort_after < L.ntask[k];
+    if (aborting) {  // fault injection: partial step, never published
+      L.tasks.resize(before + p->abort_after);
+      L.ntask[k] = p->abort_after;
+    }
+    L.table_off[k] = toff;
+    std::memcpy(L.tables.data() + toff, p->slot_req.data(), 8 * (size_t)p->R);
+    std::memcpy(L.tables.data() + toff + 8 * (size_t)p->R, p->slot_len.data(), 4 * (size_t)p->R);
+    toff += 12 * (size_t)p->R;
+    KvPoolParams &pp = L.params[k];
+    pp.src = p->pool;
+    pp.dst = p->succ_replica;
+    pp.meta = p->succ_meta;
+    pp.counter = p->counter;
+    pp.target = aborting || p->abort_after >= 0 ? ~0ull : p->issued + (unsigned long long)L.ntask[k];
+    pp.step = step;
+    pp.max_reqs = p->R;
+    pp.max_blk = p->M;
+    pp.writer_node = p->node_id;
+    pp.publish = 1;
+    pp.sys_scope = p->succ_sys ? 1 : 0;
+  }
+  return KV_OK;
+}
+
+void commit_replicate(Launch &L, kv_pool *const *pools, uint64_t step) {
+  KV_PROF(3);
+  for (int k = 0; k < L.n_pools; ++k) {
+    kv_pool *p = pools[k];
+    p->issued += (unsigned long long)L.ntask[k];
+    p->last_step_bytes = L.bytes[k];
+    p->bytes_replicated += L.bytes[k];
+    p->tasks_launched += L.ntask[k];
+    p->pub_len = p->slot_len;
+    p->last_step = step;
+    p->abort_after = -1;
+  }
+}
+
+// Copies host-resident append sources into one device staging buffer (data,
+// not descriptors) and points the launch at it.
+int stage_host_sources(DeviceCtx *ctx, Launch &L, cudaStream_t st, StageBuf **out) {
+  *out = nullptr;
+  size_t total = 0;
+  for (int k = 0; k < L.n_pools; ++k) total += L.host_src_bytes[k];
+  if (total == 0) return KV_OK;
+  StageBuf *sb = nullptr;
+  int rc = ctx->acquire(ctx->src, ctx->next_src, total, false, &sb);
+  if (rc) return rc;
+  size_t off = 0;
+  for (int k = 0; k < L.n_pools; ++k) {
+    if (!L.host_src_bytes[k]) continue;
+    CU(cudaMemcpyAsync(sb->dev + off, L.host_src[k], L.host_src_bytes[k], cudaMemcpyHostToDevice,
+                       st));
+    L.params[k].src = sb->dev + off;
+    off += L.host_src_bytes[k];
+  }
+  *out = sb;
+  return KV_OK;
+}
+
+// Stages the descriptors of up to two launches with ONE pinned H2D copy.
+int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf **out) {
+  size_t total = 0;
+  for (int i = 0; i < nl; ++i) total += align16(ls[i]->staged_bytes());
+  StageBuf *b = nullptr;
+  int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
+  if (rc) return rc;
+  size_t off = 0;
+  for (int i = 0; i < nl; ++i) {
+    Launch &L = *ls[i];
+    const size_t pbytes = align16(sizeof(KvPoolParams) * L.n_pools);
+    const size_t tbl = align16(L.tables.size());
+    char *h = b->host + off;
+    char *d = b->dev + off;
+    for (int k = 0; k < L.n_pools; ++k) {
+      if (L.kind == kKindRingPut) {
+        const size_t o = pbytes + L.table_off[k];
+        L.params[k].slot_req = reinterpret_cast<const int64_t *>(d + o);
+        L.params[k].slot_len = reinterpret_cast<const int32_t *>(d + o + 8 * (size_t)L.params[k].max_reqs);
+      }
+    }
+    std::memcpy(h, L.params.data(), sizeof(KvPoolParams) * L.n_pools);
+    if (!L.tables.empty()) std::memcpy(h + pbytes, L.tables.data(), L.tables.size());
+    std::memcpy(h + pbytes + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
+    L.params_dev = reinterpret_cast<const KvPoolParams *>(d);
+    L.tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
+    off += align16(L.staged_bytes());
+  }
+  CU(cudaMemcpyAsync(b->dev, b->host, total, cudaMemcpyHostToDevice, st));
+  *out = b;
+  return KV_OK;
+}
+
+int enqueue(Launch &L, cudaStream_t st) {
+  if (L.tasks.empty()) return KV_OK;
+  int kind = L.kind;
+  if (kind == kKindRingPut) {
+    static const bool dbg_nopub = getenv("KVRING_DEBUG_RINGPUT_NOPUB") != nullptr;
+    if (dbg_nopub) kind = kKindRestore;  // experiment knob: copy without publication
+  }
+  CU(timed_launch(kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
+                  L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()), st));
+  g_launches++;
+  L.p0->kernels++;
+  return KV_OK;
+}
+
+thread_local Launch g_append_launch, g_repl_launch;
+
+int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st) {
+  Launch &L = g_repl_launch;
+  int rc = prepare_replicate(n_pools, pools, step, L);
+  if (rc) return rc;
+  if (L.p0->device < 0) {  // tables only
+    commit_replicate(L, pools, step);
+    return KV_OK;
+  }
+  DeviceGuard dg(L.p0->device);
+  if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
+  DeviceCtx *ctx = ctx_for(L.p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  StageBuf *b = nullptr;
+  Launch *ls[1] = {&L};
+  rc = stage(ctx, ls, 1, st, &b);
+  if (rc) return rc;
+  rc = enqueue(L, st);
+  if (rc) return rc;
+  commit_replicate(L, pools, step);
+  return ctx->done(b, st);
+}
+
+}  // namespace
+
+KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream) {
+  Launch &L = g_append_launch;
+  int rc = prepare_append(n_pools, args, L);
+  if (rc) return rc;
+  if (L.p0->device < 0 || L.tasks.empty()) return KV_OK;
+  DeviceGuard dg(L.p0->device);
   if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DeviceCtx *ctx = ctx_for(p0->device);
+  DeviceCtx *ctx = ctx_for(L.p0->device);
   std::lock_guard<std::mutex> lk(ctx->mu);
-  std::vector<KvPoolParams> params(n_pools);
-  // host-resident sources (KV_SRC_HOST) are copied into ONE device staging buffer
-  size_t host_src_bytes = 0;
-  for (int k = 0; k < n_pools; ++k)
-    if (args[k].flags & KV_SRC_HOST) host_src_bytes += (size_t)rows[k] * args[k].pool->token_bytes;
-  StageBuf *sb = nullptr;
-  if (host_src_bytes > 0) {
-    int rc = ctx->acquire(ctx->src, ctx->next_src, host_src_bytes, false, &sb);
-    if (rc) return rc;
-  }
-  size_t src_off = 0;
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = args[k].pool;
-    KvPoolParams &pp = params[k];
-    std::memset(&pp, 0, sizeof pp);
-    const char *src = static_cast<const char *>(args[k].src_kv);
-    if ((args[k].flags & KV_SRC_HOST) && rows[k] > 0) {
-      const size_t bytes = (size_t)rows[k] * p->token_bytes;
-      CU(cudaMemcpyAsync(sb->dev + src_off, src, bytes, cudaMemcpyHostToDevice, st));
-      src = sb->dev + src_off;
-      src_off += bytes;
-    }
-    pp.src = src;
-    pp.dst = p->pool;
-    pp.publish = 0;
-  }
-  const size_t pbytes = sizeof(KvPoolParams) * n_pools;
-  const size_t tbytes = sizeof(KvTask) * tasks.size();
-  StageBuf *b = nullptr;
-  int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + tbytes, true, &b);
+  StageBuf *sb = nullptr, *b = nullptr;
+  rc = stage_host_sources(ctx, L, st, &sb);
   if (rc) return rc;
-  std::memcpy(b->host, params.data(), pbytes);
-  std::memcpy(b->host + pbytes, tasks.data(), tbytes);
-  CU(cudaMemcpyAsync(b->dev, b->host, pbytes + tbytes, cudaMemcpyHostToDevice, st));
-  const int grid = copy_grid(p0->device, (int)tasks.size());
-  CU(timed_launch(kKindAppend, reinterpret_cast<const KvTask *>(b->dev + pbytes),
-                 (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), n_pools,
-                 p0->geom_dev(), grid, st));
-  g_launches++;
-  p0->kernels++;
-  if (sb) {
-    int rc2 = ctx->done(sb, st);  // the staged source outlives the kernel
-    if (rc2) return rc2;
-  }
+  Launch *ls[1] = {&L};
+  rc = stage(ctx, ls, 1, st, &b);
+  if (rc) return rc;
+  rc = enqueue(L, st);
+  if (rc) return rc;
+  if (sb && (rc = ctx->done(sb, st))) return rc;  // the staged source outlives the kernel
   return ctx->done(b, st);
 }
 
@@ -666,118 +952,6 @@ KV_API int kv_append(kv_pool_t *p, int32_t n, const int64_t *req_ids, const int3
   a.flags = flags;
   return kv_append_multi(1, &a, stream);
 }
-
-namespace {
-
-int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st) {
-  if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
-  if (n_pools > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "at most %d pools per launch",
-                                                    kMaxPoolsPerLaunchHost);
-  kv_pool *p0 = pools[0];
-  if (!p0) return fail(KV_EINVAL, "null pool");
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = pools[k];
-    if (!p) return fail(KV_EINVAL, "null pool");
-    if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
-    if (!p->has_succ) return fail(KV_EPEER, "pool %d has no successor", p->node_id);
-    if (step == 0 || step <= p->last_step)
-      return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
-                  (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
-    if (p->device != p0->device || !p->same_geom(*p0))
-      return fail(KV_EINVAL, "pools of one launch must share device and geometry");
-    for (int k2 = 0; k2 < k; ++k2)
-      if (pools[k2] == p) return fail(KV_EINVAL, "pool listed twice");
-  }
-  thread_local std::vector<KvTask> tasks;
-  tasks.clear();
-  std::vector<KvPoolParams> params(n_pools);
-  std::vector<int> ntask(n_pools);
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = pools[k];
-    const size_t before = tasks.size();
-    const uint64_t bytes = build_dirty_tasks(p, (int16_t)k, tasks, false, nullptr);
-    if (tasks.size() == before) push_publish_only(tasks, (int16_t)k);
-    tasks[before].flags |= kPoolFirst;
-    ntask[k] = (int)(tasks.size() - before);
-    if (p->abort_after >= 0 && p->abort_after < ntask[k]) {
-      tasks.resize(before + p->abort_after);  // fault injection: partial step, no publish
-      ntask[k] = p->abort_after;
-    }
-    p->last_step_bytes = bytes;
-  }
-  if (p0->device < 0) {  // tables only
-    for (int k = 0; k < n_pools; ++k) {
-      kv_pool *p = pools[k];
-      p->bytes_replicated += p->last_step_bytes;
-      p->pub_len = p->slot_len;
-      p->last_step = step;
-      p->tasks_launched += ntask[k];
-    }
-    return KV_OK;
-  }
-  DeviceGuard dg(p0->device);
-  if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
-  DeviceCtx *ctx = ctx_for(p0->device);
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  const size_t pbytes = sizeof(KvPoolParams) * n_pools;
-  size_t sbytes = 0;
-  for (int k = 0; k < n_pools; ++k) sbytes += 12 * (size_t)pools[k]->R;
-  sbytes = (sbytes + 15) & ~(size_t)15;
-  const size_t tbytes = sizeof(KvTask) * tasks.size();
-  StageBuf *b = nullptr;
-  int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + sbytes + tbytes, true, &b);
-  if (rc) return rc;
-  char *h = b->host;
-  size_t off = pbytes;
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = pools[k];
-    KvPoolParams &pp = params[k];
-    std::memset(&pp, 0, sizeof pp);
-    pp.src = p->pool;
-    pp.dst = p->succ_replica;
-    pp.meta = p->succ_meta;
-    std::memcpy(h + off, p->slot_req.data(), 8 * (size_t)p->R);
-    pp.slot_req = reinterpret_cast<const int64_t *>(b->dev + off);
-    off += 8 * (size_t)p->R;
-    std::memcpy(h + off, p->slot_len.data(), 4 * (size_t)p->R);
-    pp.slot_len = reinterpret_cast<const int32_t *>(b->dev + off);
-    off += 4 * (size_t)p->R;
-    pp.counter = p->counter;
-    const bool aborting = p->abort_after >= 0;
-    p->issued += (unsigned long long)ntask[k];
-    pp.target = aborting ? ~0ull : p->issued;
-    pp.step = step;
-    pp.max_reqs = p->R;
-    pp.max_blk = p->M;
-    pp.writer_node = p->node_id;
-    pp.publish = 1;
-    pp.sys_scope = p->succ_sys ? 1 : 0;
-  }
-  std::memcpy(h, params.data(), pbytes);
-  std::memcpy(h + pbytes + sbytes, tasks.data(), tbytes);
-  CU(cudaMemcpyAsync(b->dev, h, pbytes + sbytes + tbytes, cudaMemcpyHostToDevice, st));
-  if (!tasks.empty()) {
-    const int grid = copy_grid(p0->device, (int)tasks.size());
-    static const bool dbg_nopub = getenv("KVRING_DEBUG_RINGPUT_NOPUB") != nullptr;
-    CU(timed_launch(dbg_nopub ? kKindRestore : kKindRingPut,
-                   reinterpret_cast<const KvTask *>(b->dev + pbytes + sbytes),
-                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), n_pools,
-                   p0->geom_dev(), grid, st));
-    g_launches++;
-    p0->kernels++;
-  }
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = pools[k];
-    p->bytes_replicated += p->last_step_bytes;
-    p->tasks_launched += ntask[k];
-    p->pub_len = p->slot_len;
-    p->last_step = step;
-    p->abort_after = -1;
-  }
-  return ctx->done(b, st);
-}
-
-}  // namespace
 
 KV_API int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream) {
   return replicate_impl(1, &p, step, static_cast<cudaStream_t>(stream));
@@ -856,7 +1030,7 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
   if ((long long)ents.size() > dst->free_slots.size() || need_blocks > dst->free_blocks.size())
     return fail(KV_ENOMEM, "restore target too small");
   for (auto &e : ents) {
-    if (dst->slot_of.count(e.req))
+    if (dst->slot_of.find(e.req) >= 0)
       return fail(KV_EINVAL, "request %lld already in restore target", (long long)e.req);
     for (int j = 0; j < ceil_div(e.len, B); ++j) {
       const int b = mbt[(size_t)e.slot * M + j];
@@ -868,7 +1042,7 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
   std::vector<KvTask> tasks;
   for (auto &e : ents) {
     const int s = dst->free_slots.take_min();
-    dst->slot_of[e.req] = s;
+    dst->slot_of.insert(e.req, s);
     dst->slot_req[s] = e.req;
     dst->slot_len[s] = e.len;
     dst->pub_len[s] = 0;
@@ -937,7 +1111,7 @@ KV_API int kv_pack_bytes(kv_pool_t *p, size_t *bytes_out) {
   if (!p || !bytes_out) return fail(KV_EINVAL, "null argument");
   std::vector<KvTask> tasks;
   int32_t unit = 0;
-  const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit);
+  const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit, p->task_segs);
   if (tasks.empty()) push_publish_only(tasks, 0);
   KvPackedHeader h{};
   *bytes_out = packed_layout(p, tasks.size(), bytes, &h);
@@ -952,7 +1126,7 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
   if (step == 0 || step <= p->last_step) return fail(KV_EINVAL, "step not increasing");
   std::vector<KvTask> tasks;
   int32_t unit = 0;
-  const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit);
+  const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit, p->task_segs);
   if (tasks.empty()) push_publish_only(tasks, 0);
   tasks[0].flags |= kPoolFirst;
   KvPackedHeader h{};
@@ -1049,9 +1223,8 @@ KV_API int kv_unpack(const void *packed, size_t packed_bytes, void *replica,
 KV_API int kv_query(kv_pool_t *p, int64_t req_id, int32_t *len, int32_t *blocks, int32_t cap,
                     int32_t *nblk) {
   if (!p) return fail(KV_EINVAL, "null pool");
-  auto it = p->slot_of.find(req_id);
-  if (it == p->slot_of.end()) return fail(KV_EINVAL, "unknown request %lld", (long long)req_id);
-  const int s = it->second;
+  const int s = p->slot_of.find(req_id);
+  if (s < 0) return fail(KV_EINVAL, "unknown request %lld", (long long)req_id);
   if (len) *len = p->slot_len[s];
   const int n = (int)p->slot_bt[s].size();
   if (nblk) *nblk = n;
@@ -1110,27 +1283,49 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
   cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
   thread_local cudaEvent_t ready = nullptr;
   thread_local int ready_dev = -1;
+  Launch &A = g_append_launch;
+  Launch &P = g_repl_launch;
   for (int k = 0; k < n_steps; ++k) {
     const kv_step_t &st = steps[k];
-    int dev = -1;
-    if (st.n_append > 0) {
-      int rc = kv_append_multi(st.n_append, st.append, append_stream);
+    const bool has_a = st.n_append > 0, has_p = st.n_repl > 0;
+    if (has_a) {
+      int rc = prepare_append(st.n_append, st.append, A);
       if (rc) return rc;
-      dev = st.append[0].pool->device;
     }
-    if (st.n_repl <= 0) continue;
-    if (dev < 0) dev = st.repl_pools[0]->device;
-    if (dev < 0) {  // tables-only pools: no streams involved
-      int rc = replicate_impl(st.n_repl, st.repl_pools, st.step, sr);
+    if (has_p) {
+      int rc = prepare_replicate(st.n_repl, st.repl_pools, st.step, P);
       if (rc) return rc;
+    }
+    kv_pool *p0 = has_a ? A.p0 : (has_p ? P.p0 : nullptr);
+    if (!p0) continue;
+    if (p0->device < 0) {  // tables-only pools: no device work
+      if (has_p) commit_replicate(P, st.repl_pools, st.step);
       continue;
     }
-    DeviceGuard dg(dev);
-    if (sa != sr) {
-      if (!ready || ready_dev != dev) {
+    if (has_p && P.p0->device != p0->device)
+      return fail(KV_EINVAL, "append and publication of one step must share a device");
+    DeviceGuard dg(p0->device);
+    DeviceCtx *ctx = ctx_for(p0->device);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    StageBuf *sb = nullptr, *b = nullptr;
+    int rc = KV_OK;
+    if (has_a && (rc = stage_host_sources(ctx, A, sa, &sb))) return rc;
+    Launch *ls[2];
+    int nl = 0;
+    if (has_a) ls[nl++] = &A;
+    if (has_p) ls[nl++] = &P;
+    if ((rc = stage(ctx, ls, nl, sa, &b))) return rc;  // one H2D for both launches
+    if (has_a && (rc = enqueue(A, sa))) return rc;
+    if (sb && (rc = ctx->done(sb, sa))) return rc;
+    if (!has_p) {
+      if ((rc = ctx->done(b, sa))) return rc;
+      continue;
+    }
+    if (sa != sr) {  // publication after the append (and after the staged H2D)
+      if (!ready || ready_dev != p0->device) {
         if (ready) cudaEventDestroy(ready);
         CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        ready_dev = dev;
+        ready_dev = p0->device;
       }
       CU(cudaEventRecord(ready, sa));
       CU(cudaStreamWaitEvent(sr, ready, 0));
@@ -1138,10 +1333,12 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
     if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
     g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
     g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
-    int rc = replicate_impl(st.n_repl, st.repl_pools, st.step, sr);
+    rc = enqueue(P, sr);
     g_ev_before = g_ev_after = nullptr;
     if (rc) return rc;
+    commit_replicate(P, st.repl_pools, st.step);
     if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
+    if ((rc = ctx->done(b, sr))) return rc;  // sr is ordered after sa: covers both launches
   }
   return KV_OK;
 }

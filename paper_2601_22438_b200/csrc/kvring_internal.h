@@ -88,5 +88,6 @@ cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           cudaStream_t stream);
 cudaError_t launch_meta_init(char *meta, int R, int M, cudaStream_t stream);
 int copy_grid(int device, int n_tasks);
+int resident_ctas(int device);
 
 }  // namespace kvring

@@ -25,7 +25,16 @@ namespace kvring {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 8;
+#ifndef KV_UNROLL
+#define KV_UNROLL 8
+#endif
+#ifndef KV_MIN_BLOCKS
+#define KV_MIN_BLOCKS 4
+#endif
+// 8 x 16 B loads in flight per thread, 4 resident 256-thread CTAs per SM (<= 64
+// registers, no spills): 128 KB in flight per SM.
+constexpr int kUnroll = KV_UNROLL;
+constexpr int kMinBlocks = KV_MIN_BLOCKS;
 
 __device__ __forceinline__ uint4 ld_stream(const void *p) {
   uint4 r;
@@ -136,28 +145,38 @@ template <int SRC, int DST, bool PUB>
 __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
                                           const KvPoolParams *__restrict__ params,
                                           const KvGeomDev &g, int n_pools) {
-  __shared__ int s_cnt[kMaxPoolsPerLaunch];
-  if (PUB) {
-    for (int i = threadIdx.x; i < n_pools; i += blockDim.x) s_cnt[i] = 0;
-    __syncthreads();
-  }
+  // pass 1: the copies -- identical for every kernel, no publication state live
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
     const KvPoolParams &pp = params[tk.pool];
     copy_task<SRC, DST>(tk, pp.src, pp.dst, g);
-    if (PUB) {
-      if (tk.flags & kPoolFirst) write_parity_table(pp);
-      if (threadIdx.x == 0) {
-        if ((tk.flags & kFirst) && tk.slot >= 0) {
-          int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
-          bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
-        }
-        s_cnt[tk.pool] += 1;
-      }
-    }
   }
   if (!PUB) return;
+  // pass 2: publication bookkeeping of this CTA's tasks, one task per thread:
+  // bt entries of first tasks, per-pool task counts, pools whose parity table
+  // this CTA owns (kPoolFirst).  Readers trust none of it before seq = t.
+  __shared__ int s_cnt[kMaxPoolsPerLaunch];
+  __shared__ int s_own[kMaxPoolsPerLaunch];
+  for (int i = threadIdx.x; i < n_pools; i += blockDim.x) {
+    s_cnt[i] = 0;
+    s_own[i] = 0;
+  }
   __syncthreads();
+  for (int t = blockIdx.x + (int)threadIdx.x * (int)gridDim.x; t < n_tasks;
+       t += (int)blockDim.x * (int)gridDim.x) {
+    const KvTask tk = tasks[t];
+    const KvPoolParams &pp = params[tk.pool];
+    if ((tk.flags & kFirst) && tk.slot >= 0) {
+      int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
+      bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
+    }
+    if (tk.flags & kPoolFirst) s_own[tk.pool] = 1;
+    atomicAdd(&s_cnt[tk.pool], 1);
+  }
+  __syncthreads();
+  for (int i = 0; i < n_pools; ++i)
+    if (s_own[i]) write_parity_table(params[i]);
+  __syncthreads();  // every thread's stores precede the single release below
   if (threadIdx.x == 0) {
     for (int i = 0; i < n_pools; ++i) {
       if (s_cnt[i] == 0) continue;
@@ -173,7 +192,7 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
 
 // One named kernel per role (ncu / launch lists show what ran).
 #define KV_KERNEL(NAME, SRC, DST, PUB)                                                   \
-  __global__ void __launch_bounds__(kThreads, 4)                                         \
+  __global__ void __launch_bounds__(kThreads, kMinBlocks)                                \
       NAME(const KvTask *__restrict__ tasks, int n_tasks,                                \
            const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {          \
     run_tasks<SRC, DST, PUB>(tasks, n_tasks, params, g, n_pools);                        \
@@ -260,21 +279,29 @@ __global__ void kv_meta_init_kernel(char *meta, int R, int M) {
 
 }  // namespace
 
-int copy_grid(int device, int n_tasks) {
+// Resident 256-thread CTAs of the copy kernels (kMinBlocks per SM).
+// A launch never exceeds this: extra tasks are taken by grid-stride, so a
+// decode-sized step is one wave.  KVRING_CTAS_PER_SM overrides (experiments).
+int resident_ctas(int device) {
   static int sms[64] = {0};
-  int d = device < 0 ? 0 : (device & 63);
+  static int per_sm = 0;
+  const int d = device < 0 ? 0 : (device & 63);
   if (sms[d] == 0) {
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0)
       v = 148;
+    cudaGetLastError();
     sms[d] = v;
   }
-  static int per_sm = 0;
-  if (per_sm == 0) {  // debug knob for experiments: KVRING_CTAS_PER_SM
+  if (per_sm == 0) {
     const char *e = getenv("KVRING_CTAS_PER_SM");
-    per_sm = (e && atoi(e) > 0) ? atoi(e) : 8;
+    per_sm = (e && atoi(e) > 0) ? atoi(e) : kMinBlocks;
   }
-  const int cap = sms[d] * per_sm;  // grid-stride beyond this
+  return sms[d] * per_sm;
+}
+
+int copy_grid(int device, int n_tasks) {
+  const int cap = resident_ctas(device);
   return n_tasks < cap ? (n_tasks > 0 ? n_tasks : 1) : cap;
 }
 

@@ -103,6 +103,9 @@ def test_errors_and_all_or_nothing():
             K.kv_append(h, [5], [0], None)
         assert e.value.code == K.KV_EINVAL                       # empty admission
         with pytest.raises(K.KvError) as e:
+            K.kv_append(h, [-1], [3], None)
+        assert e.value.code == K.KV_EINVAL                       # -1 marks an empty slot (R9)
+        with pytest.raises(K.KvError) as e:
             K.kv_append(h, [7, 7], [1, 1], None)
         assert e.value.code == K.KV_EINVAL
         with pytest.raises(K.KvError) as e:
