@@ -187,11 +187,11 @@ class OracleNode:
             if self.slot_req[s] < 0:
                 continue
             lo, hi = int(self.pub_len[s]), int(self.slot_len[s])
-            for pos in range(lo, hi):
-                blk = self.slot_bt[s][pos // B]
-                if self.content:
+            if self.content:
+                for pos in range(lo, hi):
+                    blk = self.slot_bt[s][pos // B]
                     m.replica[blk, :, :, :, pos % B, :] = self.primary[blk, :, :, :, pos % B, :]
-                moved += self.g.token_bytes
+            moved += (hi - lo) * self.g.token_bytes
         par = step & 1
         m.rreq[par, :] = self.slot_req
         m.rlen[par, :] = self.slot_len

@@ -1,0 +1,138 @@
+"""GPU parity on the BASELINE workloads at (near) full scale on one B200:
+C3 (Poisson arrivals, two pipelines), C4 (16 logical nodes, batch 128, failure
+of (0,2) at step 300 and restore -- stage ring into a fresh pool, and the
+paper's instance ring with promotion onto the holder), C5 (32k-token prefill
+per stage: bulk full-block replication and a bulk restore).  Tables and device
+metadata are compared with the oracle in metadata mode; valid KV slots are
+checked on samples against the closed form (the full arrays do not fit the
+oracle's host memory).  Pools are sized to the workload's peak block use
+(measured with the oracle), not the 6-12 GiB worst case."""
+import numpy as np
+import pytest
+import torch
+
+from kvgen import configs
+from kvgen.content import CONTENT_SEED, content_tokens
+from oracle.simulate import OracleRing
+
+from gpu_harness import compare_state, make_gpu, node_map
+
+pytestmark = pytest.mark.gpu
+
+
+def _sample_check(rt, drv, oring, rng, per_node=3):
+    """Sampled valid slots of every live node's primary (and its successor's
+    replica when published) equal the closed-form content."""
+    torch.cuda.synchronize()
+    g = rt.g
+    B = g.block_size
+    nm = node_map(rt, drv, oring)
+    inv = {n: c for c, n in drv.serving.items()}
+    for gid, on in nm.items():
+        if on.dead or gid not in inv:
+            continue
+        stage = inv[gid][1]
+        live = on.live()
+        if not live:
+            continue
+        items = []
+        for r, (s, ln, bt) in live.items():
+            for pos in rng.choice(ln, size=min(ln, per_node), replace=False):
+                items.append((r, int(pos), bt[int(pos) // B]))
+        want = content_tokens(CONTENT_SEED, [i[0] for i in items], [i[1] for i in items],
+                              stage * g.layers, g.layers, g.kv_heads, g.head_dim)
+        idx = torch.tensor([i[2] for i in items], device=rt.dev)
+        slot = torch.tensor([i[1] % B for i in items], device=rt.dev)
+        prim = rt.local[gid].pool[idx, :, :, :, slot].cpu().numpy().view(np.uint16)
+        assert np.array_equal(prim, want), f"node {gid} primary"
+        succ = rt.succ.get(gid)
+        if succ is not None and succ in rt.local and on.succ is not None:
+            pub = on.succ.published()
+            keep = [k for k, it in enumerate(items) if it[0] in pub and it[1] < pub[it[0]][1]]
+            if keep:
+                rep = rt.local[succ].replica[idx[keep], :, :, :, slot[keep]].cpu().numpy()
+                assert np.array_equal(rep.view(np.uint16), want[keep]), f"replica of node {gid}"
+
+
+def _run(cfg, steps, ring="stage", check_every=50, restore_mode=None):
+    rt, drv = make_gpu(cfg, ring=ring, restore_mode=restore_mode)
+    oring = OracleRing(cfg, content=False, ring=ring, schedules=drv.sched,
+                       restore_mode=restore_mode)
+    rng = np.random.default_rng(3)
+    try:
+        for t in range(steps):
+            drv.append_step(t)
+            oring.appends(t)
+            if cfg.fail_step == t:
+                drv.fail_and_restore(t, cfg.fail_node)
+                oring.fail_and_restore(t, cfg.fail_node)
+                compare_state(rt, drv, oring, content=False, tag=f"after restore {t}")
+            if t >= 1:
+                rt.replicate_all(t)
+                oring.replicate(t)
+            if t % check_every == 0 or t == steps - 1:
+                compare_state(rt, drv, oring, content=False, tag=f"step {t}")
+        _sample_check(rt, drv, oring, rng)
+        return rt, drv, oring
+    except Exception:
+        rt.destroy()
+        raise
+
+
+def test_c4_failover_stage_ring_fresh_restore():
+    cfg = configs.scaled(configs.C4, num_blocks=4096, max_reqs=256)
+    rt, drv, oring = _run(cfg, 320)
+    try:
+        ev = drv.events[0].data
+        assert ev["t_star"] == 299 and len(ev["restored"]) == 128
+        assert ev["restored"] == oring.events[0][4]
+    finally:
+        rt.destroy()
+
+
+def test_c4_paper_ring_promotion_onto_holder():
+    # the paper's ring: (0,2)'s replication target and replacement is (1,2)
+    cfg = configs.scaled(configs.C4, pipelines=2, num_blocks=8192, max_reqs=512, ring="instance")
+    rt, drv, oring = _run(cfg, 315, ring="instance")
+    try:
+        ev = drv.events[0].data
+        assert ev["dst"] == drv.coords[(1, 2)] and len(ev["restored"]) == 128
+    finally:
+        rt.destroy()
+
+
+def test_c3_poisson_two_pipelines():
+    cfg = configs.scaled(configs.C3, rps=16.0, num_blocks=2048, max_reqs=256)
+    rt, drv, oring = _run(cfg, 400, check_every=100)
+    rt.destroy()
+
+
+def test_c5_bulk_replication_and_restore():
+    """One 32,768-token request per stage: 2,048 full blocks of 256 KiB replicated in
+    one step (bulk), then stage 3 fails and is restored from stage 4's replica."""
+    from paper_2601_22438_b200 import kvring as K
+    # step 0 admits the 32k prompt, step 1 appends one token and publishes the whole
+    # request (bulk seed), step 2: stage 3 fails after its append -> t* = 1
+    cfg = configs.scaled(configs.C5, n_steps=3, fixed_output=4, fail_node=(0, 3), fail_step=2,
+                         max_reqs=2, num_blocks=2050, max_blocks_per_req=2050)
+    rt, drv, oring = _run(cfg, 3, check_every=1)
+    try:
+        g = cfg.geom
+        ev = drv.events[0].data
+        assert ev["t_star"] == 1 and ev["restored"] == [(0, 32769)]
+        for s in range(cfg.stages):
+            n = drv.serving[(0, s)]
+            assert K.kv_stats(rt.handle(n))["last_step"] == 2
+        # the restored stage holds the request at fresh block ids 0..2048
+        dst = ev["dst"]
+        ln, bt = K.kv_query(rt.handle(dst), 0)
+        assert ln == 32770 and bt == list(range(2049))
+        pos = np.random.default_rng(1).choice(32770, 64, replace=False)
+        want = content_tokens(CONTENT_SEED, [0] * 64, pos, 3 * g.layers, g.layers, g.kv_heads,
+                              g.head_dim)
+        idx = torch.tensor([bt[p // 16] for p in pos], device=rt.dev)
+        sl = torch.tensor([p % 16 for p in pos], device=rt.dev)
+        got = rt.local[dst].pool[idx, :, :, :, sl].cpu().numpy().view(np.uint16)
+        assert np.array_equal(got, want)
+    finally:
+        rt.destroy()
