@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--bulk-reps", type=int, default=5, help="C5 bulk re-seed reps (0: skip)")
     ap.add_argument("--nccl-steps", type=int, default=100,
                     help="steps replicated through the NCCL send/recv comparison (0: skip)")
+    ap.add_argument("--timeline", action="store_true",
+                    help="diagnostic: time every step and print the replication-stream timeline")
     ap.add_argument("--single-stream", action="store_true",
                     help="append and replicate on one stream (default: replication stream)")
     return ap.parse_args()
@@ -210,7 +212,7 @@ def run_kvring(args):
                    for node, e in plan.items() if node in rt.local]
             pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
             st = dict(append=app, repl_pools=pools if tt >= 1 else [], step=tt)
-            if timing and (tt - t0) % TIME_EVERY == 0:
+            if timing and (args.timeline or (tt - t0) % TIME_EVERY == 0):
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
                 evs.append(ev)
@@ -235,6 +237,7 @@ def run_kvring(args):
         dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_timed0 = t
+    K.kv_host_profile(reset=True)
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize(dev)
         w0 = time.perf_counter()
@@ -249,7 +252,17 @@ def run_kvring(args):
     t += args.steps
     del src
     launches = K.kv_kernel_launch_count() - l0
+    host_prof = {k: round(v / args.steps * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}
     ms = start.elapsed_time(end)
+    if args.timeline and rank == 0:
+        rows = [(start.elapsed_time(a) * 1e3, start.elapsed_time(b) * 1e3, start.elapsed_time(c) * 1e3)
+                for a, b, c in evs]
+        print("TIMELINE us (call, kernel_start, kernel_end) per step; host wall %.1f us/step" %
+              (wall / args.steps * 1e6), file=sys.stderr)
+        for k, (a, b, c) in enumerate(rows[:60]):
+            gap = a - rows[k - 1][2] if k else 0.0
+            print("  step %3d call %8.1f kstart %8.1f kend %8.1f  kern %6.1f  gap_from_prev %6.1f"
+                  % (k, a, b, c, c - b, gap), file=sys.stderr)
     rep_us = [a.elapsed_time(c) * 1e3 for a, b, c in evs]
     kern_us = [b.elapsed_time(c) * 1e3 for a, b, c in evs]
     step_bytes = {n: K.kv_stats(rt.handle(n))["bytes_replicated"] - bytes0[n] for n in local_nodes}
@@ -338,6 +351,7 @@ def run_kvring(args):
         "roofline": roof,
         "gpu_launches": int(tot_launch),
         "wall_s_timed": round(wall, 3),
+        "host_us_per_step": host_prof,
         "clocks": clk.summary(),
     }
     if e2e is not None:

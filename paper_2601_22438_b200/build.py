@@ -67,7 +67,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         objs.append(o)
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        _run([NVCC, *ARCH, "-shared", "-cudart=static", "-Xcompiler", "-fPIC", "-o", tmp, *objs])
+        _run([NVCC, *ARCH, "-shared", "-cudart=static", "-Xcompiler", "-fPIC", "-o", tmp, *objs,
+              "-lpthread"])
         shutil.move(tmp, LIB)
     return LIB
 

@@ -10,6 +10,7 @@
 // two byte for byte.
 #include <algorithm>
 #include <atomic>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -28,22 +29,21 @@
 
 #define KV_API extern "C" __attribute__((visibility("default")))
 
-#ifdef KV_HOST_PROFILE  // diagnostic build only: per-phase host time
+// Host-side phase counters of kv_run_steps (seconds, cumulative; kv_host_profile).
 #include <chrono>
-static double g_prof[8];
-struct ProfScope {
-  int i;
-  std::chrono::steady_clock::time_point t0;
-  explicit ProfScope(int i_) : i(i_), t0(std::chrono::steady_clock::now()) {}
-  ~ProfScope() {
-    g_prof[i] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  }
-};
-#define KV_PROF(i) ProfScope kv_prof_##i(i)
-extern "C" __attribute__((visibility("default"))) double kv_prof_get(int i) { return g_prof[i]; }
-#else
-#define KV_PROF(i)
-#endif
+namespace {
+enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue, kPhN };
+double g_phase[kPhN];
+inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+KV_API int kv_host_profile(double *out, int32_t n, int32_t reset) {
+  for (int i = 0; i < n && i < kPhN; ++i) out[i] = g_phase[i];
+  if (reset)
+    for (double &x : g_phase) x = 0;
+  return kPhN;
+}
 
 using namespace kvring;
 
@@ -191,7 +191,7 @@ struct DeviceCtx {
   StageBuf src[kRing];  // device copies of host-resident append sources (KV_SRC_HOST)
   int next_src = 0;
   unsigned long long *unpack_counter = nullptr;
-  size_t cap_hint = 1 << 16;
+  size_t cap_hint = 8u << 20;  // 8 MiB per slot: growth (cudaHostAlloc, ms) never hits a hot loop
 
   // Returns a buffer of >= bytes whose previous use has completed.
   int acquire(StageBuf *ringv, int &nxt, size_t bytes, bool want_host, StageBuf **out) {
@@ -710,7 +710,6 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
   if (rc) return rc;
   long long tokens = 0;
   {
-  KV_PROF(0);
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = args[k].pool;
     if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
@@ -726,7 +725,6 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
     tokens += rows;
   }
   }
-  KV_PROF(1);
   L.reset(kKindAppend, n_pools);
   L.p0 = pools[0];
   const int task_segs = choose_task_segs(L.p0, tokens * L.p0->combos);
@@ -760,7 +758,6 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
   int rc = check_same_device(n_pools, pools);
   if (rc) return rc;
   long long dirty = 0;
-  KV_PROF(2);
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = pools[k];
     if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
@@ -811,7 +808,6 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
 }
 
 void commit_replicate(Launch &L, kv_pool *const *pools, uint64_t step) {
-  KV_PROF(3);
   for (int k = 0; k < L.n_pools; ++k) {
     kv_pool *p = pools[k];
     p->issued += (unsigned long long)L.ntask[k];
@@ -1276,6 +1272,95 @@ KV_API int kv_sync(kv_pool_t *p) {
 // For each step: appends on the compute stream, then (after an event) the
 // publication on the replication stream -- the paper's "separate CUDA stream
 // ... to overlap the communication with computation" (§3.2).
+namespace {
+
+// Host side of one decode step, prepared ahead of its CUDA calls.
+struct StepPrep {
+  Launch A, P;
+  bool has_a = false, has_p = false;
+  int rc = KV_OK;
+  std::string err;
+};
+
+// Tables, work lists and (already) committed publication state of step k.
+// Commit happens here, before the launch: the next step's dirty ranges start
+// where this one ends; a launch error is sticky and ends the run anyway.
+void prepare_step(const kv_step_t &st, StepPrep &sp) {
+  sp.has_a = st.n_append > 0;
+  sp.has_p = st.n_repl > 0;
+  sp.rc = KV_OK;
+  if (sp.has_a && (sp.rc = prepare_append(st.n_append, st.append, sp.A))) {
+    sp.err = g_err;
+    return;
+  }
+  if (sp.has_p) {
+    if ((sp.rc = prepare_replicate(st.n_repl, st.repl_pools, st.step, sp.P))) {
+      sp.err = g_err;
+      return;
+    }
+    commit_replicate(sp.P, st.repl_pools, st.step);
+  }
+  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
+  if (p0 && sp.has_a && sp.has_p && sp.P.p0->device != p0->device) {
+    sp.rc = fail(KV_EINVAL, "append and publication of one step must share a device");
+    sp.err = g_err;
+  }
+}
+
+// CUDA side of one prepared step: one H2D for both launches, append kernel on
+// sa, event, ring-put on sr (the paper's separate replication stream).
+int issue_step(const kv_step_t &st, StepPrep &sp, cudaStream_t sa, cudaStream_t sr,
+               cudaEvent_t &ready, int &ready_dev) {
+  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
+  if (!p0 || p0->device < 0) return KV_OK;  // nothing to launch / tables-only pools
+  if (sp.has_a && sp.A.tasks.empty() && !sp.has_p) return KV_OK;
+  DeviceGuard dg(p0->device);
+  DeviceCtx *ctx = ctx_for(p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  StageBuf *sb = nullptr, *b = nullptr;
+  int rc = KV_OK;
+  double t0 = now_s();
+  if (sp.has_a && (rc = stage_host_sources(ctx, sp.A, sa, &sb))) return rc;
+  Launch *ls[2];
+  int nl = 0;
+  if (sp.has_a) ls[nl++] = &sp.A;
+  if (sp.has_p) ls[nl++] = &sp.P;
+  if ((rc = stage(ctx, ls, nl, sa, &b))) return rc;  // one H2D for both launches
+  double t1 = now_s();
+  g_phase[kPhStage] += t1 - t0;
+  if (sp.has_a && (rc = enqueue(sp.A, sa))) return rc;
+  if (sb && (rc = ctx->done(sb, sa))) return rc;
+  double t2 = now_s();
+  g_phase[kPhEnqA] += t2 - t1;
+  if (!sp.has_p) return ctx->done(b, sa);
+  if (sa != sr) {  // publication after the append (and after the staged H2D)
+    if (!ready || ready_dev != p0->device) {
+      if (ready) cudaEventDestroy(ready);
+      CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      ready_dev = p0->device;
+    }
+    CU(cudaEventRecord(ready, sa));
+    CU(cudaStreamWaitEvent(sr, ready, 0));
+  }
+  if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
+  double t3 = now_s();
+  g_phase[kPhEvents] += t3 - t2;
+  g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
+  g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
+  rc = enqueue(sp.P, sr);
+  g_ev_before = g_ev_after = nullptr;
+  if (rc) return rc;
+  if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
+  rc = ctx->done(b, sr);  // sr is ordered after sa: covers both launches
+  g_phase[kPhEnqP] += now_s() - t3;
+  return rc;
+}
+
+}  // namespace
+
+// Decode-loop driver.  For runs of >= 8 steps a helper thread prepares step
+// k+1 (allocation, tables, work lists) while this thread issues step k's CUDA
+// calls; the two meet through a 2-deep ring of StepPrep.
 KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream,
                         void *repl_stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
@@ -1283,62 +1368,51 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
   cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
   thread_local cudaEvent_t ready = nullptr;
   thread_local int ready_dev = -1;
-  Launch &A = g_append_launch;
-  Launch &P = g_repl_launch;
-  for (int k = 0; k < n_steps; ++k) {
-    const kv_step_t &st = steps[k];
-    const bool has_a = st.n_append > 0, has_p = st.n_repl > 0;
-    if (has_a) {
-      int rc = prepare_append(st.n_append, st.append, A);
+  if (n_steps < 8) {
+    thread_local StepPrep sp;
+    for (int k = 0; k < n_steps; ++k) {
+      prepare_step(steps[k], sp);
+      if (sp.rc) return sp.rc;
+      int rc = issue_step(steps[k], sp, sa, sr, ready, ready_dev);
       if (rc) return rc;
     }
-    if (has_p) {
-      int rc = prepare_replicate(st.n_repl, st.repl_pools, st.step, P);
-      if (rc) return rc;
-    }
-    kv_pool *p0 = has_a ? A.p0 : (has_p ? P.p0 : nullptr);
-    if (!p0) continue;
-    if (p0->device < 0) {  // tables-only pools: no device work
-      if (has_p) commit_replicate(P, st.repl_pools, st.step);
-      continue;
-    }
-    if (has_p && P.p0->device != p0->device)
-      return fail(KV_EINVAL, "append and publication of one step must share a device");
-    DeviceGuard dg(p0->device);
-    DeviceCtx *ctx = ctx_for(p0->device);
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    StageBuf *sb = nullptr, *b = nullptr;
-    int rc = KV_OK;
-    if (has_a && (rc = stage_host_sources(ctx, A, sa, &sb))) return rc;
-    Launch *ls[2];
-    int nl = 0;
-    if (has_a) ls[nl++] = &A;
-    if (has_p) ls[nl++] = &P;
-    if ((rc = stage(ctx, ls, nl, sa, &b))) return rc;  // one H2D for both launches
-    if (has_a && (rc = enqueue(A, sa))) return rc;
-    if (sb && (rc = ctx->done(sb, sa))) return rc;
-    if (!has_p) {
-      if ((rc = ctx->done(b, sa))) return rc;
-      continue;
-    }
-    if (sa != sr) {  // publication after the append (and after the staged H2D)
-      if (!ready || ready_dev != p0->device) {
-        if (ready) cudaEventDestroy(ready);
-        CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        ready_dev = p0->device;
-      }
-      CU(cudaEventRecord(ready, sa));
-      CU(cudaStreamWaitEvent(sr, ready, 0));
-    }
-    if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
-    g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
-    g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
-    rc = enqueue(P, sr);
-    g_ev_before = g_ev_after = nullptr;
-    if (rc) return rc;
-    commit_replicate(P, st.repl_pools, st.step);
-    if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
-    if ((rc = ctx->done(b, sr))) return rc;  // sr is ordered after sa: covers both launches
+    return KV_OK;
   }
-  return KV_OK;
+  StepPrep ring[2];  // shared with the worker (per call: reentrant across threads)
+  std::atomic<int> produced{0}, consumed{0};
+  std::atomic<bool> stop{false};
+  std::thread worker([&]() {
+    for (int k = 0; k < n_steps && !stop.load(std::memory_order_acquire); ++k) {
+      const double w0 = now_s();
+      while (k - consumed.load(std::memory_order_acquire) >= 2) {
+        if (stop.load(std::memory_order_acquire)) return;
+        std::this_thread::yield();
+      }
+      g_phase[kPhWaitIssue] += now_s() - w0;
+      StepPrep &sp = ring[k & 1];
+      const double t0 = now_s();
+      prepare_step(steps[k], sp);
+      g_phase[kPhPrepare] += now_s() - t0;
+      produced.store(k + 1, std::memory_order_release);
+      if (sp.rc) return;
+    }
+  });
+  int rc = KV_OK;
+  for (int k = 0; k < n_steps; ++k) {
+    const double w0 = now_s();
+    while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
+    g_phase[kPhWaitPrep] += now_s() - w0;
+    StepPrep &sp = ring[k & 1];
+    if (sp.rc) {
+      rc = sp.rc;
+      g_err = sp.err;
+      break;
+    }
+    rc = issue_step(steps[k], sp, sa, sr, ready, ready_dev);
+    consumed.store(k + 1, std::memory_order_release);
+    if (rc) break;
+  }
+  stop.store(true, std::memory_order_release);
+  worker.join();
+  return rc;
 }

@@ -134,27 +134,16 @@ __device__ void write_parity_table(const KvPoolParams &pp) {
 
 constexpr int kMaxPoolsPerLaunch = 64;
 
-// Grid-stride over tasks.  A CTA counts the tasks it finished per pool in
-// shared memory.  After its loop: __syncthreads(), then ONE thread adds the
-// counts with acquire-release RMWs (GPU scope, or system scope when the
-// successor is an NVLink peer) -- the bar.sync + single-release pattern of
-// CUTLASS's semaphore, so no per-thread fences.  The CTA whose RMW completes a
-// pool's count stores that pool's seq with a release store (last-CTA
-// pattern): readers that acquire seq = t see all of step t.
-template <int SRC, int DST, bool PUB>
-__device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
-                                          const KvPoolParams *__restrict__ params,
-                                          const KvGeomDev &g, int n_pools) {
-  // pass 1: the copies -- identical for every kernel, no publication state live
-  for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
-    const KvTask tk = tasks[t];
-    const KvPoolParams &pp = params[tk.pool];
-    copy_task<SRC, DST>(tk, pp.src, pp.dst, g);
-  }
-  if (!PUB) return;
-  // pass 2: publication bookkeeping of this CTA's tasks, one task per thread:
-  // bt entries of first tasks, per-pool task counts, pools whose parity table
-  // this CTA owns (kPoolFirst).  Readers trust none of it before seq = t.
+// Pass 2 of the ring-put: publication bookkeeping of this CTA's tasks, one task
+// per thread: bt entries of first tasks, per-pool task counts, pools whose
+// parity table this CTA owns (kPoolFirst).  Readers trust none of it before
+// seq = t.  Then __syncthreads() and ONE thread adds the counts with
+// acquire-release RMWs (GPU scope, or system scope when the successor is an
+// NVLink peer) -- the bar.sync + single-release pattern of CUTLASS's semaphore,
+// no per-thread fences.  The CTA whose RMW completes a pool's count stores
+// that pool's seq with a release store (last-CTA pattern, reading R9).
+__device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int n_tasks,
+                                          const KvPoolParams *__restrict__ params, int n_pools) {
   __shared__ int s_cnt[kMaxPoolsPerLaunch];
   __shared__ int s_own[kMaxPoolsPerLaunch];
   for (int i = threadIdx.x; i < n_pools; i += blockDim.x) {
@@ -188,6 +177,26 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
         st_release(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
     }
   }
+}
+
+// Grid-stride over tasks.  A CTA counts the tasks it finished per pool in
+// shared memory.  After its loop: __syncthreads(), then ONE thread adds the
+// counts with acquire-release RMWs (GPU scope, or system scope when the
+// successor is an NVLink peer) -- the bar.sync + single-release pattern of
+// CUTLASS's semaphore, so no per-thread fences.  The CTA whose RMW completes a
+// pool's count stores that pool's seq with a release store (last-CTA
+// pattern): readers that acquire seq = t see all of step t.
+template <int SRC, int DST, bool PUB>
+__device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
+                                          const KvPoolParams *__restrict__ params,
+                                          const KvGeomDev &g, int n_pools) {
+  // pass 1: the copies -- identical for every kernel, no publication state live
+  for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
+    const KvTask tk = tasks[t];
+    const KvPoolParams &pp = params[tk.pool];
+    copy_task<SRC, DST>(tk, pp.src, pp.dst, g);
+  }
+  if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools);
 }
 
 // One named kernel per role (ncu / launch lists show what ran).

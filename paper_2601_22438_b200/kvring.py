@@ -25,7 +25,7 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_last_error", "kv_meta_bytes", "kv_pack_bytes", "kv_pack_step", "kv_pool_create",
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
-            "kv_unpack", "kv_time_next_launch", "kv_run_steps"]
+            "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile"]
 
 
 class KvError(RuntimeError):
@@ -119,6 +119,7 @@ def lib() -> ctypes.CDLL:
             "kv_sync": (ctypes.c_int, [_P]),
             "kv_time_next_launch": (ctypes.c_int, [_P, _P]),
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
+            "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -329,6 +330,16 @@ def kv_dump_slots(p: int, max_reqs: int):
 def kv_time_next_launch(ev_before, ev_after) -> None:
     """ev_*: torch.cuda.Event (recorded by libkvring around its next kernel) or None."""
     _check(lib().kv_time_next_launch(_event_handle(ev_before), _event_handle(ev_after)))
+
+
+HOST_PHASES = ["prepare", "wait_prepare", "stage_h2d", "launch_append", "launch_publish",
+               "events", "worker_wait_issue"]
+
+
+def kv_host_profile(reset: bool = True) -> dict:
+    out = np.zeros(16, dtype=np.float64)
+    n = lib().kv_host_profile(_ptr(out), 16, 1 if reset else 0)
+    return {HOST_PHASES[i] if i < len(HOST_PHASES) else str(i): float(out[i]) for i in range(n)}
 
 
 def kv_sync(p: int) -> None:

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out; python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
+timeout 300 python -m pytest tests -m gpu -x -q -k "not multigpu and not configs" > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
+B="python bench.py --no-cpu-baseline --e2e-steps 0 --no-restore --nccl-steps 0 --bulk-reps 2 --steps 300"
+for ss in "" "--single-stream"; do
+  echo "== $ss" >> gpurun_out/exp7.log
+  timeout 300 $B $ss 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['wall_s_timed'], d['ring_put_kernel_us'], d['roofline']['frac'], d['bulk']['roofline']['frac']); print(d['host_us_per_step'])" >> gpurun_out/exp7.log 2>&1
+done
+nproc >> gpurun_out/exp7.log
