@@ -62,6 +62,16 @@ def parse():
     return ap.parse_args()
 
 
+def traffic_ref(kind):
+    """Captured DRAM traffic per launch (profiles/traffic.json, from ncu --set full)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)["kv_ring_put_kernel"][kind]
+        return d
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -311,8 +321,14 @@ def run_kvring(args):
     per_launch = my_bytes / args.steps
     if N == 1:
         achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
+        tr = traffic_ref("decode_step")
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "frac": round(achieved / hbm_peak, 4),
+                "traffic": tr["traffic"] if tr else None,
+                "traffic_note": ("ncu --set full of a decode-step launch (profiles/traffic.json): "
+                                 "DRAM bytes %d vs algorithmic read %d / r+w %d; writes stay in L2"
+                                 % (tr["traffic"], tr["algorithmic_read"], tr["algorithmic_rw"]))
+                                if tr else None,
                 "kernel": "kv_ring_put_kernel", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(2 * per_launch),
                 "avg_launch_us": round(avg_kern, 2)}
@@ -432,9 +448,11 @@ def run_bulk(args, rank, world, local_rank, dev, group):
     per_gpu = D / (ms * 1e-3) / 1e9
     if world == 1:
         ach = 2 * D / (ms * 1e-3) / 1e9
+        tr = traffic_ref("bulk_c5")
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(ach / hbm_peak, 4), "peak_source": src_peak,
-                "algorithmic_bytes_per_launch": int(2 * D)}
+                "algorithmic_bytes_per_launch": int(2 * D),
+                "traffic": tr["traffic"] if tr else None}
     else:
         roof = {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": round(per_gpu / NVLINK_PEAK_GBS, 4),
