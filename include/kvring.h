@@ -182,6 +182,16 @@ typedef struct {
 } kv_step_t;
 int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream, void *repl_stream);
 
+/* Re-protection after a failure (§8(f) NEXT-1; §3.2: "replication targets
+ * will be automatically adjusted to exclude the nodes under traffic rerouting").
+ * succ[n_nodes] is the ring's successor map over logical node ids; excluded
+ * (may be NULL) marks failed nodes and nodes under traffic rerouting.  Each
+ * non-excluded node's target is the first non-excluded node met by walking the
+ * successors (never itself); -1 if there is none, and -1 for excluded nodes (they
+ * neither send nor receive).  Host-only; apply with kv_set_successor (re-seed). */
+int kv_plan_targets(int32_t n_nodes, const int32_t *succ, const uint8_t *excluded,
+                    int32_t *targets);
+
 /* Fault injection: the next replicate of p executes only its first
  * `tasks` copy tasks and never publishes -- a stage dying mid-step. -1 clears. */
 int kv_inject_abort(kv_pool_t *p, int32_t tasks);

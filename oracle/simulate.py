@@ -157,6 +157,23 @@ class OracleRing:
         self.events.append(("restore", t, coord, t_star, restored, ids, n_new))
         return t_star, restored, dst
 
+    def reprotect(self, excluded_coords) -> dict:
+        """P:227 §3.2 re-protection: targets from the ring walk skipping the excluded
+        nodes (oracle/ring.py plan_replication_targets); a link is rebound (re-seeded)
+        iff its target node changes; excluded nodes stop replicating."""
+        from .ring import plan_replication_targets
+        plan = plan_replication_targets(self.cfg.pipelines, self.cfg.stages, set(excluded_coords),
+                                        ring=self.ring_fn)
+        for c in self.coords:
+            n = self.serving[c]
+            if n.dead:
+                continue
+            t = plan.get(c)
+            want = None if t is None else self.serving[t]
+            if n.succ is not want:
+                n.set_successor(want)
+        return plan
+
     def ring_fn_target(self, node: OracleNode):
         """The node ``node`` was originally linked to (ring map over logical coords)."""
         I, S = self.cfg.pipelines, self.cfg.stages

@@ -1416,3 +1416,27 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
   worker.join();
   return rc;
 }
+
+// ---- re-protection (§8(f) NEXT-1; §3.2) --------------------
+// Each non-excluded node's replication target is the first non-excluded node met
+// by walking its ring successors; never itself; -1 when none exists (the node is
+// unprotected: "replication-disabled").  Excluded nodes (failed, or under traffic
+// rerouting) neither send nor receive: -1.
+KV_API int kv_plan_targets(int32_t n_nodes, const int32_t *succ, const uint8_t *excluded,
+                           int32_t *targets) {
+  if (n_nodes <= 0 || !succ || !targets) return fail(KV_EINVAL, "bad arguments");
+  for (int i = 0; i < n_nodes; ++i)
+    if (succ[i] < 0 || succ[i] >= n_nodes) return fail(KV_EINVAL, "successor out of range");
+  for (int i = 0; i < n_nodes; ++i) {
+    targets[i] = -1;
+    if (excluded && excluded[i]) continue;
+    int j = succ[i];
+    for (int hops = 0; hops < n_nodes && j != i; ++hops, j = succ[j]) {
+      if (!(excluded && excluded[j])) {
+        targets[i] = j;
+        break;
+      }
+    }
+  }
+  return KV_OK;
+}

@@ -25,7 +25,8 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_last_error", "kv_meta_bytes", "kv_pack_bytes", "kv_pack_step", "kv_pool_create",
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
-            "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile"]
+            "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
+            "kv_plan_targets"]
 
 
 class KvError(RuntimeError):
@@ -120,6 +121,7 @@ def lib() -> ctypes.CDLL:
             "kv_time_next_launch": (ctypes.c_int, [_P, _P]),
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
+            "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -330,6 +332,19 @@ def kv_dump_slots(p: int, max_reqs: int):
 def kv_time_next_launch(ev_before, ev_after) -> None:
     """ev_*: torch.cuda.Event (recorded by libkvring around its next kernel) or None."""
     _check(lib().kv_time_next_launch(_event_handle(ev_before), _event_handle(ev_after)))
+
+
+def kv_plan_targets(succ, excluded=None):
+    """succ: successor node id per node (list); excluded: iterable of node ids.
+    Returns the re-protection targets (-1 = none / excluded)."""
+    n = len(succ)
+    sa = _i32(succ)
+    ex = np.zeros(n, dtype=np.uint8)
+    for e in (excluded or []):
+        ex[e] = 1
+    out = np.zeros(n, dtype=np.int32)
+    _check(lib().kv_plan_targets(n, _ptr(sa), _ptr(ex), _ptr(out)))
+    return [int(x) for x in out]
 
 
 HOST_PHASES = ["prepare", "wait_prepare", "stage_h2d", "launch_append", "launch_publish",

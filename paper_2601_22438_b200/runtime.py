@@ -347,6 +347,29 @@ class ScheduleDriver:
             rt.set_succ(dst, holder)
         return dst, result
 
+    def reprotect(self, excluded_coords) -> dict:
+        """Re-protection after a failure (§8(f) NEXT-1): walk the ORIGINAL ring
+        over logical coordinates skipping excluded ones (failed nodes and nodes under
+        traffic rerouting) with kv_plan_targets; rebind (re-seed) every link whose
+        target node changed; excluded nodes stop replicating.  Returns {coord: coord}."""
+        coords = sorted(self.coords)
+        idx = {c: k for k, c in enumerate(coords)}
+        node_coord = {n: c for c, n in self.coords.items()}
+        succ = [idx[node_coord[self.orig_succ[self.coords[c]]]] for c in coords]
+        excl = [idx[c] for c in excluded_coords]
+        tgt = K.kv_plan_targets(succ, excl)
+        plan = {}
+        for c in coords:
+            n = self.serving[c]
+            if n in self.rt.dead:
+                continue
+            t = tgt[idx[c]]
+            want = None if t < 0 else self.serving[coords[t]]
+            plan[c] = None if t < 0 else coords[t]
+            if self.rt.succ.get(n) != want:
+                self.rt.set_succ(n, want)
+        return plan
+
     def run(self, n_steps: int, fail_step: int | None = None, fail_coord=None, on_step=None,
             stream=None):
         for t in range(n_steps):

@@ -298,3 +298,33 @@ def test_nccl_loopback_transport_bit_exact():
         compare_state(rt, drv, oring, tag="nccl-loopback end")
     finally:
         rt.destroy()
+
+
+def test_reprotect_after_promotion_bit_exact():
+    """NEXT-1: paper ring, (0,2) fails and is promoted onto (1,2); the failed node and
+    the rerouting donor are excluded, (3,2) is re-targeted to (2,2) and
+    re-seeded; every array stays == oracle for the rest of the run."""
+    cfg = configs.scaled(configs.C1, pipelines=4, num_blocks=128, max_reqs=16,
+                         max_blocks_per_req=12, batch_cap=3, n_requests=40, n_steps=34,
+                         fixed_prompt=None, fail_node=(0, 2), fail_step=15, ring="instance")
+    sched = _churn_sched(cfg, 17)
+    rt, drv = make_gpu(cfg, ring="instance", schedules=sched)
+    oring = OracleRing(cfg, ring="instance", schedules=sched)
+    try:
+        for t in range(cfg.n_steps):
+            drv.append_step(t)
+            oring.appends(t)
+            if t == cfg.fail_step:
+                drv.fail_and_restore(t, cfg.fail_node)
+                oring.fail_and_restore(t, cfg.fail_node)
+                plan_g = drv.reprotect([(0, 2), (1, 2)])
+                plan_o = oring.reprotect([(0, 2), (1, 2)])
+                assert {c: plan_g[c] for c in plan_o} == plan_o
+                assert plan_g[(3, 2)] == (2, 2)
+            if t >= 1:
+                rt.replicate_all(t)
+                oring.replicate(t)
+            if t % 3 == 0 or t >= cfg.fail_step:
+                compare_state(rt, drv, oring, tag=f"reprotect step {t}")
+    finally:
+        rt.destroy()

@@ -145,3 +145,32 @@ def test_bad_geometry_rejected():
         with pytest.raises(K.KvError) as e:
             K.kv_pool_create(d)
         assert e.value.code == K.KV_EINVAL
+
+
+def test_plan_targets_matches_oracle_ring_walk():
+    """kv_plan_targets (C++) == the oracle's ring walk, exhaustively."""
+    import itertools
+    from oracle.ring import instance_ring, plan_replication_targets, stage_ring
+    for ring in (instance_ring, stage_ring):
+        for I in range(1, 5):
+            for S in range(1, 4):
+                coords = [(i, s) for i in range(I) for s in range(S)]
+                idx = {c: k for k, c in enumerate(coords)}
+                succ = [idx[ring(c, I, S)] for c in coords]
+                for k in range(0, 4):
+                    for excl in itertools.combinations(coords, k):
+                        got = K.kv_plan_targets(succ, [idx[c] for c in excl])
+                        want = plan_replication_targets(I, S, set(excl), ring=ring)
+                        for c in coords:
+                            w = want.get(c)
+                            assert got[idx[c]] == (-1 if w is None else idx[w]), (I, S, excl, c)
+    # the paper's example through the C ABI
+    coords = [(i, s) for i in range(4) for s in range(4)]
+    idx = {c: k for k, c in enumerate(coords)}
+    succ = [idx[instance_ring(c, 4, 4)] for c in coords]
+    excl = [(0, 2), (1, 2), (2, 1), (3, 1)]
+    base = K.kv_plan_targets(succ)
+    got = K.kv_plan_targets(succ, [idx[c] for c in excl])
+    changed = {coords[k] for k in range(16) if got[k] != base[k] and coords[k] not in excl}
+    assert changed == {(1, 1), (3, 2)}
+    assert got[idx[(1, 1)]] == idx[(0, 1)] and got[idx[(3, 2)]] == idx[(2, 2)]
