@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--interference-steps", type=int, default=60,
                     help="steps with a Llama-3.1-8B stage decode proxy on the compute stream, "
                          "replication on vs off (0: skip)")
+    ap.add_argument("--block-steps", type=int, default=100,
+                    help="steps in block-granular mode (NEXT-2), after a re-seed (0: skip)")
     ap.add_argument("--nccl-steps", type=int, default=100,
                     help="steps replicated through the NCCL send/recv comparison (0: skip)")
     ap.add_argument("--timeline", action="store_true",
@@ -167,7 +169,7 @@ def run_kvring(args):
     placement = {coords[(p, s)]: (p + s) % N for (p, s) in coords}
     succ = {coords[(p, s)]: coords[(p, (s + 1) % S)] for (p, s) in coords}
     n_total = (args.prelude + args.warmup + args.steps + args.e2e_steps + args.nccl_steps
-               + 2 * args.interference_steps + 2)
+               + 2 * args.interference_steps + args.block_steps + 3)
     scheds = configs.build_schedules(cfg, n_steps=n_total)
     rt = RingRuntime(g, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement, succ,
                      rank=rank, world=world, device=local_rank, spares=1, group=group,
@@ -300,6 +302,12 @@ def run_kvring(args):
         nccl = run_nccl(args, drv, rt, t, comp, content, dev, world)
         t += args.nccl_steps
 
+    # ---- block-granular mode (NEXT-2): completed blocks only ---------------------
+    block = None
+    if args.block_steps > 0:
+        block = run_block_mode(args, drv, rt, t, comp, repl, content, dev, world)
+        t += args.block_steps + 1
+
     # ---- restore: fail stage 2 of pipeline 0, restore into a fresh pool ---------
     restore = None
     if not args.no_restore and world == 1:
@@ -390,6 +398,8 @@ def run_kvring(args):
         line["nccl_compare"] = nccl
     if interference is not None:
         line["interference"] = interference
+    if block is not None:
+        line["block_mode"] = block
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, t_timed0, min(args.steps, 60))
     if rank == 0:
@@ -576,6 +586,73 @@ def run_interference(args, drv, rt, t0, comp, repl, content, dev, world):
             "paper": "+2.3 % avg / +2.8 % p99 latency (8 A10 nodes), +4.0 % / +3.6 % (16) "
                      "over 1 Gbps, P:99 -- context, not the target",
             "steps": n}
+
+
+def run_block_mode(args, drv, rt, t0, comp, repl, content, dev, world):
+    """NEXT-2: the paper's literal "replicate it block-by-block": only completed
+    16-token blocks are published (whole contiguous 512-KiB blocks instead of 256-B
+    token slices); the replica lags < 16 tokens per request.  One re-seed step after
+    the switch, then K timed steps through kv_run_steps."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_22438_b200 import kvring as K
+    nodes = rt.alive_local()
+    for nd in nodes:
+        K.kv_set_mode(rt.handle(nd), K.KV_MODE_BLOCKS)
+    n = args.block_steps
+    handles = [rt.handle(nd) for nd in nodes if rt.succ.get(nd) is not None]
+    steps, evs = [], []
+    for k, tt in enumerate(range(t0, t0 + n + 1)):
+        plan = drv.plan(tt)
+        app = []
+        for nd, e in plan.items():
+            if nd in rt.local:
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                app.append(dict(pool=rt.handle(nd), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"],
+                                src=content(e["stage"], ids, pos) if ids else None))
+        st = dict(append=app, repl_pools=handles, step=tt)
+        if k > 0 and k % TIME_EVERY == 0:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
+            evs.append(ev)
+        steps.append(st)
+    reseed = K.PreparedSteps(steps[:1])
+    timed = K.PreparedSteps(steps[1:])
+    K.kv_run_steps(reseed, comp.cuda_stream, repl.cuda_stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    b0 = {nd: K.kv_stats(rt.handle(nd))["bytes_replicated"] for nd in nodes}
+    st_, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st_.record(comp)
+    K.kv_run_steps(timed, comp.cuda_stream, repl.cuda_stream)
+    fin = torch.cuda.Event()
+    fin.record(repl)
+    comp.wait_event(fin)
+    en.record(comp)
+    torch.cuda.synchronize(dev)
+    ms = st_.elapsed_time(en)
+    by = sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in nodes)
+    kern = [b.elapsed_time(c) * 1e3 for a, b, c in evs]
+    lags = []
+    for nd in nodes:
+        req, ln, pub, nb = K.kv_dump_slots(rt.handle(nd), rt.R)
+        lags.extend(int(a - b) for a, b, r in zip(ln, pub, req) if r >= 0)
+    vec = torch.tensor([ms, float(by)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, by = float(mx[0]), float(sm[1])
+    return {"mode": "blocks (completed 16-token blocks only)", "steps": n,
+            "value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "ms_per_step": round(ms / n, 4),
+            "ring_put_kernel_us": {"median": round(statistics.median(kern), 2),
+                                   "avg": round(sum(kern) / len(kern), 2)},
+            "replica_lag_tokens": {"mean": round(float(np.mean(lags)), 2) if lags else 0.0,
+                                   "max": int(max(lags)) if lags else 0}}
 
 
 def run_nccl(args, drv, rt, t0, comp, content, dev, world):

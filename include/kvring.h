@@ -164,6 +164,16 @@ int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream);
 /* Same for several pools of ONE device in a single launch. */
 int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, void *stream);
 
+/* Replication granularity (reading R2; §8(f) NEXT-2).  KV_MODE_TOKENS (default):
+ * every step publishes all appended tokens (exact replica).  KV_MODE_BLOCKS: only
+ * completed blocks ("replicate it block-by-block"): whole 16-token blocks,
+ * the replica lags by <= B-1 tokens per request and the published length is a
+ * multiple of B (a request with no completed block is listed as empty).  A mode
+ * change re-seeds the link. */
+#define KV_MODE_TOKENS 0
+#define KV_MODE_BLOCKS 1
+int kv_set_mode(kv_pool_t *p, int32_t mode);
+
 /* Decode-loop driver: for each step, kv_append_multi(append) on append_stream,
  * then -- ordered after it by an event when the streams differ -- the
  * publication kv_replicate_step_multi(repl_pools, step) on repl_stream: the

@@ -78,6 +78,7 @@ class OracleNode:
         self.succ: OracleNode | None = None
         self.last_step = 0
         self.dead = False
+        self.mode = "tokens"     # "blocks": completed blocks only (P:229 literal; NEXT-2)
 
     # ------------------------------------------------------------------ allocator
     def begin_step(self) -> None:
@@ -160,6 +161,21 @@ class OracleNode:
                 row += 1
 
     # ---------------------------------------------------------------- replication
+    def set_mode(self, mode: str) -> None:
+        """Granularity reading R2: "tokens" (every step, exact) or "blocks" (P:229
+        "block-by-block": only completed blocks; the replica lags < B tokens).
+        A switch re-seeds the link."""
+        assert mode in ("tokens", "blocks")
+        self.mode = mode
+        self.pub_len[:] = 0
+
+    def published_len(self, s: int) -> int:
+        """Length a publication of slot s reaches (all tokens, or completed blocks)."""
+        ln = int(self.slot_len[s])
+        if self.mode == "blocks":
+            return max(int(self.pub_len[s]), ln - ln % self.g.block_size)
+        return ln
+
     def set_successor(self, succ: OracleNode | None) -> None:
         """Bind the ring link (SPEC S:298-306 apply_plan); a new link re-seeds: pub_len = 0."""
         self._alive()
@@ -183,24 +199,26 @@ class OracleNode:
         moved = 0
         if m.dead:
             raise OracleError(ESTATE, "successor is dead; the harness must unlink it first")
+        hi_all = np.zeros(self.R, dtype=np.int32)
         for s in range(self.R):
             if self.slot_req[s] < 0:
                 continue
-            lo, hi = int(self.pub_len[s]), int(self.slot_len[s])
+            lo, hi = int(self.pub_len[s]), self.published_len(s)
+            hi_all[s] = hi
             if self.content:
                 for pos in range(lo, hi):
                     blk = self.slot_bt[s][pos // B]
                     m.replica[blk, :, :, :, pos % B, :] = self.primary[blk, :, :, :, pos % B, :]
             moved += (hi - lo) * self.g.token_bytes
         par = step & 1
-        m.rreq[par, :] = self.slot_req
-        m.rlen[par, :] = self.slot_len
+        m.rreq[par, :] = np.where(hi_all > 0, self.slot_req, -1)
+        m.rlen[par, :] = hi_all
         for s in range(self.R):
             if self.slot_req[s] >= 0:
-                nb = len(self.slot_bt[s])
-                m.rbt[s, :nb] = self.slot_bt[s]
+                nb = ceil_div(int(hi_all[s]), B)
+                m.rbt[s, :nb] = self.slot_bt[s][:nb]
         m.rseq = step
-        self.pub_len[:] = self.slot_len
+        self.pub_len[:] = hi_all
         self.last_step = step
         return moved
 

@@ -269,6 +269,7 @@ struct kv_pool {
   long long block_bytes = 0;
   int token_bytes = 0, seg_bytes = 0, combos = 0, task_segs = 0, cps_shift = 0;
   // ring link
+  int repl_mode = KV_MODE_TOKENS;  // KV_MODE_BLOCKS: completed blocks only (NEXT-2)
   bool has_succ = false;
   bool succ_sys = true;  // successor memory is not this GPU's HBM (NVLink peer)
   int succ_node = -1, succ_replica_blocks = 0;
@@ -463,7 +464,31 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<
 }
 
 // ---- replicate --------------------------------------------------------------
-// Dirty ranges [pub_len, len) of every live slot split at block boundaries
+// Length a publication of slot s reaches: every appended token (KV_MODE_TOKENS,
+// reading R2) or the completed blocks only (KV_MODE_BLOCKS, P:229 literal).
+inline int pub_hi(const kv_pool *p, int s) {
+  const int len = p->slot_len[s];
+  if (p->repl_mode == KV_MODE_BLOCKS) return std::max(p->pub_len[s], len - len % p->g.block_size);
+  return len;
+}
+
+// Parity table of a publication: (req_id, published length); a slot with
+// nothing published yet is listed as empty (-1, 0).
+void fill_pub_table(const kv_pool *p, char *dst) {
+  int64_t *rq = reinterpret_cast<int64_t *>(dst);
+  int32_t *ln = reinterpret_cast<int32_t *>(dst + 8 * (size_t)p->R);
+  for (int s = 0; s < p->R; ++s) {
+    const int hi = p->slot_req[s] >= 0 ? pub_hi(p, s) : 0;
+    rq[s] = hi > 0 ? p->slot_req[s] : -1;
+    ln[s] = hi;
+  }
+}
+
+void commit_pub_len(kv_pool *p) {
+  for (int s = 0; s < p->R; ++s) p->pub_len[s] = p->slot_req[s] >= 0 ? pub_hi(p, s) : 0;
+}
+
+// Dirty ranges [pub_len, pub_hi) of every live slot split at block boundaries
 // (§8(a) a3); returns payload bytes.
 uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks, bool packed,
                            int32_t *packed_unit, int task_segs) {
@@ -472,7 +497,7 @@ uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks,
   for (int s = 0; s < p->R; ++s) {
     if (p->slot_req[s] < 0) continue;
     int pos = p->pub_len[s];
-    const int len = p->slot_len[s];
+    const int len = pub_hi(p, s);
     while (pos < len) {
       const int j = pos / B, lo = pos % B;
       const int n = std::min(B - lo, len - pos);
@@ -766,7 +791,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
       return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
                   (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
     for (int s = 0; s < p->R; ++s)
-      if (p->slot_req[s] >= 0) dirty += p->slot_len[s] - p->pub_len[s];
+      if (p->slot_req[s] >= 0) dirty += pub_hi(p, s) - p->pub_len[s];
   }
   L.reset(kKindRingPut, n_pools);
   L.p0 = pools[0];
@@ -788,8 +813,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
       L.ntask[k] = p->abort_after;
     }
     L.table_off[k] = toff;
-    std::memcpy(L.tables.data() + toff, p->slot_req.data(), 8 * (size_t)p->R);
-    std::memcpy(L.tables.data() + toff + 8 * (size_t)p->R, p->slot_len.data(), 4 * (size_t)p->R);
+    fill_pub_table(p, L.tables.data() + toff);
     toff += 12 * (size_t)p->R;
     KvPoolParams &pp = L.params[k];
     pp.src = p->pool;
@@ -814,7 +838,7 @@ void commit_replicate(Launch &L, kv_pool *const *pools, uint64_t step) {
     p->last_step_bytes = L.bytes[k];
     p->bytes_replicated += L.bytes[k];
     p->tasks_launched += L.ntask[k];
-    p->pub_len = p->slot_len;
+    commit_pub_len(p);
     p->last_step = step;
     p->abort_after = -1;
   }
@@ -956,6 +980,15 @@ KV_API int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream) {
 KV_API int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step,
                                    void *stream) {
   return replicate_impl(n_pools, pools, step, static_cast<cudaStream_t>(stream));
+}
+
+KV_API int kv_set_mode(kv_pool_t *p, int32_t mode) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  if (mode != KV_MODE_TOKENS && mode != KV_MODE_BLOCKS) return fail(KV_EINVAL, "unknown mode");
+  if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+  p->repl_mode = mode;
+  std::fill(p->pub_len.begin(), p->pub_len.end(), 0);  // a mode switch re-seeds the link
+  return KV_OK;
 }
 
 KV_API int kv_inject_abort(kv_pool_t *p, int32_t tasks) {
@@ -1156,8 +1189,7 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
     rt[i].src_unit = tasks[i].dst_unit;
     rt[i].dst_unit = tasks[i].src_unit;
   }
-  std::memcpy(hb + h.slot_off, p->slot_req.data(), 8 * (size_t)p->R);
-  std::memcpy(hb + h.slot_off + 8 * (size_t)p->R, p->slot_len.data(), 4 * (size_t)p->R);
+  fill_pub_table(p, hb + h.slot_off);
   pp.src = p->pool;
   pp.dst = static_cast<char *>(packed) + h.payload_off;
   std::memcpy(hb + head, &pp, pbytes);
@@ -1177,7 +1209,7 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
   if (rc) return rc;
   p->last_step_bytes = bytes;
   p->bytes_replicated += bytes;
-  p->pub_len = p->slot_len;
+  commit_pub_len(p);
   p->last_step = step;
   if (bytes_out) *bytes_out = total;
   return KV_OK;

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libkvring.so")
 
 KV_OK, KV_EINVAL, KV_ENOMEM, KV_ECUDA, KV_ESTATE, KV_ENOREPLICA, KV_EPEER = 0, -1, -2, -3, -4, -5, -6
 KV_SRC_HOST = 1
+KV_MODE_TOKENS, KV_MODE_BLOCKS = 0, 1
 CODE_NAMES = {0: "KV_OK", -1: "KV_EINVAL", -2: "KV_ENOMEM", -3: "KV_ECUDA", -4: "KV_ESTATE",
               -5: "KV_ENOREPLICA", -6: "KV_EPEER"}
 
@@ -26,7 +27,7 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
-            "kv_plan_targets"]
+            "kv_plan_targets", "kv_set_mode"]
 
 
 class KvError(RuntimeError):
@@ -122,6 +123,7 @@ def lib() -> ctypes.CDLL:
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
+            "kv_set_mode": (ctypes.c_int, [_P, _I32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -266,6 +268,10 @@ def kv_replicate_step(p: int, step: int, stream: int = 0) -> None:
 def kv_replicate_step_multi(pools, step: int, stream: int = 0) -> None:
     arr = (_P * len(pools))(*pools)
     _check(lib().kv_replicate_step_multi(len(pools), ctypes.addressof(arr), step, stream))
+
+
+def kv_set_mode(p: int, mode: int) -> None:
+    _check(lib().kv_set_mode(p, mode))
 
 
 def kv_inject_abort(p: int, tasks: int) -> None:

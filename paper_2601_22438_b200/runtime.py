@@ -51,12 +51,14 @@ class RingRuntime:
     def __init__(self, geom, num_blocks: int, max_reqs: int, max_blocks_per_req: int,
                  placement: dict[int, int], succ: dict[int, int], rank: int = 0, world: int = 1,
                  device: int | None = None, spares: int = 1, group=None,
-                 sentinel: int | None = SENTINEL_WORD, dtype_words=torch.int16):
+                 sentinel: int | None = SENTINEL_WORD, dtype_words=torch.int16,
+                 mode: int = K.KV_MODE_TOKENS):
         self.g = geom
         self.NB, self.R, self.M = num_blocks, max_reqs, max_blocks_per_req
         self.placement = dict(placement)
         self.succ = dict(succ)
         self.rank, self.world = rank, world
+        self.mode = mode
         self.device = torch.cuda.current_device() if device is None else device
         self.dev = torch.device("cuda", self.device)
         self.kg = K.geom(geom.layers, geom.kv_heads, geom.head_dim, geom.block_size, geom.elem_bytes)
@@ -117,6 +119,8 @@ class RingRuntime:
         d = K.kv_pool_desc_t(self.kg, self.NB, self.R, self.M, self.device, node, self.NB,
                              slot.pool.data_ptr(), slot.replica.data_ptr(), slot.meta.data_ptr())
         slot.handle = K.kv_pool_create(d)
+        if self.mode != K.KV_MODE_TOKENS:
+            K.kv_set_mode(slot.handle, self.mode)
         slot.node = node
         self.local[node] = slot
         return slot.handle

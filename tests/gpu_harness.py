@@ -13,7 +13,8 @@ from oracle.ring import instance_ring, stage_ring
 from oracle.simulate import OracleRing
 
 
-def make_gpu(cfg, ring="stage", device=0, spares=1, schedules=None, restore_mode=None):
+def make_gpu(cfg, ring="stage", device=0, spares=1, schedules=None, restore_mode=None,
+             mode="tokens"):
     from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
     from kvgen.configs import build_schedules
     I, S = cfg.pipelines, cfg.stages
@@ -22,8 +23,10 @@ def make_gpu(cfg, ring="stage", device=0, spares=1, schedules=None, restore_mode
     succ = {coords[c]: coords[fn(c, I, S)] for c in coords}
     placement = {n: 0 for n in coords.values()}
     torch.cuda.set_device(device)
+    from paper_2601_22438_b200 import kvring as K
     rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement,
-                     succ, rank=0, world=1, device=device, spares=spares)
+                     succ, rank=0, world=1, device=device, spares=spares,
+                     mode=K.KV_MODE_BLOCKS if mode == "blocks" else K.KV_MODE_TOKENS)
     g = cfg.geom
 
     def content(stage, ids, pos):

@@ -328,3 +328,30 @@ def test_reprotect_after_promotion_bit_exact():
                 compare_state(rt, drv, oring, tag=f"reprotect step {t}")
     finally:
         rt.destroy()
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_block_mode_with_failure_bit_exact(seed):
+    """NEXT-2 block-granular mode (completed blocks only): whole arrays == oracle,
+    including a failure, a restore at a block boundary and the resume."""
+    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=6, n_requests=60, n_steps=40, fixed_prompt=None,
+                         fail_node=(0, 1), fail_step=26)
+    sched = _churn_sched(cfg, seed)
+    rt, drv = make_gpu(cfg, schedules=sched, mode="blocks")
+    oring = OracleRing(cfg, schedules=sched, mode="blocks")
+    try:
+        for t in range(cfg.n_steps):
+            drv.append_step(t)
+            oring.appends(t)
+            if cfg.fail_step == t:
+                drv.fail_and_restore(t, cfg.fail_node)
+                oring.fail_and_restore(t, cfg.fail_node)
+            if t >= 1:
+                rt.replicate_all(t)
+                oring.replicate(t)
+            if t % 2 == 0 or t >= cfg.fail_step:
+                compare_state(rt, drv, oring, tag=f"blocks step {t}")
+        assert all(ln % 16 == 0 for _, ln in drv.events[0].data["restored"])
+    finally:
+        rt.destroy()

@@ -280,3 +280,43 @@ def test_invariants_random_run_with_failure():
     assert t_star == 16
     for (p, s), n in ring.serving.items():
         check_content(ring, n, s)          # I2 / I4 on every live slot, restored stage included
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_block_mode_equals_completed_block_copy(seed):
+    """NEXT-2 ("block-by-block", P:229 literal): the replica equals a brute-force copy
+    of every COMPLETED block of every live request, published lengths are multiples
+    of B, and the replica lags the primary by < B tokens per request."""
+    cfg = _random_cfg(seed, steps=35)
+    ring = OracleRing(cfg, schedules=_small_sched(cfg, seed), mode="blocks")
+    B = cfg.geom.block_size
+    brute = {c: np.full_like(ring.nodes[c].replica, SENTINEL_WORD) for c in ring.coords}
+    for t in range(cfg.n_steps):
+        ring.appends(t)
+        if t >= 1:
+            for c in ring.coords:
+                n = ring.nodes[c]
+                m = stage_ring(c, 1, 4)
+                for r, (s, ln, bt) in n.live().items():
+                    for j in range(ln // B):
+                        brute[m][bt[j]] = n.primary[bt[j]]
+            ring.replicate(t)
+            for c in ring.coords:
+                n = ring.nodes[c]
+                pub = n.succ.published()
+                for r, (s, ln, bt) in n.live().items():
+                    hi = pub.get(r, (s, 0, []))[1]
+                    assert hi % B == 0 and 0 <= ln - hi < B
+        check_all(ring)
+    for c in ring.coords:
+        assert np.array_equal(ring.nodes[c].replica, brute[c])
+
+
+def test_block_mode_restore_resumes_at_block_boundary():
+    cfg = configs.scaled(_random_cfg(7, NB=96, R=6, steps=30), fail_node=(0, 1), fail_step=19)
+    ring = OracleRing(cfg, schedules=_small_sched(cfg, 70), mode="blocks")
+    ring.run(check_every=1)
+    (_, t, coord, t_star, restored, ids, n_new) = ring.events[0]
+    assert t_star == 18 and all(ln % 16 == 0 for _, ln in restored)
+    for (p, s), n in ring.serving.items():
+        check_content(ring, n, s)          # I4: resumed stage == failure-free content
