@@ -32,7 +32,8 @@
 // Host-side phase counters of kv_run_steps (seconds, cumulative; kv_host_profile).
 #include <chrono>
 namespace {
-enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue, kPhN };
+enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue,
+       kPhAcquire, kPhHostCopy, kPhH2DCall, kPhN };
 double g_phase[kPhN];
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -284,6 +285,7 @@ struct kv_pool {
   std::vector<uint32_t> rel_stamp, app_stamp;  // per-slot call stamps (validation)
   uint32_t call_id = 0;
   std::vector<int64_t> scratch_ids;
+  std::vector<int> scratch_slot;  // slot of each append entry found by validation (-1: new)
   std::vector<KvTask> scratch_tasks;
   // state
   bool dead = false;
@@ -373,12 +375,14 @@ int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, lon
   const int B = p->g.block_size;
   long long need_blocks = 0, need_slots = 0, tokens = 0;
   p->scratch_ids.clear();
+  p->scratch_slot.resize(a.n > 0 ? a.n : 0);
   for (int i = 0; i < a.n; ++i) {
     const int64_t r = a.req_ids[i];
     const int n = a.n_new[i];
     if (n < 0) return fail(KV_EINVAL, "negative n_new");
     long long cur = 0;
     const int s = p->slot_of.find(r);
+    p->scratch_slot[i] = s;
     if (s >= 0) {
       if (p->app_stamp[s] == cid)
         return fail(KV_EINVAL, "request %lld twice in one append", (long long)r);
@@ -438,7 +442,7 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<
   int row = 0;
   for (int i = 0; i < a.n; ++i) {
     const int64_t r = a.req_ids[i];
-    int s = p->slot_of.find(r);
+    int s = p->scratch_slot[i];  // looked up by append_validate (releases cannot alias it)
     if (s < 0) {
       s = p->free_slots.take_min();
       p->slot_of.insert(r, s);
@@ -703,9 +707,14 @@ struct Launch {
 int choose_task_segs(const kv_pool *p, long long total_segs) {
   const int maxs = std::max(1, 32768 / p->seg_bytes);
   const long long slots = (long long)resident_ctas(p->device < 0 ? 0 : p->device);
+  static int min_segs = -1;  // experiment knob KVRING_MIN_TASK_SEGS (default 16)
+  if (min_segs < 0) {
+    const char *e = getenv("KVRING_MIN_TASK_SEGS");
+    min_segs = (e && atoi(e) > 0) ? atoi(e) : 16;
+  }
   long long t = (total_segs + slots - 1) / std::max(1LL, slots);
   t = (t + 15) & ~15LL;
-  t = std::max<long long>(std::min(maxs, 16), t);
+  t = std::max<long long>(std::min(maxs, min_segs), t);
   return (int)std::min<long long>(maxs, t);
 }
 
@@ -871,8 +880,11 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
   size_t total = 0;
   for (int i = 0; i < nl; ++i) total += align16(ls[i]->staged_bytes());
   StageBuf *b = nullptr;
+  const double ta = now_s();
   int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
   if (rc) return rc;
+  const double tb = now_s();
+  g_phase[kPhAcquire] += tb - ta;
   size_t off = 0;
   for (int i = 0; i < nl; ++i) {
     Launch &L = *ls[i];
@@ -894,7 +906,10 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
     L.tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
     off += align16(L.staged_bytes());
   }
+  const double tc = now_s();
+  g_phase[kPhHostCopy] += tc - tb;
   CU(cudaMemcpyAsync(b->dev, b->host, total, cudaMemcpyHostToDevice, st));
+  g_phase[kPhH2DCall] += now_s() - tc;
   *out = b;
   return KV_OK;
 }
