@@ -67,6 +67,18 @@ def parse():
     return ap.parse_args()
 
 
+def bench_config(n_gpus):
+    """The workload (BASELINE.json configs[1]) as the bench line's `config` -- identical
+    for the kvring arm and the reference (oracle) arm."""
+    from kvgen import configs
+    c = configs.C2
+    g = c.geom
+    return {"workload": CFG_NAME, "pipelines": n_gpus, "stages_per_pipeline": c.stages,
+            "layers_per_stage": g.layers, "kv_heads": g.kv_heads, "head_dim": g.head_dim,
+            "block_size": g.block_size, "batch_per_pipeline": c.batch_cap,
+            "placement": "(p+s) mod N"}
+
+
 def traffic_ref(kind):
     """Captured DRAM traffic per launch (profiles/traffic.json, from ncu --set full)."""
     try:
@@ -363,14 +375,12 @@ def run_kvring(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (ShareGPT-shaped lognormal trace, closed-form KV words)",
-        "config": {"workload": CFG_NAME, "pipelines": N, "stages_per_pipeline": S,
-                   "layers_per_stage": g.layers, "kv_heads": g.kv_heads, "head_dim": g.head_dim,
-                   "block_size": g.block_size, "batch_per_pipeline": cfg.batch_cap,
-                   "placement": "(p+s) mod N", "timed_steps": [t_timed0, t_timed0 + args.steps - 1],
-                   "streams": "single" if args.single_stream else "compute+replication",
-                   "l2": "inputs > L2 (pre-generated sources %.1f GiB, pools %.1f GiB/GPU); the "
-                         "replicated slices were just written by append, as in serving"
-                         % (src_bytes / 2**30, pool_gib)},
+        "config": bench_config(N),
+        "run": {"timed_steps": [t_timed0, t_timed0 + args.steps - 1],
+                "streams": "single" if args.single_stream else "compute+replication",
+                "l2": "inputs > L2 (pre-generated sources %.1f GiB, pools %.1f GiB/GPU); the "
+                      "replicated slices were just written by append, as in serving"
+                      % (src_bytes / 2**30, pool_gib)},
         "gb_s_per_gpu": round(value / N, 2),
         "replicated_bytes": int(tot_bytes),
         "step_overhead_us": {"median": round(statistics.median(rep_us), 2),
@@ -918,11 +928,13 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
             "steps": n, "warmup": 0, "ms_per_step": round(dt / n * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": CFG_NAME, "pipelines": 1, "stages_per_pipeline": 4},
+            "data": "synthetic (ShareGPT-shaped lognormal trace, closed-form KV words)",
+            "impl": "reference",
+            "config": bench_config(args.gpus),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{n} steps from step {args.prelude} of {CFG_NAME}; "
-                                       f"host has {cores} cores"},
+                             "sample": f"{n} steps from step {args.prelude} of {CFG_NAME} "
+                                       f"(one pipeline; the oracle as it stands, numpy, one "
+                                       f"thread); host has {cores} cores"},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -99,14 +99,24 @@ __device__ __forceinline__ void copy_task(const KvTask &tk, const char *__restri
   }
 }
 
+// Release-only RMW (every CTA's count); the CTA that completes a pool then
+// issues an acquire fence before its release store of seq (synchronises with
+// every earlier release in the counter's RMW chain).
 __device__ __forceinline__ unsigned long long atom_add_release(unsigned long long *p,
                                                                unsigned long long v, bool sys) {
   unsigned long long old;
   if (sys)
-    asm volatile("atom.add.acq_rel.sys.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    asm volatile("atom.add.release.sys.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   else
-    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
   return old;
+}
+
+__device__ __forceinline__ void fence_acquire(bool sys) {
+  if (sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v, bool sys) {
@@ -173,8 +183,10 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
       const bool sys = pp.sys_scope != 0;
       const unsigned long long old =
           atom_add_release(pp.counter, (unsigned long long)s_cnt[i], sys);
-      if (old + (unsigned long long)s_cnt[i] == pp.target)
+      if (old + (unsigned long long)s_cnt[i] == pp.target) {
+        fence_acquire(sys);
         st_release(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
+      }
     }
   }
 }
@@ -257,6 +269,7 @@ __global__ void __launch_bounds__(kThreads) kv_unpack_kernel(const char *__restr
   if (threadIdx.x == 0 && s_cnt > 0) {
     const unsigned long long old = atom_add_release(counter, (unsigned long long)s_cnt, true);
     if (old + (unsigned long long)s_cnt == pp.target) {
+      fence_acquire(true);
       st_release(reinterpret_cast<unsigned long long *>(meta), pp.step, true);
       *counter = 0ull;  // per-call counter: the next unpack is stream-ordered after this one
     }

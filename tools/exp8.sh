@@ -1,7 +1,7 @@
 mkdir -p gpurun_out; python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
 timeout 300 python -m pytest tests -m gpu -x -q -k "not multigpu and not configs" > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
 B="python bench.py --no-cpu-baseline --e2e-steps 0 --no-restore --nccl-steps 0 --bulk-reps 0 --interference-steps 0 --block-steps 0 --steps 400"
-for v in "X=1" "KVRING_MIN_TASK_SEGS=128" "KVRING_MIN_TASK_SEGS=64" "X=2"; do
+for v in "X=1" "KVRING_CTAS_PER_SM=2" "KVRING_CTAS_PER_SM=3" "KVRING_CTAS_PER_SM=1"; do
   echo "== $v" >> gpurun_out/exp8.log
   env $v timeout 300 $B 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['ring_put_kernel_us'], d['roofline']['frac']); print(d['host_us_per_step'])" >> gpurun_out/exp8.log 2>&1
 done
