@@ -322,8 +322,8 @@ def run_kvring(args):
 
     # ---- restore: fail stage 2 of pipeline 0, restore into a fresh pool ---------
     restore = None
-    if not args.no_restore and world == 1:
-        restore = run_restore(drv, rt, t, dev, comp)
+    if not args.no_restore:
+        restore = run_restore(drv, rt, t, dev, comp, world)
 
     # ---- bulk leg (C5: 32k-token prefill per stage, full-block re-seed) -----------
     pool_gib = rt.n_slots * 2 * rt.replica_bytes / 2**30
@@ -809,34 +809,54 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
             "seq_readback_ok": ok}
 
 
-def run_restore(drv, rt, t, dev, stream):
-    """Fail stage 2 of pipeline 0 after the last step; restore its pool + block table
-    from its successor's replica into a fresh pool on the same GPU (local HBM path)."""
+def run_restore(drv, rt, t, dev, stream, world=1):
+    """Fail stage 2 of pipeline 0 after the last step and restore its pool + block table
+    from its successor's replica into a fresh pool: on the holder's GPU at N = 1 (local
+    HBM), on the NEXT GPU at N > 1 (the replica is read over NVLink: a remote restore)."""
     import torch
+    import torch.distributed as dist
     from paper_2601_22438_b200 import kvring as K
     torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     f = drv.coords[(0, 2)]
     holder = rt.succ[f]
     rt.fail(f, stream)
     dst = drv.next_node
     drv.next_node += 1
-    rt.new_node(dst, rt.placement[holder])
+    dst_rank = rt.placement[holder] if world == 1 else (rt.placement[holder] + 1) % world
+    rt.new_node(dst, dst_rank)
     torch.cuda.synchronize(dev)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    K.kv_time_next_launch(a, b)
-    w0 = time.perf_counter()
-    t_star, restored = rt.restore(dst, holder, stream)
-    torch.cuda.synchronize(dev)
-    wall_ms = (time.perf_counter() - w0) * 1e3
-    kern_ms = a.elapsed_time(b)
-    tok = sum(ln for _, ln in restored)
-    R = tok * rt.g.layers * 2 * rt.g.kv_heads * rt.g.head_dim * 2
+    if world > 1:
+        dist.barrier()
+    res = torch.zeros(5, dtype=torch.float64, device=dev)
+    if dst in rt.local:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        K.kv_time_next_launch(a, b)
+        w0 = time.perf_counter()
+        t_star, restored = rt.restore(dst, holder, stream)
+        torch.cuda.synchronize(dev)
+        wall_ms = (time.perf_counter() - w0) * 1e3
+        tok = sum(ln for _, ln in restored)
+        R = tok * rt.g.layers * 2 * rt.g.kv_heads * rt.g.head_dim * 2
+        res = torch.tensor([wall_ms, a.elapsed_time(b), float(t_star), float(len(restored)),
+                            float(R)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(res, op=dist.ReduceOp.SUM)   # only dst's rank contributes
+    wall_ms, kern_ms, t_star, nreq, R = [float(x) for x in res.tolist()]
     hbm_peak, _ = peaks()
-    gbs = 2 * R / (kern_ms * 1e-3) / 1e9
-    return {"ms": round(wall_ms, 3), "kernel_ms": round(kern_ms, 3), "t_star": int(t_star),
-            "requests": len(restored), "restored_bytes": int(R),
-            "kernel_gb_s_rw": round(gbs, 1), "frac_hbm": round(gbs / hbm_peak, 4),
-            "path": "local HBM (fresh pool on the holder's GPU)"}
+    out = {"ms": round(wall_ms, 3), "kernel_ms": round(kern_ms, 3), "t_star": int(t_star),
+           "requests": int(nreq), "restored_bytes": int(R)}
+    if world == 1:
+        gbs = 2 * R / (kern_ms * 1e-3) / 1e9
+        out.update(kernel_gb_s_rw=round(gbs, 1), frac_hbm=round(gbs / hbm_peak, 4),
+                   path="local HBM (fresh pool on the holder's GPU)")
+    else:
+        gbs = R / (kern_ms * 1e-3) / 1e9
+        out.update(kernel_gb_s_nvlink=round(gbs, 1), frac_nvlink=round(gbs / NVLINK_PEAK_GBS, 4),
+                   path="remote: fresh pool on GPU %d reads the holder's replica on GPU %d "
+                        "over NVLink" % (dst_rank, rt.placement[holder]))
+    return out
 
 
 # --------------------------------------------------------------------------- CPU arms
