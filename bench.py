@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-restore", action="store_true")
     ap.add_argument("--bulk-reps", type=int, default=5, help="C5 bulk re-seed reps (0: skip)")
-    ap.add_argument("--interference-steps", type=int, default=60,
+    ap.add_argument("--interference-steps", type=int, default=100,
                     help="steps with a Llama-3.1-8B stage decode proxy on the compute stream, "
                          "replication on vs off (0: skip)")
     ap.add_argument("--block-steps", type=int, default=100,
@@ -302,17 +302,17 @@ def run_kvring(args):
         e2e = run_e2e(args, drv, rt, t, comp, repl, content, dev, world)
         t += args.e2e_steps
 
-    # ---- interference with a decode proxy (NEXT-4; the paper's overhead, P:95-99) ----
-    interference = None
-    if args.interference_steps > 0:
-        interference = run_interference(args, drv, rt, t, comp, repl, content, dev, world)
-        t += 2 * args.interference_steps
-
     # ---- NCCL comparison (a6): same workload, pack -> count -> send/recv -> unpack ---
     nccl = None
     if args.nccl_steps > 0:
         nccl = run_nccl(args, drv, rt, t, comp, content, dev, world)
         t += args.nccl_steps
+
+    # ---- interference with a decode proxy (NEXT-4; the paper's overhead, P:95-99) ----
+    interference = None
+    if args.interference_steps > 0:
+        interference = run_interference(args, drv, rt, t, comp, repl, content, dev, world)
+        t += 2 * args.interference_steps
 
     # ---- block-granular mode (NEXT-2): completed blocks only ---------------------
     block = None
@@ -567,27 +567,36 @@ def run_interference(args, drv, rt, t0, comp, repl, content, dev, world):
         return K.PreparedSteps([dict(append=app, repl_pools=handles if replicate else [],
                                      step=tt)])
 
-    out = {}
+    # alternate blocks of BLK steps with and without replication so clock / thermal drift
+    # cancels; the first step of an "on" block also publishes the previous "off" block's
+    # backlog (counted against replication: conservative)
+    BLK = 10
+    per = {"on": [], "off": []}
     torch.cuda.synchronize(dev)
-    for phase, replicate in (("on", True), ("off", False)):
-        base = t0 + (0 if replicate else n)
-        preps = [prep(base + k, replicate) for k in range(n)]
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        for k in range(n):
-            ev[k].record(comp)
-            proxy.replay()
-            K.kv_run_steps(preps[k], comp.cuda_stream, repl.cuda_stream)
-        fin = torch.cuda.Event()
-        fin.record(repl)
-        comp.wait_event(fin)
-        ev[n].record(comp)
-        torch.cuda.synchronize(dev)
-        per = [ev[k].elapsed_time(ev[k + 1]) * 1e3 for k in range(n)]
-        out[phase] = {"median_us": round(statistics.median(per), 2),
-                      "mean_us": round(sum(per) / n, 2)}
+    k = 0
+    while k < 2 * n:
+        for phase, replicate in (("on", True), ("off", False)):
+            m = min(BLK, 2 * n - k)
+            if m <= 0:
+                break
+            preps = [prep(t0 + k + i, replicate) for i in range(m)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(m + 1)]
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            for i in range(m):
+                ev[i].record(comp)
+                proxy.replay()
+                K.kv_run_steps(preps[i], comp.cuda_stream, repl.cuda_stream)
+            fin = torch.cuda.Event()
+            fin.record(repl)
+            comp.wait_event(fin)
+            ev[m].record(comp)
+            torch.cuda.synchronize(dev)
+            per[phase].extend(ev[i].elapsed_time(ev[i + 1]) * 1e3 for i in range(m))
+            k += m
+    out = {ph: {"median_us": round(statistics.median(v), 2), "mean_us": round(sum(v) / len(v), 2),
+                "steps": len(v)} for ph, v in per.items()}
     a, b = out["on"]["median_us"], out["off"]["median_us"]
     return {"proxy": "Llama-3.1-8B stage decode proxy: %d stages x %d layers of bf16 GEMMs at "
                      "batch 64 (CUDA graph) on the compute stream" % (len(nodes), rt.g.layers),
@@ -595,7 +604,7 @@ def run_interference(args, drv, rt, t0, comp, repl, content, dev, world):
             "overhead_us": round(a - b, 2), "overhead_pct": round(100.0 * (a - b) / b, 3),
             "paper": "+2.3 % avg / +2.8 % p99 latency (8 A10 nodes), +4.0 % / +3.6 % (16) "
                      "over 1 Gbps, P:99 -- context, not the target",
-            "steps": n}
+            "steps": 2 * n, "blocks_of": BLK}
 
 
 def run_block_mode(args, drv, rt, t0, comp, repl, content, dev, world):

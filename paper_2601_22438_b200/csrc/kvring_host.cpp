@@ -774,6 +774,8 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
     KvPoolParams &pp = L.params[k];
     pp.src = static_cast<const char *>(args[k].src_kv);
     pp.dst = p->pool;
+    pp.src_bytes = (unsigned long long)rows * p->token_bytes;
+    pp.dst_bytes = (unsigned long long)p->NB * p->block_bytes;
     if ((args[k].flags & KV_SRC_HOST) && rows > 0) {
       L.host_src[k] = args[k].src_kv;
       L.host_src_bytes[k] = (size_t)rows * p->token_bytes;
@@ -828,6 +830,8 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.src = p->pool;
     pp.dst = p->succ_replica;
     pp.meta = p->succ_meta;
+    pp.src_bytes = (unsigned long long)p->NB * p->block_bytes;
+    pp.dst_bytes = (unsigned long long)p->succ_replica_blocks * p->block_bytes;
     pp.counter = p->counter;
     pp.target = aborting || p->abort_after >= 0 ? ~0ull : p->issued + (unsigned long long)L.ntask[k];
     pp.step = step;
@@ -1107,6 +1111,8 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
     std::memset(&pp, 0, sizeof pp);
     pp.src = static_cast<const char *>(holder_replica);
     pp.dst = dst->pool;
+    pp.src_bytes = (unsigned long long)holder_replica_blocks * dst->block_bytes;
+    pp.dst_bytes = (unsigned long long)dst->NB * dst->block_bytes;
     const size_t pbytes = sizeof pp, tbytes = sizeof(KvTask) * tasks.size();
     StageBuf *b = nullptr;
     int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + tbytes, true, &b);
@@ -1207,6 +1213,8 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
   fill_pub_table(p, hb + h.slot_off);
   pp.src = p->pool;
   pp.dst = static_cast<char *>(packed) + h.payload_off;
+  pp.src_bytes = (unsigned long long)p->NB * p->block_bytes;
+  pp.dst_bytes = h.payload_bytes;
   std::memcpy(hb + head, &pp, pbytes);
   std::memcpy(hb + head + pbytes, tasks.data(), tbytes);
   CU(cudaMemcpyAsync(packed, hb, head, cudaMemcpyHostToDevice, st));

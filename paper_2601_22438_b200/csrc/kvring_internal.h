@@ -47,6 +47,8 @@ struct alignas(16) KvPoolParams {
   int32_t max_reqs, max_blk, writer_node, publish;
   int32_t sys_scope;           // successor is an NVLink peer: system-scope fences / release
   int32_t pad0, pad1, pad2;
+  unsigned long long src_bytes;  // extent of src / dst (debug bounds checks, KV_BOUNDS_CHECK)
+  unsigned long long dst_bytes;
 };
 
 struct KvGeomDev {

@@ -73,9 +73,29 @@ __device__ __forceinline__ unsigned slice_off(const KvGeomDev &g, int s, int n_t
 // a round are issued before its stores (8 x 16 B in flight per thread).
 template <int SRC, int DST>
 __device__ __forceinline__ void copy_task(const KvTask &tk, const char *__restrict__ src,
-                                          char *__restrict__ dst, const KvGeomDev &g) {
+                                          char *__restrict__ dst, const KvGeomDev &g,
+                                          unsigned long long src_bytes,
+                                          unsigned long long dst_bytes) {
   const char *sb = src + item_base<SRC>(g, tk.src_unit, tk.tok_lo);
   char *db = dst + item_base<DST>(g, tk.dst_unit, tk.tok_lo);
+#ifdef KV_BOUNDS_CHECK
+  // debug builds: every 16-B access must stay inside its buffer (compute-sanitizer
+  // is not available on this pool); a violation traps the kernel
+  const long long sbase = item_base<SRC>(g, tk.src_unit, tk.tok_lo);
+  const long long dbase = item_base<DST>(g, tk.dst_unit, tk.tok_lo);
+  if (tk.seg_count > 0 && threadIdx.x == 0) {
+    const int last = tk.seg_begin + tk.seg_count - 1;
+    for (int s2 : {tk.seg_begin, last}) {
+      if (sbase < 0 || (unsigned long long)(sbase + slice_off<SRC>(g, s2, tk.n_tok) + g.seg_bytes) > src_bytes ||
+          dbase < 0 || (unsigned long long)(dbase + slice_off<DST>(g, s2, tk.n_tok) + g.seg_bytes) > dst_bytes ||
+          tk.n_tok <= 0 || tk.tok_lo + tk.n_tok > g.block_size)
+        __trap();
+    }
+  }
+#else
+  (void)src_bytes;
+  (void)dst_bytes;
+#endif
   const int nchunks = tk.seg_count << g.cps_shift;
   const int cmask = (1 << g.cps_shift) - 1;
   for (int base = 0; base < nchunks; base += kThreads * kUnroll) {
@@ -206,7 +226,7 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
     const KvPoolParams &pp = params[tk.pool];
-    copy_task<SRC, DST>(tk, pp.src, pp.dst, g);
+    copy_task<SRC, DST>(tk, pp.src, pp.dst, g, pp.src_bytes, pp.dst_bytes);
   }
   if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools);
 }
@@ -255,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) kv_unpack_kernel(const char *__restr
   const KvTask *tasks = reinterpret_cast<const KvTask *>(packed + h->task_off);
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
-    copy_task<kPacked, kPaged>(tk, pp.src, pp.dst, g);
+    copy_task<kPacked, kPaged>(tk, pp.src, pp.dst, g, ~0ull, ~0ull);
     if (tk.flags & kPoolFirst) write_parity_table(pp);
     if (threadIdx.x == 0) {
       if ((tk.flags & kFirst) && tk.slot >= 0) {

@@ -27,10 +27,11 @@ class NcclRing:
         self.recv_bufs = {}
         self.cap = max_packed_bytes
 
-    def _buf(self, table, key):
+    def _buf(self, table, key, need: int = 0):
+        """Per-link buffer of at least max(cap, need) bytes (grown on demand)."""
         b = table.get(key)
-        if b is None:
-            b = torch.empty(self.cap, dtype=torch.uint8, device=self.dev)
+        if b is None or b.numel() < need:
+            b = torch.empty(max(self.cap, need), dtype=torch.uint8, device=self.dev)
             table[key] = b
         return b
 
@@ -43,8 +44,8 @@ class NcclRing:
         sizes = {}
         with torch.cuda.stream(s):
             for n in out_nodes:
-                buf = self._buf(self.send_bufs, n)
-                sizes[n] = K.kv_pack_step(rt.handle(n), t, buf, self.cap, s.cuda_stream)
+                buf = self._buf(self.send_bufs, n, K.kv_pack_bytes(rt.handle(n)))
+                sizes[n] = K.kv_pack_step(rt.handle(n), t, buf, buf.numel(), s.cuda_stream)
             # links whose successor lives on this GPU never leave it: unpack directly
             for n in out_nodes:
                 m = rt.succ[n]
@@ -78,7 +79,7 @@ class NcclRing:
                 ops.append(dist.P2POp(dist.isend, self.send_bufs[n][:sizes[n]], rt.placement[m]))
             for m in remote_in:
                 (n,) = preds[m]
-                rb = self._buf(self.recv_bufs, m)
+                rb = self._buf(self.recv_bufs, m, counts[m])
                 ops.append(dist.P2POp(dist.irecv, rb[:counts[m]], rt.placement[n]))
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
