@@ -355,3 +355,51 @@ def test_block_mode_with_failure_bit_exact(seed):
         assert all(ln % 16 == 0 for _, ln in drv.events[0].data["restored"])
     finally:
         rt.destroy()
+
+
+def test_restore_errors_and_edge_cases():
+    """KV_ENOREPLICA for a holder that published nothing (seq 0) or whose memory is
+    poisoned (seq all-ones); KV_ENOMEM (all-or-nothing) for a too-small target;
+    empty and zero-token appends; publish-only steps keep seq moving."""
+    from paper_2601_22438_b200 import kvring as K
+    cfg = configs.scaled(configs.C1, stages=3, n_steps=1)
+    rt, drv = make_gpu(cfg, spares=2)
+    try:
+        h0, h1, h2 = rt.handle(0), rt.handle(1), rt.handle(2)
+        # nothing published yet: node 1 holds node 0's (empty) replica with seq 0
+        with pytest.raises(K.KvError) as e:
+            rt.restore(2, 1)
+        assert e.value.code == K.KV_ENOREPLICA
+        g = cfg.geom
+        src = torch.from_numpy(content_tokens(CONTENT_SEED, [5] * 40, range(40), 0, g.layers,
+                                              g.kv_heads, g.head_dim).view(np.int16)).cuda()
+        K.kv_append(h0, [], [], None)                       # empty append: no-op
+        K.kv_append(h0, [5], [40], src)
+        K.kv_append(h0, [5], [0], None)                     # zero tokens for a live request
+        assert K.kv_query(h0, 5) == (40, [0, 1, 2])
+        K.kv_replicate_step(h0, 1)
+        K.kv_replicate_step(h0, 2)                          # nothing dirty: publish-only
+        torch.cuda.synchronize()
+        assert rt.read_meta(1)["seq"] == 2
+        # restore into a pool too small for the 3 blocks: all-or-nothing ENOMEM
+        small = K.kv_pool_create(K.kv_pool_desc_t(rt.kg, 2, 4, 8, 0, 99, 2,
+                                                  rt.slots[3].pool.data_ptr(),
+                                                  rt.slots[3].replica.data_ptr(),
+                                                  rt.slots[3].meta.data_ptr()))
+        with pytest.raises(K.KvError) as e:
+            K.kv_restore(small, rt.replica_ptr(1), rt.NB, rt.meta_ptr(1))
+        assert e.value.code == K.KV_ENOMEM
+        assert K.kv_stats(small)["live_reqs"] == 0 and K.kv_stats(small)["free_blocks"] == 2
+        K.kv_pool_destroy(small)
+        # a poisoned holder (its memory is lost): ENOREPLICA
+        rt.fail(1)
+        torch.cuda.synchronize()
+        with pytest.raises(K.KvError) as e:
+            K.kv_restore(h2, rt.replica_ptr(1), rt.NB, rt.meta_ptr(1))
+        assert e.value.code == K.KV_ENOREPLICA
+        with pytest.raises(K.KvError) as e:
+            K.kv_append(h0, [5], [1], src)                   # h0 still alive: fine ...
+            K.kv_replicate_step(rt.handle(1), 3)            # ... but the dead pool refuses
+        assert e.value.code == K.KV_ESTATE
+    finally:
+        rt.destroy()
