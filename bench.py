@@ -475,6 +475,50 @@ def run_bulk(args, rank, world, local_rank, dev, group):
         ms_max, tot = ms, float(D)
     # sampled check: the last published seq on this GPU's replica metadata
     seq_ok = all(int(rt.read_meta(n)["seq"]) == args.bulk_reps + 1 for n in nodes)
+    # gather-pack (a4) and unpack (the NCCL receiver's scatter, a6) of the same bulk
+    # payload, each a separate HBM-bound kernel (N = 1: the successor is local)
+    pack = None
+    if world == 1:
+        bufs = {n: torch.empty(P * g.token_bytes + (8 << 20), dtype=torch.uint8, device=dev)
+                for n in nodes}
+        tp, tu = [], []
+        step = args.bulk_reps + 2
+        for rep in range(3):
+            for n in nodes:
+                rt.set_succ(n, succ[n])
+            torch.cuda.synchronize(dev)
+            sizes, evp, evu = {}, [], []
+            for n in nodes:           # kernel-only events (descriptor staging excluded)
+                e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                K.kv_time_next_launch(e[0], e[1])
+                sizes[n] = K.kv_pack_step(rt.handle(n), step, bufs[n], bufs[n].numel(),
+                                          comp.cuda_stream)
+                evp.append(e)
+            for n in nodes:
+                m = succ[n]
+                e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                K.kv_time_next_launch(e[0], e[1])
+                K.kv_unpack(bufs[n], sizes[n], rt.local[m].replica, rt.NB, rt.local[m].meta,
+                            rt.kg, rt.R, rt.M, comp.cuda_stream)
+                evu.append(e)
+            torch.cuda.synchronize(dev)
+            step += 1
+            if rep > 0:
+                tp.append(sum(x.elapsed_time(y) for x, y in evp))
+                tu.append(sum(x.elapsed_time(y) for x, y in evu))
+        pack_ok = all(int(rt.read_meta(n)["seq"]) == step - 1 for n in nodes)
+        hbm_peak, _ = peaks()
+        mp, mu = statistics.median(tp), statistics.median(tu)
+        pack = {"gather_pack": {"ms": round(mp, 4), "gb_s_rw": round(2 * D / (mp * 1e-3) / 1e9, 1),
+                                "frac_hbm": round(2 * D / (mp * 1e-3) / 1e9 / hbm_peak, 4),
+                                "kernels": len(nodes), "what": "sum of the gather-pack kernel times of "
+                                "every stage (CUDA events around each kernel), paged -> contiguous"},
+                "unpack": {"ms": round(mu, 4), "gb_s_rw": round(2 * D / (mu * 1e-3) / 1e9, 1),
+                           "frac_hbm": round(2 * D / (mu * 1e-3) / 1e9 / hbm_peak, 4),
+                           "kernels": len(nodes), "what": "sum of the unpack kernel times (into each "
+                           "successor's replica + publish), contiguous -> paged"},
+                "seq_ok": pack_ok}
+        del bufs
     rt.destroy()
     hbm_peak, src_peak = peaks()
     per_gpu = D / (ms * 1e-3) / 1e9
@@ -494,7 +538,8 @@ def run_bulk(args, rank, world, local_rank, dev, group):
             "bytes_per_link": int(P * g.token_bytes), "kernel_ms_median": round(ms, 4),
             "kernel_ms_max_over_ranks": round(ms_max, 4),
             "replicated_gb_s_total": round(tot / (ms_max * 1e-3) / 1e9, 1),
-            "roofline": roof, "reps": args.bulk_reps, "seq_ok": seq_ok}
+            "roofline": roof, "reps": args.bulk_reps, "seq_ok": seq_ok,
+            "pack_unpack": pack}
 
 
 class DecodeProxy:

@@ -1264,9 +1264,13 @@ KV_API int kv_unpack(const void *packed, size_t packed_bytes, void *replica,
   gd.block_size = g->block_size;
   gd.cps_shift = __builtin_ctz(seg / 16);
   const int grid = copy_grid(dev, (int)std::max<size_t>(1, packed_bytes / 32768 + 1));
+  cudaStream_t ust = static_cast<cudaStream_t>(stream);
+  cudaEvent_t eb = g_ev_before, ea = g_ev_after;  // kv_time_next_launch applies here too
+  g_ev_before = g_ev_after = nullptr;
+  if (eb) CU(cudaEventRecord(eb, ust));
   CU(launch_unpack(static_cast<const char *>(packed), static_cast<char *>(replica),
-                   static_cast<char *>(replica_meta), ctx->unpack_counter, gd, grid,
-                   static_cast<cudaStream_t>(stream)));
+                   static_cast<char *>(replica_meta), ctx->unpack_counter, gd, grid, ust));
+  if (ea) CU(cudaEventRecord(ea, ust));
   g_launches++;
   return KV_OK;
 }
