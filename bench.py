@@ -62,6 +62,9 @@ def parse():
                     help="steps replicated through the NCCL send/recv comparison (0: skip)")
     ap.add_argument("--timeline", action="store_true",
                     help="diagnostic: time every step and print the replication-stream timeline")
+    ap.add_argument("--loop", default="streams", choices=["fused", "streams"],
+                    help="fused: kv_run_steps_fused (append k + publication k-1 per launch, one "
+                         "stream); streams: kv_run_steps (append stream + replication stream)")
     ap.add_argument("--single-stream", action="store_true",
                     help="append and replicate on one stream (default: replication stream)")
     return ap.parse_args()
@@ -243,6 +246,10 @@ def run_kvring(args):
             if timing and (args.timeline or (tt - t0) % TIME_EVERY == 0):
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
+                if args.timeline:
+                    ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                    st.update(ev_append_start=ea[0], ev_append_end=ea[1])
+                    ev = ev + ea
                 evs.append(ev)
             steps.append(st)
         return K.PreparedSteps(steps), evs
@@ -250,7 +257,10 @@ def run_kvring(args):
     warm, _ = prepare(t, args.warmup, False)
     timed, evs = prepare(t + args.warmup, args.steps, True)
     torch.cuda.synchronize(dev)
-    K.kv_run_steps(warm, comp.cuda_stream, repl.cuda_stream)
+    if args.loop == "fused":
+        K.kv_run_steps_fused(warm, comp.cuda_stream)
+    else:
+        K.kv_run_steps(warm, comp.cuda_stream, repl.cuda_stream)
     t += args.warmup
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -270,7 +280,10 @@ def run_kvring(args):
         torch.cuda.synchronize(dev)
         w0 = time.perf_counter()
         start.record(comp)
-        K.kv_run_steps(timed, comp.cuda_stream, repl.cuda_stream)
+        if args.loop == "fused":
+            K.kv_run_steps_fused(timed, comp.cuda_stream)
+        else:
+            K.kv_run_steps(timed, comp.cuda_stream, repl.cuda_stream)
         fin = torch.cuda.Event()
         fin.record(repl)
         comp.wait_event(fin)
@@ -282,17 +295,17 @@ def run_kvring(args):
     launches = K.kv_kernel_launch_count() - l0
     host_prof = {k: round(v / args.steps * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}
     ms = start.elapsed_time(end)
+    kern_us = [e[1].elapsed_time(e[2]) * 1e3 for e in evs]
+    rep_us = kern_us if args.loop == "fused" else [e[0].elapsed_time(e[2]) * 1e3 for e in evs]
     if args.timeline and rank == 0:
-        rows = [(start.elapsed_time(a) * 1e3, start.elapsed_time(b) * 1e3, start.elapsed_time(c) * 1e3)
-                for a, b, c in evs]
-        print("TIMELINE us (call, kernel_start, kernel_end) per step; host wall %.1f us/step" %
-              (wall / args.steps * 1e6), file=sys.stderr)
-        for k, (a, b, c) in enumerate(rows[:60]):
-            gap = a - rows[k - 1][2] if k else 0.0
-            print("  step %3d call %8.1f kstart %8.1f kend %8.1f  kern %6.1f  gap_from_prev %6.1f"
-                  % (k, a, b, c, c - b, gap), file=sys.stderr)
-    rep_us = [a.elapsed_time(c) * 1e3 for a, b, c in evs]
-    kern_us = [b.elapsed_time(c) * 1e3 for a, b, c in evs]
+        T = lambda e: start.elapsed_time(e) * 1e3
+        print("TIMELINE us: append [start,end] (compute stream) | ring-put [start,end] "
+              "(replication stream); host wall %.1f us/step" % (wall / args.steps * 1e6),
+              file=sys.stderr)
+        for k, e in enumerate(evs[:80]):
+            a0, a1 = (T(e[3]), T(e[4])) if len(e) > 3 else (0, 0)
+            print("  step %3d  append %8.1f %8.1f (%5.1f)  ringput %8.1f %8.1f (%5.1f)"
+                  % (k, a0, a1, a1 - a0, T(e[1]), T(e[2]), T(e[2]) - T(e[1])), file=sys.stderr)
     step_bytes = {n: K.kv_stats(rt.handle(n))["bytes_replicated"] - bytes0[n] for n in local_nodes}
     my_bytes = float(sum(step_bytes.values()))
 
@@ -346,10 +359,33 @@ def run_kvring(args):
     hbm_peak, peak_src = peaks()
     med_kern = statistics.median(kern_us)
     avg_kern = sum(kern_us) / len(kern_us)
+    if args.loop == "fused":
+        # kv_step_fused_kernel: append of step k (D_k read from the dense source + D_k
+        # written into the pool) and publication of step k-1 (D_{k-1} read + written);
+        # over the timed run appended bytes == published bytes == my_bytes, in K+1 launches
+        n_launch = args.steps + 1
+        kname = "kv_step_fused_kernel"
+        if N == 1:
+            per = 4 * my_bytes / n_launch
+            achieved = per / (avg_kern * 1e-6) / 1e9
+            roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(achieved / hbm_peak, 4), "traffic": None, "kernel": kname,
+                    "peak_source": peak_src, "algorithmic_bytes_per_launch": int(per),
+                    "avg_launch_us": round(avg_kern, 2),
+                    "what": "append k (D r+w) + publication k-1 (D r+w) per launch, HBM"}
+        else:
+            per = my_bytes / n_launch
+            achieved = per / (avg_kern * 1e-6) / 1e9
+            roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
+                    "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                    "kernel": kname,
+                    "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
+                    "algorithmic_bytes_per_launch": int(per), "avg_launch_us": round(avg_kern, 2),
+                    "what": "NVLink bytes of the publication part per launch"}
     # ring-put algorithmic bytes per launch: D read + D written (HBM at N=1; at N>1
     # the write crosses NVLink -- reported against the NVLink per-direction peak)
-    per_launch = my_bytes / args.steps
-    if N == 1:
+    elif N == 1:
+        per_launch = my_bytes / args.steps
         achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
         tr = traffic_ref("decode_step")
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -363,6 +399,7 @@ def run_kvring(args):
                 "algorithmic_bytes_per_launch": int(2 * per_launch),
                 "avg_launch_us": round(avg_kern, 2)}
     else:
+        per_launch = my_bytes / args.steps
         achieved = per_launch / (avg_kern * 1e-6) / 1e9
         roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
@@ -383,15 +420,22 @@ def run_kvring(args):
                       % (src_bytes / 2**30, pool_gib)},
         "gb_s_per_gpu": round(value / N, 2),
         "replicated_bytes": int(tot_bytes),
+        "loop": args.loop,
         "step_overhead_us": {"median": round(statistics.median(rep_us), 2),
                              "p99": round(float(np.percentile(rep_us, 99)), 2),
                              "budget_us": 400.0, "tpot_ms": 20.0,
+                             "fused_loop_note": ("with the fused loop this is the whole fused "
+                                                 "launch (append + publication); the replication "
+                                                 "overhead proper is the interference leg")
+                             if args.loop == "fused" else None,
                              "what": "replication-stream device time per step (ring-put kernel incl. "
                                      "its launch; the step's descriptors are staged with one H2D before "
                                      "the append), CUDA events by kv_run_steps on every %d-th timed "
                                      "step" % TIME_EVERY},
-        "ring_put_kernel_us": {"median": round(med_kern, 2), "avg": round(avg_kern, 2),
-                               "sampled_launches": len(kern_us)},
+        "kernel_us": {"kernel": "kv_step_fused_kernel" if args.loop == "fused"
+                      else "kv_ring_put_kernel",
+                      "median": round(med_kern, 2), "avg": round(avg_kern, 2),
+                      "sampled_launches": len(kern_us)},
         "roofline": roof,
         "gpu_launches": int(tot_launch),
         "wall_s_timed": round(wall, 3),

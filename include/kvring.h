@@ -189,8 +189,19 @@ typedef struct {
   kv_pool_t *const *repl_pools;
   uint64_t step;
   void *ev_call, *ev_kernel_start, *ev_kernel_end, *ev_done;
+  void *ev_append_start, *ev_append_end;  /* optional: around the append kernel (append_stream) */
 } kv_step_t;
 int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream, void *repl_stream);
+
+/* Single-stream, software-pipelined form of the same loop: launch k carries the
+ * append of step k AND the publication of step k-1 in ONE kernel (their slots are
+ * disjoint: the publication reads positions < len_{k-1} of live requests, the append
+ * writes positions >= len_{k-1} or blocks quarantined >= 1 step, reading R7); one
+ * more launch publishes step n-1.  Same work as kv_run_steps with half the launches
+ * and no cross-stream event; each publication trails its append by one launch (the
+ * overlap of replication with the next step of P:229).  ev_kernel_start/end of step
+ * k bracket launch k; ev_call, ev_done, ev_append_* are ignored. */
+int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream);
 
 /* Re-protection after a failure (§8(f) NEXT-1; §3.2: "replication targets
  * will be automatically adjusted to exclude the nodes under traffic rerouting").

@@ -1387,7 +1387,13 @@ int issue_step(const kv_step_t &st, StepPrep &sp, cudaStream_t sa, cudaStream_t 
   if ((rc = stage(ctx, ls, nl, sa, &b))) return rc;  // one H2D for both launches
   double t1 = now_s();
   g_phase[kPhStage] += t1 - t0;
-  if (sp.has_a && (rc = enqueue(sp.A, sa))) return rc;
+  if (sp.has_a) {
+    g_ev_before = static_cast<cudaEvent_t>(st.ev_append_start);
+    g_ev_after = static_cast<cudaEvent_t>(st.ev_append_end);
+    rc = enqueue(sp.A, sa);
+    g_ev_before = g_ev_after = nullptr;
+    if (rc) return rc;
+  }
   if (sb && (rc = ctx->done(sb, sa))) return rc;
   double t2 = now_s();
   g_phase[kPhEnqA] += t2 - t1;
@@ -1498,4 +1504,167 @@ KV_API int kv_plan_targets(int32_t n_nodes, const int32_t *succ, const uint8_t *
     }
   }
   return KV_OK;
+}
+
+// ---- software-pipelined decode loop (single stream) --------------------------
+namespace {
+
+struct FusedPrep {
+  Launch A, P;        // append of step k, publication of step k-1
+  bool has_a = false, has_p = false;
+  int rc = KV_OK;
+  std::string err;
+};
+
+// Prepare launch k: the publication of step k-1 FIRST (its dirty ranges end at
+// len_{k-1}), then the append of step k (which moves len on).
+void prepare_fused(const kv_step_t *steps, int n_steps, int k, FusedPrep &fp) {
+  fp.rc = KV_OK;
+  fp.has_p = k >= 1 && steps[k - 1].n_repl > 0;
+  fp.has_a = k < n_steps && steps[k].n_append > 0;
+  if (fp.has_p) {
+    const kv_step_t &pv = steps[k - 1];
+    if ((fp.rc = prepare_replicate(pv.n_repl, pv.repl_pools, pv.step, fp.P))) {
+      fp.err = g_err;
+      return;
+    }
+    commit_replicate(fp.P, pv.repl_pools, pv.step);
+  }
+  if (fp.has_a && (fp.rc = prepare_append(steps[k].n_append, steps[k].append, fp.A))) {
+    fp.err = g_err;
+    return;
+  }
+  if (fp.has_a && fp.has_p && fp.A.p0->device != fp.P.p0->device) {
+    fp.rc = fail(KV_EINVAL, "append and publication of one launch must share a device");
+    fp.err = g_err;
+  }
+}
+
+// One H2D: [A params | P params] [P tables] [A tasks | P tasks]; P tasks keep
+// pool indices local to P (the kernel offsets its params pointer).
+int stage_fused(DeviceCtx *ctx, FusedPrep &fp, cudaStream_t st, StageBuf **out,
+                const KvPoolParams **params_dev, const KvTask **tasks_dev) {
+  Launch &A = fp.A, &P = fp.P;
+  const int na = fp.has_a ? A.n_pools : 0, np = fp.has_p ? P.n_pools : 0;
+  const size_t pbytes = align16(sizeof(KvPoolParams) * (size_t)(na + np));
+  const size_t tbl = fp.has_p ? align16(P.tables.size()) : 0;
+  const size_t nta = fp.has_a ? A.tasks.size() : 0, ntp = fp.has_p ? P.tasks.size() : 0;
+  const size_t total = pbytes + tbl + sizeof(KvTask) * (nta + ntp);
+  StageBuf *b = nullptr;
+  const double ta = now_s();
+  int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
+  if (rc) return rc;
+  const double tb = now_s();
+  g_phase[kPhAcquire] += tb - ta;
+  char *h = b->host, *d = b->dev;
+  for (int k = 0; k < np; ++k) {
+    P.params[k].slot_req = reinterpret_cast<const int64_t *>(d + pbytes + P.table_off[k]);
+    P.params[k].slot_len =
+        reinterpret_cast<const int32_t *>(d + pbytes + P.table_off[k] + 8 * (size_t)P.params[k].max_reqs);
+  }
+  if (na) std::memcpy(h, A.params.data(), sizeof(KvPoolParams) * na);
+  if (np) std::memcpy(h + sizeof(KvPoolParams) * na, P.params.data(), sizeof(KvPoolParams) * np);
+  if (tbl) std::memcpy(h + pbytes, P.tables.data(), P.tables.size());
+  if (nta) std::memcpy(h + pbytes + tbl, A.tasks.data(), sizeof(KvTask) * nta);
+  if (ntp) std::memcpy(h + pbytes + tbl + sizeof(KvTask) * nta, P.tasks.data(), sizeof(KvTask) * ntp);
+  const double tc = now_s();
+  g_phase[kPhHostCopy] += tc - tb;
+  CU(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, st));
+  g_phase[kPhH2DCall] += now_s() - tc;
+  *params_dev = reinterpret_cast<const KvPoolParams *>(d);
+  *tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
+  *out = b;
+  return KV_OK;
+}
+
+int issue_fused(const kv_step_t *ev_step, FusedPrep &fp, cudaStream_t st) {
+  kv_pool *p0 = fp.has_a ? fp.A.p0 : (fp.has_p ? fp.P.p0 : nullptr);
+  if (!p0 || p0->device < 0) return KV_OK;
+  DeviceGuard dg(p0->device);
+  DeviceCtx *ctx = ctx_for(p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  StageBuf *sb = nullptr, *b = nullptr;
+  int rc = KV_OK;
+  double t0 = now_s();
+  if (fp.has_a && (rc = stage_host_sources(ctx, fp.A, st, &sb))) return rc;
+  const KvPoolParams *pd = nullptr;
+  const KvTask *td = nullptr;
+  if ((rc = stage_fused(ctx, fp, st, &b, &pd, &td))) return rc;
+  double t1 = now_s();
+  g_phase[kPhStage] += t1 - t0;
+  const int na = fp.has_a ? fp.A.n_pools : 0, np = fp.has_p ? fp.P.n_pools : 0;
+  const int nta = fp.has_a ? (int)fp.A.tasks.size() : 0;
+  const int ntot = nta + (fp.has_p ? (int)fp.P.tasks.size() : 0);
+  if (ntot > 0) {
+    if (ev_step && ev_step->ev_kernel_start)
+      CU(cudaEventRecord(static_cast<cudaEvent_t>(ev_step->ev_kernel_start), st));
+    CU(launch_fused(td, nta, ntot, pd, na, np, p0->geom_dev(), copy_grid(p0->device, ntot), st));
+    if (ev_step && ev_step->ev_kernel_end)
+      CU(cudaEventRecord(static_cast<cudaEvent_t>(ev_step->ev_kernel_end), st));
+    g_launches++;
+    p0->kernels++;
+  }
+  if (sb && (rc = ctx->done(sb, st))) return rc;
+  rc = ctx->done(b, st);
+  g_phase[kPhEnqA] += now_s() - t1;
+  return rc;
+}
+
+}  // namespace
+
+// Single-stream, software-pipelined decode loop: launch k carries the append of
+// step k AND the publication of step k-1 (disjoint slots, see kv_step_fused_kernel),
+// a last launch publishes step n-1.  Same work as kv_run_steps, half the launches,
+// no cross-stream event; the publication of a step trails its append by one launch
+// -- the overlap of replication with the next step's compute of P:229.
+KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream) {
+  if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n_launch = n_steps + 1;  // + the flush of the last publication
+  if (n_steps < 8) {
+    thread_local FusedPrep fp;
+    for (int k = 0; k < n_launch; ++k) {
+      prepare_fused(steps, n_steps, k, fp);
+      if (fp.rc) return fp.rc;
+      int rc = issue_fused(k < n_steps ? &steps[k] : nullptr, fp, st);
+      if (rc) return rc;
+    }
+    return KV_OK;
+  }
+  FusedPrep ring[2];
+  std::atomic<int> produced{0}, consumed{0};
+  std::atomic<bool> stop{false};
+  std::thread worker([&]() {
+    for (int k = 0; k < n_launch && !stop.load(std::memory_order_acquire); ++k) {
+      const double w0 = now_s();
+      while (k - consumed.load(std::memory_order_acquire) >= 2) {
+        if (stop.load(std::memory_order_acquire)) return;
+        std::this_thread::yield();
+      }
+      g_phase[kPhWaitIssue] += now_s() - w0;
+      const double t0 = now_s();
+      prepare_fused(steps, n_steps, k, ring[k & 1]);
+      g_phase[kPhPrepare] += now_s() - t0;
+      produced.store(k + 1, std::memory_order_release);
+      if (ring[k & 1].rc) return;
+    }
+  });
+  int rc = KV_OK;
+  for (int k = 0; k < n_launch; ++k) {
+    const double w0 = now_s();
+    while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
+    g_phase[kPhWaitPrep] += now_s() - w0;
+    FusedPrep &fp = ring[k & 1];
+    if (fp.rc) {
+      rc = fp.rc;
+      g_err = fp.err;
+      break;
+    }
+    rc = issue_fused(k < n_steps ? &steps[k] : nullptr, fp, st);
+    consumed.store(k + 1, std::memory_order_release);
+    if (rc) break;
+  }
+  stop.store(true, std::memory_order_release);
+  worker.join();
+  return rc;
 }

@@ -119,6 +119,43 @@ __device__ __forceinline__ void copy_task(const KvTask &tk, const char *__restri
   }
 }
 
+// Paged destination with a runtime source layout (dense token-major for the
+// append part of a fused step, paged for its ring-put part): one loop body, so
+// the fused kernel keeps the 64-register budget of the single-role kernels.
+__device__ __forceinline__ void copy_task_dyn(const KvTask &tk, const char *__restrict__ src,
+                                              char *__restrict__ dst, const KvGeomDev &g,
+                                              bool src_tokmajor) {
+  const char *sb = src + (src_tokmajor ? item_base<kTokMajor>(g, tk.src_unit, tk.tok_lo)
+                                       : item_base<kPaged>(g, tk.src_unit, tk.tok_lo));
+  char *db = dst + item_base<kPaged>(g, tk.dst_unit, tk.tok_lo);
+  const int nchunks = tk.seg_count << g.cps_shift;
+  const int cmask = (1 << g.cps_shift) - 1;
+  const unsigned tstride = src_tokmajor ? (unsigned)g.token_bytes : (unsigned)g.seg_bytes;
+  const unsigned cstride = src_tokmajor ? (unsigned)g.seg_bytes
+                                        : (unsigned)(g.block_size * g.seg_bytes);
+  for (int base = 0; base < nchunks; base += kThreads * kUnroll) {
+    uint4 v[kUnroll];
+    unsigned doff[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int c = base + u * kThreads + (int)threadIdx.x;
+      if (c < nchunks) {
+        const int s = tk.seg_begin + (c >> g.cps_shift);
+        const unsigned lc = (unsigned)(c & cmask) << 4;
+        const int combo = s / tk.n_tok;
+        const int tok = s - combo * tk.n_tok;
+        doff[u] = (unsigned)(combo * g.block_size + tok) * (unsigned)g.seg_bytes + lc;
+        v[u] = ld_stream(sb + (unsigned)tok * tstride + (unsigned)combo * cstride + lc);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int c = base + u * kThreads + (int)threadIdx.x;
+      if (c < nchunks) st_stream(db + doff[u], v[u]);
+    }
+  }
+}
+
 // Release-only RMW (every CTA's count); the CTA that completes a pool then
 // issues an acquire fence before its release store of seq (synchronises with
 // every earlier release in the counter's RMW chain).
@@ -244,6 +281,27 @@ KV_KERNEL(kv_restore_remap_kernel, kPaged, kPaged, false)      // a8: replica ->
 KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false)       // a4: NCCL-variant sender
 #undef KV_KERNEL
 
+// Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
+// append of step k (tasks [0, n_append), pools params[0, n_app_pools)) and the
+// publication of step k-1 (tasks [n_append, n_tasks), pools params[n_app_pools..),
+// task pool indices local to each part).  The two parts touch disjoint slots
+// (positions >= len_{k-1} or blocks quarantined >= 1 step vs dirty positions
+// < len_{k-1}, reading R7), so they need no ordering; the task branch is uniform
+// per CTA.  The publication pass runs over the ring-put part only.
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_step_fused_kernel(const KvTask *__restrict__ tasks, int n_append, int n_tasks,
+                         const KvPoolParams *__restrict__ params, int n_app_pools,
+                         KvGeomDev g, int n_rep_pools) {
+  const KvPoolParams *rparams = params + n_app_pools;
+  for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
+    const KvTask tk = tasks[t];
+    const bool app = t < n_append;
+    const KvPoolParams &pp = app ? params[tk.pool] : rparams[tk.pool];
+    copy_task_dyn(tk, pp.src, pp.dst, g, app);
+  }
+  if (n_rep_pools > 0) publish_pass(tasks + n_append, n_tasks - n_append, rparams, n_rep_pools);
+}
+
 // Receiver of the NCCL comparison: parameters come from the packed header on
 // the device, so the receiving host never reads the buffer.  The counter is
 // per call (reset by the publishing CTA), not monotone.
@@ -367,6 +425,16 @@ cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPool
     default:
       return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const KvPoolParams *params,
+                         int n_app_pools, int n_rep_pools, const KvGeomDev &g, int grid,
+                         cudaStream_t stream) {
+  if (n_tasks <= 0) return cudaSuccess;
+  if (n_rep_pools > kMaxPoolsPerLaunch) return cudaErrorInvalidValue;
+  kv_step_fused_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_append, n_tasks, params,
+                                                       n_app_pools, g, n_rep_pools);
   return cudaGetLastError();
 }
 

@@ -27,7 +27,7 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
-            "kv_plan_targets", "kv_set_mode"]
+            "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused"]
 
 
 class KvError(RuntimeError):
@@ -63,7 +63,8 @@ class kv_step_t(ctypes.Structure):
                 ("n_repl", ctypes.c_int32), ("repl_pools", ctypes.c_void_p),
                 ("step", ctypes.c_uint64), ("ev_call", ctypes.c_void_p),
                 ("ev_kernel_start", ctypes.c_void_p), ("ev_kernel_end", ctypes.c_void_p),
-                ("ev_done", ctypes.c_void_p)]
+                ("ev_done", ctypes.c_void_p), ("ev_append_start", ctypes.c_void_p),
+                ("ev_append_end", ctypes.c_void_p)]
 
 
 class kv_stats_t(ctypes.Structure):
@@ -121,6 +122,7 @@ def lib() -> ctypes.CDLL:
             "kv_sync": (ctypes.c_int, [_P]),
             "kv_time_next_launch": (ctypes.c_int, [_P, _P]),
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
+            "kv_run_steps_fused": (ctypes.c_int, [_I32, _P, _P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_set_mode": (ctypes.c_int, [_P, _I32]),
@@ -238,7 +240,8 @@ class PreparedSteps:
             pools = st.get("repl_pools", [])
             parr = (_P * max(1, len(pools)))(*pools)
             self.keep.extend([app, keep, parr])
-            ev = [st.get(x) for x in ("ev_call", "ev_kernel_start", "ev_kernel_end", "ev_done")]
+            ev = [st.get(x) for x in ("ev_call", "ev_kernel_start", "ev_kernel_end", "ev_done",
+                                      "ev_append_start", "ev_append_end")]
             self.keep.append(ev)
             self.arr[k] = kv_step_t(len(st.get("append", [])), ctypes.addressof(app), len(pools),
                                     ctypes.addressof(parr), int(st.get("step", 0)),
@@ -259,6 +262,10 @@ def _event_handle(e):
 def kv_run_steps(prepared: "PreparedSteps", append_stream: int = 0, repl_stream: int = 0) -> None:
     _check(lib().kv_run_steps(prepared.n, ctypes.addressof(prepared.arr), append_stream,
                               repl_stream))
+
+
+def kv_run_steps_fused(prepared: "PreparedSteps", stream: int = 0) -> None:
+    _check(lib().kv_run_steps_fused(prepared.n, ctypes.addressof(prepared.arr), stream))
 
 
 def kv_replicate_step(p: int, step: int, stream: int = 0) -> None:

@@ -403,3 +403,39 @@ def test_restore_errors_and_edge_cases():
         assert e.value.code == K.KV_ESTATE
     finally:
         rt.destroy()
+
+
+@pytest.mark.parametrize("n_steps", [6, 30])
+def test_run_steps_fused_bit_exact(n_steps):
+    """kv_run_steps_fused (append of step k + publication of step k-1 in one launch,
+    final flush): whole arrays == oracle after the run (6 steps: inline path, 30:
+    helper-thread path)."""
+    from paper_2601_22438_b200 import kvring as K
+    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=6, n_requests=60, n_steps=n_steps, fixed_prompt=None,
+                         fail_node=None, fail_step=None)
+    sched = _churn_sched(cfg, 31)
+    rt, drv = make_gpu(cfg, schedules=sched)
+    oring = OracleRing(cfg, schedules=sched)
+    try:
+        steps, keep = [], []
+        for t in range(cfg.n_steps):
+            app = []
+            for node, e in drv.plan(t).items():
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = drv.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+            pools = [rt.handle(n) for n in rt.alive_local()] if t >= 1 else []
+            steps.append(dict(append=app, repl_pools=pools, step=t))
+            oring.appends(t)
+            if t >= 1:
+                oring.replicate(t)
+        prep = K.PreparedSteps(steps)
+        torch.cuda.synchronize()
+        K.kv_run_steps_fused(prep, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        compare_state(rt, drv, oring, tag="fused")
+    finally:
+        rt.destroy()

@@ -174,3 +174,35 @@ def test_plan_targets_matches_oracle_ring_walk():
     changed = {coords[k] for k in range(16) if got[k] != base[k] and coords[k] not in excl}
     assert changed == {(1, 1), (3, 2)}
     assert got[idx[(1, 1)]] == idx[(0, 1)] and got[idx[(3, 2)]] == idx[(2, 2)]
+
+
+def test_run_steps_fused_tables_match_oracle():
+    """The software-pipelined loop's host side (tables-only pools): after the final
+    flush every table and the payload byte count equal the oracle's at C2 size."""
+    cfg = configs.C2
+    ring = OracleRing(cfg, content=False)
+    sched = ring.sched
+    hs = {c: _pool(cfg, k) for k, c in enumerate(ring.coords)}
+    for c in ring.coords:
+        K.kv_set_successor(hs[c], 0, FAKE_PTR, cfg.num_blocks, FAKE_PTR)
+    try:
+        steps = []
+        for t in range(150):
+            ring.appends(t)
+            if t >= 1:
+                ring.replicate(t)
+            ev = sched[0].steps[t]
+            app = [dict(pool=hs[c], begin_step=1, release=ev.retire,
+                        req_ids=sorted(ev.decode) + [r for r, _ in ev.admit],
+                        n_new=[1] * len(ev.decode) + [pp for _, pp in ev.admit], src=None)
+                   for c in ring.coords]
+            steps.append(dict(append=app, repl_pools=[hs[c] for c in ring.coords] if t >= 1 else [],
+                              step=t))
+        K.kv_run_steps_fused(K.PreparedSteps(steps))
+        for c in ring.coords:
+            assert _tables(hs[c], cfg.max_reqs) == ring.nodes[c].live()
+            assert K.kv_stats(hs[c])["last_step"] == 149
+        assert sum(K.kv_stats(hs[c])["bytes_replicated"] for c in ring.coords) == ring.moved
+    finally:
+        for h in hs.values():
+            K.kv_pool_destroy(h)
