@@ -15,7 +15,7 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("n,transport", [(2, "p2p"), (2, "nccl"), (4, "p2p")])
+@pytest.mark.parametrize("n,transport", [(2, "p2p"), (2, "nccl"), (4, "p2p"), (4, "nccl"), (8, "p2p")])
 def test_ring_over_nvlink_parity(n, transport):
     """p2p: fused ring-put over NVLink; nccl: the comparison transport (bit-exact too)."""
     if _ngpu() < n:
