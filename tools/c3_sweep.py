@@ -1,0 +1,103 @@
+"""C3 (BASELINE.json configs[2]) replication cost vs load: two 4-stage Llama-3.1-8B
+pipelines, open-loop Poisson arrivals on a 20 ms logical decode step (§4
+"Poisson distribution under different parameters of request rate"), cap 128 per
+pipeline, ring within each pipeline.  For each RPS the decode loop runs 200 prelude
+steps then 300 steps through kv_run_steps; reported per RPS: mean live requests,
+replicated MB per step, ring-put kernel time and replication-stream time per step
+(CUDA events), against the 400 us budget (2 % of a 20 ms TPOT).  One GPU (8 logical
+nodes); with torchrun the pipelines spread over the ranks as in bench.py.
+
+    python tools/c3_sweep.py [--rps 1,2,4,8,16,32] [--steps 300]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def run(rps, steps, prelude, dev):
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED
+    from kvgen.cuda import content_tokens_cuda
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    cfg = configs.scaled(configs.C3, rps=rps, num_blocks=6144, max_reqs=256)
+    I, S = cfg.pipelines, cfg.stages
+    g = cfg.geom
+    coords = {(p, s): p * S + s for p in range(I) for s in range(S)}
+    placement = {n: 0 for n in coords.values()}
+    succ = {coords[(p, s)]: coords[(p, (s + 1) % S)] for (p, s) in coords}
+    scheds = configs.build_schedules(cfg, n_steps=prelude + steps + 2)
+    rt = RingRuntime(g, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement, succ,
+                     device=dev.index, spares=0, sentinel=None)
+
+    def content(stage, ids, pos):
+        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim, device=dev.index)
+
+    drv = ScheduleDriver(rt, scheds, coords, content)
+    comp = torch.cuda.current_stream(dev)
+    repl = torch.cuda.Stream(dev)
+    for t in range(prelude):
+        drv.append_step(t, stream=comp)
+        if t >= 1:
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            repl.wait_event(ev)
+            rt.replicate_all(t, stream=repl)
+    torch.cuda.synchronize(dev)
+    handles = [rt.handle(n) for n in rt.alive_local()]
+    steps_l, evs, live = [], [], []
+    for t in range(prelude, prelude + steps):
+        plan = drv.plan(t)
+        app = []
+        for node, e in plan.items():
+            ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+            app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                            req_ids=e["req_ids"], n_new=e["n_new"],
+                            src=content(e["stage"], ids, pos) if ids else None))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        evs.append(ev)
+        steps_l.append(dict(append=app, repl_pools=handles, step=t, ev_call=ev[0],
+                            ev_kernel_start=ev[1], ev_kernel_end=ev[2]))
+        live.append(sum(len(sc.steps[t].decode) + len(sc.steps[t].admit) for sc in scheds))
+    prep = K.PreparedSteps(steps_l)
+    b0 = sum(K.kv_stats(h)["bytes_replicated"] for h in handles)
+    torch.cuda.synchronize(dev)
+    K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
+    torch.cuda.synchronize(dev)
+    by = sum(K.kv_stats(h)["bytes_replicated"] for h in handles) - b0
+    kern = [b.elapsed_time(c) * 1e3 for a, b, c in evs]
+    call = [a.elapsed_time(c) * 1e3 for a, b, c in evs]
+    rt.destroy()
+    return {"rps": rps, "live_requests_mean": round(float(np.mean(live)), 1),
+            "replicated_mb_per_step": round(by / steps / 2**20, 3),
+            "ring_put_us": {"median": round(statistics.median(kern), 2),
+                            "p99": round(float(np.percentile(kern, 99)), 2)},
+            "replication_stream_us_per_step": {"median": round(statistics.median(call), 2),
+                                               "p99": round(float(np.percentile(call, 99)), 2)},
+            "budget_us": 400.0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rps", default="1,2,4,8,16,32")
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--prelude", type=int, default=200)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    out = [run(float(r), a.steps, a.prelude, dev) for r in a.rps.split(",")]
+    print(json.dumps({"workload": "c3_2x4_poisson (2 pipelines x 4 stages, 1 GPU, 20 ms "
+                                  "logical step, cap 128)", "sweep": out}))
+
+
+if __name__ == "__main__":
+    main()
