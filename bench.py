@@ -62,7 +62,7 @@ def parse():
                     help="steps replicated through the NCCL send/recv comparison (0: skip)")
     ap.add_argument("--timeline", action="store_true",
                     help="diagnostic: time every step and print the replication-stream timeline")
-    ap.add_argument("--loop", default="streams", choices=["fused", "streams"],
+    ap.add_argument("--loop", default="streams", choices=["fused", "streams", "pdl"],
                     help="fused: kv_run_steps_fused (append k + publication k-1 per launch, one "
                          "stream); streams: kv_run_steps (append stream + replication stream)")
     ap.add_argument("--single-stream", action="store_true",
@@ -243,7 +243,8 @@ def run_kvring(args):
                    for node, e in plan.items() if node in rt.local]
             pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
             st = dict(append=app, repl_pools=pools if tt >= 1 else [], step=tt)
-            if timing and (args.timeline or (tt - t0) % TIME_EVERY == 0):
+            every = 8 if args.loop == "pdl" else TIME_EVERY
+            if timing and (args.timeline or (tt - t0) % every == every - 1):
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
                 if args.timeline:
@@ -259,6 +260,8 @@ def run_kvring(args):
     torch.cuda.synchronize(dev)
     if args.loop == "fused":
         K.kv_run_steps_fused(warm, comp.cuda_stream)
+    elif args.loop == "pdl":
+        K.kv_run_steps_pdl(warm, comp.cuda_stream)
     else:
         K.kv_run_steps(warm, comp.cuda_stream, repl.cuda_stream)
     t += args.warmup
@@ -282,6 +285,8 @@ def run_kvring(args):
         start.record(comp)
         if args.loop == "fused":
             K.kv_run_steps_fused(timed, comp.cuda_stream)
+        elif args.loop == "pdl":
+            K.kv_run_steps_pdl(timed, comp.cuda_stream)
         else:
             K.kv_run_steps(timed, comp.cuda_stream, repl.cuda_stream)
         fin = torch.cuda.Event()
@@ -296,7 +301,8 @@ def run_kvring(args):
     host_prof = {k: round(v / args.steps * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}
     ms = start.elapsed_time(end)
     kern_us = [e[1].elapsed_time(e[2]) * 1e3 for e in evs]
-    rep_us = kern_us if args.loop == "fused" else [e[0].elapsed_time(e[2]) * 1e3 for e in evs]
+    rep_us = kern_us if args.loop in ("fused", "pdl") else [e[0].elapsed_time(e[2]) * 1e3
+                                                           for e in evs]
     if args.timeline and rank == 0:
         T = lambda e: start.elapsed_time(e) * 1e3
         print("TIMELINE us: append [start,end] (compute stream) | ring-put [start,end] "

@@ -203,6 +203,17 @@ int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream, v
  * k bracket launch k; ev_call, ev_done, ev_append_* are ignored. */
 int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream);
 
+/* Single-stream loop with programmatic dependent launch (PDL): per step the append
+ * and the publication kernels are launched back to back on ONE stream with the
+ * programmatic-serialization attribute and read their descriptors zero-copy from
+ * mapped pinned memory; the kernels order themselves (griddepcontrol): the
+ * publication of step k waits for append k, append k+1 overlaps it and waits for it
+ * before exiting (seq stays monotone).  Same work and results as kv_run_steps.
+ * ev_kernel_start/end and ev_append_start/end are honoured (each record is a stream
+ * operation that interrupts the overlap at that step); KV_SRC_HOST appends are not
+ * supported (KV_EINVAL). */
+int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream);
+
 /* Re-protection after a failure (§8(f) NEXT-1; §3.2: "replication targets
  * will be automatically adjusted to exclude the nodes under traffic rerouting").
  * succ[n_nodes] is the ring's successor map over logical node ids; excluded

@@ -1668,3 +1668,210 @@ KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *str
   worker.join();
   return rc;
 }
+
+// ---- single-stream decode loop with programmatic dependent launch ----------------
+namespace {
+
+// Zero-copy descriptor ring: mapped pinned host memory the kernels read over PCIe,
+// so no memcpy node sits between consecutive kernels (it would break the PDL
+// overlap).  64 slots; one completion event per group of 8 steps.
+struct ZcRing {
+  static constexpr int kSlots = 64, kGroup = 8, kGroups = kSlots / kGroup;
+  char *buf[kSlots] = {};
+  size_t cap[kSlots] = {};
+  cudaEvent_t ev[kGroups] = {};
+  bool pending[kGroups] = {};
+  int device = -1;
+};
+
+std::mutex g_zc_mu;
+std::map<int, std::unique_ptr<ZcRing>> g_zc;
+
+ZcRing *zc_for(int device) {
+  std::lock_guard<std::mutex> lk(g_zc_mu);
+  auto &p = g_zc[device];
+  if (!p) {
+    p.reset(new ZcRing());
+    p->device = device;
+  }
+  return p.get();
+}
+
+int zc_stage(ZcRing *z, int k, StepPrep &sp, const KvPoolParams **pa, const KvTask **ta,
+             const KvPoolParams **pp, const KvTask **tp) {
+  const int slot = (int)(k % ZcRing::kSlots);
+  if (k >= ZcRing::kSlots) {  // the group that last used this slot must have completed
+    const int g = (int)(((k - ZcRing::kSlots) / ZcRing::kGroup) % ZcRing::kGroups);
+    if (z->pending[g]) {
+      const double t0 = now_s();
+      CU(cudaEventSynchronize(z->ev[g]));
+      g_phase[kPhAcquire] += now_s() - t0;
+      z->pending[g] = false;
+    }
+  }
+  Launch *ls[2] = {sp.has_a ? &sp.A : nullptr, sp.has_p ? &sp.P : nullptr};
+  size_t total = 0;
+  for (Launch *L : ls)
+    if (L) total += align16(L->staged_bytes());
+  if (z->cap[0] == 0)  // first use: every slot at once (mapped allocations cost ms each)
+    for (int q = 0; q < ZcRing::kSlots; ++q) {
+      CU(cudaHostAlloc(reinterpret_cast<void **>(&z->buf[q]), (size_t)4 << 20,
+                       cudaHostAllocMapped | cudaHostAllocPortable));
+      z->cap[q] = (size_t)4 << 20;
+    }
+  if (z->cap[slot] < total) {  // rare (bulk steps): grow this slot
+    if (z->buf[slot]) cudaFreeHost(z->buf[slot]);
+    z->buf[slot] = nullptr;
+    z->cap[slot] = 0;
+    const size_t cap = std::max(total * 2, (size_t)4 << 20);
+    CU(cudaHostAlloc(reinterpret_cast<void **>(&z->buf[slot]), cap,
+                     cudaHostAllocMapped | cudaHostAllocPortable));
+    z->cap[slot] = cap;
+  }
+  const double tb = now_s();
+  char *h = z->buf[slot];  // UVA: the host address is the device address
+  size_t off = 0;
+  for (int i = 0; i < 2; ++i) {
+    Launch *L = ls[i];
+    if (!L) continue;
+    const size_t pbytes = align16(sizeof(KvPoolParams) * L->n_pools);
+    const size_t tbl = align16(L->tables.size());
+    char *b = h + off;
+    if (L->kind == kKindRingPut)
+      for (int q = 0; q < L->n_pools; ++q) {
+        L->params[q].slot_req = reinterpret_cast<const int64_t *>(b + pbytes + L->table_off[q]);
+        L->params[q].slot_len = reinterpret_cast<const int32_t *>(
+            b + pbytes + L->table_off[q] + 8 * (size_t)L->params[q].max_reqs);
+      }
+    std::memcpy(b, L->params.data(), sizeof(KvPoolParams) * L->n_pools);
+    if (!L->tables.empty()) std::memcpy(b + pbytes, L->tables.data(), L->tables.size());
+    std::memcpy(b + pbytes + tbl, L->tasks.data(), sizeof(KvTask) * L->tasks.size());
+    L->params_dev = reinterpret_cast<const KvPoolParams *>(b);
+    L->tasks_dev = reinterpret_cast<const KvTask *>(b + pbytes + tbl);
+    off += align16(L->staged_bytes());
+  }
+  g_phase[kPhHostCopy] += now_s() - tb;
+  *pa = ls[0] ? ls[0]->params_dev : nullptr;
+  *ta = ls[0] ? ls[0]->tasks_dev : nullptr;
+  *pp = ls[1] ? ls[1]->params_dev : nullptr;
+  *tp = ls[1] ? ls[1]->tasks_dev : nullptr;
+  return KV_OK;
+}
+
+int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
+  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
+  if (!p0 || p0->device < 0) return KV_OK;
+  DeviceGuard dg(p0->device);
+  ZcRing *z = zc_for(p0->device);
+  const KvPoolParams *pa = nullptr, *pp = nullptr;
+  const KvTask *ta = nullptr, *tp = nullptr;
+  const double t0 = now_s();
+  int rc = zc_stage(z, k, sp, &pa, &ta, &pp, &tp);
+  if (rc) return rc;
+  if (sp.has_a && sp.A.host_src_bytes.size()) {
+    for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q)
+      if (sp.A.host_src_bytes[q]) return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_pdl");
+  }
+  const double t1 = now_s();
+  g_phase[kPhStage] += t1 - t0;
+  if (sp.has_a && !sp.A.tasks.empty()) {
+    if (st.ev_append_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_start), s));
+    CU(launch_copy_pdl(kKindAppend, ta, (int)sp.A.tasks.size(), pa, sp.A.n_pools, p0->geom_dev(),
+                       copy_grid(p0->device, (int)sp.A.tasks.size()), s));
+    if (st.ev_append_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_end), s));
+    g_launches++;
+    p0->kernels++;
+  }
+  const double t2 = now_s();
+  g_phase[kPhEnqA] += t2 - t1;
+  if (sp.has_p && !sp.P.tasks.empty()) {
+    if (st.ev_kernel_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_start), s));
+    CU(launch_copy_pdl(kKindRingPut, tp, (int)sp.P.tasks.size(), pp, sp.P.n_pools, p0->geom_dev(),
+                       copy_grid(p0->device, (int)sp.P.tasks.size()), s));
+    if (st.ev_kernel_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_end), s));
+    g_launches++;
+    p0->kernels++;
+  }
+  if (k % ZcRing::kGroup == ZcRing::kGroup - 1) {  // completion of this group of 8 steps
+    const int g = (int)((k / ZcRing::kGroup) % ZcRing::kGroups);
+    if (!z->ev[g]) CU(cudaEventCreateWithFlags(&z->ev[g], cudaEventDisableTiming));
+    CU(cudaEventRecord(z->ev[g], s));
+    z->pending[g] = true;
+  }
+  g_phase[kPhEnqP] += now_s() - t2;
+  return KV_OK;
+}
+
+}  // namespace
+
+// Single-stream decode loop with programmatic dependent launch: per step the
+// append and the publication are launched back to back on ONE stream with the
+// PDL attribute, descriptors are read zero-copy from mapped pinned memory, and the
+// kernels order themselves with griddepcontrol (see kvring_kernels.cu): the
+// publication of step k starts as soon as append k completes and runs while append
+// k+1 copies -- the overlap the paper gets from a separate stream, without
+// a cross-stream event per step.  A helper thread prepares step k+1 meanwhile.
+KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream) {
+  if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // zero-copy slots are reused within a call only: drain the previous call's groups
+  for (int k = 0; k < n_steps && k < 1; ++k) {
+    const kv_step_t &st0 = steps[0];
+    kv_pool *q = st0.n_append > 0 ? st0.append[0].pool : (st0.n_repl > 0 ? st0.repl_pools[0] : nullptr);
+    if (q && q->device >= 0) {
+      ZcRing *z = zc_for(q->device);
+      for (int g = 0; g < ZcRing::kGroups; ++g)
+        if (z->pending[g]) {
+          CU(cudaEventSynchronize(z->ev[g]));
+          z->pending[g] = false;
+        }
+    }
+  }
+  StepPrep ring[2];
+  std::atomic<int> produced{0}, consumed{0};
+  std::atomic<bool> stop{false};
+  std::thread worker([&]() {
+    for (int k = 0; k < n_steps && !stop.load(std::memory_order_acquire); ++k) {
+      const double w0 = now_s();
+      while (k - consumed.load(std::memory_order_acquire) >= 2) {
+        if (stop.load(std::memory_order_acquire)) return;
+        std::this_thread::yield();
+      }
+      g_phase[kPhWaitIssue] += now_s() - w0;
+      const double t0 = now_s();
+      prepare_step(steps[k], ring[k & 1]);
+      g_phase[kPhPrepare] += now_s() - t0;
+      produced.store(k + 1, std::memory_order_release);
+      if (ring[k & 1].rc) return;
+    }
+  });
+  int rc = KV_OK;
+  for (int k = 0; k < n_steps; ++k) {
+    const double w0 = now_s();
+    while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
+    g_phase[kPhWaitPrep] += now_s() - w0;
+    StepPrep &sp = ring[k & 1];
+    if (sp.rc) {
+      rc = sp.rc;
+      g_err = sp.err;
+      break;
+    }
+    rc = issue_step_pdl(steps[k], k, sp, s);
+    if (!rc && k == n_steps - 1 && k % ZcRing::kGroup != ZcRing::kGroup - 1) {
+      // close the last partial group so the next call can drain it
+      kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
+      if (p0 && p0->device >= 0) {
+        DeviceGuard dg(p0->device);
+        ZcRing *z = zc_for(p0->device);
+        const int g = (k / ZcRing::kGroup) % ZcRing::kGroups;
+        if (!z->ev[g]) cudaEventCreateWithFlags(&z->ev[g], cudaEventDisableTiming);
+        if (cudaEventRecord(z->ev[g], s) == cudaSuccess) z->pending[g] = true;
+      }
+    }
+    consumed.store(k + 1, std::memory_order_release);
+    if (rc) break;
+  }
+  stop.store(true, std::memory_order_release);
+  worker.join();
+  return rc;
+}

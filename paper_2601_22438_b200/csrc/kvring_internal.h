@@ -88,6 +88,8 @@ cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPool
 cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const KvPoolParams *params,
                          int n_app_pools, int n_rep_pools, const KvGeomDev &g, int grid,
                          cudaStream_t stream);
+cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
+                            int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream);
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           unsigned long long *counter, const KvGeomDev &g, int grid,
                           cudaStream_t stream);

@@ -269,17 +269,48 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
 }
 
 // One named kernel per role (ncu / launch lists show what ran).
+// Programmatic dependent launch (PDL, kv_run_steps_pdl): both instructions are
+// no-ops for a kernel launched without the programmatic-serialization attribute.
+//  - ring-put k : wait for its append (griddepcontrol.wait: the primary grid has
+//                 completed and its writes are visible), then let append k+1 launch;
+//  - append k+1 : lets ring-put k+1 launch at once (it waits at its start), copies
+//                 (concurrently with ring-put k: disjoint slots, reading R7), then
+//                 waits for ring-put k before exiting -- so ring-put k+1, which
+//                 waits for append k+1, starts after ring-put k: seq stays monotone.
+// All CTAs of a primary are resident before its dependent launches (grids never
+// exceed the resident CTA count), so a waiting dependent cannot starve it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 #define KV_KERNEL(NAME, SRC, DST, PUB)                                                   \
   __global__ void __launch_bounds__(kThreads, kMinBlocks)                                \
       NAME(const KvTask *__restrict__ tasks, int n_tasks,                                \
            const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {          \
     run_tasks<SRC, DST, PUB>(tasks, n_tasks, params, g, n_pools);                        \
   }
-KV_KERNEL(kv_append_scatter_kernel, kTokMajor, kPaged, false)  // a2: model KV write stand-in
-KV_KERNEL(kv_ring_put_kernel, kPaged, kPaged, true)            // a4+a5: gather + ring hop + publish
 KV_KERNEL(kv_restore_remap_kernel, kPaged, kPaged, false)      // a8: replica -> new block ids
 KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false)       // a4: NCCL-variant sender
 #undef KV_KERNEL
+
+// a2: model KV write stand-in (dense -> paged)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_append_scatter_kernel(const KvTask *__restrict__ tasks, int n_tasks,
+                             const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {
+  pdl_launch_dependents();
+  run_tasks<kTokMajor, kPaged, false>(tasks, n_tasks, params, g, n_pools);
+  pdl_wait();
+}
+
+// a4+a5: fused gather + ring hop + publication
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_ring_put_kernel(const KvTask *__restrict__ tasks, int n_tasks,
+                       const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {
+  pdl_wait();
+  pdl_launch_dependents();
+  run_tasks<kPaged, kPaged, true>(tasks, n_tasks, params, g, n_pools);
+}
 
 // Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
 // append of step k (tasks [0, n_append), pools params[0, n_app_pools)) and the
@@ -436,6 +467,30 @@ cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const K
   kv_step_fused_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_append, n_tasks, params,
                                                        n_app_pools, g, n_rep_pools);
   return cudaGetLastError();
+}
+
+// Launch of the append / ring-put kernels with the programmatic stream
+// serialization attribute (PDL): the launch may overlap the previous kernel in
+// the stream; the kernels order themselves with griddepcontrol (see above).
+cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
+                            int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream) {
+  if (n_tasks <= 0) return cudaSuccess;
+  if (n_pools > kMaxPoolsPerLaunch) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (kind == kKindAppend)
+    return cudaLaunchKernelEx(&cfg, kv_append_scatter_kernel, tasks, n_tasks, params, g, n_pools);
+  if (kind == kKindRingPut)
+    return cudaLaunchKernelEx(&cfg, kv_ring_put_kernel, tasks, n_tasks, params, g, n_pools);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,

@@ -27,7 +27,7 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
-            "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused"]
+            "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused", "kv_run_steps_pdl"]
 
 
 class KvError(RuntimeError):
@@ -123,6 +123,7 @@ def lib() -> ctypes.CDLL:
             "kv_time_next_launch": (ctypes.c_int, [_P, _P]),
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_run_steps_fused": (ctypes.c_int, [_I32, _P, _P]),
+            "kv_run_steps_pdl": (ctypes.c_int, [_I32, _P, _P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_set_mode": (ctypes.c_int, [_P, _I32]),
@@ -266,6 +267,10 @@ def kv_run_steps(prepared: "PreparedSteps", append_stream: int = 0, repl_stream:
 
 def kv_run_steps_fused(prepared: "PreparedSteps", stream: int = 0) -> None:
     _check(lib().kv_run_steps_fused(prepared.n, ctypes.addressof(prepared.arr), stream))
+
+
+def kv_run_steps_pdl(prepared: "PreparedSteps", stream: int = 0) -> None:
+    _check(lib().kv_run_steps_pdl(prepared.n, ctypes.addressof(prepared.arr), stream))
 
 
 def kv_replicate_step(p: int, step: int, stream: int = 0) -> None:

@@ -439,3 +439,40 @@ def test_run_steps_fused_bit_exact(n_steps):
         compare_state(rt, drv, oring, tag="fused")
     finally:
         rt.destroy()
+
+
+@pytest.mark.parametrize("n_steps", [12, 90])
+def test_run_steps_pdl_bit_exact(n_steps):
+    """kv_run_steps_pdl (one stream, programmatic dependent launch, zero-copy
+    descriptors; append k+1 overlaps the publication of step k): whole arrays ==
+    oracle; 90 steps wrap the 64-slot descriptor ring."""
+    from paper_2601_22438_b200 import kvring as K
+    cfg = configs.scaled(configs.C1, num_blocks=160, max_reqs=16, max_blocks_per_req=12,
+                         batch_cap=8, n_requests=200, n_steps=n_steps, fixed_prompt=None,
+                         fail_node=None, fail_step=None)
+    sched = _churn_sched(cfg, 41)
+    rt, drv = make_gpu(cfg, schedules=sched)
+    oring = OracleRing(cfg, schedules=sched)
+    try:
+        steps, keep = [], []
+        for t in range(cfg.n_steps):
+            app = []
+            for node, e in drv.plan(t).items():
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = drv.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+            pools = [rt.handle(n) for n in rt.alive_local()] if t >= 1 else []
+            steps.append(dict(append=app, repl_pools=pools, step=t))
+            oring.appends(t)
+            if t >= 1:
+                oring.replicate(t)
+        torch.cuda.synchronize()
+        half = n_steps // 2            # two calls: the ring is drained between them
+        K.kv_run_steps_pdl(K.PreparedSteps(steps[:half]), torch.cuda.current_stream().cuda_stream)
+        K.kv_run_steps_pdl(K.PreparedSteps(steps[half:]), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        compare_state(rt, drv, oring, tag="pdl")
+    finally:
+        rt.destroy()
