@@ -136,3 +136,55 @@ def test_c5_bulk_replication_and_restore():
         assert np.array_equal(got, want)
     finally:
         rt.destroy()
+
+
+def test_c2_full_geometry_whole_arrays():
+    """C2 at BASELINE's full geometry in the bench's launch configuration (4 pools of
+    12,288 x 512 KiB blocks on one GPU, kv_run_steps with two streams), 160 steps:
+    whole pools, whole replica regions and metadata == the oracle in content mode.
+    The oracle holds the first 2,048 blocks (lowest-free-id allocation gives the same
+    block ids while use stays below that; asserted) and every GPU block beyond them
+    must still hold the sentinel -- no stray write anywhere in 48 GiB."""
+    from paper_2601_22438_b200 import kvring as K
+    full = configs.C2
+    steps = 160
+    small = configs.scaled(full, num_blocks=2048)
+    rt, drv = make_gpu(full)
+    oring = OracleRing(small, schedules=drv.sched)
+    try:
+        comp = torch.cuda.current_stream()
+        repl = torch.cuda.Stream()
+        sts, keep = [], []
+        for t in range(steps):
+            app = []
+            for node, e in drv.plan(t).items():
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = drv.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+            sts.append(dict(append=app, repl_pools=[rt.handle(n) for n in rt.alive_local()]
+                            if t >= 1 else [], step=t))
+            oring.appends(t)
+            if t >= 1:
+                oring.replicate(t)
+        for n in oring.nodes.values():
+            assert max([b for s in range(n.R) for b in n.slot_bt[s]] + [0]) < 2048
+        K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+        torch.cuda.synchronize()
+        sentinel = np.int16(np.uint16(0x5A5A).view(np.int16))
+        for c, gid in drv.coords.items():
+            on = oring.nodes[c]
+            slot = rt.local[gid]
+            for name, dev_arr, ora in (("primary", slot.pool, on.primary),
+                                       ("replica", slot.replica, on.replica)):
+                head = dev_arr[:2048].cpu().numpy().view(np.uint16)
+                assert np.array_equal(head, ora), f"{c} {name} differs"
+                tail_ok = bool((dev_arr[2048:] == int(sentinel)).all().item())
+                assert tail_ok, f"{c} {name}: a block beyond the used range was written"
+            meta = rt.read_meta(gid)
+            assert meta["seq"] == on.rseq
+            assert np.array_equal(meta["req"], on.rreq) and np.array_equal(meta["len"], on.rlen)
+            assert np.array_equal(meta["bt"], on.rbt)
+    finally:
+        rt.destroy()
