@@ -247,14 +247,15 @@ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
 
 cudaError_t timed_launch(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t st) {
+                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t st,
+                         const KvPoolParams *host_params = nullptr) {
   cudaEvent_t b = g_ev_before, a = g_ev_after;
   g_ev_before = g_ev_after = nullptr;
   if (b) {
     cudaError_t e = cudaEventRecord(b, st);
     if (e != cudaSuccess) return e;
   }
-  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st);
+  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st, host_params);
   if (e != cudaSuccess) return e;
   if (a) return cudaEventRecord(a, st);
   return cudaSuccess;
@@ -926,7 +927,8 @@ int enqueue(Launch &L, cudaStream_t st) {
     if (dbg_nopub) kind = kKindRestore;  // experiment knob: copy without publication
   }
   CU(timed_launch(kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
-                  L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()), st));
+                  L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()), st,
+                  L.params.data()));
   g_launches++;
   L.p0->kernels++;
   return KV_OK;

@@ -83,8 +83,17 @@ constexpr int kPackedMagic = 0x4B565042;
 // Launch wrappers (kvring_kernels.cu).  All return the cudaError_t of the launch.
 enum KernelKind : int { kKindAppend = 0, kKindRingPut = 1, kKindRestore = 2, kKindPack = 3 };
 constexpr int kMaxPoolsPerLaunchHost = 64;
+// Per-pool source / destination bases passed by value in the kernel parameter
+// space (hot kernels): the only parameters on the path to a CTA's first data load.
+constexpr int kInlinePools = 8;
+struct KvParamPack {
+  const char *src[kInlinePools];
+  char *dst[kInlinePools];
+  int n;  // 0: read them from the staged global copy
+};
 cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream);
+                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream,
+                        const KvPoolParams *host_params = nullptr);
 cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const KvPoolParams *params,
                          int n_app_pools, int n_rep_pools, const KvGeomDev &g, int grid,
                          cudaStream_t stream);

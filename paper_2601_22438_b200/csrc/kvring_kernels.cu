@@ -258,12 +258,21 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
 template <int SRC, int DST, bool PUB>
 __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
                                           const KvPoolParams *__restrict__ params,
-                                          const KvGeomDev &g, int n_pools) {
+                                          const KvGeomDev &g, int n_pools,
+                                          const KvParamPack *pk = nullptr) {
   // pass 1: the copies -- identical for every kernel, no publication state live
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
     const KvPoolParams &pp = params[tk.pool];
-    copy_task<SRC, DST>(tk, pp.src, pp.dst, g, pp.src_bytes, pp.dst_bytes);
+#ifdef KV_BOUNDS_CHECK
+    const unsigned long long sbytes = pp.src_bytes, dbytes = pp.dst_bytes;
+#else
+    const unsigned long long sbytes = 0, dbytes = 0;
+#endif
+    const bool inl = pk && pk->n;
+    const char *src = inl ? pk->src[tk.pool] : pp.src;
+    char *dst = inl ? pk->dst[tk.pool] : pp.dst;
+    copy_task<SRC, DST>(tk, src, dst, g, sbytes, dbytes);
   }
   if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools);
 }
@@ -294,22 +303,27 @@ KV_KERNEL(kv_restore_remap_kernel, kPaged, kPaged, false)      // a8: replica ->
 KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false)       // a4: NCCL-variant sender
 #undef KV_KERNEL
 
+// The hot kernels take the per-pool parameters (<= kInlinePools pools) by value in
+// the kernel's constant parameter space: no dependent global load precedes a CTA's
+// first data load (only its task descriptor).  More pools: the staged global copy.
 // a2: model KV write stand-in (dense -> paged)
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     kv_append_scatter_kernel(const KvTask *__restrict__ tasks, int n_tasks,
-                             const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {
+                             const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools,
+                             const __grid_constant__ KvParamPack pk) {
   pdl_launch_dependents();
-  run_tasks<kTokMajor, kPaged, false>(tasks, n_tasks, params, g, n_pools);
+  run_tasks<kTokMajor, kPaged, false>(tasks, n_tasks, params, g, n_pools, &pk);
   pdl_wait();
 }
 
 // a4+a5: fused gather + ring hop + publication
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     kv_ring_put_kernel(const KvTask *__restrict__ tasks, int n_tasks,
-                       const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {
+                       const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools,
+                       const __grid_constant__ KvParamPack pk) {
   pdl_wait();
   pdl_launch_dependents();
-  run_tasks<kPaged, kPaged, true>(tasks, n_tasks, params, g, n_pools);
+  run_tasks<kPaged, kPaged, true>(tasks, n_tasks, params, g, n_pools, &pk);
 }
 
 // Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
@@ -437,15 +451,26 @@ int copy_grid(int device, int n_tasks) {
 }
 
 cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream) {
+                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream,
+                        const KvPoolParams *host_params) {
   if (n_tasks <= 0) return cudaSuccess;
   if (n_pools > kMaxPoolsPerLaunch) return cudaErrorInvalidValue;
+  KvParamPack pk;
+  pk.n = 0;
+  if (host_params && n_pools <= kInlinePools) {
+    pk.n = n_pools;
+    for (int i = 0; i < n_pools; ++i) {
+      pk.src[i] = host_params[i].src;
+      pk.dst[i] = host_params[i].dst;
+    }
+  }
   switch (kind) {
     case kKindAppend:
-      kv_append_scatter_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
+      kv_append_scatter_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools,
+                                                               pk);
       break;
     case kKindRingPut:
-      kv_ring_put_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
+      kv_ring_put_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools, pk);
       break;
     case kKindRestore:
       kv_restore_remap_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
@@ -486,10 +511,13 @@ cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const Kv
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  KvParamPack pk;
+  pk.n = 0;  // the PDL loop reads parameters zero-copy
   if (kind == kKindAppend)
-    return cudaLaunchKernelEx(&cfg, kv_append_scatter_kernel, tasks, n_tasks, params, g, n_pools);
+    return cudaLaunchKernelEx(&cfg, kv_append_scatter_kernel, tasks, n_tasks, params, g, n_pools,
+                              pk);
   if (kind == kKindRingPut)
-    return cudaLaunchKernelEx(&cfg, kv_ring_put_kernel, tasks, n_tasks, params, g, n_pools);
+    return cudaLaunchKernelEx(&cfg, kv_ring_put_kernel, tasks, n_tasks, params, g, n_pools, pk);
   return cudaErrorInvalidValue;
 }
 
