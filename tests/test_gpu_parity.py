@@ -9,11 +9,11 @@ import torch
 from kvgen import configs
 from kvgen.content import CONTENT_SEED, content_tokens
 from kvgen.schedule import closed_loop_schedule
-from oracle.simulate import OracleRing, check_all
+from oracle.simulate import OracleRing
 
 pytestmark = pytest.mark.gpu
 
-from gpu_harness import compare_state, make_gpu, node_map  # noqa: E402
+from gpu_harness import compare_state, make_gpu  # noqa: E402
 
 
 def _run_both(cfg, ring="stage", schedules=None, every=1, fail=True, restore_mode=None):

@@ -5,11 +5,9 @@ the CPU oracle's tables step by step -- at full C2 / C4 geometry."""
 import os
 import re
 
-import numpy as np
 import pytest
 
 from kvgen import configs
-from oracle import OracleNode
 from oracle.simulate import OracleRing
 from paper_2601_22438_b200 import kvring as K
 

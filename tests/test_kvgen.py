@@ -1,6 +1,5 @@
 """Pins for the shared input generators (kvgen): published vectors and stated distributions."""
 import numpy as np
-import pytest
 
 from kvgen import configs
 from kvgen.content import (GOLDEN, content_keys, content_segment_table, content_tokens,

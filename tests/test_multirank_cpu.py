@@ -6,7 +6,6 @@ bench's `value` numerator) equal the oracle's."""
 import os
 import sys
 
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp

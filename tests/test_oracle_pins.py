@@ -18,10 +18,8 @@ import torch
 from kvgen import configs
 from kvgen.content import SENTINEL_WORD, POISON_WORD, content_tokens
 from kvgen.schedule import closed_loop_schedule
-from kvgen.trace import synth_trace
 from oracle import OracleNode, OracleError, instance_ring, stage_ring, plan_replication_targets
-from oracle.simulate import (OracleRing, check_all, check_content, check_replica_equals_primary,
-                             check_tables, full_copy_replay)
+from oracle.simulate import OracleRing, check_all, check_content, full_copy_replay
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_tables.json")))
 
