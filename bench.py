@@ -418,12 +418,13 @@ def run_kvring(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (ShareGPT-shaped lognormal trace, closed-form KV words)",
-        "config": bench_config(N),
-        "run": {"timed_steps": [t_timed0, t_timed0 + args.steps - 1],
-                "streams": "single" if args.single_stream else "compute+replication",
-                "l2": "inputs > L2 (pre-generated sources %.1f GiB, pools %.1f GiB/GPU); the "
-                      "replicated slices were just written by append, as in serving"
-                      % (src_bytes / 2**30, pool_gib)},
+        "config": dict(bench_config(N),
+                       l2="inputs larger than L2 (pre-generated sources %.1f GiB, pools %.1f GiB "
+                          "per GPU; no flush); the replicated slices were just written by the "
+                          "append, as in serving" % (src_bytes / 2**30, pool_gib)),
+        "dtype_note": "bf16 KV words moved bit-exactly as 16-bit data (no arithmetic)",
+        "run": {"timed_steps": [t_timed0, t_timed0 + args.steps - 1], "loop": args.loop,
+                "streams": "single" if args.single_stream else "compute+replication"},
         "gb_s_per_gpu": round(value / N, 2),
         "replicated_bytes": int(tot_bytes),
         "loop": args.loop,
