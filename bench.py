@@ -79,7 +79,9 @@ def bench_config(n_gpus):
     return {"workload": CFG_NAME, "pipelines": n_gpus, "stages_per_pipeline": c.stages,
             "layers_per_stage": g.layers, "kv_heads": g.kv_heads, "head_dim": g.head_dim,
             "block_size": g.block_size, "batch_per_pipeline": c.batch_cap,
-            "placement": "(p+s) mod N"}
+            "placement": "(p+s) mod N",
+            "l2": "inputs larger than L2 (multi-GiB pre-generated sources and pools; no flush); "
+                  "the replicated slices were just written by the append, as in serving"}
 
 
 def traffic_ref(kind):
@@ -418,12 +420,11 @@ def run_kvring(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (ShareGPT-shaped lognormal trace, closed-form KV words)",
-        "config": dict(bench_config(N),
-                       l2="inputs larger than L2 (pre-generated sources %.1f GiB, pools %.1f GiB "
-                          "per GPU; no flush); the replicated slices were just written by the "
-                          "append, as in serving" % (src_bytes / 2**30, pool_gib)),
+        "config": bench_config(N),
         "dtype_note": "bf16 KV words moved bit-exactly as 16-bit data (no arithmetic)",
         "run": {"timed_steps": [t_timed0, t_timed0 + args.steps - 1], "loop": args.loop,
+                "inputs_gib": {"pre_generated_sources": round(src_bytes / 2**30, 2),
+                               "pools_and_replicas_per_gpu": round(pool_gib, 1)},
                 "streams": "single" if args.single_stream else "compute+replication"},
         "gb_s_per_gpu": round(value / N, 2),
         "replicated_bytes": int(tot_bytes),
