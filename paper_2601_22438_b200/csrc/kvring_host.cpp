@@ -840,6 +840,8 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.writer_node = p->node_id;
     pp.publish = 1;
     pp.sys_scope = p->succ_sys ? 1 : 0;
+    static const int sys_per_cta = getenv("KVRING_SYS_PER_CTA") ? 1 : 0;  // experiments
+    pp.pad0 = sys_per_cta;
   }
   return KV_OK;
 }

@@ -238,8 +238,14 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
       if (s_cnt[i] == 0) continue;
       const KvPoolParams &pp = params[i];
       const bool sys = pp.sys_scope != 0;
-      const unsigned long long old =
-          atom_add_release(pp.counter, (unsigned long long)s_cnt[i], sys);
+      // Every CTA of this launch runs on this GPU, so the count RMW only needs GPU
+      // scope even when the stores went to an NVLink peer; the completing CTA then
+      // issues ONE system-scope acquire-release fence before its st.release.sys of
+      // seq.  Causality order is transitive (release.gpu -> acquire.gpu -> fence.sys
+      // -> release.sys), so a peer that acquires seq = t sees every CTA's stores.
+      // KVRING_SYS_PER_CTA=1 (experiments) restores a system-scope RMW per CTA.
+      const unsigned long long old = atom_add_release(
+          pp.counter, (unsigned long long)s_cnt[i], sys && (pp.pad0 & 1));
       if (old + (unsigned long long)s_cnt[i] == pp.target) {
         fence_acquire(sys);
         st_release(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
