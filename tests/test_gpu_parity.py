@@ -476,3 +476,41 @@ def test_run_steps_pdl_bit_exact(n_steps):
         compare_state(rt, drv, oring, tag="pdl")
     finally:
         rt.destroy()
+
+
+def test_self_loop_ring_and_max_length_requests():
+    """Degenerate cases: a one-stage ring (the pool's successor is itself, so it
+    replicates into its own replica region) and requests that fill exactly
+    max_blocks_per_req blocks (one more token is KV_ENOMEM, all-or-nothing)."""
+    from paper_2601_22438_b200 import kvring as K
+    M = 6
+    cfg = configs.scaled(configs.C1, stages=1, num_blocks=40, max_reqs=8, max_blocks_per_req=M,
+                         batch_cap=3, n_requests=6, n_steps=20, fixed_prompt=None,
+                         fail_node=None, fail_step=None)
+    p = np.array([M * 16 - 8, 5, M * 16 - 12, 17, 30, 2])
+    o = np.array([8, 30, 12, 3, 5, 9])              # requests 0 and 2 end at exactly M blocks
+    sched = [closed_loop_schedule(p, o, cfg.n_steps, cfg.batch_cap)]
+    rt, drv = make_gpu(cfg, schedules=sched)
+    oring = OracleRing(cfg, schedules=sched)
+    try:
+        assert rt.succ[0] == 0
+        lens = []
+        for t in range(cfg.n_steps):
+            drv.append_step(t)
+            oring.appends(t)
+            if t >= 1:
+                rt.replicate_all(t)
+                oring.replicate(t)
+            compare_state(rt, drv, oring, tag=f"self-loop {t}")
+            lens.extend(ln for _, ln, _ in oring.nodes[(0, 0)].live().values())
+        assert max(lens) == M * 16
+        h = rt.handle(0)
+        live = oring.nodes[(0, 0)].live()
+        full = [r for r, (_, ln, _) in live.items() if ln == M * 16]
+        if full:
+            with pytest.raises(K.KvError) as e:
+                K.kv_append(h, [full[0]], [1], torch.zeros(1, 2, 2, 8, 128, dtype=torch.int16,
+                                                           device="cuda"))
+            assert e.value.code == K.KV_ENOMEM
+    finally:
+        rt.destroy()
