@@ -571,6 +571,35 @@ def run_bulk(args, rank, world, local_rank, dev, group):
                            "successor's replica + publish), contiguous -> paged"},
                 "seq_ok": pack_ok}
         del bufs
+    # copy-engine variant (NEXT-4): the same full-block re-seed moved by cudaMemcpyAsync
+    # runs (zero SMs for the payload), the ring-put kernel writing the bt entries and
+    # publishing after them; events around the whole call on the stream
+    tce = []
+    step0 = args.bulk_reps + 10
+    for rep in range(args.bulk_reps + 1):
+        for n in nodes:
+            rt.set_succ(n, succ[n])
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(comp)
+        K.kv_replicate_step_ce(handles, step0 + rep, comp.cuda_stream)
+        b.record(comp)
+        torch.cuda.synchronize(dev)
+        if rep > 0:
+            tce.append(a.elapsed_time(b))
+    mce = statistics.median(tce)
+    ce_ok = all(int(rt.read_meta(n)["seq"]) == step0 + args.bulk_reps for n in nodes)
+    vce = torch.tensor([mce], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vce, op=dist.ReduceOp.MAX)
+    mce_max = float(vce[0])
+    ce = {"ms_median": round(mce, 4), "ms_max_over_ranks": round(mce_max, 4),
+          "replicated_gb_s_total": round(tot / (mce_max * 1e-3) / 1e9, 1),
+          "what": "kv_replicate_step_ce: one cudaMemcpyAsync per run of consecutive full "
+                  "blocks + the publishing ring-put kernel; events around the whole call",
+          "seq_ok": ce_ok}
     rt.destroy()
     hbm_peak, src_peak = peaks()
     per_gpu = D / (ms * 1e-3) / 1e9
@@ -591,7 +620,7 @@ def run_bulk(args, rank, world, local_rank, dev, group):
             "kernel_ms_max_over_ranks": round(ms_max, 4),
             "replicated_gb_s_total": round(tot / (ms_max * 1e-3) / 1e9, 1),
             "roofline": roof, "reps": args.bulk_reps, "seq_ok": seq_ok,
-            "pack_unpack": pack}
+            "pack_unpack": pack, "copy_engine": ce}
 
 
 class DecodeProxy:

@@ -224,6 +224,14 @@ int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream);
 int kv_plan_targets(int32_t n_nodes, const int32_t *succ, const uint8_t *excluded,
                     int32_t *targets);
 
+/* Copy-engine variant (§8(f) NEXT-4, zero-SM bulk copies): like
+ * kv_replicate_step_multi, but every FULL block of the dirty set is moved by the
+ * copy engines (consecutive block ids coalesced into one cudaMemcpyAsync, peer
+ * capable); partial blocks still go through the ring-put kernel, which is
+ * stream-ordered after the copies, writes all bt entries and publishes seq.  Same
+ * replica bytes and metadata as kv_replicate_step_multi. */
+int kv_replicate_step_ce(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, void *stream);
+
 /* Fault injection: the next replicate of p executes only its first
  * `tasks` copy tasks and never publishes -- a stage dying mid-step. -1 clears. */
 int kv_inject_abort(kv_pool_t *p, int32_t tasks);

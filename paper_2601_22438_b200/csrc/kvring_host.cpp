@@ -495,7 +495,8 @@ void commit_pub_len(kv_pool *p) {
 // Dirty ranges [pub_len, pub_hi) of every live slot split at block boundaries
 // (§8(a) a3); returns payload bytes.
 uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks, bool packed,
-                           int32_t *packed_unit, int task_segs) {
+                           int32_t *packed_unit, int task_segs,
+                           std::vector<int> *ce_blocks = nullptr) {
   const int B = p->g.block_size;
   uint64_t bytes = 0;
   for (int s = 0; s < p->R; ++s) {
@@ -506,7 +507,19 @@ uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks,
       const int j = pos / B, lo = pos % B;
       const int n = std::min(B - lo, len - pos);
       const int blk = p->slot_bt[s][j];
-      if (packed) {
+      if (ce_blocks && lo == 0 && n == B) {
+        // copy-engine variant: the whole block moves by cudaMemcpyAsync; the kernel
+        // only writes its bt entry (a zero-slice task) and counts it for publication
+        KvTask t{};
+        t.src_unit = t.dst_unit = blk;
+        t.pool = pidx;
+        t.slot = (int16_t)s;
+        t.j = (int16_t)j;
+        t.n_tok = (int16_t)B;
+        t.flags = kFirst;
+        tasks.push_back(t);
+        ce_blocks->push_back(blk);
+      } else if (packed) {
         push_item(tasks, pidx, blk, *packed_unit, s, j, lo, n, p->combos, task_segs);
         *packed_unit += n * p->combos;
       } else {
@@ -679,6 +692,8 @@ struct Launch {
   std::vector<uint64_t> bytes;     // replicate: payload bytes per pool
   std::vector<const void *> host_src;  // append: host sources (KV_SRC_HOST), per pool
   std::vector<size_t> host_src_bytes;
+  std::vector<std::vector<int>> ce_blocks;  // copy-engine variant: full blocks per pool
+  bool use_ce = false;
   // filled by stage()
   const KvPoolParams *params_dev = nullptr;
   const KvTask *tasks_dev = nullptr;
@@ -693,6 +708,9 @@ struct Launch {
     bytes.assign(n, 0);
     host_src.assign(n, nullptr);
     host_src_bytes.assign(n, 0);
+    if ((int)ce_blocks.size() < n) ce_blocks.resize(n);
+    for (auto &v : ce_blocks) v.clear();
+    use_ce = false;
     params_dev = nullptr;
     tasks_dev = nullptr;
   }
@@ -786,7 +804,8 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
 
 // Validates the pools and builds the dirty work list (§8(a) a3); state is
 // committed by commit_replicate once the launch is enqueued.
-int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch &L) {
+int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch &L,
+                      bool use_ce = false) {
   if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
   if (n_pools > kMaxPoolsPerLaunchHost)
     return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
@@ -806,6 +825,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
   }
   L.reset(kKindRingPut, n_pools);
   L.p0 = pools[0];
+  L.use_ce = use_ce;
   const int task_segs = choose_task_segs(L.p0, dirty * L.p0->combos);
   size_t toff = 0;
   for (int k = 0; k < n_pools; ++k) toff += 12 * (size_t)pools[k]->R;
@@ -814,7 +834,8 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = pools[k];
     const size_t before = L.tasks.size();
-    L.bytes[k] = build_dirty_tasks(p, (int16_t)k, L.tasks, false, nullptr, task_segs);
+    L.bytes[k] = build_dirty_tasks(p, (int16_t)k, L.tasks, false, nullptr, task_segs,
+                                   use_ce ? &L.ce_blocks[k] : nullptr);
     if (L.tasks.size() == before) push_publish_only(L.tasks, (int16_t)k);
     L.tasks[before].flags |= kPoolFirst;
     L.ntask[k] = (int)(L.tasks.size() - before);
@@ -937,9 +958,32 @@ int enqueue(Launch &L, cudaStream_t st) {
 
 thread_local Launch g_append_launch, g_repl_launch;
 
-int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st) {
+// Copy-engine runs of the full blocks of a ring-put launch (consecutive block ids
+// coalesced; the replica mirrors block ids, R5), issued before the kernel on the
+// same stream: the kernel's publication is stream-ordered after them.
+int issue_ce_copies(Launch &L, kv_pool *const *pools, cudaStream_t st) {
+  for (int k = 0; k < L.n_pools; ++k) {
+    std::vector<int> &v = L.ce_blocks[k];
+    if (v.empty()) continue;
+    kv_pool *p = pools[k];
+    std::sort(v.begin(), v.end());
+    size_t i = 0;
+    while (i < v.size()) {
+      size_t e = i + 1;
+      while (e < v.size() && v[e] == v[e - 1] + 1) ++e;
+      const size_t off = (size_t)v[i] * (size_t)p->block_bytes;
+      CU(cudaMemcpyAsync(p->succ_replica + off, p->pool + off,
+                         (e - i) * (size_t)p->block_bytes, cudaMemcpyDefault, st));
+      i = e;
+    }
+  }
+  return KV_OK;
+}
+
+int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st,
+                   bool use_ce = false) {
   Launch &L = g_repl_launch;
-  int rc = prepare_replicate(n_pools, pools, step, L);
+  int rc = prepare_replicate(n_pools, pools, step, L, use_ce);
   if (rc) return rc;
   if (L.p0->device < 0) {  // tables only
     commit_replicate(L, pools, step);
@@ -953,6 +997,7 @@ int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream
   Launch *ls[1] = {&L};
   rc = stage(ctx, ls, 1, st, &b);
   if (rc) return rc;
+  if (use_ce && (rc = issue_ce_copies(L, pools, st))) return rc;
   rc = enqueue(L, st);
   if (rc) return rc;
   commit_replicate(L, pools, step);
@@ -1002,6 +1047,11 @@ KV_API int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream) {
 KV_API int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step,
                                    void *stream) {
   return replicate_impl(n_pools, pools, step, static_cast<cudaStream_t>(stream));
+}
+
+KV_API int kv_replicate_step_ce(int32_t n_pools, kv_pool_t *const *pools, uint64_t step,
+                                void *stream) {
+  return replicate_impl(n_pools, pools, step, static_cast<cudaStream_t>(stream), true);
 }
 
 KV_API int kv_set_mode(kv_pool_t *p, int32_t mode) {

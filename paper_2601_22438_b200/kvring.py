@@ -27,7 +27,8 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
-            "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused", "kv_run_steps_pdl"]
+            "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused", "kv_run_steps_pdl",
+            "kv_replicate_step_ce"]
 
 
 class KvError(RuntimeError):
@@ -124,6 +125,7 @@ def lib() -> ctypes.CDLL:
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_run_steps_fused": (ctypes.c_int, [_I32, _P, _P]),
             "kv_run_steps_pdl": (ctypes.c_int, [_I32, _P, _P]),
+            "kv_replicate_step_ce": (ctypes.c_int, [_I32, _P, _U64, _P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_set_mode": (ctypes.c_int, [_P, _I32]),
@@ -284,6 +286,11 @@ def kv_replicate_step_multi(pools, step: int, stream: int = 0) -> None:
 
 def kv_set_mode(p: int, mode: int) -> None:
     _check(lib().kv_set_mode(p, mode))
+
+
+def kv_replicate_step_ce(pools, step: int, stream: int = 0) -> None:
+    arr = (_P * len(pools))(*pools)
+    _check(lib().kv_replicate_step_ce(len(pools), ctypes.addressof(arr), step, stream))
 
 
 def kv_inject_abort(p: int, tasks: int) -> None:

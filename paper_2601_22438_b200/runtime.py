@@ -59,6 +59,7 @@ class RingRuntime:
         self.succ = dict(succ)
         self.rank, self.world = rank, world
         self.mode = mode
+        self.copy_engine = False   # replicate_all through kv_replicate_step_ce (NEXT-4)
         self.device = torch.cuda.current_device() if device is None else device
         self.dev = torch.device("cuda", self.device)
         self.kg = K.geom(geom.layers, geom.kv_heads, geom.head_dim, geom.block_size, geom.elem_bytes)
@@ -158,7 +159,8 @@ class RingRuntime:
         nodes = [n for n in (self.alive_local() if nodes is None else nodes)
                  if self.succ.get(n) is not None]
         if nodes:
-            K.kv_replicate_step_multi([self.handle(n) for n in nodes], step, self._stream(stream))
+            fn = K.kv_replicate_step_ce if self.copy_engine else K.kv_replicate_step_multi
+            fn([self.handle(n) for n in nodes], step, self._stream(stream))
 
     def _stream(self, stream) -> int:
         if stream is None:

@@ -54,8 +54,9 @@ def _sample_check(rt, drv, oring, rng, per_node=3):
                 assert np.array_equal(rep.view(np.uint16), want[keep]), f"replica of node {gid}"
 
 
-def _run(cfg, steps, ring="stage", check_every=50, restore_mode=None):
+def _run(cfg, steps, ring="stage", check_every=50, restore_mode=None, copy_engine=False):
     rt, drv = make_gpu(cfg, ring=ring, restore_mode=restore_mode)
+    rt.copy_engine = copy_engine
     oring = OracleRing(cfg, content=False, ring=ring, schedules=drv.sched,
                        restore_mode=restore_mode)
     rng = np.random.default_rng(3)
@@ -107,15 +108,17 @@ def test_c3_poisson_two_pipelines():
     rt.destroy()
 
 
-def test_c5_bulk_replication_and_restore():
+@pytest.mark.parametrize("copy_engine", [False, True])
+def test_c5_bulk_replication_and_restore(copy_engine):
     """One 32,768-token request per stage: 2,048 full blocks of 256 KiB replicated in
-    one step (bulk), then stage 3 fails and is restored from stage 4's replica."""
+    one step (bulk; kernel or copy-engine variant), then stage 3 fails and is restored
+    from stage 4's replica."""
     from paper_2601_22438_b200 import kvring as K
     # step 0 admits the 32k prompt, step 1 appends one token and publishes the whole
     # request (bulk seed), step 2: stage 3 fails after its append -> t* = 1
     cfg = configs.scaled(configs.C5, n_steps=3, fixed_output=4, fail_node=(0, 3), fail_step=2,
                          max_reqs=2, num_blocks=2050, max_blocks_per_req=2050)
-    rt, drv, oring = _run(cfg, 3, check_every=1)
+    rt, drv, oring = _run(cfg, 3, check_every=1, copy_engine=copy_engine)
     try:
         g = cfg.geom
         ev = drv.events[0].data

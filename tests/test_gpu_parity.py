@@ -16,8 +16,10 @@ pytestmark = pytest.mark.gpu
 from gpu_harness import compare_state, make_gpu  # noqa: E402
 
 
-def _run_both(cfg, ring="stage", schedules=None, every=1, fail=True, restore_mode=None):
+def _run_both(cfg, ring="stage", schedules=None, every=1, fail=True, restore_mode=None,
+              copy_engine=False):
     rt, drv = make_gpu(cfg, ring=ring, schedules=schedules, restore_mode=restore_mode)
+    rt.copy_engine = copy_engine
     oring = OracleRing(cfg, ring=ring, schedules=drv.sched, restore_mode=restore_mode)
     try:
         for t in range(cfg.n_steps):
@@ -514,3 +516,15 @@ def test_self_loop_ring_and_max_length_requests():
             assert e.value.code == K.KV_ENOMEM
     finally:
         rt.destroy()
+
+
+@pytest.mark.parametrize("seed", [0, 4])
+def test_copy_engine_variant_bit_exact(seed):
+    """NEXT-4: full blocks by cudaMemcpyAsync runs, partial blocks + bt entries +
+    publication by the ring-put kernel -- same replicas and metadata as the oracle,
+    through churn (prefills of many full blocks, retire/admit) and a restore."""
+    cfg = configs.scaled(configs.C1, num_blocks=160, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=6, n_requests=60, n_steps=40, fixed_prompt=None,
+                         fail_node=(0, 2), fail_step=21)
+    rt, drv, oring = _run_both(cfg, schedules=_churn_sched(cfg, seed), copy_engine=True)
+    rt.destroy()

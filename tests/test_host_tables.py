@@ -46,9 +46,12 @@ def _tables(h, R):
     return out
 
 
-@pytest.mark.parametrize("name,steps", [("c1_tiny", 9), ("c2_pp4_b64", 260), ("c4_failover_16", 60)])
-def test_tables_match_oracle(name, steps):
-    """Slots, lengths, block ids and per-step payload bytes == oracle (metadata mode)."""
+@pytest.mark.parametrize("name,steps,ce", [("c1_tiny", 9, False), ("c2_pp4_b64", 260, False),
+                                           ("c4_failover_16", 60, False),
+                                           ("c2_pp4_b64", 120, True)])
+def test_tables_match_oracle(name, steps, ce):
+    """Slots, lengths, block ids and per-step payload bytes == oracle (metadata mode);
+    ce: the copy-engine variant's work-list split (NEXT-4) keeps the same tables/bytes."""
     cfg = configs.ALL[name]
     cfg = configs.scaled(cfg, fail_step=None, fail_node=None)
     ring = OracleRing(cfg, content=False)
@@ -73,7 +76,8 @@ def test_tables_match_oracle(name, steps):
                 before = {c: ring.nodes[c].pub_len.copy() for c in coords}
                 moved0 = ring.moved
                 ring.replicate(t)
-                K.kv_replicate_step_multi([hs[c] for c in coords], t)
+                (K.kv_replicate_step_ce if ce else K.kv_replicate_step_multi)(
+                    [hs[c] for c in coords], t)
                 total = sum(K.kv_stats(hs[c])["last_step_bytes"] for c in coords)
                 assert total == ring.moved - moved0
             for c in coords:
