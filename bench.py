@@ -163,7 +163,7 @@ def run_kvring(args):
     from kvgen.content import CONTENT_SEED
     from kvgen.cuda import content_tokens_cuda
     from paper_2601_22438_b200 import kvring as K
-    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver, StreamOrder
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -200,13 +200,15 @@ def run_kvring(args):
     comp = torch.cuda.current_stream(dev)
     repl = comp if args.single_stream else torch.cuda.Stream(dev)
 
+    order = StreamOrder(comp, repl)
+
     def step(t):
+        order.before_append()
         drv.append_step(t, stream=comp)
         if t >= 1:
-            ready = torch.cuda.Event()
-            ready.record(comp)
-            repl.wait_event(ready)
+            order.before_publish()
             rt.replicate_all(t, stream=repl)
+            order.after_publish()
 
     # ---- prelude: reach steady state (untimed) --------------------------------
     t = 0
@@ -875,6 +877,7 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
     import torch
     import torch.distributed as dist
     from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import StreamOrder
     n = args.e2e_steps
     host = {}
     h2d = 0
@@ -903,13 +906,14 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     st.record(comp)
+    order = StreamOrder(comp, repl)
     for k in range(n):
         tt = t0 + k
+        order.before_append()
         _append_host(drv, tt, host[tt], comp)
-        ready = torch.cuda.Event()
-        ready.record(comp)
-        repl.wait_event(ready)
+        order.before_publish()
         rt.replicate_all(tt, stream=repl)
+        order.after_publish()
         with torch.cuda.stream(repl):
             for i, sd in enumerate(seq_dev):
                 if sd is not None:

@@ -178,7 +178,12 @@ int kv_set_mode(kv_pool_t *p, int32_t mode);
  * then -- ordered after it by an event when the streams differ -- the
  * publication kv_replicate_step_multi(repl_pools, step) on repl_stream: the
  * paper's "separate CUDA stream ... to overlap the communication with
- * computation" (§3.2).  Optional cudaEvent_t handles are recorded on
+ * computation" (§3.2).  The append of step k also waits (event) for the
+ * publication of step k-2 (steps counted across calls on the same stream pair; on
+ * a new pair the first append waits for everything already on repl_stream):
+ * blocks freed by a retiring request are reused
+ * one step later (reading R7) and must not be overwritten while a lagging
+ * publication still reads them.  Optional cudaEvent_t handles are recorded on
  * repl_stream before the publication's H2D (ev_call), around its kernel
  * (ev_kernel_start / ev_kernel_end) and after it (ev_done).  Stops at the
  * first error (steps before it stay applied). */
@@ -205,8 +210,11 @@ int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream);
 
 /* Single-stream loop with programmatic dependent launch (PDL): per step the append
  * and the publication kernels are launched back to back on ONE stream with the
- * programmatic-serialization attribute and read their descriptors zero-copy from
- * mapped pinned memory; the kernels order themselves (griddepcontrol): the
+ * programmatic-serialization attribute and carry their descriptors (pool
+ * parameters, publication tables, tasks; <= 28 KiB) in the kernel parameter space,
+ * so no copy node sits between kernels -- a step whose descriptors do not fit is
+ * staged by one H2D and launched normally (it serialises); the kernels order
+ * themselves (griddepcontrol): the
  * publication of step k waits for append k, append k+1 overlaps it and waits for it
  * before exiting (seq stays monotone).  Same work and results as kv_run_steps.
  * ev_kernel_start/end and ev_append_start/end are honoured (each record is a stream

@@ -32,7 +32,7 @@
 #include <chrono>
 namespace {
 enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue,
-       kPhAcquire, kPhHostCopy, kPhH2DCall, kPhN };
+       kPhAcquire, kPhHostCopy, kPhH2DCall, kPhPrepAppend, kPhPrepRepl, kPhCommit, kPhN };
 double g_phase[kPhN];
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -262,6 +262,52 @@ cudaError_t timed_launch(int kind, const KvTask *tasks, int n_tasks, const KvPoo
 
 }  // namespace
 
+// Growable array of POD tasks: no value-initialisation on growth and no
+// per-element capacity check on the emission path (push_item reserves once per
+// item) -- the host builds ~1k tasks per decode step.
+class TaskVec {
+ public:
+  TaskVec() = default;
+  TaskVec(const TaskVec &) = delete;
+  TaskVec &operator=(const TaskVec &) = delete;
+  ~TaskVec() { std::free(d_); }
+  size_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+  KvTask *data() { return d_; }
+  const KvTask *data() const { return d_; }
+  KvTask &operator[](size_t i) { return d_[i]; }
+  const KvTask &operator[](size_t i) const { return d_[i]; }
+  void clear() { n_ = 0; }
+  void resize(size_t n) {  // new elements are uninitialised (shrink in practice)
+    reserve(n);
+    n_ = n;
+  }
+  void reserve(size_t n) {
+    if (n <= cap_) return;
+    size_t c = cap_ ? cap_ : 1024;
+    while (c < n) c *= 2;
+    KvTask *d = static_cast<KvTask *>(std::realloc(d_, c * sizeof(KvTask)));
+    if (!d) throw std::bad_alloc();
+    d_ = d;
+    cap_ = c;
+  }
+  KvTask *grow(size_t k) {  // k uninitialised slots at the end
+    reserve(n_ + k);
+    KvTask *p = d_ + n_;
+    n_ += k;
+    return p;
+  }
+  void push_back(const KvTask &t) { *grow(1) = t; }
+  KvTask *begin() { return d_; }
+  KvTask *end() { return d_ + n_; }
+  const KvTask *begin() const { return d_; }
+  const KvTask *end() const { return d_ + n_; }
+
+ private:
+  KvTask *d_ = nullptr;
+  size_t n_ = 0, cap_ = 0;
+};
+
 struct kv_pool {
   kv_geom_t g{};
   int NB = 0, R = 0, M = 0, device = -1, node_id = 0, replica_blocks = 0;
@@ -286,7 +332,7 @@ struct kv_pool {
   uint32_t call_id = 0;
   std::vector<int64_t> scratch_ids;
   std::vector<int> scratch_slot;  // slot of each append entry found by validation (-1: new)
-  std::vector<KvTask> scratch_tasks;
+  TaskVec scratch_tasks;
   // state
   bool dead = false;
   uint64_t last_step = 0;
@@ -326,27 +372,26 @@ int validate_geom(const kv_geom_t *g) {
 
 // Appends the tasks of one item (n_tok tokens x combos slices) split into
 // tasks of <= task_segs slices.
-inline void push_item(std::vector<KvTask> &out, int16_t pool, int src_unit, int dst_unit, int slot,
+inline void push_item(TaskVec &out, int16_t pool, int src_unit, int dst_unit, int slot,
                       int j, int tok_lo, int n_tok, int combos, int task_segs) {
   const int nseg = n_tok * combos;
-  for (int b = 0; b < nseg; b += task_segs) {
-    KvTask t;
-    t.src_unit = src_unit;
-    t.dst_unit = dst_unit;
-    t.pool = pool;
-    t.slot = (int16_t)slot;
-    t.j = (int16_t)j;
-    t.tok_lo = (int16_t)tok_lo;
-    t.n_tok = (int16_t)n_tok;
-    t.flags = b == 0 ? kFirst : 0;
-    t.seg_begin = b;
-    t.seg_count = std::min(task_segs, nseg - b);
-    t.pad = 0;
-    out.push_back(t);
+  KvTask *t = out.grow((size_t)((nseg + task_segs - 1) / task_segs));
+  for (int b = 0; b < nseg; b += task_segs, ++t) {
+    t->src_unit = src_unit;
+    t->dst_unit = dst_unit;
+    t->pool = pool;
+    t->slot = (int16_t)slot;
+    t->j = (int16_t)j;
+    t->tok_lo = (int16_t)tok_lo;
+    t->n_tok = (int16_t)n_tok;
+    t->flags = b == 0 ? kFirst : 0;
+    t->seg_begin = b;
+    t->seg_count = std::min(task_segs, nseg - b);
+    t->pad = 0;
   }
 }
 
-inline void push_publish_only(std::vector<KvTask> &out, int16_t pool) {
+inline void push_publish_only(TaskVec &out, int16_t pool) {
   KvTask t{};
   t.pool = pool;
   t.slot = -1;
@@ -436,7 +481,7 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
 
 // Applies the appends to the tables and emits the scatter tasks (src rows are
 // token rows of the dense source, `row_base` added).
-void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, std::vector<KvTask> &tasks,
+void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, TaskVec &tasks,
                int task_segs) {
   const int B = p->g.block_size;
   int row = 0;
@@ -494,7 +539,7 @@ void commit_pub_len(kv_pool *p) {
 
 // Dirty ranges [pub_len, pub_hi) of every live slot split at block boundaries
 // (§8(a) a3); returns payload bytes.
-uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, std::vector<KvTask> &tasks, bool packed,
+uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, TaskVec &tasks, bool packed,
                            int32_t *packed_unit, int task_segs,
                            std::vector<int> *ce_blocks = nullptr) {
   const int B = p->g.block_size;
@@ -687,7 +732,7 @@ struct Launch {
   std::vector<KvPoolParams> params;
   std::vector<char> tables;        // replicate: per pool slot_req[R] (8R B) then slot_len[R] (4R B)
   std::vector<size_t> table_off;   // per pool offset into `tables`
-  std::vector<KvTask> tasks;
+  TaskVec tasks;
   std::vector<int> ntask;          // replicate: tasks per pool
   std::vector<uint64_t> bytes;     // replicate: payload bytes per pool
   std::vector<const void *> host_src;  // append: host sources (KV_SRC_HOST), per pool
@@ -1140,7 +1185,7 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
     }
   }
   // 2. allocate (req_id asc, j asc, lowest free ids) and build the remap tasks.
-  std::vector<KvTask> tasks;
+  TaskVec tasks;
   for (auto &e : ents) {
     const int s = dst->free_slots.take_min();
     dst->slot_of.insert(e.req, s);
@@ -1212,7 +1257,7 @@ size_t packed_layout(kv_pool *p, size_t n_tasks, uint64_t payload_bytes, KvPacke
 
 KV_API int kv_pack_bytes(kv_pool_t *p, size_t *bytes_out) {
   if (!p || !bytes_out) return fail(KV_EINVAL, "null argument");
-  std::vector<KvTask> tasks;
+  TaskVec tasks;
   int32_t unit = 0;
   const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit, p->task_segs);
   if (tasks.empty()) push_publish_only(tasks, 0);
@@ -1227,7 +1272,7 @@ KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, s
   if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
   if (p->device < 0) return fail(KV_ESTATE, "pack needs a device pool");
   if (step == 0 || step <= p->last_step) return fail(KV_EINVAL, "step not increasing");
-  std::vector<KvTask> tasks;
+  TaskVec tasks;
   int32_t unit = 0;
   const uint64_t bytes = build_dirty_tasks(p, 0, tasks, true, &unit, p->task_segs);
   if (tasks.empty()) push_publish_only(tasks, 0);
@@ -1401,16 +1446,22 @@ void prepare_step(const kv_step_t &st, StepPrep &sp) {
   sp.has_a = st.n_append > 0;
   sp.has_p = st.n_repl > 0;
   sp.rc = KV_OK;
+  const double t0 = now_s();
   if (sp.has_a && (sp.rc = prepare_append(st.n_append, st.append, sp.A))) {
     sp.err = g_err;
     return;
   }
+  const double t1 = now_s();
+  g_phase[kPhPrepAppend] += t1 - t0;
   if (sp.has_p) {
     if ((sp.rc = prepare_replicate(st.n_repl, st.repl_pools, st.step, sp.P))) {
       sp.err = g_err;
       return;
     }
+    const double t2 = now_s();
+    g_phase[kPhPrepRepl] += t2 - t1;
     commit_replicate(sp.P, st.repl_pools, st.step);
+    g_phase[kPhCommit] += now_s() - t2;
   }
   kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
   if (p0 && sp.has_a && sp.has_p && sp.P.p0->device != p0->device) {
@@ -1419,10 +1470,38 @@ void prepare_step(const kv_step_t &st, StepPrep &sp) {
   }
 }
 
+// Cross-stream order of the two-stream loop: ring-put k after append k (event
+// `ready`), and append k after ring-put k-2 -- blocks a retiring request frees in
+// step k-1 are reused from step k on (quarantine, reading R7), and the ring-put
+// that last read them is k-2's, which may otherwise still lag on its stream.
+struct StreamOrder {
+  static constexpr int kN = 4;
+  cudaEvent_t ready = nullptr;
+  cudaEvent_t rdone[kN] = {};
+  long long rstep[kN] = {-1, -1, -1, -1};
+  long long n = 0;  // steps issued on this stream pair (continues across calls)
+  cudaStream_t sa = nullptr, sr = nullptr;
+  int dev = -1;
+  int ensure(int device) {
+    if (dev == device) return KV_OK;
+    if (ready) cudaEventDestroy(ready);
+    for (auto &e : rdone)
+      if (e) cudaEventDestroy(e);
+    ready = nullptr;
+    for (auto &e : rdone) e = nullptr;
+    for (auto &r : rstep) r = -1;
+    sa = sr = nullptr;
+    CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    for (auto &e : rdone) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    dev = device;
+    return KV_OK;
+  }
+};
+
 // CUDA side of one prepared step: one H2D for both launches, append kernel on
 // sa, event, ring-put on sr (the paper's separate replication stream).
-int issue_step(const kv_step_t &st, StepPrep &sp, cudaStream_t sa, cudaStream_t sr,
-               cudaEvent_t &ready, int &ready_dev) {
+int issue_step(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa, cudaStream_t sr,
+               StreamOrder &so) {
   kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
   if (!p0 || p0->device < 0) return KV_OK;  // nothing to launch / tables-only pools
   if (sp.has_a && sp.A.tasks.empty() && !sp.has_p) return KV_OK;
@@ -1440,7 +1519,10 @@ int issue_step(const kv_step_t &st, StepPrep &sp, cudaStream_t sa, cudaStream_t 
   if ((rc = stage(ctx, ls, nl, sa, &b))) return rc;  // one H2D for both launches
   double t1 = now_s();
   g_phase[kPhStage] += t1 - t0;
+  if (sa != sr && (rc = so.ensure(p0->device))) return rc;
   if (sp.has_a) {
+    if (sa != sr && k >= 2 && so.rstep[(k - 2) % StreamOrder::kN] == k - 2)
+      CU(cudaStreamWaitEvent(sa, so.rdone[(k - 2) % StreamOrder::kN], 0));
     g_ev_before = static_cast<cudaEvent_t>(st.ev_append_start);
     g_ev_after = static_cast<cudaEvent_t>(st.ev_append_end);
     rc = enqueue(sp.A, sa);
@@ -1452,13 +1534,8 @@ int issue_step(const kv_step_t &st, StepPrep &sp, cudaStream_t sa, cudaStream_t 
   g_phase[kPhEnqA] += t2 - t1;
   if (!sp.has_p) return ctx->done(b, sa);
   if (sa != sr) {  // publication after the append (and after the staged H2D)
-    if (!ready || ready_dev != p0->device) {
-      if (ready) cudaEventDestroy(ready);
-      CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-      ready_dev = p0->device;
-    }
-    CU(cudaEventRecord(ready, sa));
-    CU(cudaStreamWaitEvent(sr, ready, 0));
+    CU(cudaEventRecord(so.ready, sa));
+    CU(cudaStreamWaitEvent(sr, so.ready, 0));
   }
   if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
   double t3 = now_s();
@@ -1469,6 +1546,10 @@ int issue_step(const kv_step_t &st, StepPrep &sp, cudaStream_t sa, cudaStream_t 
   g_ev_before = g_ev_after = nullptr;
   if (rc) return rc;
   if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
+  if (sa != sr) {
+    CU(cudaEventRecord(so.rdone[k % StreamOrder::kN], sr));
+    so.rstep[k % StreamOrder::kN] = k;
+  }
   rc = ctx->done(b, sr);  // sr is ordered after sa: covers both launches
   g_phase[kPhEnqP] += now_s() - t3;
   return rc;
@@ -1484,14 +1565,28 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
   cudaStream_t sa = static_cast<cudaStream_t>(append_stream);
   cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
-  thread_local cudaEvent_t ready = nullptr;
-  thread_local int ready_dev = -1;
+  thread_local StreamOrder so;
+  if (sa != sr && n_steps > 0) {
+    const kv_step_t &s0 = steps[0];
+    kv_pool *q = s0.n_append > 0 ? s0.append[0].pool : (s0.n_repl > 0 ? s0.repl_pools[0] : nullptr);
+    if (q && q->device >= 0 && (so.sa != sa || so.sr != sr || so.dev != q->device)) {
+      // a new stream pair: everything already on sr precedes this call's appends
+      DeviceGuard dg(q->device);
+      int rc = so.ensure(q->device);
+      if (rc) return rc;
+      for (auto &r : so.rstep) r = -1;
+      CU(cudaEventRecord(so.rdone[0], sr));
+      CU(cudaStreamWaitEvent(sa, so.rdone[0], 0));
+      so.sa = sa;
+      so.sr = sr;
+    }
+  }
   if (n_steps < 8) {
     thread_local StepPrep sp;
     for (int k = 0; k < n_steps; ++k) {
       prepare_step(steps[k], sp);
       if (sp.rc) return sp.rc;
-      int rc = issue_step(steps[k], sp, sa, sr, ready, ready_dev);
+      int rc = issue_step(steps[k], so.n++, sp, sa, sr, so);
       if (rc) return rc;
     }
     return KV_OK;
@@ -1526,7 +1621,7 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
       g_err = sp.err;
       break;
     }
-    rc = issue_step(steps[k], sp, sa, sr, ready, ready_dev);
+    rc = issue_step(steps[k], so.n++, sp, sa, sr, so);
     consumed.store(k + 1, std::memory_order_release);
     if (rc) break;
   }
@@ -1725,132 +1820,98 @@ KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *str
 // ---- single-stream decode loop with programmatic dependent launch ----------------
 namespace {
 
-// Zero-copy descriptor ring: mapped pinned host memory the kernels read over PCIe,
-// so no memcpy node sits between consecutive kernels (it would break the PDL
-// overlap).  64 slots; one completion event per group of 8 steps.
-struct ZcRing {
-  static constexpr int kSlots = 64, kGroup = 8, kGroups = kSlots / kGroup;
-  char *buf[kSlots] = {};
-  size_t cap[kSlots] = {};
-  cudaEvent_t ev[kGroups] = {};
-  bool pending[kGroups] = {};
-  int device = -1;
-};
-
-std::mutex g_zc_mu;
-std::map<int, std::unique_ptr<ZcRing>> g_zc;
-
-ZcRing *zc_for(int device) {
-  std::lock_guard<std::mutex> lk(g_zc_mu);
-  auto &p = g_zc[device];
-  if (!p) {
-    p.reset(new ZcRing());
-    p->device = device;
-  }
-  return p.get();
+// Inline descriptors (KvInlineDesc): a launch whose tables + tasks fit the kernel
+// parameter space travels with the launch itself (KVRING_INLINE=0 disables).
+bool inline_fits(const Launch &L) {
+  static const int enabled = [] {
+    const char *e = getenv("KVRING_INLINE");
+    return e ? atoi(e) : 1;
+  }();
+  return enabled && L.n_pools <= kInlinePools &&
+         align16(L.tables.size()) + sizeof(KvTask) * L.tasks.size() <= (size_t)kInlineBytes;
 }
 
-int zc_stage(ZcRing *z, int k, StepPrep &sp, const KvPoolParams **pa, const KvTask **ta,
-             const KvPoolParams **pp, const KvTask **tp) {
-  const int slot = (int)(k % ZcRing::kSlots);
-  if (k >= ZcRing::kSlots) {  // the group that last used this slot must have completed
-    const int g = (int)(((k - ZcRing::kSlots) / ZcRing::kGroup) % ZcRing::kGroups);
-    if (z->pending[g]) {
-      const double t0 = now_s();
-      CU(cudaEventSynchronize(z->ev[g]));
-      g_phase[kPhAcquire] += now_s() - t0;
-      z->pending[g] = false;
+void fill_inline(const Launch &L, KvInlineDesc &d) {
+  const size_t tbl = align16(L.tables.size());
+  d.n_tasks = (int32_t)L.tasks.size();
+  d.n_pools = L.n_pools;
+  d.task_off = (int32_t)tbl;
+  d.pad = 0;
+  for (int q = 0; q < L.n_pools; ++q) {
+    d.pools[q] = L.params[q];
+    if (L.kind == kKindRingPut) {
+      d.pools[q].slot_req = reinterpret_cast<const int64_t *>(L.table_off[q]);
+      d.pools[q].slot_len = reinterpret_cast<const int32_t *>(
+          L.table_off[q] + 8 * (size_t)L.params[q].max_reqs);
     }
   }
-  Launch *ls[2] = {sp.has_a ? &sp.A : nullptr, sp.has_p ? &sp.P : nullptr};
-  size_t total = 0;
-  for (Launch *L : ls)
-    if (L) total += align16(L->staged_bytes());
-  if (z->cap[0] == 0)  // first use: every slot at once (mapped allocations cost ms each)
-    for (int q = 0; q < ZcRing::kSlots; ++q) {
-      CU(cudaHostAlloc(reinterpret_cast<void **>(&z->buf[q]), (size_t)4 << 20,
-                       cudaHostAllocMapped | cudaHostAllocPortable));
-      z->cap[q] = (size_t)4 << 20;
-    }
-  if (z->cap[slot] < total) {  // rare (bulk steps): grow this slot
-    if (z->buf[slot]) cudaFreeHost(z->buf[slot]);
-    z->buf[slot] = nullptr;
-    z->cap[slot] = 0;
-    const size_t cap = std::max(total * 2, (size_t)4 << 20);
-    CU(cudaHostAlloc(reinterpret_cast<void **>(&z->buf[slot]), cap,
-                     cudaHostAllocMapped | cudaHostAllocPortable));
-    z->cap[slot] = cap;
-  }
-  const double tb = now_s();
-  char *h = z->buf[slot];  // UVA: the host address is the device address
-  size_t off = 0;
-  for (int i = 0; i < 2; ++i) {
-    Launch *L = ls[i];
-    if (!L) continue;
-    const size_t pbytes = align16(sizeof(KvPoolParams) * L->n_pools);
-    const size_t tbl = align16(L->tables.size());
-    char *b = h + off;
-    if (L->kind == kKindRingPut)
-      for (int q = 0; q < L->n_pools; ++q) {
-        L->params[q].slot_req = reinterpret_cast<const int64_t *>(b + pbytes + L->table_off[q]);
-        L->params[q].slot_len = reinterpret_cast<const int32_t *>(
-            b + pbytes + L->table_off[q] + 8 * (size_t)L->params[q].max_reqs);
-      }
-    std::memcpy(b, L->params.data(), sizeof(KvPoolParams) * L->n_pools);
-    if (!L->tables.empty()) std::memcpy(b + pbytes, L->tables.data(), L->tables.size());
-    std::memcpy(b + pbytes + tbl, L->tasks.data(), sizeof(KvTask) * L->tasks.size());
-    L->params_dev = reinterpret_cast<const KvPoolParams *>(b);
-    L->tasks_dev = reinterpret_cast<const KvTask *>(b + pbytes + tbl);
-    off += align16(L->staged_bytes());
-  }
-  g_phase[kPhHostCopy] += now_s() - tb;
-  *pa = ls[0] ? ls[0]->params_dev : nullptr;
-  *ta = ls[0] ? ls[0]->tasks_dev : nullptr;
-  *pp = ls[1] ? ls[1]->params_dev : nullptr;
-  *tp = ls[1] ? ls[1]->tasks_dev : nullptr;
-  return KV_OK;
+  if (!L.tables.empty()) std::memcpy(d.data, L.tables.data(), L.tables.size());
+  std::memcpy(d.data + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
 }
 
+// One step of the PDL loop: launches whose descriptors fit the parameter space go
+// inline with the PDL attribute (no copy node between kernels); larger ones (bulk
+// prefill steps) are staged by one H2D and launched normally -- that step
+// serialises, the kernels' griddepcontrol calls are then no-ops.
 int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
+  (void)k;
   kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
   if (!p0 || p0->device < 0) return KV_OK;
   DeviceGuard dg(p0->device);
-  ZcRing *z = zc_for(p0->device);
-  const KvPoolParams *pa = nullptr, *pp = nullptr;
-  const KvTask *ta = nullptr, *tp = nullptr;
-  const double t0 = now_s();
-  int rc = zc_stage(z, k, sp, &pa, &ta, &pp, &tp);
-  if (rc) return rc;
-  if (sp.has_a && sp.A.host_src_bytes.size()) {
+  const bool has_a = sp.has_a && !sp.A.tasks.empty(), has_p = sp.has_p && !sp.P.tasks.empty();
+  if (sp.has_a)
     for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q)
-      if (sp.A.host_src_bytes[q]) return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_pdl");
+      if (sp.A.host_src_bytes[q])
+        return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_pdl");
+  const bool inl_a = has_a && inline_fits(sp.A), inl_p = has_p && inline_fits(sp.P);
+  const double t0 = now_s();
+  thread_local std::unique_ptr<KvInlineDesc> da, dp;
+  if (inl_a) {
+    if (!da) da.reset(new KvInlineDesc());
+    fill_inline(sp.A, *da);
   }
+  if (inl_p) {
+    if (!dp) dp.reset(new KvInlineDesc());
+    fill_inline(sp.P, *dp);
+  }
+  DeviceCtx *ctx = ctx_for(p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  Launch *ls[2];
+  int nl = 0;
+  if (has_a && !inl_a) ls[nl++] = &sp.A;
+  if (has_p && !inl_p) ls[nl++] = &sp.P;
+  StageBuf *b = nullptr;
+  int rc = KV_OK;
+  if (nl && (rc = stage(ctx, ls, nl, s, &b))) return rc;
   const double t1 = now_s();
   g_phase[kPhStage] += t1 - t0;
-  if (sp.has_a && !sp.A.tasks.empty()) {
+  if (has_a) {
     if (st.ev_append_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_start), s));
-    CU(launch_copy_pdl(kKindAppend, ta, (int)sp.A.tasks.size(), pa, sp.A.n_pools, p0->geom_dev(),
-                       copy_grid(p0->device, (int)sp.A.tasks.size()), s));
+    if (inl_a) {
+      CU(launch_copy_inline(kKindAppend, *da, p0->geom_dev(),
+                            copy_grid(p0->device, (int)sp.A.tasks.size()), s, true));
+      g_launches++;
+      p0->kernels++;
+    } else if ((rc = enqueue(sp.A, s))) {
+      return rc;
+    }
     if (st.ev_append_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_end), s));
-    g_launches++;
-    p0->kernels++;
   }
   const double t2 = now_s();
   g_phase[kPhEnqA] += t2 - t1;
-  if (sp.has_p && !sp.P.tasks.empty()) {
+  if (has_p) {
     if (st.ev_kernel_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_start), s));
-    CU(launch_copy_pdl(kKindRingPut, tp, (int)sp.P.tasks.size(), pp, sp.P.n_pools, p0->geom_dev(),
-                       copy_grid(p0->device, (int)sp.P.tasks.size()), s));
+    if (inl_p) {
+      CU(launch_copy_inline(kKindRingPut, *dp, p0->geom_dev(),
+                            copy_grid(p0->device, (int)sp.P.tasks.size()), s, true));
+      g_launches++;
+      p0->kernels++;
+    } else if ((rc = enqueue(sp.P, s))) {
+      return rc;
+    }
     if (st.ev_kernel_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_end), s));
-    g_launches++;
-    p0->kernels++;
   }
-  if (k % ZcRing::kGroup == ZcRing::kGroup - 1) {  // completion of this group of 8 steps
-    const int g = (int)((k / ZcRing::kGroup) % ZcRing::kGroups);
-    if (!z->ev[g]) CU(cudaEventCreateWithFlags(&z->ev[g], cudaEventDisableTiming));
-    CU(cudaEventRecord(z->ev[g], s));
-    z->pending[g] = true;
-  }
+  if (b && (rc = ctx->done(b, s))) return rc;
   g_phase[kPhEnqP] += now_s() - t2;
   return KV_OK;
 }
@@ -1859,7 +1920,7 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
 
 // Single-stream decode loop with programmatic dependent launch: per step the
 // append and the publication are launched back to back on ONE stream with the
-// PDL attribute, descriptors are read zero-copy from mapped pinned memory, and the
+// PDL attribute, descriptors travel in the kernel parameter space (inline), and the
 // kernels order themselves with griddepcontrol (see kvring_kernels.cu): the
 // publication of step k starts as soon as append k completes and runs while append
 // k+1 copies -- the overlap the paper gets from a separate stream, without
@@ -1867,19 +1928,6 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
 KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // zero-copy slots are reused within a call only: drain the previous call's groups
-  for (int k = 0; k < n_steps && k < 1; ++k) {
-    const kv_step_t &st0 = steps[0];
-    kv_pool *q = st0.n_append > 0 ? st0.append[0].pool : (st0.n_repl > 0 ? st0.repl_pools[0] : nullptr);
-    if (q && q->device >= 0) {
-      ZcRing *z = zc_for(q->device);
-      for (int g = 0; g < ZcRing::kGroups; ++g)
-        if (z->pending[g]) {
-          CU(cudaEventSynchronize(z->ev[g]));
-          z->pending[g] = false;
-        }
-    }
-  }
   StepPrep ring[2];
   std::atomic<int> produced{0}, consumed{0};
   std::atomic<bool> stop{false};
@@ -1910,17 +1958,6 @@ KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *strea
       break;
     }
     rc = issue_step_pdl(steps[k], k, sp, s);
-    if (!rc && k == n_steps - 1 && k % ZcRing::kGroup != ZcRing::kGroup - 1) {
-      // close the last partial group so the next call can drain it
-      kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
-      if (p0 && p0->device >= 0) {
-        DeviceGuard dg(p0->device);
-        ZcRing *z = zc_for(p0->device);
-        const int g = (k / ZcRing::kGroup) % ZcRing::kGroups;
-        if (!z->ev[g]) cudaEventCreateWithFlags(&z->ev[g], cudaEventDisableTiming);
-        if (cudaEventRecord(z->ev[g], s) == cudaSuccess) z->pending[g] = true;
-      }
-    }
     consumed.store(k + 1, std::memory_order_release);
     if (rc) break;
   }

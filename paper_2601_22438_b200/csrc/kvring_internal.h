@@ -99,6 +99,19 @@ cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const K
                          cudaStream_t stream);
 cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
                             int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream);
+// A launch carried entirely in the kernel's parameter space (<= 32 KiB since
+// CUDA 12.1): per-pool parameters, the ring-put's publication tables and the task
+// list.  No H2D staging copy and no dependent global load before a CTA's first
+// data load; ring-put pools carry their table offsets (into `data`) in
+// slot_req / slot_len.
+constexpr int kInlineBytes = 28 * 1024;
+struct KvInlineDesc {
+  int32_t n_tasks, n_pools, task_off, pad;
+  KvPoolParams pools[kInlinePools];
+  alignas(16) char data[kInlineBytes];
+};
+cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,
+                               cudaStream_t stream, bool pdl);
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           unsigned long long *counter, const KvGeomDev &g, int grid,
                           cudaStream_t stream);

@@ -186,15 +186,22 @@ __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long 
 // Parity-`step` (req_id, len) table of one pool (reading R9).  Written by the
 // CTA that owns the pool's first task, BEFORE that CTA's release: a reader
 // only trusts parity t once it acquires seq = t, so writing it early is safe.
-__device__ void write_parity_table(const KvPoolParams &pp) {
+// tbl_base != nullptr: an inline launch, slot_req / slot_len hold offsets into it.
+__device__ void write_parity_table(const KvPoolParams &pp, const char *tbl_base) {
   char *meta = pp.meta;
   const int R = pp.max_reqs;
   const int par = (int)(pp.step & 1ull);
   int64_t *mreq = reinterpret_cast<int64_t *>(meta + 32) + (size_t)par * R;
   int32_t *mlen = reinterpret_cast<int32_t *>(meta + 32 + 16 * (size_t)R) + (size_t)par * R;
+  const int64_t *sreq = tbl_base ? reinterpret_cast<const int64_t *>(
+                                       tbl_base + reinterpret_cast<size_t>(pp.slot_req))
+                                 : pp.slot_req;
+  const int32_t *slen = tbl_base ? reinterpret_cast<const int32_t *>(
+                                       tbl_base + reinterpret_cast<size_t>(pp.slot_len))
+                                 : pp.slot_len;
   for (int s = threadIdx.x; s < R; s += blockDim.x) {
-    mreq[s] = pp.slot_req[s];
-    mlen[s] = pp.slot_len[s];
+    mreq[s] = sreq[s];
+    mlen[s] = slen[s];
   }
   if (threadIdx.x == 0) *reinterpret_cast<int32_t *>(meta + 8) = pp.writer_node;
 }
@@ -210,7 +217,8 @@ constexpr int kMaxPoolsPerLaunch = 64;
 // no per-thread fences.  The CTA whose RMW completes a pool's count stores
 // that pool's seq with a release store (last-CTA pattern, reading R9).
 __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int n_tasks,
-                                          const KvPoolParams *__restrict__ params, int n_pools) {
+                                          const KvPoolParams *__restrict__ params, int n_pools,
+                                          const char *tbl_base = nullptr) {
   __shared__ int s_cnt[kMaxPoolsPerLaunch];
   __shared__ int s_own[kMaxPoolsPerLaunch];
   for (int i = threadIdx.x; i < n_pools; i += blockDim.x) {
@@ -231,7 +239,7 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
   }
   __syncthreads();
   for (int i = 0; i < n_pools; ++i)
-    if (s_own[i]) write_parity_table(params[i]);
+    if (s_own[i]) write_parity_table(params[i], tbl_base);
   __syncthreads();  // every thread's stores precede the single release below
   if (threadIdx.x == 0) {
     for (int i = 0; i < n_pools; ++i) {
@@ -265,7 +273,8 @@ template <int SRC, int DST, bool PUB>
 __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
                                           const KvPoolParams *__restrict__ params,
                                           const KvGeomDev &g, int n_pools,
-                                          const KvParamPack *pk = nullptr) {
+                                          const KvParamPack *pk = nullptr,
+                                          const char *tbl_base = nullptr) {
   // pass 1: the copies -- identical for every kernel, no publication state live
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
@@ -280,7 +289,7 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
     char *dst = inl ? pk->dst[tk.pool] : pp.dst;
     copy_task<SRC, DST>(tk, src, dst, g, sbytes, dbytes);
   }
-  if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools);
+  if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools, tbl_base);
 }
 
 // One named kernel per role (ncu / launch lists show what ran).
@@ -330,6 +339,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   pdl_wait();
   pdl_launch_dependents();
   run_tasks<kPaged, kPaged, true>(tasks, n_tasks, params, g, n_pools, &pk);
+}
+
+// Inline-descriptor twins of the two hot kernels (KvInlineDesc: parameters, tables
+// and tasks in the kernel's parameter space; same PDL protocol as above).
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_append_scatter_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDesc d) {
+  pdl_launch_dependents();
+  run_tasks<kTokMajor, kPaged, false>(reinterpret_cast<const KvTask *>(d.data + d.task_off),
+                                      d.n_tasks, d.pools, g, d.n_pools);
+  pdl_wait();
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_ring_put_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDesc d) {
+  pdl_wait();
+  pdl_launch_dependents();
+  run_tasks<kPaged, kPaged, true>(reinterpret_cast<const KvTask *>(d.data + d.task_off),
+                                  d.n_tasks, d.pools, g, d.n_pools, nullptr, d.data);
 }
 
 // Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
@@ -385,7 +412,7 @@ __global__ void __launch_bounds__(kThreads) kv_unpack_kernel(const char *__restr
   for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
     const KvTask tk = tasks[t];
     copy_task<kPacked, kPaged>(tk, pp.src, pp.dst, g, ~0ull, ~0ull);
-    if (tk.flags & kPoolFirst) write_parity_table(pp);
+    if (tk.flags & kPoolFirst) write_parity_table(pp, nullptr);
     if (threadIdx.x == 0) {
       if ((tk.flags & kFirst) && tk.slot >= 0) {
         int32_t *bt = reinterpret_cast<int32_t *>(meta + 32 + 24 * (size_t)pp.max_reqs);
@@ -524,6 +551,25 @@ cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const Kv
                               pk);
   if (kind == kKindRingPut)
     return cudaLaunchKernelEx(&cfg, kv_ring_put_kernel, tasks, n_tasks, params, g, n_pools, pk);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,
+                               cudaStream_t stream, bool pdl) {
+  if (d.n_tasks <= 0) return cudaSuccess;
+  if (d.n_pools > kInlinePools) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (kind == kKindAppend) return cudaLaunchKernelEx(&cfg, kv_append_scatter_inl_kernel, g, d);
+  if (kind == kKindRingPut) return cudaLaunchKernelEx(&cfg, kv_ring_put_inl_kernel, g, d);
   return cudaErrorInvalidValue;
 }
 

@@ -374,7 +374,7 @@ def kv_plan_targets(succ, excluded=None):
 
 HOST_PHASES = ["prepare", "wait_prepare", "stage_h2d", "launch_append", "launch_publish",
                "events", "worker_wait_issue", "stage.acquire_wait", "stage.host_copy",
-               "stage.h2d_call"]
+               "stage.h2d_call", "prepare.append", "prepare.replicate", "prepare.commit"]
 
 
 def kv_host_profile(reset: bool = True) -> dict:

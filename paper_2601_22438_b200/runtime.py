@@ -24,6 +24,32 @@ from . import kvring as K
 SENTINEL_WORD = 0x5A5A
 
 
+class StreamOrder:
+    """Cross-stream order of a hand-written two-stream decode loop, the same rule
+    kv_run_steps applies natively: the publication of step k after append k, and
+    append k after the publication of step k-2 (blocks a retiring request frees
+    are reused one step later, reading R7, and must not be overwritten while a
+    lagging publication still reads them)."""
+
+    def __init__(self, comp, repl):
+        self.comp, self.repl = comp, repl
+        self.done: list = []
+
+    def before_append(self) -> None:
+        if len(self.done) >= 2:
+            self.comp.wait_event(self.done[-2])
+
+    def before_publish(self) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.comp)
+        self.repl.wait_event(ev)
+
+    def after_publish(self) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.repl)
+        self.done = self.done[-1:] + [ev]
+
+
 def _meta_stride(R: int, M: int) -> int:
     return (K.kv_meta_bytes(R, M) + 4095) // 4096 * 4096
 

@@ -27,7 +27,7 @@ def run(rps, steps, prelude, dev):
     from kvgen.content import CONTENT_SEED
     from kvgen.cuda import content_tokens_cuda
     from paper_2601_22438_b200 import kvring as K
-    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver, StreamOrder
     cfg = configs.scaled(configs.C3, rps=rps, num_blocks=6144, max_reqs=256)
     I, S = cfg.pipelines, cfg.stages
     g = cfg.geom
@@ -45,13 +45,14 @@ def run(rps, steps, prelude, dev):
     drv = ScheduleDriver(rt, scheds, coords, content)
     comp = torch.cuda.current_stream(dev)
     repl = torch.cuda.Stream(dev)
+    order = StreamOrder(comp, repl)
     for t in range(prelude):
+        order.before_append()
         drv.append_step(t, stream=comp)
         if t >= 1:
-            ev = torch.cuda.Event()
-            ev.record(comp)
-            repl.wait_event(ev)
+            order.before_publish()
             rt.replicate_all(t, stream=repl)
+            order.after_publish()
     torch.cuda.synchronize(dev)
     handles = [rt.handle(n) for n in rt.alive_local()]
     steps_l, evs, live = [], [], []

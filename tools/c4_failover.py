@@ -35,7 +35,7 @@ def main():
     from kvgen.cuda import content_tokens_cuda
     from oracle.simulate import OracleRing
     from paper_2601_22438_b200 import kvring as K
-    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver, StreamOrder
     from gpu_harness import compare_state
 
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -66,12 +66,14 @@ def main():
                        restore_mode="promote")
     comp = torch.cuda.current_stream(dev)
     repl = torch.cuda.Stream(dev)
+    order = StreamOrder(comp, repl)
     step_us = {"before": [], "after": []}
     restore = {}
     ok = 1
     for t in range(steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(comp)
+        order.before_append()
         drv.append_step(t, stream=comp)
         oring.appends(t)
         if t == cfg.fail_step:
@@ -98,10 +100,9 @@ def main():
             drv.reprotect([(0, 2), (1, 2)])
             oring.reprotect([(0, 2), (1, 2)])
         if t >= 1:
-            ready = torch.cuda.Event()
-            ready.record(comp)
-            repl.wait_event(ready)
+            order.before_publish()
             rt.replicate_all(t, stream=repl)
+            order.after_publish()
         done = torch.cuda.Event()
         done.record(repl)
         comp.wait_event(done)
