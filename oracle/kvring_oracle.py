@@ -13,7 +13,10 @@ Paper passages this follows:
 
 Layout (reading R4): a block is uint16 [L][2][H][B][d]; the pool is
 [NB][L][2][H][B][d].  The replica region of node m mirrors the block ids of
-its ring predecessor (R5).  Replica metadata (R9): ``seq`` (0 = nothing
+its ring predecessor (R5).  Shared-capacity mode (§8(f) NEXT-3
+§3.2, SPEC S:152/S:158/S:312, reading R17): the holder keeps its predecessor's
+replica blocks inside its OWN pool, allocated from its own free list, and drops
+them (oldest request first) when its primary needs the memory.  Replica metadata (R9): ``seq`` (0 = nothing
 published), parity double-buffered (req_id, len) per request slot, and one bt
 row per slot.
 """
@@ -79,6 +82,18 @@ class OracleNode:
         self.last_step = 0
         self.dead = False
         self.mode = "tokens"     # "blocks": completed blocks only (P:229 literal; NEXT-2)
+        # shared-capacity mode (NEXT-3, reading R17).  Predecessor side: the holder
+        # and, per slot, the holder block ids of the request's replica, whether
+        # its replica was dropped, and its admission order (eviction age).
+        self.holder: OracleNode | None = None
+        self.rep_bt: list[list[int]] = [[] for _ in range(max_reqs)]
+        self.dropped = np.zeros(max_reqs, dtype=bool)
+        self.admit_seq = np.zeros(max_reqs, dtype=np.int64)
+        self.admit_ctr = 0
+        # holder side: the predecessor whose replicas live in this pool
+        self.rep_src: OracleNode | None = None
+        self.evictions = 0       # requests whose replica this holder evicted
+        self.drops = 0           # requests whose replica could not grow (predecessor side)
 
     # ------------------------------------------------------------------ allocator
     def begin_step(self) -> None:
@@ -96,6 +111,9 @@ class OracleNode:
                 raise OracleError(EINVAL, f"unknown request {r}")
         for r in req_ids:
             s = self.slot_of.pop(r)
+            if self.holder is not None:
+                self._free_rep(s)
+                self.dropped[s] = False
             self.q_blocks.extend(self.slot_bt[s])
             self.q_slots.append(s)
             self.slot_bt[s] = []
@@ -138,8 +156,11 @@ class OracleNode:
             if new_total > self.M:
                 raise OracleError(ENOMEM, f"request {r} exceeds max_blocks_per_req")
             need_blocks += new_total - ceil_div(cur, B)
-        if need_slots > len(self.free_slots) or need_blocks > len(self.free_blocks):
+        census = self.rep_src.census() if self.rep_src is not None else 0
+        if need_slots > len(self.free_slots) or need_blocks > len(self.free_blocks) + census:
             raise OracleError(ENOMEM, "pool or slots exhausted")
+        if need_blocks > len(self.free_blocks):
+            self._evict_for(need_blocks)        # drop replicated KV under pressure
         row = 0
         for r, n in zip(req_ids, n_new):
             if r not in self.slot_of:
@@ -149,6 +170,7 @@ class OracleNode:
                 self.slot_req[s] = r
                 self.slot_len[s] = 0
                 self.pub_len[s] = 0
+                self._admitted(s)
             s = self.slot_of[r]
             for _ in range(n):
                 ln = int(self.slot_len[s])
@@ -171,16 +193,101 @@ class OracleNode:
 
     def published_len(self, s: int) -> int:
         """Length a publication of slot s reaches (all tokens, or completed blocks)."""
+        if self.holder is not None and self.dropped[s]:
+            return 0                            # dropped replica: never published again
         ln = int(self.slot_len[s])
         if self.mode == "blocks":
             return max(int(self.pub_len[s]), ln - ln % self.g.block_size)
         return ln
 
-    def set_successor(self, succ: OracleNode | None) -> None:
-        """Bind the ring link (SPEC S:298-306 apply_plan); a new link re-seeds: pub_len = 0."""
+    def set_successor(self, succ: OracleNode | None, shared: bool = False) -> None:
+        """Bind the ring link (SPEC S:298-306 apply_plan); a new link re-seeds: pub_len = 0.
+
+        ``shared``: the successor keeps the replica in its own pool (NEXT-3, R17).
+        Replicas held by a previous shared successor are freed first; a holder
+        serves one predecessor, so another predecessor's replicas in ``succ`` are
+        dropped and that predecessor unlinked from it."""
         self._alive()
+        if self.holder is not None:
+            self._free_all_reps()
+            self.holder.rep_src = None
+            self.holder = None
         self.succ = succ
         self.pub_len[:] = 0
+        self.dropped[:] = False
+        if shared:
+            if succ is None or succ is self:
+                raise OracleError(EINVAL, "shared mode needs another successor")
+            old = succ.rep_src
+            if old is not None and old is not self:
+                old._free_all_reps()
+                old.holder = None
+                old.succ = None
+            self.holder = succ
+            succ.rep_src = self
+
+    # ------------------------------------------------ shared capacity (NEXT-3, R17)
+    # P:233-235 §3.2: "KevlarFlow utilizes such memory headroom to temporarily
+    # handle rerouted traffic and the replicated KV cache.  When memory pressure
+    # happens, KevlarFlow drops the replicated KV cache and recomputes them if
+    # needed."  SPEC S:158 (replica blocks go first, oldest request first; primary
+    # blocks are never evicted), S:312 (no admission is rejected while evicting
+    # replicas could make room).
+    def census(self) -> int:
+        """Replica blocks this node's replicas occupy in its holder (predecessor side)."""
+        return sum(len(b) for b in self.rep_bt)
+
+    def _admitted(self, s: int) -> None:
+        self.admit_ctr += 1
+        self.admit_seq[s] = self.admit_ctr
+        self.dropped[s] = False
+        self.rep_bt[s] = []
+
+    def _free_rep(self, s: int) -> None:
+        """Free slot s's replica blocks in the holder AT ONCE, after removing the
+        request from the holder's published table (parity of the published step):
+        a restore can then never read the reused blocks (the device does the same
+        with two small memsets ordered before any reuse)."""
+        h = self.holder
+        if h is None or not self.rep_bt[s]:
+            return
+        if self.last_step > 0 and not h.dead:
+            par = self.last_step & 1
+            h.rreq[par, s] = -1
+            h.rlen[par, s] = 0
+        h.free_blocks.update(self.rep_bt[s])
+        self.rep_bt[s] = []
+
+    def _free_all_reps(self) -> None:
+        for s in range(self.R):
+            self._free_rep(s)
+
+    def _evict_for(self, need_blocks: int) -> None:
+        """Holder side: drop the predecessor's replicas, oldest request first, until
+        ``need_blocks`` blocks are free."""
+        pred = self.rep_src
+        order = sorted((int(pred.admit_seq[s]), s) for s in range(pred.R)
+                       if pred.slot_req[s] >= 0 and pred.rep_bt[s])
+        for _, s in order:
+            if len(self.free_blocks) >= need_blocks:
+                break
+            pred._free_rep(s)
+            pred.dropped[s] = True
+            self.evictions += 1
+
+    def drop_replicas(self) -> None:
+        """Holder side: free every replica block held for the predecessor (after a
+        restore read them, or on demand); a dead predecessor is unlinked."""
+        pred = self.rep_src
+        if pred is None:
+            return
+        for s in range(pred.R):
+            if pred.rep_bt[s]:
+                pred._free_rep(s)
+                pred.dropped[s] = True
+        if pred.dead:
+            pred.holder = None
+            self.rep_src = None
 
     def replicate(self, step: int) -> int:
         """§8(c) step 5: copy tokens [pub_len, len) of every live slot to succ's replica.
@@ -200,15 +307,31 @@ class OracleNode:
         if m.dead:
             raise OracleError(ESTATE, "successor is dead; the harness must unlink it first")
         hi_all = np.zeros(self.R, dtype=np.int32)
+        shared = self.holder is not None
         for s in range(self.R):
             if self.slot_req[s] < 0:
                 continue
             lo, hi = int(self.pub_len[s]), self.published_len(s)
+            if shared and hi > lo:
+                # replica blocks come from the holder's own free list (R6 order);
+                # if it cannot hold the growth, this request's replica is dropped
+                grow = ceil_div(hi, B) - len(self.rep_bt[s])
+                if grow > len(m.free_blocks):
+                    self._free_rep(s)
+                    self.dropped[s] = True
+                    self.drops += 1
+                    continue
+                for _ in range(grow):
+                    self.rep_bt[s].append(m._take_block())
             hi_all[s] = hi
             if self.content:
                 for pos in range(lo, hi):
                     blk = self.slot_bt[s][pos // B]
-                    m.replica[blk, :, :, :, pos % B, :] = self.primary[blk, :, :, :, pos % B, :]
+                    if shared:
+                        dst = self.rep_bt[s][pos // B]
+                        m.primary[dst, :, :, :, pos % B, :] = self.primary[blk, :, :, :, pos % B, :]
+                    else:
+                        m.replica[blk, :, :, :, pos % B, :] = self.primary[blk, :, :, :, pos % B, :]
             moved += (hi - lo) * self.g.token_bytes
         par = step & 1
         m.rreq[par, :] = np.where(hi_all > 0, self.slot_req, -1)
@@ -216,7 +339,7 @@ class OracleNode:
         for s in range(self.R):
             if self.slot_req[s] >= 0:
                 nb = ceil_div(int(hi_all[s]), B)
-                m.rbt[s, :nb] = self.slot_bt[s][:nb]
+                m.rbt[s, :nb] = (self.rep_bt[s] if shared else self.slot_bt[s])[:nb]
         m.rseq = step
         self.pub_len[:] = hi_all
         self.last_step = step
@@ -243,7 +366,9 @@ class OracleNode:
         rebuild bt.  Returns (t*, [(req_id, resume_len)]).  The restored
         requests start unpublished (pub_len = 0).  ``holder`` may be this very
         node (promotion on the replication target, P:225 / reading R10): the
-        copy then runs from its replica region into its own primary pool.
+        copy then runs from its replica region into its own primary pool.  A
+        shared-capacity holder (NEXT-3) keeps the replica in its own pool; the
+        copy reads it there (the caller frees it afterwards: drop_replicas).
         """
         self._alive()
         if holder.dead or holder.rseq == 0:
@@ -260,6 +385,7 @@ class OracleNode:
             if r in self.slot_of:
                 raise OracleError(EINVAL, f"request {r} already present in restore target")
         out = []
+        store = holder.primary if holder.rep_src is not None else holder.replica
         for r, ln, hs in entries:
             s = min(self.free_slots)
             self.free_slots.remove(s)
@@ -267,13 +393,14 @@ class OracleNode:
             self.slot_req[s] = r
             self.slot_len[s] = ln
             self.pub_len[s] = 0
+            self._admitted(s)
             for j in range(ceil_div(ln, B)):
                 new = self._take_block()
                 self.slot_bt[s].append(new)
                 if self.content:
                     src_blk = int(holder.rbt[hs, j])
                     valid = min(B, ln - j * B)
-                    self.primary[new, :, :, :, :valid, :] = holder.replica[src_blk, :, :, :, :valid, :]
+                    self.primary[new, :, :, :, :valid, :] = store[src_blk, :, :, :, :valid, :]
             out.append((r, ln))
         return t_star, out
 

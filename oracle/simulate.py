@@ -28,7 +28,7 @@ from .ring import instance_ring, stage_ring
 class OracleRing:
     def __init__(self, cfg: Config, content: bool = True, ring: str | None = None,
                  restore_mode: str | None = None, seed: int = CONTENT_SEED,
-                 schedules=None, mode: str = "tokens"):
+                 schedules=None, mode: str = "tokens", shared: bool = False):
         self.cfg = cfg
         self.g = cfg.geom
         self.seed = seed
@@ -42,9 +42,10 @@ class OracleRing:
                                     node_id=k, content=content)
                       for k, c in enumerate(self.coords)}
         self.mode = mode
+        self.shared = shared      # NEXT-3: replicas inside the holder's own pool (R17)
         for c in self.coords:
             self.nodes[c].set_mode(mode)
-            self.nodes[c].set_successor(self.nodes[self.ring_fn(c, I, S)])
+            self.nodes[c].set_successor(self.nodes[self.ring_fn(c, I, S)], shared=shared)
         self.serving = dict(self.nodes)         # logical (pipeline, stage) -> node serving it
         self.extra_nodes: list[OracleNode] = []
         self.sched = schedules if schedules is not None else build_schedules(cfg)
@@ -128,6 +129,8 @@ class OracleRing:
         else:
             dst = holder
         t_star, restored = dst.restore_from(holder)
+        if self.shared:
+            holder.drop_replicas()    # the restore has read them; f is dead
         # resume: re-append what the replica lacks (<= 1 token per request, R3) and
         # re-admit requests absent from it (admitted in the unpublished step)
         keys = [k for k, n in self.serving.items() if n is f]
@@ -155,8 +158,8 @@ class OracleRing:
         if self.restore_mode == "fresh":
             for n in self.all_nodes():
                 if n is not dst and not n.dead and self.ring_fn_target(n) is f:
-                    n.set_successor(dst)
-            dst.set_successor(holder)
+                    n.set_successor(dst, shared=self.shared)
+            dst.set_successor(holder, shared=self.shared)
         self.events.append(("restore", t, coord, t_star, restored, ids, n_new))
         return t_star, restored, dst
 
@@ -174,7 +177,7 @@ class OracleRing:
             t = plan.get(c)
             want = None if t is None else self.serving[t]
             if n.succ is not want:
-                n.set_successor(want)
+                n.set_successor(want, shared=self.shared and want is not None)
         return plan
 
     def ring_fn_target(self, node: OracleNode):
@@ -221,12 +224,19 @@ def check_replica_equals_primary(n: OracleNode) -> None:
         hi = n.published_len(s)
         if hi > 0:
             want[r] = (s, hi, bt[:ceil_div(hi, B)])
+    if n.holder is not None:
+        # shared capacity (NEXT-3): the replica lives in the holder's pool at its own
+        # block ids; dropped requests are absent
+        want = {r: (s, hi, n.rep_bt[s][:ceil_div(hi, B)]) for r, (s, hi, _) in want.items()
+                if not n.dropped[s]}
     assert pub == want, "published metadata != primary tables"
     if n.content:
+        store = m.primary if n.holder is not None else m.replica
         for r, (s, ln, bt) in want.items():
             for j, blk in enumerate(bt):
                 v = min(B, ln - j * B)
-                assert np.array_equal(m.replica[blk, :, :, :, :v], n.primary[blk, :, :, :, :v]), (r, j)
+                src = n.slot_bt[s][j]
+                assert np.array_equal(store[blk, :, :, :, :v], n.primary[src, :, :, :, :v]), (r, j)
 
 
 def check_content(ring: OracleRing, node: OracleNode, stage: int, sample: int | None = None,
@@ -257,6 +267,8 @@ def check_tables(n: OracleNode) -> None:
         return
     B = n.g.block_size
     used = [b for s in range(n.R) for b in n.slot_bt[s]]
+    if n.rep_src is not None:      # shared capacity: the predecessor's replica blocks
+        used += [b for s in range(n.rep_src.R) for b in n.rep_src.rep_bt[s]]
     assert len(used) == len(set(used)), "block used twice"
     parts = [set(used), set(n.free_blocks), set(n.q_blocks)]
     assert sum(len(p) for p in parts) == n.NB and set().union(*parts) == set(range(n.NB))
