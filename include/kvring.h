@@ -116,6 +116,34 @@ int kv_pool_destroy(kv_pool_t *p);
 int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
                      int32_t succ_replica_blocks, void *succ_meta);
 
+/* Shared-capacity link (§8(f) NEXT-3, reading R17): §3.2 "KevlarFlow
+ * utilizes such memory headroom to temporarily handle ... the replicated KV
+ * cache.  When memory pressure happens, KevlarFlow drops the replicated KV cache
+ * and recomputes them if needed".
+ *   - holder h keeps p's replica IN ITS OWN POOL: replica blocks come from h's
+ *     free list (lowest id, R6) when p publishes; h's metadata bt rows hold h's
+ *     block ids (restore: pass h's pool as holder_replica, h's NB as its size);
+ *   - when an append on h needs more blocks than are free, h evicts p's
+ *     replicas, oldest admission first, until it fits; an append is rejected
+ *     (KV_ENOMEM, nothing changes) only if free + all replica blocks cannot
+ *     cover it;
+ *   - a request whose replica cannot grow (h full) is dropped, as is an evicted
+ *     one: it is listed as absent from then on and never re-sent (recompute on
+ *     failure);
+ *   - freed replica blocks are reusable AT ONCE: the entry that referenced them
+ *     is withdrawn from the published table (two memsets, flushed before the
+ *     next launch touching h).  Stream order needed: an append on h after the
+ *     ring-put of the previous step (kv_run_steps does it; the fused / PDL loops
+ *     reject shared pools, KV_EINVAL).
+ * Same device, geometry, max_reqs and max_blocks_per_req; one predecessor per
+ * holder (a previous one is unlinked, its replicas freed).  Re-seeds p. */
+int kv_set_successor_shared(kv_pool_t *p, kv_pool_t *holder);
+
+/* Holder side: free every replica block held for the predecessor (after a
+ * restore has read them -- promotion or fresh -- or on demand); those requests
+ * count as dropped.  A dead predecessor is unlinked.  Host-only. */
+int kv_drop_replicas(kv_pool_t *holder);
+
 /* Step boundary: blocks and slots quarantined by the
  * previous step become allocatable. */
 int kv_begin_step(kv_pool_t *p);
@@ -287,6 +315,11 @@ typedef struct {
   uint64_t tasks_launched;     /* copy tasks issued by replicate kernels      */
   uint64_t kernels_launched;   /* kernels issued by this pool (all kinds)     */
   uint64_t last_step_bytes;    /* payload bytes of the latest replicate       */
+  int64_t replica_blocks_held; /* shared capacity: predecessor replica blocks in this pool */
+  uint64_t replica_evictions;  /* shared capacity: replicas this holder evicted (requests) */
+  uint64_t replica_drops;      /* shared capacity: replicas dropped on growth (requests)   */
+  int32_t shared_holder;       /* node id of the shared-capacity holder, -1 if none        */
+  int32_t pad0;
 } kv_stats_t;
 int kv_stats(kv_pool_t *p, kv_stats_t *out);
 /* Per-slot tables: req_id (-1 empty), len, pub_len, nblk; arrays of max_reqs. */

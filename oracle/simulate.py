@@ -4,7 +4,8 @@ Drives every logical node of a config through the step protocol of SURVEY
 §8(c) (steps 1-7):
 
 for each step t:
-  per serving node, in node order: begin_step; release the retiring requests
+  per serving node, in serving order (by the first logical coordinate it
+  serves): begin_step; release the retiring requests
   of every pipeline it serves; ONE append with the decodes of all its
   requests in ascending req_id, then the admissions (pipeline order, FCFS);
   [failure at t: fail(f) after the appends, unlink pred(f), then restore:
@@ -86,7 +87,15 @@ class OracleRing:
     def appends(self, t: int):
         """Per serving node: begin_step, releases, one append (harness protocol)."""
         groups = self.served_by()
-        for node in self.all_nodes():
+        # serving order: by the first logical coordinate a node serves (a fresh
+        # restore pool takes the failed node's place); the order matters only
+        # between a shared-capacity holder and its predecessor (NEXT-3)
+        order = []
+        for key in sorted(self.serving):
+            n = self.serving[key]
+            if all(n is not m for m in order):
+                order.append(n)
+        for node in order:
             if node.dead or id(node) not in groups:
                 continue
             keys = groups[id(node)]

@@ -333,6 +333,25 @@ struct kv_pool {
   std::vector<int64_t> scratch_ids;
   std::vector<int> scratch_slot;  // slot of each append entry found by validation (-1: new)
   TaskVec scratch_tasks;
+  // shared-capacity mode (§8(f) NEXT-3, reading R17): the successor
+  // `holder` keeps this pool's replicas in ITS OWN pool.  Predecessor side: per
+  // slot the holder block ids of the replica, whether it was dropped, and the
+  // admission order (eviction age).  Holder side: `rep_src`, the predecessor whose
+  // replicas it holds, the census of those blocks, and published-table entries to
+  // invalidate on the device before freed replica blocks are reused.
+  kv_pool *holder = nullptr, *rep_src = nullptr;
+  std::vector<std::vector<int32_t>> rep_bt;
+  std::vector<uint8_t> dropped;
+  std::vector<uint64_t> admit_seq;
+  uint64_t admit_ctr = 0;
+  long long census = 0;                       // predecessor side: replica blocks in holder
+  struct Inval {
+    char *meta;
+    int par, slot;
+  };
+  std::vector<Inval> pending_inval;           // holder side
+  uint64_t rep_evictions = 0, rep_drops = 0;
+  long long scratch_need = 0;                 // blocks the current append needs
   // state
   bool dead = false;
   uint64_t last_step = 0;
@@ -400,6 +419,58 @@ inline void push_publish_only(TaskVec &out, int16_t pool) {
   out.push_back(t);
 }
 
+// ---- shared capacity (NEXT-3, reading R17) ----------------------------------
+// A replica block is freed AT ONCE, after its request is withdrawn from the
+// holder's published table (the parity of the step last published): the device
+// does that with two small memsets, flushed ahead of the next launch that may
+// reuse the block (the holder's append, or the predecessor's ring-put).
+void free_rep(kv_pool *p, int s) {
+  kv_pool *h = p->holder;
+  if (!h || p->rep_bt[s].empty()) return;
+  if (p->last_step > 0 && !h->dead && h->device >= 0)
+    h->pending_inval.push_back({p->succ_meta, (int)(p->last_step & 1), s});
+  for (int b : p->rep_bt[s]) h->free_blocks.insert(b);
+  p->census -= (long long)p->rep_bt[s].size();
+  p->rep_bt[s].clear();
+}
+
+void free_all_reps(kv_pool *p) {
+  for (int s = 0; s < p->R; ++s) free_rep(p, s);
+}
+
+// Holder side: drop the predecessor's replicas, oldest admission first, until
+// `need` blocks are free ("drops the replicated KV cache").
+void evict_for(kv_pool *h, long long need) {
+  kv_pool *pred = h->rep_src;
+  if (!pred) return;
+  std::vector<std::pair<uint64_t, int>> order;
+  for (int s = 0; s < pred->R; ++s)
+    if (pred->slot_req[s] >= 0 && !pred->rep_bt[s].empty())
+      order.push_back({pred->admit_seq[s], s});
+  std::sort(order.begin(), order.end());
+  for (auto &o : order) {
+    if (h->free_blocks.size() >= need) break;
+    free_rep(pred, o.second);
+    pred->dropped[o.second] = 1;
+    h->rep_evictions++;
+  }
+}
+
+// Unlinks a shared predecessor from its holder (replicas freed).
+void unlink_holder(kv_pool *p) {
+  if (!p->holder) return;
+  free_all_reps(p);
+  if (p->holder->rep_src == p) p->holder->rep_src = nullptr;
+  p->holder = nullptr;
+}
+
+void admitted(kv_pool *p, int s) {
+  p->admit_seq[s] = ++p->admit_ctr;
+  p->dropped[s] = 0;
+  p->census -= (long long)p->rep_bt[s].size();  // (empty: freed at release)
+  p->rep_bt[s].clear();
+}
+
 // ---- append ---------------------------------------------------------------
 // Validates one pool's releases + appends against `free_b` / `free_s` free
 // blocks / slots (the counts after the optional begin_step).  No allocation
@@ -452,9 +523,13 @@ int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, lon
       if (p->scratch_ids[i] == p->scratch_ids[i - 1])
         return fail(KV_EINVAL, "request %lld twice in one append", (long long)p->scratch_ids[i]);
   }
-  if (need_slots > free_s || need_blocks > free_b)
+  // a shared-capacity holder may evict its predecessor's replicas to make room
+  // (no rejection while the census could cover the need)
+  const long long census = p->rep_src ? p->rep_src->census : 0;
+  if (need_slots > free_s || need_blocks > free_b + census)
     return fail(KV_ENOMEM, "pool %d exhausted (need %lld blocks / %lld slots, free %lld / %lld)",
                 p->node_id, need_blocks, need_slots, free_b, free_s);
+  p->scratch_need = need_blocks;
   if (tokens > 0x7fffffffLL) return fail(KV_EINVAL, "too many tokens in one append");
   return KV_OK;
 }
@@ -470,6 +545,10 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
   for (int i = 0; i < n; ++i) {
     const int s = p->slot_of.find(ids[i]);
     p->slot_of.erase(ids[i]);
+    if (p->holder) {
+      free_rep(p, s);
+      p->dropped[s] = 0;
+    }
     for (int b : p->slot_bt[s]) p->q_blocks.push_back(b);
     p->slot_bt[s].clear();
     p->q_slots.push_back(s);
@@ -495,6 +574,7 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, TaskVec &tas
       p->slot_len[s] = 0;
       p->pub_len[s] = 0;
       p->slot_bt[s].clear();
+      admitted(p, s);
     }
     int len = p->slot_len[s];
     int left = a.n_new[i];
@@ -516,6 +596,7 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, TaskVec &tas
 // Length a publication of slot s reaches: every appended token (KV_MODE_TOKENS,
 // reading R2) or the completed blocks only (KV_MODE_BLOCKS, P:229 literal).
 inline int pub_hi(const kv_pool *p, int s) {
+  if (p->holder && p->dropped[s]) return 0;  // a dropped replica is never re-sent
   const int len = p->slot_len[s];
   if (p->repl_mode == KV_MODE_BLOCKS) return std::max(p->pub_len[s], len - len % p->g.block_size);
   return len;
@@ -544,15 +625,31 @@ uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, TaskVec &tasks, bool packed
                            std::vector<int> *ce_blocks = nullptr) {
   const int B = p->g.block_size;
   uint64_t bytes = 0;
+  kv_pool *h = p->holder;
   for (int s = 0; s < p->R; ++s) {
     if (p->slot_req[s] < 0) continue;
     int pos = p->pub_len[s];
     const int len = pub_hi(p, s);
+    if (h && pos < len) {
+      // shared capacity: the replica's blocks come from the holder's free list
+      // (lowest id, R6); a request whose replica cannot grow is dropped
+      const long long grow = (long long)ceil_div(len, B) - (long long)p->rep_bt[s].size();
+      if (grow > h->free_blocks.size()) {
+        free_rep(p, s);
+        p->dropped[s] = 1;
+        p->rep_drops++;
+        continue;
+      }
+      for (long long k = 0; k < grow; ++k) p->rep_bt[s].push_back(h->free_blocks.take_min());
+      p->census += grow;
+    }
     while (pos < len) {
       const int j = pos / B, lo = pos % B;
       const int n = std::min(B - lo, len - pos);
       const int blk = p->slot_bt[s][j];
-      if (ce_blocks && lo == 0 && n == B) {
+      if (h) {
+        push_item(tasks, pidx, blk, p->rep_bt[s][j], s, j, lo, n, p->combos, task_segs);
+      } else if (ce_blocks && lo == 0 && n == B) {
         // copy-engine variant: the whole block moves by cudaMemcpyAsync; the kernel
         // only writes its bt entry (a zero-slice task) and counts it for publication
         KvTask t{};
@@ -642,6 +739,9 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
   p->app_stamp.assign(p->R, 0);
   p->slot_of.init(p->R);
   for (auto &v : p->slot_bt) v.reserve(8);
+  p->rep_bt.assign(p->R, {});
+  p->dropped.assign(p->R, 0);
+  p->admit_seq.assign(p->R, 0);
   if (p->device >= 0) {
     DeviceGuard dg(p->device);
     if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", p->device);
@@ -659,6 +759,14 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
 
 KV_API int kv_pool_destroy(kv_pool_t *p) {
   if (!p) return KV_OK;
+  if (p->holder) unlink_holder(p);
+  if (p->rep_src) {
+    p->rep_src->census = 0;
+    for (auto &v : p->rep_src->rep_bt) v.clear();
+    p->rep_src->holder = nullptr;
+    p->rep_src->has_succ = false;
+    p->rep_src = nullptr;
+  }
   if (p->counter) {
     DeviceGuard dg(p->device);
     cudaDeviceSynchronize();
@@ -672,6 +780,8 @@ KV_API int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
                             int32_t succ_replica_blocks, void *succ_meta) {
   if (!p) return fail(KV_EINVAL, "null pool");
   if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+  unlink_holder(p);  // leaving shared-capacity mode frees the replicas it held
+  std::fill(p->dropped.begin(), p->dropped.end(), 0);
   if (succ_replica == nullptr) {
     p->has_succ = false;
     p->succ_replica = nullptr;
@@ -697,6 +807,44 @@ KV_API int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
     p->succ_meta = static_cast<char *>(succ_meta);
   }
   std::fill(p->pub_len.begin(), p->pub_len.end(), 0);  // re-seed the new link
+  return KV_OK;
+}
+
+KV_API int kv_set_successor_shared(kv_pool_t *p, kv_pool_t *h) {
+  if (!p || !h) return fail(KV_EINVAL, "null pool");
+  if (p == h) return fail(KV_EINVAL, "a pool cannot hold its own replicas");
+  if (p->dead || h->dead) return fail(KV_ESTATE, "pool is dead");
+  if (p->device != h->device || !p->same_geom(*h) || p->R != h->R || p->M != h->M)
+    return fail(KV_EINVAL, "shared capacity needs the same device, geometry, max_reqs, max_blocks");
+  unlink_holder(p);
+  if (h->rep_src && h->rep_src != p) unlink_holder(h->rep_src);  // one predecessor per holder
+  if (h->rep_src == p) h->rep_src = nullptr;
+  p->holder = h;
+  h->rep_src = p;
+  p->has_succ = true;
+  p->succ_sys = false;
+  p->succ_node = h->node_id;
+  p->succ_replica = h->pool;  // the replica lives in the holder's own pool
+  p->succ_replica_blocks = h->NB;
+  p->succ_meta = h->meta;
+  std::fill(p->pub_len.begin(), p->pub_len.end(), 0);  // re-seed
+  std::fill(p->dropped.begin(), p->dropped.end(), 0);
+  return KV_OK;
+}
+
+KV_API int kv_drop_replicas(kv_pool_t *h) {
+  if (!h) return fail(KV_EINVAL, "null pool");
+  kv_pool *pred = h->rep_src;
+  if (!pred) return KV_OK;
+  for (int s = 0; s < pred->R; ++s)
+    if (!pred->rep_bt[s].empty()) {
+      free_rep(pred, s);
+      pred->dropped[s] = 1;
+    }
+  if (pred->dead) {
+    pred->holder = nullptr;
+    h->rep_src = nullptr;
+  }
   return KV_OK;
 }
 
@@ -739,6 +887,8 @@ struct Launch {
   std::vector<size_t> host_src_bytes;
   std::vector<std::vector<int>> ce_blocks;  // copy-engine variant: full blocks per pool
   bool use_ce = false;
+  std::vector<kv_pool::Inval> inval;  // shared capacity: published entries to withdraw first
+  int max_reqs_inval = 0;
   // filled by stage()
   const KvPoolParams *params_dev = nullptr;
   const KvTask *tasks_dev = nullptr;
@@ -756,6 +906,7 @@ struct Launch {
     if ((int)ce_blocks.size() < n) ce_blocks.resize(n);
     for (auto &v : ce_blocks) v.clear();
     use_ce = false;
+    inval.clear();
     params_dev = nullptr;
     tasks_dev = nullptr;
   }
@@ -764,6 +915,21 @@ struct Launch {
            sizeof(KvTask) * tasks.size();
   }
 };
+
+// Moves the pending published-entry invalidations of every holder this launch
+// touches (its pools, and the holders of its pools) into the launch.
+void collect_inval(Launch &L, kv_pool *const *pools, int n) {
+  auto take = [&](kv_pool *h) {
+    if (!h || h->pending_inval.empty()) return;
+    L.max_reqs_inval = h->R;
+    L.inval.insert(L.inval.end(), h->pending_inval.begin(), h->pending_inval.end());
+    h->pending_inval.clear();
+  };
+  for (int k = 0; k < n; ++k) {
+    take(pools[k]);
+    take(pools[k]->holder);
+  }
+}
 
 // Task size for one launch: spread the launch's slices over every resident CTA
 // (SMs x 4) so a decode-sized step runs in one wave, capped at 32 KiB per task.
@@ -829,6 +995,7 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
     kv_pool *p = args[k].pool;
     if (args[k].begin_step) do_begin_step(p);
     do_release(p, args[k].n_release, args[k].release_ids);
+    if (p->scratch_need > p->free_blocks.size()) evict_for(p, p->scratch_need);
     const size_t before = L.tasks.size();
     do_append(p, args[k], (int16_t)k, L.tasks, task_segs);
     L.ntask[k] = (int)(L.tasks.size() - before);
@@ -844,6 +1011,7 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
       L.host_src_bytes[k] = (size_t)rows * p->token_bytes;
     }
   }
+  collect_inval(L, pools, n_pools);
   return KV_OK;
 }
 
@@ -909,6 +1077,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     static const int sys_per_cta = getenv("KVRING_SYS_PER_CTA") ? 1 : 0;  // experiments
     pp.pad0 = sys_per_cta;
   }
+  collect_inval(L, pools, n_pools);
   return KV_OK;
 }
 
@@ -986,7 +1155,23 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
   return KV_OK;
 }
 
+// Shared capacity: withdraw the freed replicas' published entries (req_id -1,
+// len 0 in the published parity) before this launch may reuse their blocks.
+int flush_inval(Launch &L, cudaStream_t st) {
+  for (const auto &iv : L.inval) {
+    const int R = L.max_reqs_inval;
+    CU(cudaMemsetAsync(iv.meta + 32 + ((size_t)iv.par * R + iv.slot) * 8, 0xFF, 8, st));
+    CU(cudaMemsetAsync(iv.meta + meta_off_len(R) + ((size_t)iv.par * R + iv.slot) * 4, 0, 4, st));
+  }
+  L.inval.clear();
+  return KV_OK;
+}
+
 int enqueue(Launch &L, cudaStream_t st) {
+  if (!L.inval.empty() && L.p0 && L.p0->device >= 0) {
+    int rc = flush_inval(L, st);
+    if (rc) return rc;
+  }
   if (L.tasks.empty()) return KV_OK;
   int kind = L.kind;
   if (kind == kKindRingPut) {
@@ -1055,7 +1240,12 @@ KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *
   Launch &L = g_append_launch;
   int rc = prepare_append(n_pools, args, L);
   if (rc) return rc;
-  if (L.p0->device < 0 || L.tasks.empty()) return KV_OK;
+  if (L.p0->device < 0) return KV_OK;
+  if (L.tasks.empty()) {
+    if (L.inval.empty()) return KV_OK;
+    DeviceGuard dg(L.p0->device);
+    return flush_inval(L, static_cast<cudaStream_t>(stream));
+  }
   DeviceGuard dg(L.p0->device);
   if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1193,6 +1383,7 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
     dst->slot_len[s] = e.len;
     dst->pub_len[s] = 0;
     dst->slot_bt[s].clear();
+    admitted(dst, s);
     for (int j = 0; j < ceil_div(e.len, B); ++j) {
       const int nb = dst->free_blocks.take_min();
       dst->slot_bt[s].push_back(nb);
@@ -1268,6 +1459,7 @@ KV_API int kv_pack_bytes(kv_pool_t *p, size_t *bytes_out) {
 
 KV_API int kv_pack_step(kv_pool_t *p, uint64_t step, void *packed, size_t cap, size_t *bytes_out,
                         void *stream) {
+  if (p && p->holder) return fail(KV_EINVAL, "kv_pack_step does not support shared-capacity links");
   if (!p || !packed) return fail(KV_EINVAL, "null argument");
   if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
   if (p->device < 0) return fail(KV_ESTATE, "pack needs a device pool");
@@ -1401,6 +1593,10 @@ KV_API int kv_stats(kv_pool_t *p, kv_stats_t *o) {
   o->tasks_launched = p->tasks_launched;
   o->kernels_launched = p->kernels;
   o->last_step_bytes = p->last_step_bytes;
+  o->replica_blocks_held = p->rep_src ? p->rep_src->census : 0;
+  o->replica_evictions = p->rep_evictions;
+  o->replica_drops = p->rep_drops;
+  o->shared_holder = p->holder ? p->holder->node_id : -1;
   return KV_OK;
 }
 
@@ -1435,6 +1631,7 @@ namespace {
 struct StepPrep {
   Launch A, P;
   bool has_a = false, has_p = false;
+  bool shared = false;  // a pool of this step is in shared-capacity mode (NEXT-3)
   int rc = KV_OK;
   std::string err;
 };
@@ -1442,10 +1639,23 @@ struct StepPrep {
 // Tables, work lists and (already) committed publication state of step k.
 // Commit happens here, before the launch: the next step's dirty ranges start
 // where this one ends; a launch error is sticky and ends the run anyway.
+bool any_shared(const kv_step_t &st) {
+  for (int i = 0; i < st.n_append; ++i) {
+    const kv_pool *p = st.append[i].pool;
+    if (p && (p->holder || p->rep_src)) return true;
+  }
+  for (int i = 0; i < st.n_repl; ++i) {
+    const kv_pool *p = st.repl_pools[i];
+    if (p && (p->holder || p->rep_src)) return true;
+  }
+  return false;
+}
+
 void prepare_step(const kv_step_t &st, StepPrep &sp) {
   sp.has_a = st.n_append > 0;
   sp.has_p = st.n_repl > 0;
   sp.rc = KV_OK;
+  sp.shared = any_shared(st);
   const double t0 = now_s();
   if (sp.has_a && (sp.rc = prepare_append(st.n_append, st.append, sp.A))) {
     sp.err = g_err;
@@ -1504,7 +1714,7 @@ int issue_step(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa, 
                StreamOrder &so) {
   kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
   if (!p0 || p0->device < 0) return KV_OK;  // nothing to launch / tables-only pools
-  if (sp.has_a && sp.A.tasks.empty() && !sp.has_p) return KV_OK;
+  if (sp.has_a && sp.A.tasks.empty() && sp.A.inval.empty() && !sp.has_p) return KV_OK;
   DeviceGuard dg(p0->device);
   DeviceCtx *ctx = ctx_for(p0->device);
   std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1521,8 +1731,11 @@ int issue_step(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa, 
   g_phase[kPhStage] += t1 - t0;
   if (sa != sr && (rc = so.ensure(p0->device))) return rc;
   if (sp.has_a) {
-    if (sa != sr && k >= 2 && so.rstep[(k - 2) % StreamOrder::kN] == k - 2)
-      CU(cudaStreamWaitEvent(sa, so.rdone[(k - 2) % StreamOrder::kN], 0));
+    // shared capacity: a freed replica block may be reused by this very append, so
+    // the ring-put that last wrote it (k-1) must be complete
+    const int lag = sp.shared ? 1 : 2;
+    if (sa != sr && k >= lag && so.rstep[(k - lag) % StreamOrder::kN] == k - lag)
+      CU(cudaStreamWaitEvent(sa, so.rdone[(k - lag) % StreamOrder::kN], 0));
     g_ev_before = static_cast<cudaEvent_t>(st.ev_append_start);
     g_ev_after = static_cast<cudaEvent_t>(st.ev_append_end);
     rc = enqueue(sp.A, sa);
@@ -1766,6 +1979,9 @@ int issue_fused(const kv_step_t *ev_step, FusedPrep &fp, cudaStream_t st) {
 // no cross-stream event; the publication of a step trails its append by one launch
 // -- the overlap of replication with the next step's compute of P:229.
 KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream) {
+  for (int k = 0; k < n_steps && steps; ++k)
+    if (any_shared(steps[k]))
+      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps (append after ring-put k-1)");
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int n_launch = n_steps + 1;  // + the flush of the last publication
@@ -1927,6 +2143,9 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
 // a cross-stream event per step.  A helper thread prepares step k+1 meanwhile.
 KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
+  for (int k = 0; k < n_steps; ++k)
+    if (any_shared(steps[k]))
+      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps (append after ring-put k-1)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   StepPrep ring[2];
   std::atomic<int> produced{0}, consumed{0};

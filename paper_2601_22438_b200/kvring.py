@@ -28,7 +28,7 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
             "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused", "kv_run_steps_pdl",
-            "kv_replicate_step_ce"]
+            "kv_replicate_step_ce", "kv_set_successor_shared", "kv_drop_replicas"]
 
 
 class KvError(RuntimeError):
@@ -75,7 +75,10 @@ class kv_stats_t(ctypes.Structure):
                 ("dead", ctypes.c_int32), ("has_successor", ctypes.c_int32),
                 ("last_step", ctypes.c_uint64), ("bytes_replicated", ctypes.c_uint64),
                 ("tasks_launched", ctypes.c_uint64), ("kernels_launched", ctypes.c_uint64),
-                ("last_step_bytes", ctypes.c_uint64)]
+                ("last_step_bytes", ctypes.c_uint64),
+                ("replica_blocks_held", ctypes.c_int64), ("replica_evictions", ctypes.c_uint64),
+                ("replica_drops", ctypes.c_uint64), ("shared_holder", ctypes.c_int32),
+                ("pad0", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -126,6 +129,8 @@ def lib() -> ctypes.CDLL:
             "kv_run_steps_fused": (ctypes.c_int, [_I32, _P, _P]),
             "kv_run_steps_pdl": (ctypes.c_int, [_I32, _P, _P]),
             "kv_replicate_step_ce": (ctypes.c_int, [_I32, _P, _U64, _P]),
+            "kv_set_successor_shared": (ctypes.c_int, [_P, _P]),
+            "kv_drop_replicas": (ctypes.c_int, [_P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_set_mode": (ctypes.c_int, [_P, _I32]),
@@ -286,6 +291,14 @@ def kv_replicate_step_multi(pools, step: int, stream: int = 0) -> None:
 
 def kv_set_mode(p: int, mode: int) -> None:
     _check(lib().kv_set_mode(p, mode))
+
+
+def kv_set_successor_shared(p: int, holder: int) -> None:
+    _check(lib().kv_set_successor_shared(p, holder))
+
+
+def kv_drop_replicas(holder: int) -> None:
+    _check(lib().kv_drop_replicas(holder))
 
 
 def kv_replicate_step_ce(pools, step: int, stream: int = 0) -> None:

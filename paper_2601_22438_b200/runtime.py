@@ -78,8 +78,11 @@ class RingRuntime:
                  placement: dict[int, int], succ: dict[int, int], rank: int = 0, world: int = 1,
                  device: int | None = None, spares: int = 1, group=None,
                  sentinel: int | None = SENTINEL_WORD, dtype_words=torch.int16,
-                 mode: int = K.KV_MODE_TOKENS):
+                 mode: int = K.KV_MODE_TOKENS, shared: bool = False):
         self.g = geom
+        # shared capacity (NEXT-3): a successor on this rank keeps the replica in
+        # its own pool (kv_set_successor_shared); the replica regions stay unused
+        self.shared = shared
         self.NB, self.R, self.M = num_blocks, max_reqs, max_blocks_per_req
         self.placement = dict(placement)
         self.succ = dict(succ)
@@ -164,6 +167,10 @@ class RingRuntime:
         h = self.local[node].handle
         if m is None or m in self.dead:
             K.kv_set_successor(h, -1, None, 0, None)
+        elif self.shared:
+            if m not in self.local:
+                raise RuntimeError("shared-capacity links need the successor on this rank")
+            K.kv_set_successor_shared(h, self.local[m].handle)
         else:
             K.kv_set_successor(h, m, self.replica_ptr(m), self.NB, self.meta_ptr(m))
 
@@ -217,7 +224,14 @@ class RingRuntime:
             self._create(node, self.slots[k])
 
     def restore(self, dst: int, holder: int, stream=None):
-        """kv_restore into local pool ``dst`` from ``holder``'s replica (local or peer)."""
+        """kv_restore into local pool ``dst`` from ``holder``'s replica (local or peer).
+        Shared capacity: the replica is read from the holder's own pool, whose
+        replica blocks are then freed (kv_drop_replicas)."""
+        if self.shared:
+            out = K.kv_restore(self.handle(dst), self.local[holder].pool.data_ptr(), self.NB,
+                               self.meta_ptr(holder), self._stream(stream))
+            K.kv_drop_replicas(self.handle(holder))
+            return out
         return K.kv_restore(self.handle(dst), self.replica_ptr(holder), self.NB,
                             self.meta_ptr(holder), self._stream(stream))
 

@@ -14,7 +14,7 @@ from oracle.simulate import OracleRing
 
 
 def make_gpu(cfg, ring="stage", device=0, spares=1, schedules=None, restore_mode=None,
-             mode="tokens"):
+             mode="tokens", shared=False):
     from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
     from kvgen.configs import build_schedules
     I, S = cfg.pipelines, cfg.stages
@@ -26,7 +26,8 @@ def make_gpu(cfg, ring="stage", device=0, spares=1, schedules=None, restore_mode
     from paper_2601_22438_b200 import kvring as K
     rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement,
                      succ, rank=0, world=1, device=device, spares=spares,
-                     mode=K.KV_MODE_BLOCKS if mode == "blocks" else K.KV_MODE_TOKENS)
+                     mode=K.KV_MODE_BLOCKS if mode == "blocks" else K.KV_MODE_TOKENS,
+                     shared=shared)
     g = cfg.geom
 
     def content(stage, ids, pos):
@@ -78,3 +79,11 @@ def compare_state(rt, drv, oring: OracleRing, content: bool = True, tag="", only
                     live[int(req[s])] = (s, int(ln[s]), K.kv_query(rt.handle(gid), int(req[s]))[1])
             assert live == on.live(), (tag, gid)
             assert np.array_equal(pub, on.pub_len), (tag, gid)
+            st = K.kv_stats(rt.handle(gid))
+            assert st["free_blocks"] == len(on.free_blocks), (tag, gid)
+            assert st["quarantined_blocks"] == len(on.q_blocks), (tag, gid)
+            # shared capacity (NEXT-3): evictions, drops and the held-replica census
+            assert st["replica_evictions"] == on.evictions, (tag, gid)
+            assert st["replica_drops"] == on.drops, (tag, gid)
+            held = on.rep_src.census() if on.rep_src is not None else 0
+            assert st["replica_blocks_held"] == held, (tag, gid, st["replica_blocks_held"], held)

@@ -17,10 +17,12 @@ from gpu_harness import compare_state, make_gpu  # noqa: E402
 
 
 def _run_both(cfg, ring="stage", schedules=None, every=1, fail=True, restore_mode=None,
-              copy_engine=False):
-    rt, drv = make_gpu(cfg, ring=ring, schedules=schedules, restore_mode=restore_mode)
+              copy_engine=False, shared=False):
+    rt, drv = make_gpu(cfg, ring=ring, schedules=schedules, restore_mode=restore_mode,
+                       shared=shared)
     rt.copy_engine = copy_engine
-    oring = OracleRing(cfg, ring=ring, schedules=drv.sched, restore_mode=restore_mode)
+    oring = OracleRing(cfg, ring=ring, schedules=drv.sched, restore_mode=restore_mode,
+                       shared=shared)
     try:
         for t in range(cfg.n_steps):
             drv.append_step(t)
@@ -241,16 +243,19 @@ def test_c2_full_size_sampled():
         rt.destroy()
 
 
-def test_run_steps_two_streams_bit_exact():
+@pytest.mark.parametrize("shared", [False, True])
+def test_run_steps_two_streams_bit_exact(shared):
     """kv_run_steps (the native decode loop the bench times: append on one stream,
-    publish on a second stream after an event) == oracle, whole arrays."""
+    publish on a second stream after an event) == oracle, whole arrays; shared:
+    the NEXT-3 shared-capacity links under memory pressure (evictions + drops)."""
     from paper_2601_22438_b200 import kvring as K
-    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
-                         batch_cap=6, n_requests=60, n_steps=30, fixed_prompt=None,
+    cfg = configs.scaled(configs.C1, num_blocks=28 if shared else 96, max_reqs=12,
+                         max_blocks_per_req=12, batch_cap=5 if shared else 6, n_requests=60,
+                         n_steps=40 if shared else 30, fixed_prompt=None,
                          fail_node=None, fail_step=None)
-    sched = _churn_sched(cfg, 21)
-    rt, drv = make_gpu(cfg, schedules=sched)
-    oring = OracleRing(cfg, schedules=sched)
+    sched = _churn_sched(cfg, 1 if shared else 21)
+    rt, drv = make_gpu(cfg, schedules=sched, shared=shared)
+    oring = OracleRing(cfg, schedules=sched, shared=shared)
     try:
         comp = torch.cuda.current_stream()
         repl = torch.cuda.Stream()
@@ -273,6 +278,11 @@ def test_run_steps_two_streams_bit_exact():
         K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
         torch.cuda.synchronize()
         compare_state(rt, drv, oring, tag="run_steps")
+        if shared:
+            assert sum(n.evictions for n in oring.nodes.values()) > 0
+            assert sum(n.drops for n in oring.nodes.values()) > 0
+            with pytest.raises(K.KvError):     # the PDL / fused loops refuse shared pools
+                K.kv_run_steps_pdl(K.PreparedSteps(steps[:1]), comp.cuda_stream)
     finally:
         rt.destroy()
 
@@ -528,3 +538,28 @@ def test_copy_engine_variant_bit_exact(seed):
                          fail_node=(0, 2), fail_step=21)
     rt, drv, oring = _run_both(cfg, schedules=_churn_sched(cfg, seed), copy_engine=True)
     rt.destroy()
+
+
+# (seed, ring, restore, blocks, batch cap, slots): evictions AND drops occur (oracle pins)
+SHARED_PRESSURE = [(0, "stage", "fresh", 32, 5, 12), (1, "stage", "fresh", 28, 5, 12),
+                   (4, "instance", "promote", 48, 5, 24)]
+
+
+@pytest.mark.parametrize("seed,ring,restore_mode,nb,cap,slots", SHARED_PRESSURE)
+def test_shared_capacity_pressure_bit_exact(seed, ring, restore_mode, nb, cap, slots):
+    """NEXT-3 (reading R17): replicas in the holder's own pool, evicted oldest-first
+    when the holder's appends need the memory, dropped when they cannot grow; a
+    failure restored from the shared holder (fresh pool, or promotion onto the
+    holder).  Whole pools, metadata, tables, evictions, drops and census == oracle
+    at every step."""
+    cfg = configs.scaled(configs.C1, num_blocks=nb, max_reqs=slots, max_blocks_per_req=12,
+                         batch_cap=cap, n_requests=60, n_steps=40, fixed_prompt=None,
+                         pipelines=2 if ring == "instance" else 1, ring=ring,
+                         fail_node=(0, 2) if ring == "instance" else (0, 1), fail_step=23)
+    rt, drv, oring = _run_both(cfg, ring=ring, schedules=_churn_sched(cfg, seed),
+                               restore_mode=restore_mode, shared=True)
+    try:
+        assert sum(n.evictions for n in oring.all_nodes()) > 0
+        assert sum(n.drops for n in oring.all_nodes()) > 0
+    finally:
+        rt.destroy()

@@ -208,3 +208,48 @@ def test_run_steps_fused_tables_match_oracle():
     finally:
         for h in hs.values():
             K.kv_pool_destroy(h)
+
+
+@pytest.mark.parametrize("seed,nb", [(0, 32), (1, 28), (3, 24)])
+def test_shared_capacity_tables_match_oracle(seed, nb):
+    """NEXT-3 (reading R17) on tables-only pools: the C++ allocator, eviction
+    (oldest admission first), drops on growth and the held-replica census equal
+    the oracle's step by step under memory pressure (stage ring, no failure)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_oracle_shared import _pressure_cfg, _sched
+    cfg = _pressure_cfg(num_blocks=nb, fail_node=None, fail_step=None)
+    sch = _sched(cfg, seed)
+    ring = OracleRing(cfg, content=False, shared=True, schedules=sch)
+    coords = ring.coords
+    hs = {c: _pool(cfg, k) for k, c in enumerate(coords)}
+    S = cfg.stages
+    for c in coords:
+        K.kv_set_successor_shared(hs[c], hs[(c[0], (c[1] + 1) % S)])
+    try:
+        for t in range(cfg.n_steps):
+            ring.appends(t)
+            for c in coords:       # one call per node, node order (the harness protocol)
+                ev = sch[c[0]].steps[t]
+                K.kv_append_multi([dict(pool=hs[c], begin_step=1, release=ev.retire,
+                                        req_ids=sorted(ev.decode) + [r for r, _ in ev.admit],
+                                        n_new=[1] * len(ev.decode) + [pp for _, pp in ev.admit],
+                                        src=None)])
+            if t >= 1:
+                ring.replicate(t)
+                for c in coords:
+                    K.kv_replicate_step(hs[c], t)
+            for c in coords:
+                n = ring.nodes[c]
+                st = K.kv_stats(hs[c])
+                assert _tables(hs[c], cfg.max_reqs) == n.live(), (t, c)
+                assert st["free_blocks"] == len(n.free_blocks), (t, c)
+                assert st["quarantined_blocks"] == len(n.q_blocks), (t, c)
+                assert st["replica_evictions"] == n.evictions, (t, c)
+                assert st["replica_drops"] == n.drops, (t, c)
+                assert st["replica_blocks_held"] == n.rep_src.census(), (t, c)
+        assert sum(n.evictions for n in ring.nodes.values()) > 0
+        assert sum(n.drops for n in ring.nodes.values()) > 0
+    finally:
+        for h in hs.values():
+            K.kv_pool_destroy(h)
