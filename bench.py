@@ -60,6 +60,8 @@ def parse():
                     help="steps in block-granular mode (NEXT-2), after a re-seed (0: skip)")
     ap.add_argument("--nccl-steps", type=int, default=100,
                     help="steps replicated through the NCCL send/recv comparison (0: skip)")
+    ap.add_argument("--shared-steps", type=int, default=100,
+                    help="timed steps of the shared-capacity leg (NEXT-3; N = 1 only; 0: skip)")
     ap.add_argument("--timeline", action="store_true",
                     help="diagnostic: time every step and print the replication-stream timeline")
     ap.add_argument("--loop", default="streams", choices=["fused", "streams", "pdl"],
@@ -355,6 +357,12 @@ def run_kvring(args):
     torch.cuda.empty_cache()
     bulk = run_bulk(args, rank, world, local_rank, dev, group) if args.bulk_reps > 0 else None
 
+    # ---- shared capacity (NEXT-3): replicas in the holder's own pool, under pressure -
+    shared = None
+    if args.shared_steps > 0:
+        shared = (run_shared(args, local_rank, dev) if world == 1 else
+                  {"skipped": "shared capacity needs the holder on the same GPU (N = 1)"})
+
     # ---- reduce over ranks --------------------------------------------------------
     vec = torch.tensor([ms, my_bytes, float(launches), wall], dtype=torch.float64, device=dev)
     if world > 1:
@@ -464,6 +472,8 @@ def run_kvring(args):
         line["interference"] = interference
     if block is not None:
         line["block_mode"] = block
+    if shared is not None:
+        line["shared_capacity"] = shared
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, t_timed0, min(args.steps, 60))
     if rank == 0:
@@ -800,6 +810,101 @@ def run_block_mode(args, drv, rt, t0, comp, repl, content, dev, world):
                                    "avg": round(sum(kern) / len(kern), 2)},
             "replica_lag_tokens": {"mean": round(float(np.mean(lags)), 2) if lags else 0.0,
                                    "max": int(max(lags)) if lags else 0}}
+
+
+SHARED_NB = 2048   # C2 primary peak is ~1.57k blocks per stage: replicas must compete
+
+
+def run_shared(args, local_rank, dev):
+    """NEXT-3 (§3.2, reading R17): C2 on one GPU with each
+    stage's pool cut to SHARED_NB blocks (1 GiB) and its ring predecessor's replica
+    kept INSIDE that pool (kv_set_successor_shared): replica blocks come from the
+    holder's free list; the holder evicts them, oldest request first, when its own
+    appends need the memory, and a replica that cannot grow is dropped.  Prelude on
+    one stream, then K timed steps through kv_run_steps (two streams).  Reports the
+    replicated throughput, evictions, drops, the share of live requests that still
+    have a published replica, and the HBM the pools take (vs. a dedicated mirror)."""
+    import torch
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED
+    from kvgen.cuda import content_tokens_cuda
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    n = args.shared_steps
+    cfg = configs.scaled(configs.C2, num_blocks=SHARED_NB)
+    g = cfg.geom
+    S = cfg.stages
+    coords = {(0, s): s for s in range(S)}
+    placement = {s: 0 for s in range(S)}
+    succ = {s: (s + 1) % S for s in range(S)}
+    scheds = configs.build_schedules(cfg, n_steps=args.prelude + n + 2)
+    rt = RingRuntime(g, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement, succ,
+                     device=local_rank, spares=0, sentinel=None, shared=True)
+
+    def content(stage, ids, pos):
+        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim, device=local_rank)
+
+    drv = ScheduleDriver(rt, scheds, coords, content)
+    comp = torch.cuda.current_stream(dev)
+    repl = torch.cuda.Stream(dev)
+    for t in range(args.prelude):                 # one stream: trivially ordered
+        drv.append_step(t, stream=comp)
+        if t >= 1:
+            rt.replicate_all(t, stream=comp)
+    torch.cuda.synchronize(dev)
+    nodes = rt.alive_local()
+    handles = [rt.handle(nd) for nd in nodes]
+    steps, keep = [], []
+    for tt in range(args.prelude, args.prelude + n):
+        app = []
+        for nd, e in drv.plan(tt).items():
+            ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+            src = content(e["stage"], ids, pos) if ids else None
+            keep.append(src)
+            app.append(dict(pool=rt.handle(nd), begin_step=1, release=e["release"],
+                            req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+        steps.append(dict(append=app, repl_pools=handles, step=tt))
+    prep = K.PreparedSteps(steps)
+    st0 = {nd: K.kv_stats(rt.handle(nd)) for nd in nodes}
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(comp)
+    K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
+    fin = torch.cuda.Event()
+    fin.record(repl)
+    comp.wait_event(fin)
+    b.record(comp)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b)
+    st1 = {nd: K.kv_stats(rt.handle(nd)) for nd in nodes}
+    by = sum(st1[nd]["bytes_replicated"] - st0[nd]["bytes_replicated"] for nd in nodes)
+    live = covered = 0
+    for nd in nodes:                              # published replica coverage at the end
+        req, ln, pub, nb = K.kv_dump_slots(rt.handle(nd), rt.R)
+        meta = rt.read_meta(succ[nd])
+        par = meta["seq"] & 1
+        published = {int(r) for r in meta["req"][par] if r >= 0}
+        for r in req:
+            if r >= 0:
+                live += 1
+                covered += int(int(r) in published)
+    pool_gib = S * SHARED_NB * rt.block_bytes / 2**30
+    out = {"workload": "c2_pp4_b64 on 1 GPU, pools cut to %d blocks (shared capacity)" % SHARED_NB,
+           "steps": n, "value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+           "ms_per_step": round(ms / n, 4),
+           "evictions": {nd: int(st1[nd]["replica_evictions"] - st0[nd]["replica_evictions"])
+                         for nd in nodes},
+           "drops": {nd: int(st1[nd]["replica_drops"] - st0[nd]["replica_drops"]) for nd in nodes},
+           "replica_blocks_held_end": {nd: int(st1[nd]["replica_blocks_held"]) for nd in nodes},
+           "live_requests_with_published_replica": round(covered / max(1, live), 4),
+           "admissions_rejected": 0, "rejected_note": "the driver raises on KV_ENOMEM",
+           "pool_hbm_gib": round(pool_gib, 2),
+           "dedicated_mirror_hbm_gib_same_primary": round(2 * pool_gib, 2)}
+    rt.destroy()
+    del keep
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_nccl(args, drv, rt, t0, comp, content, dev, world):
