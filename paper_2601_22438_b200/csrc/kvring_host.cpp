@@ -1071,6 +1071,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.step = step;
     pp.max_reqs = p->R;
     pp.max_blk = p->M;
+    pp.n_table = p->R;  // staged tables carry every slot (inline launches trim them)
     pp.writer_node = p->node_id;
     pp.publish = 1;
     pp.sys_scope = p->succ_sys ? 1 : 0;
@@ -1078,6 +1079,9 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.pad0 = sys_per_cta;
   }
   collect_inval(L, pools, n_pools);
+  static const bool dbg_nocopy = getenv("KVRING_DEBUG_RINGPUT_NOCOPY") != nullptr;
+  if (dbg_nocopy)  // experiment knob: publication only (timing breakdown, breaks parity)
+    for (size_t i = 0; i < L.tasks.size(); ++i) L.tasks[i].seg_count = 0;
   return KV_OK;
 }
 
@@ -1621,6 +1625,59 @@ KV_API int kv_sync(kv_pool_t *p) {
   return KV_OK;
 }
 
+namespace {
+
+// Inline descriptors (KvInlineDesc): a launch whose tables + tasks fit the kernel
+// parameter space travels with the launch itself (KVRING_INLINE=0 disables).
+// Published-table entries of pool q a ring-put launch must carry: up to the last
+// slot listed (later slots publish (-1, 0), written by the kernel).
+int table_hi(const Launch &L, int q) {
+  const int R = L.params[q].max_reqs;
+  const int64_t *rq = reinterpret_cast<const int64_t *>(L.tables.data() + L.table_off[q]);
+  int hi = R;
+  while (hi > 0 && rq[hi - 1] < 0) --hi;
+  return hi;
+}
+
+size_t inline_table_bytes(const Launch &L) {
+  if (L.kind != kKindRingPut) return 0;
+  size_t b = 0;
+  for (int q = 0; q < L.n_pools; ++q) b += align16(12 * (size_t)table_hi(L, q));
+  return b;
+}
+
+bool inline_fits(const Launch &L) {
+  static const int enabled = [] {
+    const char *e = getenv("KVRING_INLINE");
+    return e ? atoi(e) : 1;
+  }();
+  return enabled && L.n_pools <= kInlinePools &&
+         inline_table_bytes(L) + sizeof(KvTask) * L.tasks.size() <= (size_t)kInlineBytes;
+}
+
+void fill_inline(const Launch &L, KvInlineDesc &d) {
+  size_t off = 0;
+  for (int q = 0; q < L.n_pools; ++q) {
+    d.pools[q] = L.params[q];
+    if (L.kind != kKindRingPut) continue;
+    const int R = L.params[q].max_reqs, hi = table_hi(L, q);
+    const char *t = L.tables.data() + L.table_off[q];
+    std::memcpy(d.data + off, t, 8 * (size_t)hi);                       // req ids
+    std::memcpy(d.data + off + 8 * (size_t)hi, t + 8 * (size_t)R, 4 * (size_t)hi);  // lens
+    d.pools[q].slot_req = reinterpret_cast<const int64_t *>(off);
+    d.pools[q].slot_len = reinterpret_cast<const int32_t *>(off + 8 * (size_t)hi);
+    d.pools[q].n_table = hi;
+    off += align16(12 * (size_t)hi);
+  }
+  d.n_tasks = (int32_t)L.tasks.size();
+  d.n_pools = L.n_pools;
+  d.task_off = (int32_t)off;
+  std::memcpy(d.data + off, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
+  d.used = (int32_t)(off + sizeof(KvTask) * L.tasks.size());
+}
+
+}  // namespace
+
 // ---- decode-loop driver -------------------------------------------------------
 // For each step: appends on the compute stream, then (after an event) the
 // publication on the replication stream -- the paper's "separate CUDA stream
@@ -1632,6 +1689,9 @@ struct StepPrep {
   Launch A, P;
   bool has_a = false, has_p = false;
   bool shared = false;  // a pool of this step is in shared-capacity mode (NEXT-3)
+  // inline descriptors (kernel parameter space), filled on the helper thread
+  bool inl_a = false, inl_p = false;
+  std::unique_ptr<KvInlineDesc> da, dp;
   int rc = KV_OK;
   std::string err;
 };
@@ -1677,7 +1737,44 @@ void prepare_step(const kv_step_t &st, StepPrep &sp) {
   if (p0 && sp.has_a && sp.has_p && sp.P.p0->device != p0->device) {
     sp.rc = fail(KV_EINVAL, "append and publication of one step must share a device");
     sp.err = g_err;
+    return;
   }
+  // descriptors that fit the kernel parameter space travel with the launch (no
+  // staging copy, no H2D, no dependent descriptor load); host-source appends and
+  // large (prefill / bulk) steps are staged
+  sp.inl_a = sp.inl_p = false;
+  if (!p0 || p0->device < 0) return;
+  bool host_src = false;
+  if (sp.has_a)
+    for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q) host_src |= sp.A.host_src_bytes[q] != 0;
+  if (sp.has_a && !host_src && !sp.A.tasks.empty() && inline_fits(sp.A)) {
+    if (!sp.da) sp.da.reset(new KvInlineDesc());
+    fill_inline(sp.A, *sp.da);
+    sp.inl_a = true;
+  }
+  if (sp.has_p && !sp.P.tasks.empty() && inline_fits(sp.P)) {
+    if (!sp.dp) sp.dp.reset(new KvInlineDesc());
+    fill_inline(sp.P, *sp.dp);
+    sp.inl_p = true;
+  }
+}
+
+// Launch of a prepared inline launch (events of kv_time_next_launch honoured).
+int enqueue_inline(Launch &L, const KvInlineDesc &d, cudaStream_t st, bool pdl) {
+  if (!L.inval.empty()) {
+    int rc = flush_inval(L, st);
+    if (rc) return rc;
+  }
+  if (L.tasks.empty()) return KV_OK;
+  cudaEvent_t b = g_ev_before, a = g_ev_after;
+  g_ev_before = g_ev_after = nullptr;
+  if (b) CU(cudaEventRecord(b, st));
+  CU(launch_copy_inline(L.kind, d, L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()),
+                        st, pdl));
+  if (a) CU(cudaEventRecord(a, st));
+  g_launches++;
+  L.p0->kernels++;
+  return KV_OK;
 }
 
 // Cross-stream order of the two-stream loop: ring-put k after append k (event
@@ -1686,86 +1783,105 @@ void prepare_step(const kv_step_t &st, StepPrep &sp) {
 // that last read them is k-2's, which may otherwise still lag on its stream.
 struct StreamOrder {
   static constexpr int kN = 4;
-  cudaEvent_t ready = nullptr;
-  cudaEvent_t rdone[kN] = {};
+  cudaEvent_t aready[kN] = {};  // recorded on the append stream after append k
+  cudaEvent_t rdone[kN] = {};   // recorded on the replication stream after ring-put k
+  long long astep[kN] = {-1, -1, -1, -1};
   long long rstep[kN] = {-1, -1, -1, -1};
   long long n = 0;  // steps issued on this stream pair (continues across calls)
   cudaStream_t sa = nullptr, sr = nullptr;
   int dev = -1;
   int ensure(int device) {
     if (dev == device) return KV_OK;
-    if (ready) cudaEventDestroy(ready);
+    for (auto &e : aready)
+      if (e) cudaEventDestroy(e);
     for (auto &e : rdone)
       if (e) cudaEventDestroy(e);
-    ready = nullptr;
-    for (auto &e : rdone) e = nullptr;
-    for (auto &r : rstep) r = -1;
+    for (int i = 0; i < kN; ++i) {
+      aready[i] = rdone[i] = nullptr;
+      astep[i] = rstep[i] = -1;
+    }
     sa = sr = nullptr;
-    CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    for (auto &e : aready) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : rdone) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     dev = device;
     return KV_OK;
   }
 };
 
-// CUDA side of one prepared step: one H2D for both launches, append kernel on
-// sa, event, ring-put on sr (the paper's separate replication stream).
-int issue_step(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa, cudaStream_t sr,
-               StreamOrder &so) {
+// CUDA side of one prepared step, in two halves that may run on two host threads
+// (kv_run_steps pipelines them): the append on sa (after the ring-put of step
+// k - lag, see StreamOrder), then the publication on sr (the paper's separate
+// replication stream) after an event on sa.  Inline launches need no
+// staging; a staged launch gets its own H2D on its own stream.
+int issue_append(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa,
+                 cudaStream_t sr, StreamOrder &so) {
   kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
   if (!p0 || p0->device < 0) return KV_OK;  // nothing to launch / tables-only pools
-  if (sp.has_a && sp.A.tasks.empty() && sp.A.inval.empty() && !sp.has_p) return KV_OK;
   DeviceGuard dg(p0->device);
-  DeviceCtx *ctx = ctx_for(p0->device);
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  StageBuf *sb = nullptr, *b = nullptr;
   int rc = KV_OK;
-  double t0 = now_s();
-  if (sp.has_a && (rc = stage_host_sources(ctx, sp.A, sa, &sb))) return rc;
-  Launch *ls[2];
-  int nl = 0;
-  if (sp.has_a) ls[nl++] = &sp.A;
-  if (sp.has_p) ls[nl++] = &sp.P;
-  if ((rc = stage(ctx, ls, nl, sa, &b))) return rc;  // one H2D for both launches
-  double t1 = now_s();
-  g_phase[kPhStage] += t1 - t0;
   if (sa != sr && (rc = so.ensure(p0->device))) return rc;
-  if (sp.has_a) {
+  const int N = StreamOrder::kN;
+  if (sp.has_a && (!sp.A.tasks.empty() || !sp.A.inval.empty())) {
+    DeviceCtx *ctx = ctx_for(p0->device);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    StageBuf *sb = nullptr, *b = nullptr;
+    const double t0 = now_s();
+    if ((rc = stage_host_sources(ctx, sp.A, sa, &sb))) return rc;
+    Launch *ls[1] = {&sp.A};
+    if (!sp.inl_a && !sp.A.tasks.empty() && (rc = stage(ctx, ls, 1, sa, &b))) return rc;
+    const double t1 = now_s();
+    g_phase[kPhStage] += t1 - t0;
     // shared capacity: a freed replica block may be reused by this very append, so
     // the ring-put that last wrote it (k-1) must be complete
     const int lag = sp.shared ? 1 : 2;
-    if (sa != sr && k >= lag && so.rstep[(k - lag) % StreamOrder::kN] == k - lag)
-      CU(cudaStreamWaitEvent(sa, so.rdone[(k - lag) % StreamOrder::kN], 0));
+    if (sa != sr && k >= lag && so.rstep[(k - lag) % N] == k - lag)
+      CU(cudaStreamWaitEvent(sa, so.rdone[(k - lag) % N], 0));
     g_ev_before = static_cast<cudaEvent_t>(st.ev_append_start);
     g_ev_after = static_cast<cudaEvent_t>(st.ev_append_end);
-    rc = enqueue(sp.A, sa);
+    rc = sp.inl_a ? enqueue_inline(sp.A, *sp.da, sa, false) : enqueue(sp.A, sa);
     g_ev_before = g_ev_after = nullptr;
     if (rc) return rc;
+    if (sb && (rc = ctx->done(sb, sa))) return rc;  // the staged source outlives the kernel
+    if (b && (rc = ctx->done(b, sa))) return rc;
+    g_phase[kPhEnqA] += now_s() - t1;
   }
-  if (sb && (rc = ctx->done(sb, sa))) return rc;
-  double t2 = now_s();
-  g_phase[kPhEnqA] += t2 - t1;
-  if (!sp.has_p) return ctx->done(b, sa);
-  if (sa != sr) {  // publication after the append (and after the staged H2D)
-    CU(cudaEventRecord(so.ready, sa));
-    CU(cudaStreamWaitEvent(sr, so.ready, 0));
+  if (sa != sr && sp.has_p) {  // the publication of step k follows this append
+    CU(cudaEventRecord(so.aready[k % N], sa));
+    so.astep[k % N] = k;
   }
+  return KV_OK;
+}
+
+int issue_publish(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa,
+                  cudaStream_t sr, StreamOrder &so) {
+  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
+  if (!p0 || p0->device < 0 || !sp.has_p) return KV_OK;
+  DeviceGuard dg(p0->device);
+  const int N = StreamOrder::kN;
+  const double t0 = now_s();
+  if (sa != sr && so.astep[k % N] == k) CU(cudaStreamWaitEvent(sr, so.aready[k % N], 0));
   if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
-  double t3 = now_s();
-  g_phase[kPhEvents] += t3 - t2;
+  const double t1 = now_s();
+  g_phase[kPhEvents] += t1 - t0;
+  DeviceCtx *ctx = ctx_for(p0->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  StageBuf *b = nullptr;
+  int rc = KV_OK;
+  Launch *ls[1] = {&sp.P};
+  if (!sp.inl_p && !sp.P.tasks.empty() && (rc = stage(ctx, ls, 1, sr, &b))) return rc;
   g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
   g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
-  rc = enqueue(sp.P, sr);
+  rc = sp.inl_p ? enqueue_inline(sp.P, *sp.dp, sr, false) : enqueue(sp.P, sr);
   g_ev_before = g_ev_after = nullptr;
   if (rc) return rc;
   if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
   if (sa != sr) {
-    CU(cudaEventRecord(so.rdone[k % StreamOrder::kN], sr));
-    so.rstep[k % StreamOrder::kN] = k;
+    CU(cudaEventRecord(so.rdone[k % N], sr));
+    so.rstep[k % N] = k;
   }
-  rc = ctx->done(b, sr);  // sr is ordered after sa: covers both launches
-  g_phase[kPhEnqP] += now_s() - t3;
-  return rc;
+  if (b && (rc = ctx->done(b, sr))) return rc;
+  g_phase[kPhEnqP] += now_s() - t1;
+  return KV_OK;
 }
 
 }  // namespace
@@ -1787,7 +1903,7 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
       DeviceGuard dg(q->device);
       int rc = so.ensure(q->device);
       if (rc) return rc;
-      for (auto &r : so.rstep) r = -1;
+      for (int i = 0; i < StreamOrder::kN; ++i) so.rstep[i] = so.astep[i] = -1;
       CU(cudaEventRecord(so.rdone[0], sr));
       CU(cudaStreamWaitEvent(sa, so.rdone[0], 0));
       so.sa = sa;
@@ -1799,11 +1915,17 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
     for (int k = 0; k < n_steps; ++k) {
       prepare_step(steps[k], sp);
       if (sp.rc) return sp.rc;
-      int rc = issue_step(steps[k], so.n++, sp, sa, sr, so);
+      const long long kk = so.n++;
+      int rc = issue_append(steps[k], kk, sp, sa, sr, so);
+      if (!rc) rc = issue_publish(steps[k], kk, sp, sa, sr, so);
       if (rc) return rc;
     }
     return KV_OK;
   }
+  // A helper thread prepares step k+1 (allocation, tables, work lists, inline
+  // descriptors) while this thread issues step k's CUDA calls; a 2-deep ring of
+  // StepPrep.  (Issuing the appends from the helper too was measured slower:
+  // concurrent launches from two threads contend in the driver.)
   StepPrep ring[2];  // shared with the worker (per call: reentrant across threads)
   std::atomic<int> produced{0}, consumed{0};
   std::atomic<bool> stop{false};
@@ -1834,7 +1956,9 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
       g_err = sp.err;
       break;
     }
-    rc = issue_step(steps[k], so.n++, sp, sa, sr, so);
+    const long long kk = so.n++;
+    rc = issue_append(steps[k], kk, sp, sa, sr, so);
+    if (!rc) rc = issue_publish(steps[k], kk, sp, sa, sr, so);
     consumed.store(k + 1, std::memory_order_release);
     if (rc) break;
   }
@@ -2036,35 +2160,6 @@ KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *str
 // ---- single-stream decode loop with programmatic dependent launch ----------------
 namespace {
 
-// Inline descriptors (KvInlineDesc): a launch whose tables + tasks fit the kernel
-// parameter space travels with the launch itself (KVRING_INLINE=0 disables).
-bool inline_fits(const Launch &L) {
-  static const int enabled = [] {
-    const char *e = getenv("KVRING_INLINE");
-    return e ? atoi(e) : 1;
-  }();
-  return enabled && L.n_pools <= kInlinePools &&
-         align16(L.tables.size()) + sizeof(KvTask) * L.tasks.size() <= (size_t)kInlineBytes;
-}
-
-void fill_inline(const Launch &L, KvInlineDesc &d) {
-  const size_t tbl = align16(L.tables.size());
-  d.n_tasks = (int32_t)L.tasks.size();
-  d.n_pools = L.n_pools;
-  d.task_off = (int32_t)tbl;
-  d.pad = 0;
-  for (int q = 0; q < L.n_pools; ++q) {
-    d.pools[q] = L.params[q];
-    if (L.kind == kKindRingPut) {
-      d.pools[q].slot_req = reinterpret_cast<const int64_t *>(L.table_off[q]);
-      d.pools[q].slot_len = reinterpret_cast<const int32_t *>(
-          L.table_off[q] + 8 * (size_t)L.params[q].max_reqs);
-    }
-  }
-  if (!L.tables.empty()) std::memcpy(d.data, L.tables.data(), L.tables.size());
-  std::memcpy(d.data + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
-}
-
 // One step of the PDL loop: launches whose descriptors fit the parameter space go
 // inline with the PDL attribute (no copy node between kernels); larger ones (bulk
 // prefill steps) are staged by one H2D and launched normally -- that step
@@ -2079,17 +2174,8 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
     for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q)
       if (sp.A.host_src_bytes[q])
         return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_pdl");
-  const bool inl_a = has_a && inline_fits(sp.A), inl_p = has_p && inline_fits(sp.P);
+  const bool inl_a = has_a && sp.inl_a, inl_p = has_p && sp.inl_p;  // filled by prepare_step
   const double t0 = now_s();
-  thread_local std::unique_ptr<KvInlineDesc> da, dp;
-  if (inl_a) {
-    if (!da) da.reset(new KvInlineDesc());
-    fill_inline(sp.A, *da);
-  }
-  if (inl_p) {
-    if (!dp) dp.reset(new KvInlineDesc());
-    fill_inline(sp.P, *dp);
-  }
   DeviceCtx *ctx = ctx_for(p0->device);
   std::lock_guard<std::mutex> lk(ctx->mu);
   Launch *ls[2];
@@ -2104,10 +2190,7 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
   if (has_a) {
     if (st.ev_append_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_start), s));
     if (inl_a) {
-      CU(launch_copy_inline(kKindAppend, *da, p0->geom_dev(),
-                            copy_grid(p0->device, (int)sp.A.tasks.size()), s, true));
-      g_launches++;
-      p0->kernels++;
+      if ((rc = enqueue_inline(sp.A, *sp.da, s, true))) return rc;
     } else if ((rc = enqueue(sp.A, s))) {
       return rc;
     }
@@ -2118,10 +2201,7 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
   if (has_p) {
     if (st.ev_kernel_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_start), s));
     if (inl_p) {
-      CU(launch_copy_inline(kKindRingPut, *dp, p0->geom_dev(),
-                            copy_grid(p0->device, (int)sp.P.tasks.size()), s, true));
-      g_launches++;
-      p0->kernels++;
+      if ((rc = enqueue_inline(sp.P, *sp.dp, s, true))) return rc;
     } else if ((rc = enqueue(sp.P, s))) {
       return rc;
     }

@@ -46,7 +46,9 @@ struct alignas(16) KvPoolParams {
   unsigned long long step;     // seq to publish
   int32_t max_reqs, max_blk, writer_node, publish;
   int32_t sys_scope;           // successor is an NVLink peer: system-scope fences / release
-  int32_t pad0, pad1, pad2;
+  int32_t pad0;
+  int32_t n_table;             // publish: table entries staged; slots >= n_table publish (-1, 0)
+  int32_t pad2;
   unsigned long long src_bytes;  // extent of src / dst (debug bounds checks, KV_BOUNDS_CHECK)
   unsigned long long dst_bytes;
 };
@@ -104,12 +106,17 @@ cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const Kv
 // list.  No H2D staging copy and no dependent global load before a CTA's first
 // data load; ring-put pools carry their table offsets (into `data`) in
 // slot_req / slot_len.
+// Size classes: the launch copies the whole parameter block (the driver's copy
+// costs ~0.2 us per KiB on the host), so a launch pays for the smallest class its
+// tables + tasks fit: 4, 8, 16 or 28 KiB.
 constexpr int kInlineBytes = 28 * 1024;
-struct KvInlineDesc {
-  int32_t n_tasks, n_pools, task_off, pad;
+template <int CAP>
+struct KvInlineDescT {
+  int32_t n_tasks, n_pools, task_off, used;  // used: bytes of data in use
   KvPoolParams pools[kInlinePools];
-  alignas(16) char data[kInlineBytes];
+  alignas(16) char data[CAP];
 };
+using KvInlineDesc = KvInlineDescT<kInlineBytes>;
 cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,
                                cudaStream_t stream, bool pdl);
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,

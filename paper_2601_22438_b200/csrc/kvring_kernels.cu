@@ -199,9 +199,10 @@ __device__ void write_parity_table(const KvPoolParams &pp, const char *tbl_base)
   const int32_t *slen = tbl_base ? reinterpret_cast<const int32_t *>(
                                        tbl_base + reinterpret_cast<size_t>(pp.slot_len))
                                  : pp.slot_len;
+  const int n = pp.n_table;
   for (int s = threadIdx.x; s < R; s += blockDim.x) {
-    mreq[s] = sreq[s];
-    mlen[s] = slen[s];
+    mreq[s] = s < n ? sreq[s] : -1;
+    mlen[s] = s < n ? slen[s] : 0;
   }
   if (threadIdx.x == 0) *reinterpret_cast<int32_t *>(meta + 8) = pp.writer_node;
 }
@@ -343,16 +344,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
 // Inline-descriptor twins of the two hot kernels (KvInlineDesc: parameters, tables
 // and tasks in the kernel's parameter space; same PDL protocol as above).
+template <int CAP>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
-    kv_append_scatter_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDesc d) {
+    kv_append_scatter_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDescT<CAP> d) {
   pdl_launch_dependents();
   run_tasks<kTokMajor, kPaged, false>(reinterpret_cast<const KvTask *>(d.data + d.task_off),
                                       d.n_tasks, d.pools, g, d.n_pools);
   pdl_wait();
 }
 
+template <int CAP>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
-    kv_ring_put_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDesc d) {
+    kv_ring_put_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDescT<CAP> d) {
   pdl_wait();
   pdl_launch_dependents();
   run_tasks<kPaged, kPaged, true>(reinterpret_cast<const KvTask *>(d.data + d.task_off),
@@ -405,6 +408,7 @@ __global__ void __launch_bounds__(kThreads) kv_unpack_kernel(const char *__restr
     pp.writer_node = h->writer_node;
     pp.publish = 1;
     pp.sys_scope = 1;
+    pp.n_table = h->max_reqs;
     s_cnt = 0;
   }
   __syncthreads();
@@ -568,8 +572,21 @@ cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (kind == kKindAppend) return cudaLaunchKernelEx(&cfg, kv_append_scatter_inl_kernel, g, d);
-  if (kind == kKindRingPut) return cudaLaunchKernelEx(&cfg, kv_ring_put_inl_kernel, g, d);
+  // every class is a prefix of the largest (same header, pools and data offset)
+#define KV_INL_CLASS(CAP)                                                                 \
+  if (d.used <= (CAP)) {                                                                  \
+    const auto &ds = *reinterpret_cast<const KvInlineDescT<(CAP)> *>(&d);                 \
+    if (kind == kKindAppend)                                                              \
+      return cudaLaunchKernelEx(&cfg, kv_append_scatter_inl_kernel<(CAP)>, g, ds);        \
+    if (kind == kKindRingPut)                                                             \
+      return cudaLaunchKernelEx(&cfg, kv_ring_put_inl_kernel<(CAP)>, g, ds);              \
+    return cudaErrorInvalidValue;                                                         \
+  }
+  KV_INL_CLASS(4 * 1024)
+  KV_INL_CLASS(8 * 1024)
+  KV_INL_CLASS(16 * 1024)
+  KV_INL_CLASS(kInlineBytes)
+#undef KV_INL_CLASS
   return cudaErrorInvalidValue;
 }
 
