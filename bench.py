@@ -86,14 +86,19 @@ def bench_config(n_gpus):
                   "the replicated slices were just written by the append, as in serving"}
 
 
-def traffic_ref(kind):
+def traffic_ref(kind, kernel="kv_ring_put_kernel"):
     """Captured DRAM traffic per launch (profiles/traffic.json, from ncu --set full)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            d = json.load(f)["kv_ring_put_kernel"][kind]
+            d = json.load(f)[kernel][kind]
         return d
     except Exception:
         return None
+
+
+# the timed decode steps launch the inline-descriptor ring-put (descriptors in the
+# kernel parameter space); steps whose descriptors exceed 28 KiB use the staged one
+RINGPUT = "kv_ring_put_inl_kernel (staged kv_ring_put_kernel for large steps)"
 
 
 def peaks():
@@ -405,7 +410,7 @@ def run_kvring(args):
     elif N == 1:
         per_launch = my_bytes / args.steps
         achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
-        tr = traffic_ref("decode_step")
+        tr = traffic_ref("decode_step", "kv_ring_put_inl_kernel")
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4),
                 "traffic": tr["traffic"] if tr else None,
@@ -413,7 +418,7 @@ def run_kvring(args):
                                  "DRAM bytes %d vs algorithmic read %d / r+w %d; writes stay in L2"
                                  % (tr["traffic"], tr["algorithmic_read"], tr["algorithmic_rw"]))
                                 if tr else None,
-                "kernel": "kv_ring_put_kernel", "peak_source": peak_src,
+                "kernel": RINGPUT, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(2 * per_launch),
                 "avg_launch_us": round(avg_kern, 2)}
     else:
@@ -421,7 +426,7 @@ def run_kvring(args):
         achieved = per_launch / (avg_kern * 1e-6) / 1e9
         roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
-                "kernel": "kv_ring_put_kernel",
+                "kernel": RINGPUT,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
                 "algorithmic_bytes_per_launch": int(per_launch), "avg_launch_us": round(avg_kern, 2)}
     value = tot_bytes / (ms_max * 1e-3) / 1e9
@@ -447,11 +452,10 @@ def run_kvring(args):
                                                  "overhead proper is the interference leg")
                              if args.loop == "fused" else None,
                              "what": "replication-stream device time per step (ring-put kernel incl. "
-                                     "its launch; the step's descriptors are staged with one H2D before "
-                                     "the append), CUDA events by kv_run_steps on every %d-th timed "
-                                     "step" % TIME_EVERY},
+                                     "its launch and its wait for the step's append), CUDA events by "
+                                     "kv_run_steps on every %d-th timed step" % TIME_EVERY},
         "kernel_us": {"kernel": "kv_step_fused_kernel" if args.loop == "fused"
-                      else "kv_ring_put_kernel",
+                      else RINGPUT,
                       "median": round(med_kern, 2), "avg": round(avg_kern, 2),
                       "sampled_launches": len(kern_us)},
         "roofline": roof,
