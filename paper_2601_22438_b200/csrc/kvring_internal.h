@@ -99,8 +99,6 @@ cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPool
 cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const KvPoolParams *params,
                          int n_app_pools, int n_rep_pools, const KvGeomDev &g, int grid,
                          cudaStream_t stream);
-cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                            int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream);
 // A launch carried entirely in the kernel's parameter space (<= 32 KiB since
 // CUDA 12.1): per-pool parameters, the ring-put's publication tables and the task
 // list.  No H2D staging copy and no dependent global load before a CTA's first

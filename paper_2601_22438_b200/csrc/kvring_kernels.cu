@@ -7,13 +7,16 @@
 //   restore-remap   (replica -> pool at new block ids,       a8, §3.2)
 //
 // Pure data movement: no tensor cores (HBM / NVLink bound, DESIGN.md
-// "Rooflines").  Each CTA takes one 32-KiB task at a time; each thread keeps
+// "Rooflines").  Each CTA takes one <= 32-KiB task at a time; each thread keeps
 // 8 independent 16-B loads in flight (L1::no_allocate streaming loads), then
-// stores them (16-B stores; peer addresses go over NVLink).  Tasks that finish
-// bump a per-pool monotone counter after a system-scope fence; the CTA that
-// completes a pool's last task writes the parity metadata and then the seq
-// flag with st.release.sys (reading R9: a reader that acquires seq = t sees
-// everything of step t).
+// stores them (16-B stores; peer addresses go over NVLink).  Publication runs in
+// a second pass: each CTA adds its per-pool task counts to a monotone counter
+// with one release RMW (GPU scope); the CTA that completes a pool's count issues
+// an acquire-release fence (system scope for an NVLink successor) and stores the
+// seq flag with st.release (reading R9: a reader that acquires seq = t sees
+// everything of step t).  The hot kernels exist twice: with descriptors staged in
+// global memory, and "inline" with parameters, tables and tasks in the kernel
+// parameter space (KvInlineDescT, 4-28 KiB size classes) for decode-size steps.
 #include <cstdlib>
 
 #include <cuda_runtime.h>
@@ -529,33 +532,6 @@ cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const K
   kv_step_fused_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_append, n_tasks, params,
                                                        n_app_pools, g, n_rep_pools);
   return cudaGetLastError();
-}
-
-// Launch of the append / ring-put kernels with the programmatic stream
-// serialization attribute (PDL): the launch may overlap the previous kernel in
-// the stream; the kernels order themselves with griddepcontrol (see above).
-cudaError_t launch_copy_pdl(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                            int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream) {
-  if (n_tasks <= 0) return cudaSuccess;
-  if (n_pools > kMaxPoolsPerLaunch) return cudaErrorInvalidValue;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  KvParamPack pk;
-  pk.n = 0;  // the PDL loop reads parameters zero-copy
-  if (kind == kKindAppend)
-    return cudaLaunchKernelEx(&cfg, kv_append_scatter_kernel, tasks, n_tasks, params, g, n_pools,
-                              pk);
-  if (kind == kKindRingPut)
-    return cudaLaunchKernelEx(&cfg, kv_ring_put_kernel, tasks, n_tasks, params, g, n_pools, pk);
-  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,

@@ -5,7 +5,8 @@
 //   mode 2: src contiguous         -> dst contiguous                     (full blocks)
 //   mode 3: src 256 B @4 KiB       -> dst contiguous                     (gather-pack)
 // Tasks target random 512-KiB blocks of a large pool (like live requests).
-// Usage: copybench [n_tasks] [warm(0/1)] [unroll-variant]
+// Usage: copybench [n_tasks] [warm(0/1)] [peer(0/1): destination on GPU 1 over NVLink]
+//                  [streams(1/2): 2 = two such copies launched concurrently on two streams]
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -65,11 +66,25 @@ __global__ void touch(const Task *tasks, int n, const char *src, int mode, unsig
 int main(int argc, char **argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 600;
   const int warm = argc > 2 ? atoi(argv[2]) : 1;
+  const int peer = argc > 3 ? atoi(argv[3]) : 0;
+  const int nstreams = argc > 4 ? atoi(argv[4]) : 1;
+  cudaStream_t s2;
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaEvent_t e2a, e2b;
+  cudaEventCreate(&e2a);
+  cudaEventCreate(&e2b);
   const size_t pool = 6ull << 30, flushb = 512ull << 20;
   char *src, *dst, *fl;
   unsigned *sink;
   CK(cudaMalloc(&src, pool));
-  CK(cudaMalloc(&dst, pool));
+  if (peer) {
+    CK(cudaSetDevice(1));
+    CK(cudaMalloc(&dst, pool));
+    CK(cudaSetDevice(0));
+    CK(cudaDeviceEnablePeerAccess(1, 0));
+  } else {
+    CK(cudaMalloc(&dst, pool));
+  }
   CK(cudaMalloc(&fl, flushb));
   CK(cudaMalloc(&sink, 4));
   CK(cudaMemset(src, 1, pool));
@@ -103,6 +118,12 @@ int main(int argc, char **argv) {
         if (warm) touch<<<sms * 4, 256>>>(d, n, src, mode, sink);
         const int grid = n < sms * 4 ? n : sms * 4;
         cudaEventRecord(a);
+        if (nstreams == 2) {  // a second, identical copy on another stream (other bytes)
+          cudaEventRecord(e2a, 0);
+          cudaStreamWaitEvent(s2, e2a, 0);
+          if (mode == 1) k<1, 8><<<grid, 256, 0, s2>>>(d, n, src, dst);  // same bytes: timing only
+          cudaEventRecord(e2b, s2);
+        }
         if (variant == 0) {
           if (mode == 0) k<0, 8><<<grid, 256>>>(d, n, src, dst);
           if (mode == 1) k<1, 8><<<grid, 256>>>(d, n, src, dst);
@@ -114,16 +135,17 @@ int main(int argc, char **argv) {
           if (mode == 2) k<2, 4><<<grid, 256>>>(d, n, src, dst);
           if (mode == 3) k<3, 4><<<grid, 256>>>(d, n, src, dst);
         }
+        if (nstreams == 2) cudaStreamWaitEvent(0, e2b, 0);
         cudaEventRecord(b);
         CK(cudaEventSynchronize(b));
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         if (r > 2) { best = ms < best ? ms : best; sum += ms; }
       }
-      const double bytes = 2.0 * n * 32768;
-      printf("%-30s n=%5d warm=%d U=%d  best %7.2f us  avg %7.2f us  -> %7.1f GB/s (r+w, best)\n",
-             names[mode], n, warm, variant == 0 ? 8 : 4, best * 1e3, sum / (reps - 3) * 1e3,
-             bytes / (best * 1e-3) / 1e9);
+      const double bytes = (peer ? 1.0 : 2.0) * n * 32768 * (mode == 1 ? nstreams : 1);
+      printf("%-30s n=%5d x%d warm=%d U=%d peer=%d best %7.2f us  avg %7.2f us  -> %7.1f GB/s (%s, best)\n",
+             names[mode], n, mode == 1 ? nstreams : 1, warm, variant == 0 ? 8 : 4, peer, best * 1e3, sum / (reps - 3) * 1e3,
+             bytes / (best * 1e-3) / 1e9, peer ? "NVLink payload" : "r+w");
     }
     cudaFree(d);
   }

@@ -1,0 +1,8 @@
+# N=2 NVLink decode ring-put: grid / task-size knobs (interleaved, 2 rounds)
+mkdir -p gpurun_out; python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
+B="bench.py --gpus 2 --no-cpu-baseline --e2e-steps 0 --no-restore --nccl-steps 0 --bulk-reps 0 --interference-steps 0 --block-steps 0 --shared-steps 0 --steps 300"
+for r in 1 2; do
+for v in "X=1" "KVRING_MIN_TASK_SEGS=128" "KVRING_CTAS_PER_SM=2" "KVRING_MIN_TASK_SEGS=64"; do
+  echo "== $v round $r" >> gpurun_out/exp23.log
+  env $v timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29571 $B 2>/dev/null | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['kernel_us']['median'], d['kernel_us']['avg'], d['roofline']['frac'], {k: d['host_us_per_step'][k] for k in ('prepare','wait_prepare','stage.acquire_wait','launch_append','launch_publish')})" >> gpurun_out/exp23.log 2>&1
+done; done
