@@ -191,9 +191,13 @@ struct DeviceCtx {
   StageBuf src[kRing];  // device copies of host-resident append sources (KV_SRC_HOST)
   int next_src = 0;
   unsigned long long *unpack_counter = nullptr;
-  size_t cap_hint = 8u << 20;  // 8 MiB per slot: growth (cudaHostAlloc, ms) never hits a hot loop
+  size_t cap_hint = 8u << 20;       // descriptor slots: 8 MiB (growth never hits a hot loop)
+  size_t src_cap_hint = 64u << 20;  // host-source slots: 64 MiB (a 2k-token prefill per stage)
 
-  // Returns a buffer of >= bytes whose previous use has completed.
+  // Returns a buffer of >= bytes whose previous use has completed.  Growth
+  // (cudaFree synchronises the device; cudaHostAlloc costs ms) resizes EVERY slot
+  // of the ring at once, doubling, so it happens a handful of times per process
+  // instead of once per slot and size.
   int acquire(StageBuf *ringv, int &nxt, size_t bytes, bool want_host, StageBuf **out) {
     StageBuf &b = ringv[nxt];
     nxt = (nxt + 1) % kRing;
@@ -203,16 +207,24 @@ struct DeviceCtx {
     }
     if (b.cap < bytes) {
       size_t cap = std::max(bytes, b.cap * 2);
-      cap = std::max(cap, cap_hint);
+      cap = std::max(cap, want_host ? cap_hint : src_cap_hint);
       cap = (cap + 4095) & ~(size_t)4095;
-      if (b.host) cudaFreeHost(b.host);
-      if (b.dev) cudaFree(b.dev);
-      b.host = nullptr;
-      b.dev = nullptr;
-      b.cap = 0;
-      if (want_host) CU(cudaHostAlloc(reinterpret_cast<void **>(&b.host), cap, cudaHostAllocDefault));
-      CU(cudaMalloc(reinterpret_cast<void **>(&b.dev), cap));
-      b.cap = cap;
+      for (int i = 0; i < kRing; ++i) {
+        StageBuf &r = ringv[i];
+        if (r.cap >= cap) continue;
+        if (r.pending) {
+          CU(cudaEventSynchronize(r.ev));
+          r.pending = false;
+        }
+        if (r.host) cudaFreeHost(r.host);
+        if (r.dev) cudaFree(r.dev);
+        r.host = nullptr;
+        r.dev = nullptr;
+        r.cap = 0;
+        if (want_host) CU(cudaHostAlloc(reinterpret_cast<void **>(&r.host), cap, cudaHostAllocDefault));
+        CU(cudaMalloc(reinterpret_cast<void **>(&r.dev), cap));
+        r.cap = cap;
+      }
     }
     if (!b.ev) CU(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
     *out = &b;
