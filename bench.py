@@ -1108,7 +1108,7 @@ def run_restore(drv, rt, t, dev, stream, world=1):
 
 
 # --------------------------------------------------------------------------- CPU arms
-def oracle_sample(cfg, t_start: int, n_steps: int):
+def oracle_sample(cfg, t_start: int, n_steps: int, warmup: int = 0):
     """Time the CPU oracle (as it stands) over steps [t_start, t_start+n) of the same
     workload.  Steps before t_start run in metadata mode to reach the same state;
     the sampled steps run with content (numpy copies), sources pre-generated."""
@@ -1116,12 +1116,13 @@ def oracle_sample(cfg, t_start: int, n_steps: int):
     from kvgen.content import CONTENT_SEED, content_tokens
     from oracle.simulate import OracleRing
     from kvgen.configs import scaled
-    scheds = build_schedules(cfg, n_steps=t_start + n_steps + 1)
+    n_total = warmup + n_steps          # content-mode steps: warm-up (untimed) + timed
+    scheds = build_schedules(cfg, n_steps=t_start + n_total + 1)
     # metadata-only pass over the whole sample to find the highest block id used,
     # so the sampled pools hold exactly the blocks the workload touches
     meta = OracleRing(cfg, content=False, schedules=scheds)
     peak = 0
-    for tt in range(t_start + n_steps):
+    for tt in range(t_start + n_total):
         meta.appends(tt)
         if tt >= 1:
             meta.replicate(tt)
@@ -1142,7 +1143,7 @@ def oracle_sample(cfg, t_start: int, n_steps: int):
         n.replica = np.full(shape, 0x5A5A, dtype=np.uint16)
     ring.content = True
     srcs = {}
-    for tt in range(t_start, t_start + n_steps):
+    for tt in range(t_start, t_start + n_total):
         srcs[tt] = {}
         for c, n in ring.nodes.items():
             p, s = c
@@ -1157,9 +1158,20 @@ def oracle_sample(cfg, t_start: int, n_steps: int):
             srcs[tt][c] = (ev.retire, ids, nn,
                            content_tokens(CONTENT_SEED, tid, tpos, s * g.layers, g.layers,
                                           g.kv_heads, g.head_dim))
+    def one(tt):
+        for c, n in ring.nodes.items():
+            rel, ids, nn, src = srcs[tt][c]
+            n.begin_step()
+            n.release(rel)
+            n.append(ids, nn, src)
+        for c, n in ring.nodes.items():
+            ring.moved += n.replicate(tt)
+
+    for tt in range(t_start, t_start + warmup):
+        one(tt)
     moved0 = ring.moved
     t0 = time.perf_counter()
-    for tt in range(t_start, t_start + n_steps):
+    for tt in range(t_start + warmup, t_start + n_total):
         for c, n in ring.nodes.items():
             rel, ids, nn, src = srcs[tt][c]
             n.begin_step()
@@ -1189,18 +1201,21 @@ def run_reference(args):
         return
     from kvgen import configs
     cfg = configs.C2
-    n = max(1, min(args.steps, 60))
-    by, dt = oracle_sample(cfg, args.prelude, n)
+    # the oracle as it stands (~14 ms per C2 step): K timed steps after W warm-up steps,
+    # capped so the run stays within a few minutes
+    n = max(1, min(args.steps, 400))
+    w = max(0, min(args.warmup, 50))
+    by, dt = oracle_sample(cfg, args.prelude, n, warmup=w)
     value = by / dt / 1e9
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
-            "steps": n, "warmup": 0, "ms_per_step": round(dt / n * 1e3, 3),
+            "steps": n, "warmup": w, "ms_per_step": round(dt / n * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (ShareGPT-shaped lognormal trace, closed-form KV words)",
             "impl": "reference",
             "config": bench_config(args.gpus),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{n} steps from step {args.prelude} of {CFG_NAME} "
+                             "sample": f"{n} steps from step {args.prelude + w} of {CFG_NAME} "
                                        f"(one pipeline; the oracle as it stands, numpy, one "
                                        f"thread); host has {cores} cores"},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
