@@ -309,7 +309,8 @@ def run_kvring(args):
     t += args.steps
     del src
     launches = K.kv_kernel_launch_count() - l0
-    host_prof = {k: round(v / args.steps * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}
+    host_prof = {k: round(v / args.steps * (1.0 if k.startswith("n_") else 1e6), 2)
+                 for k, v in K.kv_host_profile(reset=True).items()}
     ms = start.elapsed_time(end)
     kern_us = [e[1].elapsed_time(e[2]) * 1e3 for e in evs]
     rep_us = kern_us if args.loop in ("fused", "pdl") else [e[0].elapsed_time(e[2]) * 1e3

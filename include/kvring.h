@@ -341,10 +341,14 @@ uint64_t kv_kernel_launch_count(void);
 int kv_time_next_launch(void *ev_before, void *ev_after);
 
 /* Host-side phase counters of kv_run_steps (seconds, cumulative since the last
- * reset): [0] prepare (tables + work lists, helper thread), [1] issue thread
- * waiting for prepare, [2] descriptor staging + H2D call, [3] append launch,
- * [4] publication launch, [5] stream-ordering events, [6] helper waiting for
- * the issue thread.  Copies min(n, count) values; returns the count. */
+ * reset; diagnostics, updated without synchronisation): [0] prepare (tables +
+ * work lists, helper thread), [1] issue thread waiting for prepare, [2] append
+ * staging + H2D call, [3] append launch, [4] publication launch, [5]
+ * stream-ordering events, [6] helper waiting for the issue thread, [7] staging
+ * ring waits, [8] staging host copies, [9] H2D calls, [10..12] prepare split
+ * (append / replicate / commit), [13] publication staging, [14] / [15] COUNTS of
+ * inline-descriptor / staged launches.  Copies min(n, count) values; returns the
+ * count. */
 int kv_host_profile(double *out, int32_t n, int32_t reset);
 
 #ifdef __cplusplus

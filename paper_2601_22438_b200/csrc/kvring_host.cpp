@@ -32,7 +32,8 @@
 #include <chrono>
 namespace {
 enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue,
-       kPhAcquire, kPhHostCopy, kPhH2DCall, kPhPrepAppend, kPhPrepRepl, kPhCommit, kPhN };
+       kPhAcquire, kPhHostCopy, kPhH2DCall, kPhPrepAppend, kPhPrepRepl, kPhCommit,
+       kPhPubStage, kPhInlineLaunches, kPhStagedLaunches, kPhN };
 double g_phase[kPhN];
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -1171,6 +1172,11 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
   return KV_OK;
 }
 
+// Grid of a copy launch: one CTA per task up to the resident CTA count (capping the
+// append's grid so the concurrent ring-put finds free CTA slots was measured: no
+// gain, profiles/r01/exp25.log).
+int launch_grid(const Launch &L) { return copy_grid(L.p0->device, (int)L.tasks.size()); }
+
 // Shared capacity: withdraw the freed replicas' published entries (req_id -1,
 // len 0 in the published parity) before this launch may reuse their blocks.
 int flush_inval(Launch &L, cudaStream_t st) {
@@ -1195,8 +1201,8 @@ int enqueue(Launch &L, cudaStream_t st) {
     if (dbg_nopub) kind = kKindRestore;  // experiment knob: copy without publication
   }
   CU(timed_launch(kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
-                  L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()), st,
-                  L.params.data()));
+                  L.p0->geom_dev(), launch_grid(L), st, L.params.data()));
+  g_phase[kPhStagedLaunches] += 1.0;
   g_launches++;
   L.p0->kernels++;
   return KV_OK;
@@ -1781,8 +1787,8 @@ int enqueue_inline(Launch &L, const KvInlineDesc &d, cudaStream_t st, bool pdl) 
   cudaEvent_t b = g_ev_before, a = g_ev_after;
   g_ev_before = g_ev_after = nullptr;
   if (b) CU(cudaEventRecord(b, st));
-  CU(launch_copy_inline(L.kind, d, L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()),
-                        st, pdl));
+  CU(launch_copy_inline(L.kind, d, L.p0->geom_dev(), launch_grid(L), st, pdl));
+  g_phase[kPhInlineLaunches] += 1.0;  // a count (kv_host_profile divides like the times)
   if (a) CU(cudaEventRecord(a, st));
   g_launches++;
   L.p0->kernels++;
@@ -1881,6 +1887,7 @@ int issue_publish(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t s
   int rc = KV_OK;
   Launch *ls[1] = {&sp.P};
   if (!sp.inl_p && !sp.P.tasks.empty() && (rc = stage(ctx, ls, 1, sr, &b))) return rc;
+  g_phase[kPhPubStage] += now_s() - t1;
   g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
   g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
   rc = sp.inl_p ? enqueue_inline(sp.P, *sp.dp, sr, false) : enqueue(sp.P, sr);

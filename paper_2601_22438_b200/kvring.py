@@ -387,7 +387,8 @@ def kv_plan_targets(succ, excluded=None):
 
 HOST_PHASES = ["prepare", "wait_prepare", "stage_h2d", "launch_append", "launch_publish",
                "events", "worker_wait_issue", "stage.acquire_wait", "stage.host_copy",
-               "stage.h2d_call", "prepare.append", "prepare.replicate", "prepare.commit"]
+               "stage.h2d_call", "prepare.append", "prepare.replicate", "prepare.commit",
+               "publish.stage", "n_inline_launches", "n_staged_launches"]
 
 
 def kv_host_profile(reset: bool = True) -> dict:
