@@ -34,15 +34,19 @@ namespace {
 enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue,
        kPhAcquire, kPhHostCopy, kPhH2DCall, kPhPrepAppend, kPhPrepRepl, kPhCommit,
        kPhPubStage, kPhInlineLaunches, kPhStagedLaunches, kPhN };
-double g_phase[kPhN];
+// Two threads (helper + issue) add to them: relaxed atomics, integer nanoseconds.
+std::atomic<long long> g_phase_ns[kPhN];
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+inline void phase_add(int i, double v) {
+  g_phase_ns[i].fetch_add((long long)(v * 1e9), std::memory_order_relaxed);
+}
 }  // namespace
 KV_API int kv_host_profile(double *out, int32_t n, int32_t reset) {
-  for (int i = 0; i < n && i < kPhN; ++i) out[i] = g_phase[i];
+  for (int i = 0; i < n && i < kPhN; ++i) out[i] = g_phase_ns[i].load() * 1e-9;
   if (reset)
-    for (double &x : g_phase) x = 0;
+    for (auto &x : g_phase_ns) x.store(0);
   return kPhN;
 }
 
@@ -1142,7 +1146,7 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
   int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
   if (rc) return rc;
   const double tb = now_s();
-  g_phase[kPhAcquire] += tb - ta;
+  phase_add(kPhAcquire, tb - ta);
   size_t off = 0;
   for (int i = 0; i < nl; ++i) {
     Launch &L = *ls[i];
@@ -1165,9 +1169,9 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
     off += align16(L.staged_bytes());
   }
   const double tc = now_s();
-  g_phase[kPhHostCopy] += tc - tb;
+  phase_add(kPhHostCopy, tc - tb);
   CU(cudaMemcpyAsync(b->dev, b->host, total, cudaMemcpyHostToDevice, st));
-  g_phase[kPhH2DCall] += now_s() - tc;
+  phase_add(kPhH2DCall, now_s() - tc);
   *out = b;
   return KV_OK;
 }
@@ -1202,7 +1206,7 @@ int enqueue(Launch &L, cudaStream_t st) {
   }
   CU(timed_launch(kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
                   L.p0->geom_dev(), launch_grid(L), st, L.params.data()));
-  g_phase[kPhStagedLaunches] += 1.0;
+  phase_add(kPhStagedLaunches, 1.0);
   g_launches++;
   L.p0->kernels++;
   return KV_OK;
@@ -1740,16 +1744,16 @@ void prepare_step(const kv_step_t &st, StepPrep &sp) {
     return;
   }
   const double t1 = now_s();
-  g_phase[kPhPrepAppend] += t1 - t0;
+  phase_add(kPhPrepAppend, t1 - t0);
   if (sp.has_p) {
     if ((sp.rc = prepare_replicate(st.n_repl, st.repl_pools, st.step, sp.P))) {
       sp.err = g_err;
       return;
     }
     const double t2 = now_s();
-    g_phase[kPhPrepRepl] += t2 - t1;
+    phase_add(kPhPrepRepl, t2 - t1);
     commit_replicate(sp.P, st.repl_pools, st.step);
-    g_phase[kPhCommit] += now_s() - t2;
+    phase_add(kPhCommit, now_s() - t2);
   }
   kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
   if (p0 && sp.has_a && sp.has_p && sp.P.p0->device != p0->device) {
@@ -1788,7 +1792,7 @@ int enqueue_inline(Launch &L, const KvInlineDesc &d, cudaStream_t st, bool pdl) 
   g_ev_before = g_ev_after = nullptr;
   if (b) CU(cudaEventRecord(b, st));
   CU(launch_copy_inline(L.kind, d, L.p0->geom_dev(), launch_grid(L), st, pdl));
-  g_phase[kPhInlineLaunches] += 1.0;  // a count (kv_host_profile divides like the times)
+  phase_add(kPhInlineLaunches, 1.0);  // a count (kv_host_profile divides like the times)
   if (a) CU(cudaEventRecord(a, st));
   g_launches++;
   L.p0->kernels++;
@@ -1848,7 +1852,7 @@ int issue_append(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa
     Launch *ls[1] = {&sp.A};
     if (!sp.inl_a && !sp.A.tasks.empty() && (rc = stage(ctx, ls, 1, sa, &b))) return rc;
     const double t1 = now_s();
-    g_phase[kPhStage] += t1 - t0;
+    phase_add(kPhStage, t1 - t0);
     // shared capacity: a freed replica block may be reused by this very append, so
     // the ring-put that last wrote it (k-1) must be complete
     const int lag = sp.shared ? 1 : 2;
@@ -1861,7 +1865,7 @@ int issue_append(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa
     if (rc) return rc;
     if (sb && (rc = ctx->done(sb, sa))) return rc;  // the staged source outlives the kernel
     if (b && (rc = ctx->done(b, sa))) return rc;
-    g_phase[kPhEnqA] += now_s() - t1;
+    phase_add(kPhEnqA, now_s() - t1);
   }
   if (sa != sr && sp.has_p) {  // the publication of step k follows this append
     CU(cudaEventRecord(so.aready[k % N], sa));
@@ -1880,14 +1884,14 @@ int issue_publish(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t s
   if (sa != sr && so.astep[k % N] == k) CU(cudaStreamWaitEvent(sr, so.aready[k % N], 0));
   if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
   const double t1 = now_s();
-  g_phase[kPhEvents] += t1 - t0;
+  phase_add(kPhEvents, t1 - t0);
   DeviceCtx *ctx = ctx_for(p0->device);
   std::lock_guard<std::mutex> lk(ctx->mu);
   StageBuf *b = nullptr;
   int rc = KV_OK;
   Launch *ls[1] = {&sp.P};
   if (!sp.inl_p && !sp.P.tasks.empty() && (rc = stage(ctx, ls, 1, sr, &b))) return rc;
-  g_phase[kPhPubStage] += now_s() - t1;
+  phase_add(kPhPubStage, now_s() - t1);
   g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
   g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
   rc = sp.inl_p ? enqueue_inline(sp.P, *sp.dp, sr, false) : enqueue(sp.P, sr);
@@ -1899,7 +1903,7 @@ int issue_publish(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t s
     so.rstep[k % N] = k;
   }
   if (b && (rc = ctx->done(b, sr))) return rc;
-  g_phase[kPhEnqP] += now_s() - t1;
+  phase_add(kPhEnqP, now_s() - t1);
   return KV_OK;
 }
 
@@ -1955,11 +1959,11 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
         if (stop.load(std::memory_order_acquire)) return;
         std::this_thread::yield();
       }
-      g_phase[kPhWaitIssue] += now_s() - w0;
+      phase_add(kPhWaitIssue, now_s() - w0);
       StepPrep &sp = ring[k & 1];
       const double t0 = now_s();
       prepare_step(steps[k], sp);
-      g_phase[kPhPrepare] += now_s() - t0;
+      phase_add(kPhPrepare, now_s() - t0);
       produced.store(k + 1, std::memory_order_release);
       if (sp.rc) return;
     }
@@ -1968,7 +1972,7 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
   for (int k = 0; k < n_steps; ++k) {
     const double w0 = now_s();
     while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
-    g_phase[kPhWaitPrep] += now_s() - w0;
+    phase_add(kPhWaitPrep, now_s() - w0);
     StepPrep &sp = ring[k & 1];
     if (sp.rc) {
       rc = sp.rc;
@@ -2059,7 +2063,7 @@ int stage_fused(DeviceCtx *ctx, FusedPrep &fp, cudaStream_t st, StageBuf **out,
   int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
   if (rc) return rc;
   const double tb = now_s();
-  g_phase[kPhAcquire] += tb - ta;
+  phase_add(kPhAcquire, tb - ta);
   char *h = b->host, *d = b->dev;
   for (int k = 0; k < np; ++k) {
     P.params[k].slot_req = reinterpret_cast<const int64_t *>(d + pbytes + P.table_off[k]);
@@ -2072,9 +2076,9 @@ int stage_fused(DeviceCtx *ctx, FusedPrep &fp, cudaStream_t st, StageBuf **out,
   if (nta) std::memcpy(h + pbytes + tbl, A.tasks.data(), sizeof(KvTask) * nta);
   if (ntp) std::memcpy(h + pbytes + tbl + sizeof(KvTask) * nta, P.tasks.data(), sizeof(KvTask) * ntp);
   const double tc = now_s();
-  g_phase[kPhHostCopy] += tc - tb;
+  phase_add(kPhHostCopy, tc - tb);
   CU(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, st));
-  g_phase[kPhH2DCall] += now_s() - tc;
+  phase_add(kPhH2DCall, now_s() - tc);
   *params_dev = reinterpret_cast<const KvPoolParams *>(d);
   *tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
   *out = b;
@@ -2095,7 +2099,7 @@ int issue_fused(const kv_step_t *ev_step, FusedPrep &fp, cudaStream_t st) {
   const KvTask *td = nullptr;
   if ((rc = stage_fused(ctx, fp, st, &b, &pd, &td))) return rc;
   double t1 = now_s();
-  g_phase[kPhStage] += t1 - t0;
+  phase_add(kPhStage, t1 - t0);
   const int na = fp.has_a ? fp.A.n_pools : 0, np = fp.has_p ? fp.P.n_pools : 0;
   const int nta = fp.has_a ? (int)fp.A.tasks.size() : 0;
   const int ntot = nta + (fp.has_p ? (int)fp.P.tasks.size() : 0);
@@ -2110,7 +2114,7 @@ int issue_fused(const kv_step_t *ev_step, FusedPrep &fp, cudaStream_t st) {
   }
   if (sb && (rc = ctx->done(sb, st))) return rc;
   rc = ctx->done(b, st);
-  g_phase[kPhEnqA] += now_s() - t1;
+  phase_add(kPhEnqA, now_s() - t1);
   return rc;
 }
 
@@ -2148,10 +2152,10 @@ KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *str
         if (stop.load(std::memory_order_acquire)) return;
         std::this_thread::yield();
       }
-      g_phase[kPhWaitIssue] += now_s() - w0;
+      phase_add(kPhWaitIssue, now_s() - w0);
       const double t0 = now_s();
       prepare_fused(steps, n_steps, k, ring[k & 1]);
-      g_phase[kPhPrepare] += now_s() - t0;
+      phase_add(kPhPrepare, now_s() - t0);
       produced.store(k + 1, std::memory_order_release);
       if (ring[k & 1].rc) return;
     }
@@ -2160,7 +2164,7 @@ KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *str
   for (int k = 0; k < n_launch; ++k) {
     const double w0 = now_s();
     while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
-    g_phase[kPhWaitPrep] += now_s() - w0;
+    phase_add(kPhWaitPrep, now_s() - w0);
     FusedPrep &fp = ring[k & 1];
     if (fp.rc) {
       rc = fp.rc;
@@ -2205,7 +2209,7 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
   int rc = KV_OK;
   if (nl && (rc = stage(ctx, ls, nl, s, &b))) return rc;
   const double t1 = now_s();
-  g_phase[kPhStage] += t1 - t0;
+  phase_add(kPhStage, t1 - t0);
   if (has_a) {
     if (st.ev_append_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_start), s));
     if (inl_a) {
@@ -2216,7 +2220,7 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
     if (st.ev_append_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_end), s));
   }
   const double t2 = now_s();
-  g_phase[kPhEnqA] += t2 - t1;
+  phase_add(kPhEnqA, t2 - t1);
   if (has_p) {
     if (st.ev_kernel_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_start), s));
     if (inl_p) {
@@ -2227,7 +2231,7 @@ int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
     if (st.ev_kernel_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_end), s));
   }
   if (b && (rc = ctx->done(b, s))) return rc;
-  g_phase[kPhEnqP] += now_s() - t2;
+  phase_add(kPhEnqP, now_s() - t2);
   return KV_OK;
 }
 
@@ -2256,10 +2260,10 @@ KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *strea
         if (stop.load(std::memory_order_acquire)) return;
         std::this_thread::yield();
       }
-      g_phase[kPhWaitIssue] += now_s() - w0;
+      phase_add(kPhWaitIssue, now_s() - w0);
       const double t0 = now_s();
       prepare_step(steps[k], ring[k & 1]);
-      g_phase[kPhPrepare] += now_s() - t0;
+      phase_add(kPhPrepare, now_s() - t0);
       produced.store(k + 1, std::memory_order_release);
       if (ring[k & 1].rc) return;
     }
@@ -2268,7 +2272,7 @@ KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *strea
   for (int k = 0; k < n_steps; ++k) {
     const double w0 = now_s();
     while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
-    g_phase[kPhWaitPrep] += now_s() - w0;
+    phase_add(kPhWaitPrep, now_s() - w0);
     StepPrep &sp = ring[k & 1];
     if (sp.rc) {
       rc = sp.rc;
