@@ -173,8 +173,13 @@ def test_c2_full_geometry_whole_arrays():
                 oring.replicate(t)
         for n in oring.nodes.values():
             assert max([b for s in range(n.R) for b in n.slot_bt[s]] + [0]) < 2048
+        K.kv_host_profile(reset=True)
         K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
         torch.cuda.synchronize()
+        prof = K.kv_host_profile(reset=True)
+        # both launch paths ran: decode steps with descriptors in the kernel parameter
+        # space, prefill-heavy steps staged in global memory
+        assert prof["n_inline_launches"] > 0 and prof["n_staged_launches"] > 0, prof
         sentinel = np.int16(np.uint16(0x5A5A).view(np.int16))
         for c, gid in drv.coords.items():
             on = oring.nodes[c]
