@@ -264,14 +264,15 @@ thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
 
 cudaError_t timed_launch(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
                          int n_pools, const KvGeomDev &g, int grid, cudaStream_t st,
-                         const KvPoolParams *host_params = nullptr) {
+                         const KvPoolParams *host_params = nullptr, int split = 1) {
   cudaEvent_t b = g_ev_before, a = g_ev_after;
   g_ev_before = g_ev_after = nullptr;
   if (b) {
     cudaError_t e = cudaEventRecord(b, st);
     if (e != cudaSuccess) return e;
   }
-  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st, host_params);
+  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st, host_params,
+                              split);
   if (e != cudaSuccess) return e;
   if (a) return cudaEventRecord(a, st);
   return cudaSuccess;
@@ -906,6 +907,7 @@ struct Launch {
   bool use_ce = false;
   std::vector<kv_pool::Inval> inval;  // shared capacity: published entries to withdraw first
   int max_reqs_inval = 0;
+  int split = 1;                      // CTA units per task (whole-item tasks)
   // filled by stage()
   const KvPoolParams *params_dev = nullptr;
   const KvTask *tasks_dev = nullptr;
@@ -924,6 +926,7 @@ struct Launch {
     for (auto &v : ce_blocks) v.clear();
     use_ce = false;
     inval.clear();
+    split = 1;
     params_dev = nullptr;
     tasks_dev = nullptr;
   }
@@ -964,6 +967,22 @@ int choose_task_segs(const kv_pool *p, long long total_segs) {
   return (int)std::min<long long>(maxs, t);
 }
 
+// Whole-item tasks (<= 32 KiB each, fewer descriptors to stage or carry in the
+// parameter space) split on the device into `split` CTA units so a decode step still
+// spreads over every resident CTA (KVRING_MIN_TASK_SEGS > 0: the old sizing, split 1).
+int whole_item_segs(const kv_pool *p) { return std::max(1, 32768 / p->seg_bytes); }
+
+int choose_split(const kv_pool *p, size_t n_tasks) {
+  if (n_tasks == 0) return 1;
+  const long long slots = (long long)resident_ctas(p->device < 0 ? 0 : p->device);
+  return (int)std::max(1LL, std::min(8LL, slots / (long long)n_tasks));
+}
+
+bool legacy_task_sizing() {
+  static const bool legacy = getenv("KVRING_MIN_TASK_SEGS") != nullptr;
+  return legacy;
+}
+
 int check_same_device(int n, kv_pool *const *pools) {
   kv_pool *p0 = pools[0];
   for (int k = 0; k < n; ++k) {
@@ -979,7 +998,7 @@ int check_same_device(int n, kv_pool *const *pools) {
 
 // Validates every pool (all-or-nothing), applies begin_step / releases / appends
 // to the host tables and builds the scatter tasks.
-int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
+int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L, bool allow_split = true) {
   if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
   if (n_pools > kMaxPoolsPerLaunchHost)
     return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
@@ -1007,7 +1026,9 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
   }
   L.reset(kKindAppend, n_pools);
   L.p0 = pools[0];
-  const int task_segs = choose_task_segs(L.p0, tokens * L.p0->combos);
+  const bool whole = allow_split && !legacy_task_sizing();
+  const int task_segs =
+      whole ? whole_item_segs(L.p0) : choose_task_segs(L.p0, tokens * L.p0->combos);
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = args[k].pool;
     if (args[k].begin_step) do_begin_step(p);
@@ -1029,13 +1050,14 @@ int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L) {
     }
   }
   collect_inval(L, pools, n_pools);
+  if (whole) L.split = choose_split(L.p0, L.tasks.size());
   return KV_OK;
 }
 
 // Validates the pools and builds the dirty work list (§8(a) a3); state is
 // committed by commit_replicate once the launch is enqueued.
 int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch &L,
-                      bool use_ce = false) {
+                      bool use_ce = false, bool allow_split = true) {
   if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
   if (n_pools > kMaxPoolsPerLaunchHost)
     return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
@@ -1056,7 +1078,9 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
   L.reset(kKindRingPut, n_pools);
   L.p0 = pools[0];
   L.use_ce = use_ce;
-  const int task_segs = choose_task_segs(L.p0, dirty * L.p0->combos);
+  const bool whole = allow_split && !legacy_task_sizing();
+  const int task_segs =
+      whole ? whole_item_segs(L.p0) : choose_task_segs(L.p0, dirty * L.p0->combos);
   size_t toff = 0;
   for (int k = 0; k < n_pools; ++k) toff += 12 * (size_t)pools[k]->R;
   L.tables.resize(toff);
@@ -1084,7 +1108,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.src_bytes = (unsigned long long)p->NB * p->block_bytes;
     pp.dst_bytes = (unsigned long long)p->succ_replica_blocks * p->block_bytes;
     pp.counter = p->counter;
-    pp.target = aborting || p->abort_after >= 0 ? ~0ull : p->issued + (unsigned long long)L.ntask[k];
+    pp.target = aborting || p->abort_after >= 0 ? ~0ull : 0ull;  // + units, set below
     pp.step = step;
     pp.max_reqs = p->R;
     pp.max_blk = p->M;
@@ -1096,6 +1120,10 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.pad0 = sys_per_cta;
   }
   collect_inval(L, pools, n_pools);
+  if (whole) L.split = choose_split(L.p0, L.tasks.size());
+  for (int k = 0; k < n_pools; ++k)  // the counter counts CTA units: tasks x split
+    if (L.params[k].target == 0ull)
+      L.params[k].target = pools[k]->issued + (unsigned long long)L.ntask[k] * L.split;
   static const bool dbg_nocopy = getenv("KVRING_DEBUG_RINGPUT_NOCOPY") != nullptr;
   if (dbg_nocopy)  // experiment knob: publication only (timing breakdown, breaks parity)
     for (size_t i = 0; i < L.tasks.size(); ++i) L.tasks[i].seg_count = 0;
@@ -1105,7 +1133,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
 void commit_replicate(Launch &L, kv_pool *const *pools, uint64_t step) {
   for (int k = 0; k < L.n_pools; ++k) {
     kv_pool *p = pools[k];
-    p->issued += (unsigned long long)L.ntask[k];
+    p->issued += (unsigned long long)L.ntask[k] * L.split;
     p->last_step_bytes = L.bytes[k];
     p->bytes_replicated += L.bytes[k];
     p->tasks_launched += L.ntask[k];
@@ -1179,7 +1207,9 @@ int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf *
 // Grid of a copy launch: one CTA per task up to the resident CTA count (capping the
 // append's grid so the concurrent ring-put finds free CTA slots was measured: no
 // gain, profiles/r01/exp25.log).
-int launch_grid(const Launch &L) { return copy_grid(L.p0->device, (int)L.tasks.size()); }
+int launch_grid(const Launch &L) {
+  return copy_grid(L.p0->device, (int)L.tasks.size() * L.split);
+}
 
 // Shared capacity: withdraw the freed replicas' published entries (req_id -1,
 // len 0 in the published parity) before this launch may reuse their blocks.
@@ -1199,13 +1229,8 @@ int enqueue(Launch &L, cudaStream_t st) {
     if (rc) return rc;
   }
   if (L.tasks.empty()) return KV_OK;
-  int kind = L.kind;
-  if (kind == kKindRingPut) {
-    static const bool dbg_nopub = getenv("KVRING_DEBUG_RINGPUT_NOPUB") != nullptr;
-    if (dbg_nopub) kind = kKindRestore;  // experiment knob: copy without publication
-  }
-  CU(timed_launch(kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
-                  L.p0->geom_dev(), launch_grid(L), st, L.params.data()));
+  CU(timed_launch(L.kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
+                  L.p0->geom_dev(), launch_grid(L), st, L.params.data(), L.split));
   phase_add(kPhStagedLaunches, 1.0);
   g_launches++;
   L.p0->kernels++;
@@ -1694,6 +1719,7 @@ void fill_inline(const Launch &L, KvInlineDesc &d) {
   d.n_tasks = (int32_t)L.tasks.size();
   d.n_pools = L.n_pools;
   d.task_off = (int32_t)off;
+  d.split = L.split;
   std::memcpy(d.data + off, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
   d.used = (int32_t)(off + sizeof(KvTask) * L.tasks.size());
 }
@@ -2032,13 +2058,13 @@ void prepare_fused(const kv_step_t *steps, int n_steps, int k, FusedPrep &fp) {
   fp.has_a = k < n_steps && steps[k].n_append > 0;
   if (fp.has_p) {
     const kv_step_t &pv = steps[k - 1];
-    if ((fp.rc = prepare_replicate(pv.n_repl, pv.repl_pools, pv.step, fp.P))) {
+    if ((fp.rc = prepare_replicate(pv.n_repl, pv.repl_pools, pv.step, fp.P, false, false))) {
       fp.err = g_err;
       return;
     }
     commit_replicate(fp.P, pv.repl_pools, pv.step);
   }
-  if (fp.has_a && (fp.rc = prepare_append(steps[k].n_append, steps[k].append, fp.A))) {
+  if (fp.has_a && (fp.rc = prepare_append(steps[k].n_append, steps[k].append, fp.A, false))) {
     fp.err = g_err;
     return;
   }

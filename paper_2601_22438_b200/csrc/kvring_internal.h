@@ -93,9 +93,12 @@ struct KvParamPack {
   char *dst[kInlinePools];
   int n;  // 0: read them from the staged global copy
 };
+// split: each task is processed as `split` CTA units (a contiguous share of its
+// slices each), so the host emits whole-item tasks (<= 32 KiB) and the device still
+// spreads a decode step over every resident CTA; the publication counts units.
 cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream,
-                        const KvPoolParams *host_params = nullptr);
+                        const KvPoolParams *host_params = nullptr, int split = 1);
 cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const KvPoolParams *params,
                          int n_app_pools, int n_rep_pools, const KvGeomDev &g, int grid,
                          cudaStream_t stream);
@@ -111,6 +114,7 @@ constexpr int kInlineBytes = 28 * 1024;
 template <int CAP>
 struct KvInlineDescT {
   int32_t n_tasks, n_pools, task_off, used;  // used: bytes of data in use
+  int32_t split, pad0, pad1, pad2;           // CTA units per task (see launch_copy)
   KvPoolParams pools[kInlinePools];
   alignas(16) char data[CAP];
 };

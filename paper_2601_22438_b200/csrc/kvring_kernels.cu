@@ -222,7 +222,7 @@ constexpr int kMaxPoolsPerLaunch = 64;
 // that pool's seq with a release store (last-CTA pattern, reading R9).
 __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int n_tasks,
                                           const KvPoolParams *__restrict__ params, int n_pools,
-                                          const char *tbl_base = nullptr) {
+                                          const char *tbl_base = nullptr, int split = 1) {
   __shared__ int s_cnt[kMaxPoolsPerLaunch];
   __shared__ int s_own[kMaxPoolsPerLaunch];
   for (int i = threadIdx.x; i < n_pools; i += blockDim.x) {
@@ -230,15 +230,18 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
     s_own[i] = 0;
   }
   __syncthreads();
-  for (int t = blockIdx.x + (int)threadIdx.x * (int)gridDim.x; t < n_tasks;
-       t += (int)blockDim.x * (int)gridDim.x) {
-    const KvTask tk = tasks[t];
+  // the units this CTA copied (u = blockIdx.x + i * gridDim.x), one per thread
+  const int n_units = n_tasks * split;
+  for (int u = blockIdx.x + (int)threadIdx.x * (int)gridDim.x; u < n_units;
+       u += (int)blockDim.x * (int)gridDim.x) {
+    const KvTask tk = tasks[u / split];
+    const bool lead = (u % split) == 0;  // bt entry / table ownership: once per task
     const KvPoolParams &pp = params[tk.pool];
-    if ((tk.flags & kFirst) && tk.slot >= 0) {
+    if (lead && (tk.flags & kFirst) && tk.slot >= 0) {
       int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
       bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
     }
-    if (tk.flags & kPoolFirst) s_own[tk.pool] = 1;
+    if (lead && (tk.flags & kPoolFirst)) s_own[tk.pool] = 1;
     atomicAdd(&s_cnt[tk.pool], 1);
   }
   __syncthreads();
@@ -278,10 +281,18 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
                                           const KvPoolParams *__restrict__ params,
                                           const KvGeomDev &g, int n_pools,
                                           const KvParamPack *pk = nullptr,
-                                          const char *tbl_base = nullptr) {
-  // pass 1: the copies -- identical for every kernel, no publication state live
-  for (int t = blockIdx.x; t < n_tasks; t += gridDim.x) {
-    const KvTask tk = tasks[t];
+                                          const char *tbl_base = nullptr, int split = 1) {
+  // pass 1: the copies -- identical for every kernel, no publication state live.
+  // Unit u = task u / split, share u % split of its slices.
+  const int n_units = n_tasks * split;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    KvTask tk = tasks[u / split];
+    if (split > 1) {
+      const int per = (tk.seg_count + split - 1) / split;
+      const int b0 = (u % split) * per;
+      tk.seg_begin += b0;
+      tk.seg_count = max(0, min(per, tk.seg_count - b0));
+    }
     const KvPoolParams &pp = params[tk.pool];
 #ifdef KV_BOUNDS_CHECK
     const unsigned long long sbytes = pp.src_bytes, dbytes = pp.dst_bytes;
@@ -293,7 +304,7 @@ __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int 
     char *dst = inl ? pk->dst[tk.pool] : pp.dst;
     copy_task<SRC, DST>(tk, src, dst, g, sbytes, dbytes);
   }
-  if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools, tbl_base);
+  if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools, tbl_base, split);
 }
 
 // One named kernel per role (ncu / launch lists show what ran).
@@ -329,9 +340,9 @@ KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false)       // a4: NCCL-varia
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     kv_append_scatter_kernel(const KvTask *__restrict__ tasks, int n_tasks,
                              const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools,
-                             const __grid_constant__ KvParamPack pk) {
+                             const __grid_constant__ KvParamPack pk, int split) {
   pdl_launch_dependents();
-  run_tasks<kTokMajor, kPaged, false>(tasks, n_tasks, params, g, n_pools, &pk);
+  run_tasks<kTokMajor, kPaged, false>(tasks, n_tasks, params, g, n_pools, &pk, nullptr, split);
   pdl_wait();
 }
 
@@ -339,10 +350,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     kv_ring_put_kernel(const KvTask *__restrict__ tasks, int n_tasks,
                        const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools,
-                       const __grid_constant__ KvParamPack pk) {
+                       const __grid_constant__ KvParamPack pk, int split) {
   pdl_wait();
   pdl_launch_dependents();
-  run_tasks<kPaged, kPaged, true>(tasks, n_tasks, params, g, n_pools, &pk);
+  run_tasks<kPaged, kPaged, true>(tasks, n_tasks, params, g, n_pools, &pk, nullptr, split);
 }
 
 // Inline-descriptor twins of the two hot kernels (KvInlineDesc: parameters, tables
@@ -352,7 +363,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     kv_append_scatter_inl_kernel(KvGeomDev g, const __grid_constant__ KvInlineDescT<CAP> d) {
   pdl_launch_dependents();
   run_tasks<kTokMajor, kPaged, false>(reinterpret_cast<const KvTask *>(d.data + d.task_off),
-                                      d.n_tasks, d.pools, g, d.n_pools);
+                                      d.n_tasks, d.pools, g, d.n_pools, nullptr, nullptr,
+                                      d.split);
   pdl_wait();
 }
 
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   pdl_wait();
   pdl_launch_dependents();
   run_tasks<kPaged, kPaged, true>(reinterpret_cast<const KvTask *>(d.data + d.task_off),
-                                  d.n_tasks, d.pools, g, d.n_pools, nullptr, d.data);
+                                  d.n_tasks, d.pools, g, d.n_pools, nullptr, d.data, d.split);
 }
 
 // Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
@@ -492,7 +504,7 @@ int copy_grid(int device, int n_tasks) {
 
 cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream,
-                        const KvPoolParams *host_params) {
+                        const KvPoolParams *host_params, int split) {
   if (n_tasks <= 0) return cudaSuccess;
   if (n_pools > kMaxPoolsPerLaunch) return cudaErrorInvalidValue;
   KvParamPack pk;
@@ -507,15 +519,18 @@ cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPool
   switch (kind) {
     case kKindAppend:
       kv_append_scatter_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools,
-                                                               pk);
+                                                               pk, split);
       break;
     case kKindRingPut:
-      kv_ring_put_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools, pk);
+      kv_ring_put_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools, pk,
+                                                         split);
       break;
     case kKindRestore:
+      if (split != 1) return cudaErrorInvalidValue;
       kv_restore_remap_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
       break;
     case kKindPack:
+      if (split != 1) return cudaErrorInvalidValue;
       kv_gather_pack_kernel<<<grid, kThreads, 0, stream>>>(tasks, n_tasks, params, g, n_pools);
       break;
     default:

@@ -14,6 +14,38 @@ __global__ void k(const __grid_constant__ Blob<N> p) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && p.b[N - 1] == 123) printf("x");
 }
 
+__global__ void spin(long long ns) {
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > ns) break;
+  }
+}
+
+// GPU-side rate: the launches are queued behind a 30 ms spin kernel, so the device
+// drains a full queue; events around the queued launches time the device only.
+template <int N>
+void run_gpu(cudaStream_t s) {
+  Blob<N> p{};
+  const int iters = 500;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  spin<<<1, 1, 0, s>>>(30000000ll);
+  cudaEventRecord(a, s);
+  for (int i = 0; i < iters; ++i) {
+    p.b[0] = (char)i;
+    k<N><<<592, 256, 0, s>>>(p);
+  }
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("params %6d B: device %.2f us/launch (queued)\n", N, ms * 1e3 / iters);
+}
+
 template <int N>
 void run(cudaStream_t s) {
   Blob<N> p{};
@@ -37,5 +69,6 @@ int main() {
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   run<256>(s); run<1024>(s); run<4096>(s); run<8192>(s); run<16384>(s); run<28672>(s); run<32000>(s);
+  run_gpu<256>(s); run_gpu<4096>(s); run_gpu<8192>(s); run_gpu<16384>(s); run_gpu<28672>(s);
   return 0;
 }
