@@ -45,7 +45,7 @@
  *        off 32+16R     int32 len[2][R]
  *        off 32+24R     int32 bt[R][M] block ids in the predecessor's pool
  *                       (entries j < ceil(len/B) of a listed slot are valid)
- *    seq is stored last with st.release.sys after a system-scope fence, so a
+ *    seq is stored last, right after a system-scope acquire-release fence, so a
  *    reader that acquires seq = t sees parity t's lengths, rows and KV slices.
  */
 #ifndef KVRING_H

@@ -1115,7 +1115,10 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.n_table = p->R;  // staged tables carry every slot (inline launches trim them)
     pp.writer_node = p->node_id;
     pp.publish = 1;
-    pp.sys_scope = p->succ_sys ? 1 : 0;
+    // KVRING_DEBUG_GPU_SCOPE=1 (experiments only: measures the cost of the system-scope
+    // publication; a remote reader could then see seq before the data)
+    static const bool dbg_gpu_scope = getenv("KVRING_DEBUG_GPU_SCOPE") != nullptr;
+    pp.sys_scope = p->succ_sys && !dbg_gpu_scope ? 1 : 0;
     static const int sys_per_cta = getenv("KVRING_SYS_PER_CTA") ? 1 : 0;  // experiments
     pp.pad0 = sys_per_cta;
   }

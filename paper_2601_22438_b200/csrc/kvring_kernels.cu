@@ -13,7 +13,7 @@
 // a second pass: each CTA adds its per-pool task counts to a monotone counter
 // with one release RMW (GPU scope); the CTA that completes a pool's count issues
 // an acquire-release fence (system scope for an NVLink successor) and stores the
-// seq flag with st.release (reading R9: a reader that acquires seq = t sees
+// seq flag right after it (release pattern; reading R9: a reader that acquires seq = t sees
 // everything of step t).  The hot kernels exist twice: with descriptors staged in
 // global memory, and "inline" with parameters, tables and tasks in the kernel
 // parameter space (KvInlineDescT, 4-28 KiB size classes) for decode-size steps.
@@ -179,11 +179,16 @@ __device__ __forceinline__ void fence_acquire(bool sys) {
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v, bool sys) {
+// The store of seq right after fence_acquire: a fence.acq_rel followed by a strong
+// (relaxed) store is a release pattern in the PTX memory model, so the store needs no
+// second fence (st.release would emit another MEMBAR; at system scope that second
+// MEMBAR.SYS costs microseconds per step over NVLink).
+__device__ __forceinline__ void st_after_fence(unsigned long long *p, unsigned long long v,
+                                               bool sys) {
   if (sys)
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Parity-`step` (req_id, len) table of one pool (reading R9).  Written by the
@@ -255,15 +260,16 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
       const bool sys = pp.sys_scope != 0;
       // Every CTA of this launch runs on this GPU, so the count RMW only needs GPU
       // scope even when the stores went to an NVLink peer; the completing CTA then
-      // issues ONE system-scope acquire-release fence before its st.release.sys of
-      // seq.  Causality order is transitive (release.gpu -> acquire.gpu -> fence.sys
-      // -> release.sys), so a peer that acquires seq = t sees every CTA's stores.
+      // issues ONE system-scope acquire-release fence before its (relaxed) store of
+      // seq.  Causality order is transitive (release.gpu -> fence.acq_rel.sys, which
+      // acquires the count and releases the seq store that follows it), so a peer that
+      // acquires seq = t sees every CTA's stores.
       // KVRING_SYS_PER_CTA=1 (experiments) restores a system-scope RMW per CTA.
       const unsigned long long old = atom_add_release(
           pp.counter, (unsigned long long)s_cnt[i], sys && (pp.pad0 & 1));
       if (old + (unsigned long long)s_cnt[i] == pp.target) {
         fence_acquire(sys);
-        st_release(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
+        st_after_fence(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
       }
     }
   }
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(kThreads) kv_unpack_kernel(const char *__restr
     const unsigned long long old = atom_add_release(counter, (unsigned long long)s_cnt, true);
     if (old + (unsigned long long)s_cnt == pp.target) {
       fence_acquire(true);
-      st_release(reinterpret_cast<unsigned long long *>(meta), pp.step, true);
+      st_after_fence(reinterpret_cast<unsigned long long *>(meta), pp.step, true);
       *counter = 0ull;  // per-call counter: the next unpack is stream-ordered after this one
     }
   }
