@@ -1097,7 +1097,10 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
     return {"value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d // n), "d2h_bytes_per_step": int(d2h // n),
             "steps": n, "ms_per_step": round(ms / n, 4), "wall_s": round(wall, 3),
-            "seq_readback_ok": ok}
+            "seq_readback_ok": ok,
+            "path": "kv_append_multi(KV_SRC_HOST) on pinned host tensors (the scatter kernel "
+                    "reads them over PCIe, zero copy) + kv_replicate_step_multi; per step a "
+                    "D2H read-back of the published seq flags"}
 
 
 def run_restore(drv, rt, t, dev, stream, world=1):

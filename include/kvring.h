@@ -157,8 +157,10 @@ int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids);
  * (a new block = lowest free id whenever len % B == 0); an unknown req_id is an
  * admission (slot = lowest free slot, then ceil(n_new/B) blocks).  src_kv is
  * dense [sum n_new][L][2][H][d] in entry order, on the device, or on the host
- * when flags & KV_SRC_HOST (copied by the library inside the call's stream
- * order; pinned memory recommended).  All-or-nothing: KV_ENOMEM / KV_EINVAL
+ * when flags & KV_SRC_HOST: pinned (page-locked) host memory is read by the
+ * scatter kernel directly over PCIe (zero copy; it must stay valid until the
+ * kernel has run), pageable host memory is copied into a library staging buffer
+ * in the call's stream order.  All-or-nothing: KV_ENOMEM / KV_EINVAL
  * leave the tables unchanged.  Launches one scatter kernel. */
 #define KV_SRC_HOST 1
 int kv_append(kv_pool_t *p, int32_t n, const int64_t *req_ids, const int32_t *n_new,

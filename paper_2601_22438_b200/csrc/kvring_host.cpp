@@ -1151,7 +1151,23 @@ void commit_replicate(Launch &L, kv_pool *const *pools, uint64_t step) {
 int stage_host_sources(DeviceCtx *ctx, Launch &L, cudaStream_t st, StageBuf **out) {
   *out = nullptr;
   size_t total = 0;
-  for (int k = 0; k < L.n_pools; ++k) total += L.host_src_bytes[k];
+  for (int k = 0; k < L.n_pools; ++k) {
+    if (!L.host_src_bytes[k]) continue;
+    // pinned (page-locked, hence mapped under UVA) host memory: the append kernel reads
+    // it directly over PCIe -- no staging copy and no staging buffer to grow
+    cudaPointerAttributes at;
+    void *dptr = nullptr;
+    if (cudaPointerGetAttributes(&at, L.host_src[k]) == cudaSuccess &&
+        at.type == cudaMemoryTypeHost &&
+        cudaHostGetDevicePointer(&dptr, const_cast<void *>(L.host_src[k]), 0) == cudaSuccess &&
+        dptr) {
+      L.params[k].src = static_cast<const char *>(dptr);
+      L.host_src_bytes[k] = 0;
+      continue;
+    }
+    cudaGetLastError();
+    total += L.host_src_bytes[k];
+  }
   if (total == 0) return KV_OK;
   StageBuf *sb = nullptr;
   int rc = ctx->acquire(ctx->src, ctx->next_src, total, false, &sb);
