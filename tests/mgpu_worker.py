@@ -61,7 +61,49 @@ def main():
     if transport == "nccl":
         from paper_2601_22438_b200.nccl_compare import NcclRing
         nccl = NcclRing(rt, 64 << 20)
-    for t in range(cfg.n_steps):
+    if transport == "runsteps":
+        # the bench's launch path: kv_run_steps on two streams (helper-thread prepare,
+        # inline descriptors, system-scope publication over NVLink), in chunks around
+        # the failure step
+        comp = torch.cuda.current_stream(dev)
+        repl = torch.cuda.Stream(dev)
+        keep = []
+
+        def chunk(t0, t1):
+            sts = []
+            for tt in range(t0, t1):
+                app = []
+                for node, e in drv.plan(tt).items():
+                    if node not in rt.local:
+                        continue
+                    ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                    src = content(e["stage"], ids, pos) if ids else None
+                    keep.append(src)
+                    app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                    req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+                pools = [rt.handle(n) for n in rt.alive_local() if rt.succ.get(n) is not None]
+                sts.append(dict(append=app, repl_pools=pools if tt >= 1 else [], step=tt))
+                oring.appends(tt)
+                if tt >= 1:
+                    oring.replicate(tt)
+            K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            compare_state(rt, drv, oring, tag=f"rank {rank} run_steps {t0}..{t1 - 1}")
+            dist.barrier()
+
+        chunk(0, cfg.fail_step)
+        t = cfg.fail_step
+        drv.append_step(t)
+        oring.appends(t)
+        drv.fail_and_restore(t, cfg.fail_node)
+        oring.fail_and_restore(t, cfg.fail_node)
+        rt.replicate_all(t)
+        oring.replicate(t)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        chunk(cfg.fail_step + 1, cfg.n_steps)
+    for t in range(cfg.n_steps if transport != "runsteps" else 0):
         drv.append_step(t)
         oring.appends(t)
         if t == cfg.fail_step:
