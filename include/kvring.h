@@ -214,7 +214,7 @@ int kv_set_mode(kv_pool_t *p, int32_t mode);
  * blocks freed by a retiring request are reused
  * one step later (reading R7) and must not be overwritten while a lagging
  * publication still reads them.  Optional cudaEvent_t handles are recorded on
- * repl_stream before the publication's H2D (ev_call), around its kernel
+ * repl_stream before the publication (ev_call), around its kernel
  * (ev_kernel_start / ev_kernel_end) and after it (ev_done).  Stops at the
  * first error (steps before it stay applied). */
 typedef struct {

@@ -1,6 +1,7 @@
 // libkvring host core: C ABI (include/kvring.h), allocator and block tables
 // (N2), ring link state, work-list / task builder (N4), staging of the
-// per-step descriptors (one H2D per call) and kernel launches.
+// per-step descriptors (kernel parameter space for decode-size launches, one H2D
+// per launch otherwise) and kernel launches.
 //
 // Paper: KevlarFlow (arXiv 2601.22438) P:223-229 §3.2 (background replication
 // of each request's KV, block representation, separate stream, promotion on
@@ -1184,7 +1185,8 @@ int stage_host_sources(DeviceCtx *ctx, Launch &L, cudaStream_t st, StageBuf **ou
   return KV_OK;
 }
 
-// Stages the descriptors of up to two launches with ONE pinned H2D copy.
+// Stages the descriptors of up to two launches with ONE pinned H2D copy (launches that
+// do not carry them inline in the kernel parameter space).
 int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf **out) {
   size_t total = 0;
   for (int i = 0; i < nl; ++i) total += align16(ls[i]->staged_bytes());
