@@ -354,7 +354,7 @@ def run_kvring(args):
     # ---- floor of a decode hop: a publication with nothing dirty ("empty
     # launch + one P2P flag store"), same pools, same stream, same launch path; the
     # last leg that replicates on these pools (its step numbers are not schedule steps)
-    floor = run_floor(rt, t + 10, repl, dev, world)
+    floor = run_floor(rt, t + 10, comp, repl, dev, world)
 
     # ---- restore: fail stage 2 of pipeline 0, restore into a fresh pool ---------
     restore = None
@@ -826,37 +826,41 @@ def run_block_mode(args, drv, rt, t0, comp, repl, content, dev, world):
 FLOOR_REPS = 50
 
 
-def run_floor(rt, t0, repl, dev, world):
-    """Per-step floor of the publication: kv_replicate_step_multi on every local pool with
-    no dirty token (one publish-only task per pool: bt / parity table / release seq, over
-    NVLink when the successor is remote), FLOOR_REPS times, CUDA events on the replication
-    stream around each call (max over ranks).  The decode-step ring-put is compared with it."""
+def run_floor(rt, t0, comp, repl, dev, world):
+    """Per-step floor of the publication on the timed loop's own path: FLOOR_REPS steps
+    of kv_run_steps with no append and nothing dirty (one publish-only task per pool:
+    bt / parity table / release seq, over NVLink when the successor is remote), timed
+    exactly like step_overhead_us (events from before the publication to after its
+    kernel, on the replication stream; max over ranks).  The decode-step ring-put is
+    compared with it."""
     import torch
     import torch.distributed as dist
     from paper_2601_22438_b200 import kvring as K
     nodes = [n for n in rt.alive_local() if rt.succ.get(n) is not None]
     handles = [rt.handle(n) for n in nodes]
+    sts, evs = [], []
+    for k in range(FLOOR_REPS + 1):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        evs.append(ev)
+        sts.append(dict(append=[], repl_pools=handles, step=t0 + k, ev_call=ev[0],
+                        ev_kernel_start=ev[1], ev_kernel_end=ev[2]))
+    prep = K.PreparedSteps(sts)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    K.kv_replicate_step_multi(handles, t0, repl.cuda_stream)     # warm
-    us = []
-    for k in range(FLOOR_REPS):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(repl)
-        K.kv_replicate_step_multi(handles, t0 + 1 + k, repl.cuda_stream)
-        b.record(repl)
-        us.append((a, b))
+    K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
     torch.cuda.synchronize(dev)
-    vals = sorted(x.elapsed_time(y) * 1e3 for x, y in us)
-    med = vals[len(vals) // 2]
-    v = torch.tensor([med], dtype=torch.float64, device=dev)
+    call = sorted(e[0].elapsed_time(e[2]) * 1e3 for e in evs[1:])
+    kern = sorted(e[1].elapsed_time(e[2]) * 1e3 for e in evs[1:])
+    v = torch.tensor([call[len(call) // 2], kern[len(kern) // 2]], dtype=torch.float64,
+                     device=dev)
     if world > 1:
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-    return {"median": round(float(v[0]), 2), "reps": FLOOR_REPS, "pools": len(nodes),
-            "what": "publication with nothing dirty: launch + bt/parity tables + release seq "
-                    "(one publish-only task per pool), events around the call on the "
-                    "replication stream; the decode-step ring-put's own floor"}
+    return {"median": round(float(v[0]), 2), "kernel_median": round(float(v[1]), 2),
+            "reps": FLOOR_REPS, "pools": len(nodes),
+            "what": "kv_run_steps steps with nothing dirty (one publish-only task per pool: "
+                    "launch + bt/parity tables + release seq), timed like step_overhead_us "
+                    "(median) and kernel_us (kernel_median); the decode-step ring-put's floor"}
 
 
 SHARED_NB = 2048   # C2 primary peak is ~1.57k blocks per stage: replicas must compete
