@@ -342,16 +342,17 @@ def test_reprotect_after_promotion_bit_exact():
         rt.destroy()
 
 
-@pytest.mark.parametrize("seed", [2, 3])
-def test_block_mode_with_failure_bit_exact(seed):
+@pytest.mark.parametrize("seed,shared", [(2, False), (3, False), (0, True)])
+def test_block_mode_with_failure_bit_exact(seed, shared):
     """NEXT-2 block-granular mode (completed blocks only): whole arrays == oracle,
-    including a failure, a restore at a block boundary and the resume."""
-    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
-                         batch_cap=6, n_requests=60, n_steps=40, fixed_prompt=None,
-                         fail_node=(0, 1), fail_step=26)
+    including a failure, a restore at a block boundary and the resume; shared: combined
+    with shared-capacity replicas under pressure (NEXT-3)."""
+    cfg = configs.scaled(configs.C1, num_blocks=28 if shared else 96, max_reqs=12,
+                         max_blocks_per_req=12, batch_cap=5 if shared else 6, n_requests=60,
+                         n_steps=40, fixed_prompt=None, fail_node=(0, 1), fail_step=26)
     sched = _churn_sched(cfg, seed)
-    rt, drv = make_gpu(cfg, schedules=sched, mode="blocks")
-    oring = OracleRing(cfg, schedules=sched, mode="blocks")
+    rt, drv = make_gpu(cfg, schedules=sched, mode="blocks", shared=shared)
+    oring = OracleRing(cfg, schedules=sched, mode="blocks", shared=shared)
     try:
         for t in range(cfg.n_steps):
             drv.append_step(t)
