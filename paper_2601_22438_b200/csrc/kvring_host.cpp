@@ -816,8 +816,18 @@ KV_API int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
     if (p->device >= 0) {
       cudaPointerAttributes at;
       if (cudaPointerGetAttributes(&at, succ_replica) == cudaSuccess &&
-          at.type == cudaMemoryTypeDevice && at.device == p->device)
-        p->succ_sys = false;
+          at.type == cudaMemoryTypeDevice) {
+        if (at.device == p->device) {
+          p->succ_sys = false;
+        } else {
+          // a successor on another GPU of this process (plain cudaMalloc memory, not an
+          // IPC / symmetric-memory mapping): the stores need peer access
+          DeviceGuard dg(p->device);
+          int can = 0;
+          if (cudaDeviceCanAccessPeer(&can, p->device, at.device) == cudaSuccess && can)
+            cudaDeviceEnablePeerAccess(at.device, 0);  // already enabled: harmless error
+        }
+      }
       cudaGetLastError();
     }
     p->succ_node = succ_node;
