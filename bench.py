@@ -430,8 +430,15 @@ def run_kvring(args):
     else:
         per_launch = my_bytes / args.steps
         achieved = per_launch / (avg_kern * 1e-6) / 1e9
+        tr = traffic_ref("decode_step_nvlink", "kv_ring_put_inl_kernel")
         roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
-                "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
+                "traffic": (tr["dram_read"] if tr else None),
+                "nvlink_traffic_note": ("ncu of a decode-only launch (tools/nvlink_profile.py, "
+                                        "profiles/traffic.json): nvltx user bytes %d / wire "
+                                        "bytes %d vs algorithmic %d"
+                                        % (tr["nvltx_bytes_data_user"], tr["nvltx_bytes"],
+                                           tr["algorithmic_nvlink"])) if tr else None,
                 "kernel": RINGPUT,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
                 "algorithmic_bytes_per_launch": int(per_launch), "avg_launch_us": round(avg_kern, 2)}
