@@ -94,6 +94,21 @@ def test_ragged_geometry_and_big_prefill():
     rt.destroy()
 
 
+@pytest.mark.parametrize("heads,head_dim,block", [(4, 64, 16), (2, 256, 32), (1, 8, 4)])
+def test_other_head_geometries_bit_exact(heads, head_dim, block):
+    """Slice sizes other than 256 B (128 B, 512 B, 16 B: other 16-B chunk counts per
+    slice), other KV-head counts and block sizes, through churn and a failure."""
+    cfg = configs.scaled(configs.C1, geom=configs.Geometry(layers=2, kv_heads=heads,
+                                                           head_dim=head_dim,
+                                                           block_size=block),
+                         num_blocks=600 if block == 4 else 160, max_reqs=12,
+                         max_blocks_per_req=64 if block == 4 else 16, batch_cap=5,
+                         n_requests=40, n_steps=24, fixed_prompt=None, fail_node=(0, 2),
+                         fail_step=15)
+    rt, drv, oring = _run_both(cfg, schedules=_churn_sched(cfg, 9))
+    rt.destroy()
+
+
 def test_abort_mid_step_keeps_last_published_replica():
     """A stage dying mid-replicate leaves its successor's replica at the last
     published step (R7/R9): restore == oracle restore of the previous step."""
