@@ -64,9 +64,13 @@ def parse():
                     help="timed steps of the shared-capacity leg (NEXT-3; N = 1 only; 0: skip)")
     ap.add_argument("--timeline", action="store_true",
                     help="diagnostic: time every step and print the replication-stream timeline")
-    ap.add_argument("--loop", default="streams", choices=["fused", "streams", "pdl"],
-                    help="fused: kv_run_steps_fused (append k + publication k-1 per launch, one "
-                         "stream); streams: kv_run_steps (append stream + replication stream)")
+    ap.add_argument("--loop", default="auto", choices=["auto", "fused", "streams", "pdl", "graph"],
+                    help="streams: kv_run_steps (append stream + replication stream); graph: "
+                         "kv_run_steps_graph (the same steps as CUDA graphs of 8 steps); pdl: "
+                         "one stream with programmatic dependent launch; fused: append k + "
+                         "publication k-1 per launch; auto (default): graph on 1 GPU (measured "
+                         "+7-9 %%, profiles/r01/exp37.log), streams over NVLink (equal or better "
+                         "there, exp36.log)")
     ap.add_argument("--single-stream", action="store_true",
                     help="append and replicate on one stream (default: replication stream)")
     return ap.parse_args()
@@ -176,6 +180,8 @@ def run_kvring(args):
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     N = args.gpus
+    if args.loop == "auto":
+        args.loop = "graph" if N == 1 else "streams"
     if world != N:
         raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}; launch N>1 with torch.distributed.run")
     torch.cuda.set_device(local_rank)
@@ -273,6 +279,8 @@ def run_kvring(args):
         K.kv_run_steps_fused(warm, comp.cuda_stream)
     elif args.loop == "pdl":
         K.kv_run_steps_pdl(warm, comp.cuda_stream)
+    elif args.loop == "graph":
+        K.kv_run_steps_graph(warm, comp.cuda_stream, repl.cuda_stream)
     else:
         K.kv_run_steps(warm, comp.cuda_stream, repl.cuda_stream)
     t += args.warmup
@@ -298,6 +306,8 @@ def run_kvring(args):
             K.kv_run_steps_fused(timed, comp.cuda_stream)
         elif args.loop == "pdl":
             K.kv_run_steps_pdl(timed, comp.cuda_stream)
+        elif args.loop == "graph":
+            K.kv_run_steps_graph(timed, comp.cuda_stream, repl.cuda_stream)
         else:
             K.kv_run_steps(timed, comp.cuda_stream, repl.cuda_stream)
         fin = torch.cuda.Event()
@@ -313,7 +323,7 @@ def run_kvring(args):
                  for k, v in K.kv_host_profile(reset=True).items()}
     ms = start.elapsed_time(end)
     kern_us = [e[1].elapsed_time(e[2]) * 1e3 for e in evs]
-    rep_us = kern_us if args.loop in ("fused", "pdl") else [e[0].elapsed_time(e[2]) * 1e3
+    rep_us = kern_us if args.loop in ("fused", "pdl", "graph") else [e[0].elapsed_time(e[2]) * 1e3
                                                            for e in evs]
     if args.timeline and rank == 0:
         T = lambda e: start.elapsed_time(e) * 1e3

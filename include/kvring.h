@@ -252,6 +252,19 @@ int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream);
  * supported (KV_EINVAL). */
 int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream);
 
+/* CUDA-graph decode loop: the same work and results as kv_run_steps, issued as one
+ * CUDA graph per group of 8 steps -- per step an append kernel node and a ring-put
+ * kernel node whose graph edges are kv_run_steps' stream-order rules (append k
+ * after append k-1 and after ring-put k-2, reading R7; ring-put k after append k
+ * and after ring-put k-1), the group's descriptors staged by one H2D memcpy node.
+ * Groups alternate between the two (distinct) streams and are chained by
+ * event-wait nodes; on return both streams are ordered after the last group.
+ * ev_kernel_start / ev_kernel_end are recorded around each ring-put node; ev_call,
+ * ev_done and ev_append_* are ignored.  KV_SRC_HOST appends and shared-capacity
+ * pools are not supported (KV_EINVAL). */
+int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *append_stream,
+                       void *repl_stream);
+
 /* Re-protection after a failure (§8(f) NEXT-1; §3.2: "replication targets
  * will be automatically adjusted to exclude the nodes under traffic rerouting").
  * succ[n_nodes] is the ring's successor map over logical node ids; excluded

@@ -1770,6 +1770,7 @@ struct StepPrep {
   bool shared = false;  // a pool of this step is in shared-capacity mode (NEXT-3)
   // inline descriptors (kernel parameter space), filled on the helper thread
   bool inl_a = false, inl_p = false;
+  bool no_inline = false;  // the graph loop stages every step's descriptors
   std::unique_ptr<KvInlineDesc> da, dp;
   int rc = KV_OK;
   std::string err;
@@ -1822,7 +1823,7 @@ void prepare_step(const kv_step_t &st, StepPrep &sp) {
   // staging copy, no H2D, no dependent descriptor load); host-source appends and
   // large (prefill / bulk) steps are staged
   sp.inl_a = sp.inl_p = false;
-  if (!p0 || p0->device < 0) return;
+  if (!p0 || p0->device < 0 || sp.no_inline) return;
   bool host_src = false;
   if (sp.has_a)
     for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q) host_src |= sp.A.host_src_bytes[q] != 0;
@@ -2044,6 +2045,313 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
   }
   stop.store(true, std::memory_order_release);
   worker.join();
+  return rc;
+}
+
+// ---- CUDA-graph decode loop ---------------------------------------------------
+// The same work as kv_run_steps, issued as one CUDA graph per group of kGraphSteps
+// steps: per step an append kernel node and a ring-put kernel node with the
+// stream-order constraints of kv_run_steps as graph edges (append k after append
+// k-1 and after ring-put k-2 -- R7 --, ring-put k after append k and after ring-put
+// k-1), all descriptors of the group staged by ONE H2D memcpy node.  A kernel node
+// costs the device < 1 us instead of 2-4 us for a stream launch and the host a
+// ~0.3 us parameter update instead of a 3-6 us launch (tools/launchbench.cu).
+// Consecutive groups run on the two streams and are chained by event-wait nodes,
+// so group g+1 overlaps the tail of group g exactly like consecutive steps do.
+namespace {
+
+constexpr int kGraphSteps = 8;
+
+struct GraphLoop {
+  static constexpr int kEv = 4, kSlots = 4;
+  int device = -1;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge[2] = {};
+  cudaGraphNode_t mc = nullptr, wait_a = nullptr, wait_r2 = nullptr, wait_r1 = nullptr;
+  cudaGraphNode_t an[kGraphSteps] = {}, rn[kGraphSteps] = {};
+  cudaGraphNode_t es[kGraphSteps] = {}, ee[kGraphSteps] = {};
+  cudaGraphNode_t rec_a = nullptr, rec_r2 = nullptr, rec_r1 = nullptr;
+  cudaEvent_t ev_a[kEv] = {}, ev_r2[kEv] = {}, ev_r1[kEv] = {};
+  cudaEvent_t start_a = nullptr, start_r = nullptr, join = nullptr;
+  cudaEvent_t dummy[2 * kGraphSteps] = {};
+  StageBuf slot[kSlots];
+  KvNodeArgs args[2 * kGraphSteps];
+  long long group = 0;
+
+  int make_event(cudaEvent_t *e) {
+    CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return KV_OK;
+  }
+  int build(int dev) {
+    device = dev;
+    for (int i = 0; i < kEv; ++i) {
+      int rc = make_event(&ev_a[i]);
+      if (!rc) rc = make_event(&ev_r2[i]);
+      if (!rc) rc = make_event(&ev_r1[i]);
+      if (rc) return rc;
+    }
+    for (auto &e : dummy)
+      if (int rc = make_event(&e)) return rc;
+    if (int rc = make_event(&start_a)) return rc;
+    if (int rc = make_event(&start_r)) return rc;
+    if (int rc = make_event(&join)) return rc;
+    for (auto &sl : slot) {
+      const size_t cap = 32u << 20;
+      CU(cudaHostAlloc(reinterpret_cast<void **>(&sl.host), cap, cudaHostAllocDefault));
+      CU(cudaMalloc(reinterpret_cast<void **>(&sl.dev), cap));
+      sl.cap = cap;
+      CU(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+    }
+    CU(cudaGraphCreate(&g, 0));
+    CU(cudaGraphAddMemcpyNode1D(&mc, g, nullptr, 0, slot[0].dev, slot[0].host, 16,
+                                cudaMemcpyHostToDevice));
+    CU(cudaGraphAddEventWaitNode(&wait_a, g, nullptr, 0, start_a));
+    CU(cudaGraphAddEventWaitNode(&wait_r2, g, nullptr, 0, start_r));
+    CU(cudaGraphAddEventWaitNode(&wait_r1, g, nullptr, 0, start_r));
+    // experiment knob KVRING_GRAPH_LAG=1: append k waits for ring-put k-1 (no overlap of
+    // an append with the previous publication); default 2 (reading R7's minimum)
+    static const int lag = [] {
+      const char *e = getenv("KVRING_GRAPH_LAG");
+      return e && atoi(e) == 1 ? 1 : 2;
+    }();
+    for (int k = 0; k < kGraphSteps; ++k) {
+      cudaKernelNodeParams kp{};
+      kernel_node_params(kKindAppend, 1, args[2 * k], kp);
+      cudaGraphNode_t lagdep =
+          lag == 2 ? (k >= 2 ? ee[k - 2] : (k == 0 ? wait_r2 : wait_r1))
+                   : (k >= 1 ? ee[k - 1] : wait_r1);
+      cudaGraphNode_t da[3] = {mc, k > 0 ? an[k - 1] : wait_a, lagdep};
+      CU(cudaGraphAddKernelNode(&an[k], g, da, 3, &kp));
+      cudaGraphNode_t ds[2] = {an[k], k > 0 ? ee[k - 1] : wait_r1};
+      CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
+      kernel_node_params(kKindRingPut, 1, args[2 * k + 1], kp);
+      CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
+      CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
+    }
+    CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[kGraphSteps - 1], 1, ev_a[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_r2, g, &ee[kGraphSteps - 2], 1, ev_r2[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_r1, g, &ee[kGraphSteps - 1], 1, ev_r1[0]));
+    for (auto &x : ge) CU(cudaGraphInstantiate(&x, g, 0));
+    return KV_OK;
+  }
+};
+
+std::mutex g_graph_mu;
+std::map<int, std::unique_ptr<GraphLoop>> g_graph;
+
+// Packs one launch's descriptors (params, publication tables, tasks) into a group
+// slot at `off` and points the launch at the device copy.
+void pack_launch(Launch &L, char *h, char *d, size_t &off) {
+  const size_t pbytes = align16(sizeof(KvPoolParams) * L.n_pools);
+  const size_t tbl = align16(L.tables.size());
+  for (int k = 0; k < L.n_pools; ++k)
+    if (L.kind == kKindRingPut) {
+      const size_t o = off + pbytes + L.table_off[k];
+      L.params[k].slot_req = reinterpret_cast<const int64_t *>(d + o);
+      L.params[k].slot_len = reinterpret_cast<const int32_t *>(d + o + 8 * (size_t)L.params[k].max_reqs);
+    }
+  std::memcpy(h + off, L.params.data(), sizeof(KvPoolParams) * L.n_pools);
+  if (!L.tables.empty()) std::memcpy(h + off + pbytes, L.tables.data(), L.tables.size());
+  std::memcpy(h + off + pbytes + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
+  L.params_dev = reinterpret_cast<const KvPoolParams *>(d + off);
+  L.tasks_dev = reinterpret_cast<const KvTask *>(d + off + pbytes + tbl);
+  off += align16(L.staged_bytes());
+}
+
+int set_kernel_node(cudaGraphExec_t ge, cudaGraphNode_t node, Launch *L, bool present,
+                    KvNodeArgs &a, int kind) {
+  cudaKernelNodeParams kp{};
+  a = KvNodeArgs{};
+  int grid = 1;
+  if (present && L && !L->tasks.empty()) {
+    a.tasks = L->tasks_dev;
+    a.n_tasks = (int)L->tasks.size();
+    a.params = L->params_dev;
+    a.g = L->p0->geom_dev();
+    a.n_pools = L->n_pools;
+    a.split = L->split;
+    if (L->n_pools <= kInlinePools) {
+      a.pk.n = L->n_pools;
+      for (int q = 0; q < L->n_pools; ++q) {
+        a.pk.src[q] = L->params[q].src;
+        a.pk.dst[q] = L->params[q].dst;
+      }
+    }
+    grid = launch_grid(*L);
+  }
+  kernel_node_params(kind, grid, a, kp);
+  CU(cudaGraphExecKernelNodeSetParams(ge, node, &kp));
+  CU(cudaGraphNodeSetEnabled(ge, node, present ? 1 : 0));
+  return KV_OK;
+}
+
+// Issues group [k0, k0 + n) of prepared steps (n <= kGraphSteps).
+int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n,
+                cudaStream_t sa, cudaStream_t sr, bool first) {
+  const int N = GraphLoop::kEv;
+  const long long gi = G.group++;
+  StageBuf &sl = G.slot[gi % GraphLoop::kSlots];
+  const double t0 = now_s();
+  if (sl.pending) {
+    CU(cudaEventSynchronize(sl.ev));
+    sl.pending = false;
+  }
+  phase_add(kPhAcquire, now_s() - t0);
+  size_t need = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sp[i]->has_a) need += align16(sp[i]->A.staged_bytes());
+    if (sp[i]->has_p) need += align16(sp[i]->P.staged_bytes());
+  }
+  if (need > sl.cap) {  // rare (bulk steps): grow this slot
+    if (sl.host) cudaFreeHost(sl.host);
+    if (sl.dev) cudaFree(sl.dev);
+    const size_t cap = std::max(need * 2, sl.cap);
+    CU(cudaHostAlloc(reinterpret_cast<void **>(&sl.host), cap, cudaHostAllocDefault));
+    CU(cudaMalloc(reinterpret_cast<void **>(&sl.dev), cap));
+    sl.cap = cap;
+  }
+  const double t1 = now_s();
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sp[i]->has_a && !sp[i]->A.tasks.empty()) pack_launch(sp[i]->A, sl.host, sl.dev, off);
+    if (sp[i]->has_p && !sp[i]->P.tasks.empty()) pack_launch(sp[i]->P, sl.host, sl.dev, off);
+  }
+  phase_add(kPhHostCopy, now_s() - t1);
+  const int par = (int)(gi & 1);
+  cudaGraphExec_t ge = G.ge[par];
+  cudaStream_t st = par ? sr : sa;
+  CU(cudaGraphExecMemcpyNodeSetParams1D(ge, G.mc, sl.dev, sl.host, off > 0 ? off : 16,
+                                        cudaMemcpyHostToDevice));
+  const int pe = (int)((gi + N - 1) % N);
+  CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_a, first ? G.start_a : G.ev_a[pe]));
+  CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r2, first ? G.start_r : G.ev_r2[pe]));
+  CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r1, first ? G.start_r : G.ev_r1[pe]));
+  for (int k = 0; k < kGraphSteps; ++k) {
+    const bool on = k < n;
+    StepPrep *s = on ? sp[k] : nullptr;
+    int rc = set_kernel_node(ge, G.an[k], s ? &s->A : nullptr, on && s->has_a, G.args[2 * k],
+                             kKindAppend);
+    if (!rc)
+      rc = set_kernel_node(ge, G.rn[k], s ? &s->P : nullptr, on && s->has_p,
+                           G.args[2 * k + 1], kKindRingPut);
+    if (rc) return rc;
+    cudaEvent_t e0 = G.dummy[2 * k], e1 = G.dummy[2 * k + 1];
+    if (on && steps[k].ev_kernel_start) e0 = static_cast<cudaEvent_t>(steps[k].ev_kernel_start);
+    if (on && steps[k].ev_kernel_end) e1 = static_cast<cudaEvent_t>(steps[k].ev_kernel_end);
+    CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.es[k], e0));
+    CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.ee[k], e1));
+    if (on) {
+      if (s->has_a && !s->A.tasks.empty()) {
+        g_launches++;
+        s->A.p0->kernels++;
+      }
+      if (s->has_p && !s->P.tasks.empty()) {
+        g_launches++;
+        s->P.p0->kernels++;
+      }
+    }
+  }
+  CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_a, G.ev_a[gi % N]));
+  CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r2, G.ev_r2[gi % N]));
+  CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r1, G.ev_r1[gi % N]));
+  const double t2 = now_s();
+  CU(cudaGraphLaunch(ge, st));
+  CU(cudaEventRecord(sl.ev, st));
+  sl.pending = true;
+  phase_add(kPhEnqP, now_s() - t2);
+  return KV_OK;
+}
+
+}  // namespace
+
+KV_API int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *append_stream,
+                              void *repl_stream) {
+  if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
+  if (n_steps == 0) return KV_OK;
+  cudaStream_t sa = static_cast<cudaStream_t>(append_stream);
+  cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
+  if (sa == sr) return fail(KV_EINVAL, "kv_run_steps_graph needs two distinct streams");
+  kv_pool *p0 = nullptr;
+  for (int k = 0; k < n_steps; ++k) {
+    if (any_shared(steps[k]))
+      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps");
+    for (int i = 0; i < steps[k].n_append; ++i) {
+      if (steps[k].append[i].flags & KV_SRC_HOST)
+        return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_graph");
+      if (!p0) p0 = steps[k].append[i].pool;
+    }
+    if (!p0 && steps[k].n_repl > 0) p0 = steps[k].repl_pools[0];
+  }
+  if (!p0) return fail(KV_EINVAL, "no pools");
+  if (p0->device < 0) return fail(KV_ESTATE, "kv_run_steps_graph needs device pools");
+  DeviceGuard dg(p0->device);
+  GraphLoop *G;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto &up = g_graph[p0->device];
+    if (!up) {
+      up.reset(new GraphLoop());
+      if (int rc = up->build(p0->device)) {
+        up.reset();
+        return rc;
+      }
+    }
+    G = up.get();
+  }
+  // earlier work on both streams precedes the first group
+  CU(cudaEventRecord(G->start_a, sa));
+  CU(cudaEventRecord(G->start_r, sr));
+  const int R = 2 * kGraphSteps;  // prepared-step ring shared with the helper
+  std::vector<StepPrep> ring(R);
+  for (auto &x : ring) x.no_inline = true;
+  std::atomic<int> produced{0}, consumed{0};
+  std::atomic<bool> stop{false};
+  std::thread worker([&]() {
+    for (int k = 0; k < n_steps && !stop.load(std::memory_order_acquire); ++k) {
+      const double w0 = now_s();
+      while (k - consumed.load(std::memory_order_acquire) >= R) {
+        if (stop.load(std::memory_order_acquire)) return;
+        std::this_thread::yield();
+      }
+      phase_add(kPhWaitIssue, now_s() - w0);
+      const double t0 = now_s();
+      prepare_step(steps[k], ring[k % R]);
+      phase_add(kPhPrepare, now_s() - t0);
+      produced.store(k + 1, std::memory_order_release);
+      if (ring[k % R].rc) return;
+    }
+  });
+  int rc = KV_OK;
+  cudaStream_t last = sa;
+  for (int k0 = 0; k0 < n_steps && !rc; k0 += kGraphSteps) {
+    const int n = std::min(kGraphSteps, n_steps - k0);
+    const double w0 = now_s();
+    while (produced.load(std::memory_order_acquire) < k0 + n) {
+      if (ring[(produced.load() + R - 1) % R].rc && produced.load() > 0) break;
+      std::this_thread::yield();
+    }
+    phase_add(kPhWaitPrep, now_s() - w0);
+    StepPrep *sp[kGraphSteps];
+    for (int i = 0; i < n; ++i) {
+      sp[i] = &ring[(k0 + i) % R];
+      if (produced.load(std::memory_order_acquire) <= k0 + i || sp[i]->rc) {
+        rc = sp[i]->rc ? sp[i]->rc : KV_EINVAL;
+        g_err = sp[i]->err;
+        break;
+      }
+    }
+    if (rc) break;
+    rc = issue_group(*G, steps + k0, sp, n, sa, sr, k0 == 0);
+    last = (G->group - 1) & 1 ? sr : sa;
+    consumed.store(k0 + n, std::memory_order_release);
+  }
+  stop.store(true, std::memory_order_release);
+  worker.join();
+  if (!rc) {  // both streams end after the last group
+    cudaStream_t other = last == sa ? sr : sa;
+    CU(cudaEventRecord(G->join, last));
+    CU(cudaStreamWaitEvent(other, G->join, 0));
+  }
   return rc;
 }
 

@@ -121,6 +121,21 @@ struct KvInlineDescT {
 using KvInlineDesc = KvInlineDescT<kInlineBytes>;
 cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,
                                cudaStream_t stream, bool pdl);
+// Arguments of a staged append / ring-put launch as a CUDA graph kernel node (the
+// graph decode loop updates them per step with cudaGraphExecKernelNodeSetParams).
+struct KvNodeArgs {
+  const KvTask *tasks = nullptr;
+  int n_tasks = 0;
+  const KvPoolParams *params = nullptr;
+  KvGeomDev g{};
+  int n_pools = 0;
+  KvParamPack pk{};
+  int split = 1;
+  void *ptrs[7] = {};
+};
+// Fills kp (function, grid, block, argument pointers into a) for kind
+// kKindAppend / kKindRingPut; a must outlive the call that consumes kp.
+void kernel_node_params(int kind, int grid, KvNodeArgs &a, cudaKernelNodeParams &kp);
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           unsigned long long *counter, const KvGeomDev &g, int grid,
                           cudaStream_t stream);

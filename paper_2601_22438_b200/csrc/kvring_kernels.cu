@@ -508,6 +508,23 @@ int copy_grid(int device, int n_tasks) {
   return n_tasks < cap ? (n_tasks > 0 ? n_tasks : 1) : cap;
 }
 
+void kernel_node_params(int kind, int grid, KvNodeArgs &a, cudaKernelNodeParams &kp) {
+  a.ptrs[0] = &a.tasks;
+  a.ptrs[1] = &a.n_tasks;
+  a.ptrs[2] = &a.params;
+  a.ptrs[3] = &a.g;
+  a.ptrs[4] = &a.n_pools;
+  a.ptrs[5] = &a.pk;
+  a.ptrs[6] = &a.split;
+  kp.func = kind == kKindAppend ? reinterpret_cast<void *>(kv_append_scatter_kernel)
+                                : reinterpret_cast<void *>(kv_ring_put_kernel);
+  kp.gridDim = dim3(grid > 0 ? grid : 1);
+  kp.blockDim = dim3(kThreads);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = a.ptrs;
+  kp.extra = nullptr;
+}
+
 cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream,
                         const KvPoolParams *host_params, int split) {

@@ -28,7 +28,8 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
             "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused", "kv_run_steps_pdl",
-            "kv_replicate_step_ce", "kv_set_successor_shared", "kv_drop_replicas"]
+            "kv_replicate_step_ce", "kv_set_successor_shared", "kv_drop_replicas",
+            "kv_run_steps_graph"]
 
 
 class KvError(RuntimeError):
@@ -130,6 +131,7 @@ def lib() -> ctypes.CDLL:
             "kv_run_steps_pdl": (ctypes.c_int, [_I32, _P, _P]),
             "kv_replicate_step_ce": (ctypes.c_int, [_I32, _P, _U64, _P]),
             "kv_set_successor_shared": (ctypes.c_int, [_P, _P]),
+            "kv_run_steps_graph": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_drop_replicas": (ctypes.c_int, [_P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
@@ -270,6 +272,11 @@ def _event_handle(e):
 def kv_run_steps(prepared: "PreparedSteps", append_stream: int = 0, repl_stream: int = 0) -> None:
     _check(lib().kv_run_steps(prepared.n, ctypes.addressof(prepared.arr), append_stream,
                               repl_stream))
+
+
+def kv_run_steps_graph(prepared: "PreparedSteps", append_stream: int, repl_stream: int) -> None:
+    _check(lib().kv_run_steps_graph(prepared.n, ctypes.addressof(prepared.arr), append_stream,
+                                    repl_stream))
 
 
 def kv_run_steps_fused(prepared: "PreparedSteps", stream: int = 0) -> None:

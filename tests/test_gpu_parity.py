@@ -469,6 +469,60 @@ def test_run_steps_fused_bit_exact(n_steps):
         rt.destroy()
 
 
+@pytest.mark.parametrize("n_steps,fail", [(5, False), (30, False), (41, True)])
+def test_run_steps_graph_bit_exact(n_steps, fail):
+    """kv_run_steps_graph (one CUDA graph per 8 steps, two streams, event-chained
+    groups; partial last group) == oracle, whole arrays, churn; with `fail` a stage fails
+    mid-run (restore through the C ABI between two graph runs)."""
+    from paper_2601_22438_b200 import kvring as K
+    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=6, n_requests=60, n_steps=n_steps, fixed_prompt=None,
+                         fail_node=(0, 2) if fail else None, fail_step=19 if fail else None)
+    sched = _churn_sched(cfg, 33)
+    rt, drv = make_gpu(cfg, schedules=sched)
+    oring = OracleRing(cfg, schedules=sched)
+    comp = torch.cuda.current_stream()
+    repl = torch.cuda.Stream()
+    keep = []
+
+    def run(t0, t1):
+        sts = []
+        for t in range(t0, t1):
+            app = []
+            for node, e in drv.plan(t).items():
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = drv.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+            pools = [rt.handle(n) for n in rt.alive_local() if rt.succ.get(n) is not None]
+            sts.append(dict(append=app, repl_pools=pools if t >= 1 else [], step=t))
+            oring.appends(t)
+            if t >= 1:
+                oring.replicate(t)
+        K.kv_run_steps_graph(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+        torch.cuda.synchronize()
+        compare_state(rt, drv, oring, tag=f"graph {t0}..{t1 - 1}")
+
+    try:
+        if not fail:
+            run(0, n_steps)
+        else:
+            run(0, cfg.fail_step)
+            t = cfg.fail_step
+            drv.append_step(t)
+            oring.appends(t)
+            drv.fail_and_restore(t, cfg.fail_node)
+            oring.fail_and_restore(t, cfg.fail_node)
+            rt.replicate_all(t)
+            oring.replicate(t)
+            torch.cuda.synchronize()
+            compare_state(rt, drv, oring, tag="after restore")
+            run(t + 1, n_steps)
+    finally:
+        rt.destroy()
+
+
 @pytest.mark.parametrize("n_steps", [12, 90])
 def test_run_steps_pdl_bit_exact(n_steps):
     """kv_run_steps_pdl (one stream, programmatic dependent launch, zero-copy

@@ -15,11 +15,13 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("n,transport", [(2, "p2p"), (2, "nccl"), (2, "runsteps"), (4, "p2p"),
-                                         (4, "nccl"), (4, "runsteps"), (8, "p2p")])
+@pytest.mark.parametrize("n,transport", [(2, "p2p"), (2, "nccl"), (2, "runsteps"), (2, "graph"),
+                                         (4, "p2p"), (4, "nccl"), (4, "runsteps"), (4, "graph"),
+                                         (8, "p2p")])
 def test_ring_over_nvlink_parity(n, transport):
     """p2p: fused ring-put over NVLink; nccl: the comparison transport (bit-exact too);
-    runsteps: the bench's native two-stream loop (kv_run_steps) over NVLink."""
+    runsteps / graph: the native decode loops (kv_run_steps, kv_run_steps_graph) over
+    NVLink."""
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",

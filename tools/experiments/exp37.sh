@@ -1,0 +1,8 @@
+# N=1: graph vs streams, 3 interleaved rounds
+mkdir -p gpurun_out; python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
+B="bench.py --no-cpu-baseline --e2e-steps 0 --no-restore --nccl-steps 0 --bulk-reps 0 --interference-steps 0 --block-steps 0 --shared-steps 0 --steps 400"
+for r in 1 2 3; do
+for v in streams graph; do
+  echo "== $v round $r" >> gpurun_out/exp37.log
+  timeout 300 python $B --loop $v 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['kernel_us']['median'], d['kernel_us']['avg'], d['roofline']['frac'])" >> gpurun_out/exp37.log 2>&1
+done; done
