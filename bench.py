@@ -103,6 +103,7 @@ def traffic_ref(kind, kernel="kv_ring_put_kernel"):
 # the timed decode steps launch the inline-descriptor ring-put (descriptors in the
 # kernel parameter space); steps whose descriptors exceed 28 KiB use the staged one
 RINGPUT = "kv_ring_put_inl_kernel (staged kv_ring_put_kernel for large steps)"
+RINGPUT_GRAPH = "kv_ring_put_kernel (CUDA-graph kernel nodes, kv_run_steps_graph)"
 
 
 def peaks():
@@ -426,7 +427,8 @@ def run_kvring(args):
     elif N == 1:
         per_launch = my_bytes / args.steps
         achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
-        tr = traffic_ref("decode_step", "kv_ring_put_inl_kernel")
+        tr = (traffic_ref("decode_step") if args.loop == "graph"
+              else traffic_ref("decode_step", "kv_ring_put_inl_kernel"))
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4),
                 "traffic": tr["traffic"] if tr else None,
@@ -434,7 +436,8 @@ def run_kvring(args):
                                  "DRAM bytes %d vs algorithmic read %d / r+w %d; writes stay in L2"
                                  % (tr["traffic"], tr["algorithmic_read"], tr["algorithmic_rw"]))
                                 if tr else None,
-                "kernel": RINGPUT, "peak_source": peak_src,
+                "kernel": RINGPUT_GRAPH if args.loop == "graph" else RINGPUT,
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(2 * per_launch),
                 "avg_launch_us": round(avg_kern, 2)}
     else:
@@ -478,7 +481,7 @@ def run_kvring(args):
                                      "its launch and its wait for the step's append), CUDA events by "
                                      "kv_run_steps on every %d-th timed step" % TIME_EVERY},
         "kernel_us": {"kernel": "kv_step_fused_kernel" if args.loop == "fused"
-                      else RINGPUT,
+                      else (RINGPUT_GRAPH if args.loop == "graph" else RINGPUT),
                       "median": round(med_kern, 2), "avg": round(avg_kern, 2),
                       "sampled_launches": len(kern_us)},
         "roofline": roof,
