@@ -2077,6 +2077,7 @@ struct GraphLoop {
   StageBuf slot[kSlots];
   KvNodeArgs args[2 * kGraphSteps];
   long long group = 0;
+  std::mutex mu;  // one call at a time per device (the graph and its slots are shared)
 
   int make_event(cudaEvent_t *e) {
     CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -2298,6 +2299,7 @@ KV_API int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *app
     }
     G = up.get();
   }
+  std::lock_guard<std::mutex> call_lock(G->mu);
   // earlier work on both streams precedes the first group
   CU(cudaEventRecord(G->start_a, sa));
   CU(cudaEventRecord(G->start_r, sr));
