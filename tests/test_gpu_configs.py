@@ -141,9 +141,11 @@ def test_c5_bulk_replication_and_restore(copy_engine):
         rt.destroy()
 
 
-def test_c2_full_geometry_whole_arrays():
-    """C2 at BASELINE's full geometry in the bench's launch configuration (4 pools of
-    12,288 x 512 KiB blocks on one GPU, kv_run_steps with two streams), 160 steps:
+@pytest.mark.parametrize("loop", ["graph", "streams"])
+def test_c2_full_geometry_whole_arrays(loop):
+    """C2 at BASELINE's full geometry in the bench's launch configurations (4 pools of
+    12,288 x 512 KiB blocks on one GPU; kv_run_steps_graph -- the bench default on one
+    GPU -- and kv_run_steps with two streams), 160 steps:
     whole pools, whole replica regions and metadata == the oracle in content mode.
     The oracle holds the first 2,048 blocks (lowest-free-id allocation gives the same
     block ids while use stays below that; asserted) and every GPU block beyond them
@@ -174,12 +176,16 @@ def test_c2_full_geometry_whole_arrays():
         for n in oring.nodes.values():
             assert max([b for s in range(n.R) for b in n.slot_bt[s]] + [0]) < 2048
         K.kv_host_profile(reset=True)
-        K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+        if loop == "graph":
+            K.kv_run_steps_graph(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+        else:
+            K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
         torch.cuda.synchronize()
         prof = K.kv_host_profile(reset=True)
-        # both launch paths ran: decode steps with descriptors in the kernel parameter
-        # space, prefill-heavy steps staged in global memory
-        assert prof["n_inline_launches"] > 0 and prof["n_staged_launches"] > 0, prof
+        if loop == "streams":
+            # both launch paths ran: decode steps with descriptors in the kernel parameter
+            # space, prefill-heavy steps staged in global memory
+            assert prof["n_inline_launches"] > 0 and prof["n_staged_launches"] > 0, prof
         sentinel = np.int16(np.uint16(0x5A5A).view(np.int16))
         for c, gid in drv.coords.items():
             on = oring.nodes[c]
