@@ -2127,6 +2127,7 @@ struct GraphLoop {
       CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
       kernel_node_params(kKindRingPut, 1, args[2 * k + 1], kp);
       CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
+
       CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
     }
     CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[kGraphSteps - 1], 1, ev_a[0]));
