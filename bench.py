@@ -68,9 +68,9 @@ def parse():
                     help="streams: kv_run_steps (append stream + replication stream); graph: "
                          "kv_run_steps_graph (the same steps as CUDA graphs of 8 steps); pdl: "
                          "one stream with programmatic dependent launch; fused: append k + "
-                         "publication k-1 per launch; auto (default): graph on 1 GPU (measured "
-                         "+7-9 %%, profiles/r01/exp37.log), streams over NVLink (equal or better "
-                         "there, exp36.log)")
+                         "publication k-1 per launch; auto (default): graph (measured +7-13 %% "
+                         "on 1 GPU, +2.5-3.5 %% on 2 and 4 GPUs over the two-stream loop, "
+                         "profiles/r01/exp37.log, exp39-41.log)")
     ap.add_argument("--single-stream", action="store_true",
                     help="append and replicate on one stream (default: replication stream)")
     return ap.parse_args()
@@ -182,7 +182,7 @@ def run_kvring(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     N = args.gpus
     if args.loop == "auto":
-        args.loop = "graph" if N == 1 else "streams"
+        args.loop = "graph"
     if world != N:
         raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}; launch N>1 with torch.distributed.run")
     torch.cuda.set_device(local_rank)
