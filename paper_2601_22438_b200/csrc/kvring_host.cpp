@@ -2049,7 +2049,7 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
 }
 
 // ---- CUDA-graph decode loop ---------------------------------------------------
-// The same work as kv_run_steps, issued as one CUDA graph per group of kGraphSteps
+// The same work as kv_run_steps, issued as one CUDA graph per group of graph_steps() (8)
 // steps: per step an append kernel node and a ring-put kernel node with the
 // stream-order constraints of kv_run_steps as graph edges (append k after append
 // k-1 and after ring-put k-2 -- R7 --, ring-put k after append k and after ring-put
@@ -2060,7 +2060,16 @@ KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_st
 // so group g+1 overlaps the tail of group g exactly like consecutive steps do.
 namespace {
 
-constexpr int kGraphSteps = 8;
+constexpr int kGraphMax = 32;  // node arrays; the group size itself: graph_steps()
+// Steps per graph (KVRING_GRAPH_STEPS, 2..32, default 8), read once per process.
+int graph_steps() {
+  static const int n = [] {
+    const char *e = getenv("KVRING_GRAPH_STEPS");
+    const int v = e ? atoi(e) : 8;
+    return std::max(2, std::min(kGraphMax, v));
+  }();
+  return n;
+}
 
 struct GraphLoop {
   static constexpr int kEv = 4, kSlots = 4;
@@ -2068,14 +2077,15 @@ struct GraphLoop {
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge[2] = {};
   cudaGraphNode_t mc = nullptr, wait_a = nullptr, wait_r2 = nullptr, wait_r1 = nullptr;
-  cudaGraphNode_t an[kGraphSteps] = {}, rn[kGraphSteps] = {};
-  cudaGraphNode_t es[kGraphSteps] = {}, ee[kGraphSteps] = {};
+  cudaGraphNode_t an[kGraphMax] = {}, rn[kGraphMax] = {};
+  cudaGraphNode_t es[kGraphMax] = {}, ee[kGraphMax] = {};
   cudaGraphNode_t rec_a = nullptr, rec_r2 = nullptr, rec_r1 = nullptr;
   cudaEvent_t ev_a[kEv] = {}, ev_r2[kEv] = {}, ev_r1[kEv] = {};
   cudaEvent_t start_a = nullptr, start_r = nullptr, join = nullptr;
-  cudaEvent_t dummy[2 * kGraphSteps] = {};
+  cudaEvent_t dummy[2 * kGraphMax] = {};
   StageBuf slot[kSlots];
-  KvNodeArgs args[2 * kGraphSteps];
+  KvNodeArgs args[2 * kGraphMax];
+  int steps = 8;  // group size of this graph
   long long group = 0;
   std::mutex mu;  // one call at a time per device (the graph and its slots are shared)
 
@@ -2115,7 +2125,8 @@ struct GraphLoop {
       const char *e = getenv("KVRING_GRAPH_LAG");
       return e && atoi(e) == 1 ? 1 : 2;
     }();
-    for (int k = 0; k < kGraphSteps; ++k) {
+    steps = graph_steps();
+    for (int k = 0; k < steps; ++k) {
       cudaKernelNodeParams kp{};
       kernel_node_params(kKindAppend, 1, args[2 * k], kp);
       cudaGraphNode_t lagdep =
@@ -2134,9 +2145,9 @@ struct GraphLoop {
 
       CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
     }
-    CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[kGraphSteps - 1], 1, ev_a[0]));
-    CU(cudaGraphAddEventRecordNode(&rec_r2, g, &ee[kGraphSteps - 2], 1, ev_r2[0]));
-    CU(cudaGraphAddEventRecordNode(&rec_r1, g, &ee[kGraphSteps - 1], 1, ev_r1[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[steps - 1], 1, ev_a[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_r2, g, &ee[steps - 2], 1, ev_r2[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_r1, g, &ee[steps - 1], 1, ev_r1[0]));
     for (auto &x : ge) CU(cudaGraphInstantiate(&x, g, 0));
     return KV_OK;
   }
@@ -2191,7 +2202,7 @@ int set_kernel_node(cudaGraphExec_t ge, cudaGraphNode_t node, Launch *L, bool pr
   return KV_OK;
 }
 
-// Issues group [k0, k0 + n) of prepared steps (n <= kGraphSteps).
+// Issues group [k0, k0 + n) of prepared steps (n <= G.steps).
 int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n,
                 cudaStream_t sa, cudaStream_t sr, bool first) {
   const int N = GraphLoop::kEv;
@@ -2232,7 +2243,7 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
   CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_a, first ? G.start_a : G.ev_a[pe]));
   CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r2, first ? G.start_r : G.ev_r2[pe]));
   CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r1, first ? G.start_r : G.ev_r1[pe]));
-  for (int k = 0; k < kGraphSteps; ++k) {
+  for (int k = 0; k < G.steps; ++k) {
     const bool on = k < n;
     StepPrep *s = on ? sp[k] : nullptr;
     int rc = set_kernel_node(ge, G.an[k], s ? &s->A : nullptr, on && s->has_a, G.args[2 * k],
@@ -2308,7 +2319,8 @@ KV_API int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *app
   // earlier work on both streams precedes the first group
   CU(cudaEventRecord(G->start_a, sa));
   CU(cudaEventRecord(G->start_r, sr));
-  const int R = 2 * kGraphSteps;  // prepared-step ring shared with the helper
+  const int GS = G->steps;
+  const int R = 2 * GS;  // prepared-step ring shared with the helper
   std::vector<StepPrep> ring(R);
   for (auto &x : ring) x.no_inline = true;
   std::atomic<int> produced{0}, consumed{0};
@@ -2330,15 +2342,15 @@ KV_API int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *app
   });
   int rc = KV_OK;
   cudaStream_t last = sa;
-  for (int k0 = 0; k0 < n_steps && !rc; k0 += kGraphSteps) {
-    const int n = std::min(kGraphSteps, n_steps - k0);
+  for (int k0 = 0; k0 < n_steps && !rc; k0 += GS) {
+    const int n = std::min(GS, n_steps - k0);
     const double w0 = now_s();
     while (produced.load(std::memory_order_acquire) < k0 + n) {
       if (ring[(produced.load() + R - 1) % R].rc && produced.load() > 0) break;
       std::this_thread::yield();
     }
     phase_add(kPhWaitPrep, now_s() - w0);
-    StepPrep *sp[kGraphSteps];
+    StepPrep *sp[kGraphMax];
     for (int i = 0; i < n; ++i) {
       sp[i] = &ring[(k0 + i) % R];
       if (produced.load(std::memory_order_acquire) <= k0 + i || sp[i]->rc) {
