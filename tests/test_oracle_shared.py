@@ -20,7 +20,7 @@ from kvgen.configs import Geometry
 from kvgen.content import content_tokens
 from kvgen.schedule import closed_loop_schedule
 from oracle import OracleNode, OracleError
-from oracle.simulate import OracleRing, check_all, check_content, check_tables
+from oracle.simulate import OracleRing, check_all, check_tables
 
 G = Geometry(layers=1, kv_heads=1, head_dim=8, block_size=2)
 
