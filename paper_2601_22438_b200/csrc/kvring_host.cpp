@@ -2077,14 +2077,16 @@ struct GraphLoop {
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge[2] = {};
   cudaGraphNode_t mc = nullptr, wait_a = nullptr, wait_r2 = nullptr, wait_r1 = nullptr;
-  cudaGraphNode_t an[kGraphMax] = {}, rn[kGraphMax] = {};
+  cudaGraphNode_t an[kGraphMax] = {}, rn[kGraphMax] = {}, pn[kGraphMax] = {};
   cudaGraphNode_t es[kGraphMax] = {}, ee[kGraphMax] = {};
-  cudaGraphNode_t rec_a = nullptr, rec_r2 = nullptr, rec_r1 = nullptr;
-  cudaEvent_t ev_a[kEv] = {}, ev_r2[kEv] = {}, ev_r1[kEv] = {};
+  cudaGraphNode_t rec_a = nullptr, rec_r2 = nullptr, rec_r1 = nullptr, rec_p = nullptr;
+  cudaGraphNode_t wait_p = nullptr;
+  cudaEvent_t ev_a[kEv] = {}, ev_r2[kEv] = {}, ev_r1[kEv] = {}, ev_p[kEv] = {};
+  bool split_pub = false;  // ring-put = copy node + separate publication node
   cudaEvent_t start_a = nullptr, start_r = nullptr, join = nullptr;
   cudaEvent_t dummy[2 * kGraphMax] = {};
   StageBuf slot[kSlots];
-  KvNodeArgs args[2 * kGraphMax];
+  KvNodeArgs args[3 * kGraphMax];
   int steps = 8;  // group size of this graph
   long long group = 0;
   std::mutex mu;  // one call at a time per device (the graph and its slots are shared)
@@ -2099,6 +2101,7 @@ struct GraphLoop {
       int rc = make_event(&ev_a[i]);
       if (!rc) rc = make_event(&ev_r2[i]);
       if (!rc) rc = make_event(&ev_r1[i]);
+      if (!rc) rc = make_event(&ev_p[i]);
       if (rc) return rc;
     }
     for (auto &e : dummy)
@@ -2119,6 +2122,14 @@ struct GraphLoop {
     CU(cudaGraphAddEventWaitNode(&wait_a, g, nullptr, 0, start_a));
     CU(cudaGraphAddEventWaitNode(&wait_r2, g, nullptr, 0, start_r));
     CU(cudaGraphAddEventWaitNode(&wait_r1, g, nullptr, 0, start_r));
+    // the publication as its own node (KVRING_GRAPH_SPLIT_PUB=0: inside the ring-put):
+    // the copies lose the per-CTA release RMW and bar.sync tail (ring-put node 10.7 vs
+    // 14.3 us median, +5 % steps/s, profiles/r01/exp43.log)
+    split_pub = [] {
+      const char *e = getenv("KVRING_GRAPH_SPLIT_PUB");
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (split_pub) CU(cudaGraphAddEventWaitNode(&wait_p, g, nullptr, 0, start_r));
     // experiment knob KVRING_GRAPH_LAG=1: append k waits for ring-put k-1 (no overlap of
     // an append with the previous publication); default 2 (reading R7's minimum)
     static const int lag = [] {
@@ -2140,14 +2151,19 @@ struct GraphLoop {
       CU(cudaGraphAddKernelNode(&an[k], g, da, k > 0 ? 4 : 3, &kp));
       cudaGraphNode_t ds[2] = {an[k], k > 0 ? ee[k - 1] : wait_r1};
       CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
-      kernel_node_params(kKindRingPut, 1, args[2 * k + 1], kp);
+      kernel_node_params(split_pub ? kKindRingPutCopy : kKindRingPut, 1, args[2 * k + 1], kp);
       CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
-
       CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
+      if (split_pub) {  // publication k after copies k and publication k-1 (seq order)
+        kernel_node_params(kKindPublish, 1, args[2 * kGraphMax + k], kp);
+        cudaGraphNode_t dp[2] = {ee[k], k > 0 ? pn[k - 1] : wait_p};
+        CU(cudaGraphAddKernelNode(&pn[k], g, dp, 2, &kp));
+      }
     }
     CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[steps - 1], 1, ev_a[0]));
     CU(cudaGraphAddEventRecordNode(&rec_r2, g, &ee[steps - 2], 1, ev_r2[0]));
     CU(cudaGraphAddEventRecordNode(&rec_r1, g, &ee[steps - 1], 1, ev_r1[0]));
+    if (split_pub) CU(cudaGraphAddEventRecordNode(&rec_p, g, &pn[steps - 1], 1, ev_p[0]));
     for (auto &x : ge) CU(cudaGraphInstantiate(&x, g, 0));
     return KV_OK;
   }
@@ -2194,7 +2210,7 @@ int set_kernel_node(cudaGraphExec_t ge, cudaGraphNode_t node, Launch *L, bool pr
         a.pk.dst[q] = L->params[q].dst;
       }
     }
-    grid = launch_grid(*L);
+    grid = kind == kKindPublish ? L->n_pools : launch_grid(*L);  // publication: CTA per pool
   }
   kernel_node_params(kind, grid, a, kp);
   CU(cudaGraphExecKernelNodeSetParams(ge, node, &kp));
@@ -2243,6 +2259,8 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
   CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_a, first ? G.start_a : G.ev_a[pe]));
   CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r2, first ? G.start_r : G.ev_r2[pe]));
   CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r1, first ? G.start_r : G.ev_r1[pe]));
+  if (G.split_pub)
+    CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_p, first ? G.start_r : G.ev_p[pe]));
   for (int k = 0; k < G.steps; ++k) {
     const bool on = k < n;
     StepPrep *s = on ? sp[k] : nullptr;
@@ -2250,7 +2268,10 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
                              kKindAppend);
     if (!rc)
       rc = set_kernel_node(ge, G.rn[k], s ? &s->P : nullptr, on && s->has_p,
-                           G.args[2 * k + 1], kKindRingPut);
+                           G.args[2 * k + 1], G.split_pub ? kKindRingPutCopy : kKindRingPut);
+    if (!rc && G.split_pub)
+      rc = set_kernel_node(ge, G.pn[k], s ? &s->P : nullptr, on && s->has_p,
+                           G.args[2 * kGraphMax + k], kKindPublish);
     if (rc) return rc;
     cudaEvent_t e0 = G.dummy[2 * k], e1 = G.dummy[2 * k + 1];
     if (on && steps[k].ev_kernel_start) e0 = static_cast<cudaEvent_t>(steps[k].ev_kernel_start);
@@ -2271,6 +2292,7 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
   CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_a, G.ev_a[gi % N]));
   CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r2, G.ev_r2[gi % N]));
   CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r1, G.ev_r1[gi % N]));
+  if (G.split_pub) CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_p, G.ev_p[gi % N]));
   const double t2 = now_s();
   CU(cudaGraphLaunch(ge, st));
   CU(cudaEventRecord(sl.ev, st));

@@ -83,7 +83,8 @@ struct alignas(16) KvPackedHeader {
 constexpr int kPackedMagic = 0x4B565042;
 
 // Launch wrappers (kvring_kernels.cu).  All return the cudaError_t of the launch.
-enum KernelKind : int { kKindAppend = 0, kKindRingPut = 1, kKindRestore = 2, kKindPack = 3 };
+enum KernelKind : int { kKindAppend = 0, kKindRingPut = 1, kKindRestore = 2, kKindPack = 3,
+                        kKindRingPutCopy = 4, kKindPublish = 5 };
 constexpr int kMaxPoolsPerLaunchHost = 64;
 // Per-pool source / destination bases passed by value in the kernel parameter
 // space (hot kernels): the only parameters on the path to a CTA's first data load.

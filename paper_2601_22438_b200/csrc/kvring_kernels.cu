@@ -383,6 +383,51 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                                   d.n_tasks, d.pools, g, d.n_pools, nullptr, d.data, d.split);
 }
 
+// Split publication (graph loop): the ring-put's copies without the publication pass
+// (no per-CTA release RMW, no bar.sync tail), and a separate publication kernel node
+// that runs after it -- the kernel boundary orders every copy before the metadata.
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_ring_put_copy_kernel(const KvTask *__restrict__ tasks, int n_tasks,
+                            const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools,
+                            const __grid_constant__ KvParamPack pk, int split) {
+  run_tasks<kPaged, kPaged, false>(tasks, n_tasks, params, g, n_pools, &pk, nullptr, split);
+}
+
+// One CTA per pool: the bt entries of its first tasks, its parity table, the task
+// counter advanced by its units (kept equal to the host's `issued`), then ONE
+// acquire-release fence and the seq store (reading R9).  An aborted launch (target
+// all-ones, kv_inject_abort) publishes nothing.
+__global__ void __launch_bounds__(kThreads)
+    kv_publish_kernel(const KvTask *__restrict__ tasks, int n_tasks,
+                      const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools,
+                      const __grid_constant__ KvParamPack pk, int split) {
+  (void)g;
+  (void)pk;
+  const int q = blockIdx.x;
+  if (q >= n_pools) return;
+  const KvPoolParams &pp = params[q];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
+  for (int t = threadIdx.x; t < n_tasks; t += blockDim.x) {
+    const KvTask tk = tasks[t];
+    if (tk.pool != q) continue;
+    if ((tk.flags & kFirst) && tk.slot >= 0) bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
+    atomicAdd(&s_n, 1);
+  }
+  write_parity_table(pp, nullptr);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(pp.counter, (unsigned long long)s_n * (unsigned long long)split);
+    if (pp.target != ~0ull) {
+      const bool sys = pp.sys_scope != 0;
+      fence_acquire(sys);
+      st_after_fence(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
+    }
+  }
+}
+
 // Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
 // append of step k (tasks [0, n_append), pools params[0, n_app_pools)) and the
 // publication of step k-1 (tasks [n_append, n_tasks), pools params[n_app_pools..),
@@ -517,7 +562,9 @@ void kernel_node_params(int kind, int grid, KvNodeArgs &a, cudaKernelNodeParams 
   a.ptrs[5] = &a.pk;
   a.ptrs[6] = &a.split;
   kp.func = kind == kKindAppend ? reinterpret_cast<void *>(kv_append_scatter_kernel)
-                                : reinterpret_cast<void *>(kv_ring_put_kernel);
+            : kind == kKindRingPutCopy ? reinterpret_cast<void *>(kv_ring_put_copy_kernel)
+            : kind == kKindPublish     ? reinterpret_cast<void *>(kv_publish_kernel)
+                                       : reinterpret_cast<void *>(kv_ring_put_kernel);
   kp.gridDim = dim3(grid > 0 ? grid : 1);
   kp.blockDim = dim3(kThreads);
   kp.sharedMemBytes = 0;
