@@ -103,7 +103,8 @@ def traffic_ref(kind, kernel="kv_ring_put_kernel"):
 # the timed decode steps launch the inline-descriptor ring-put (descriptors in the
 # kernel parameter space); steps whose descriptors exceed 28 KiB use the staged one
 RINGPUT = "kv_ring_put_inl_kernel (staged kv_ring_put_kernel for large steps)"
-RINGPUT_GRAPH = "kv_ring_put_kernel (CUDA-graph kernel nodes, kv_run_steps_graph)"
+RINGPUT_GRAPH = ("kv_ring_put_copy_kernel (CUDA-graph copy nodes of kv_run_steps_graph; the "
+                 "publication is a separate kv_publish_kernel node)")
 
 
 def peaks():

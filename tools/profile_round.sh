@@ -16,7 +16,7 @@ $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:kv_ --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
 # ring-put launches: 199 prelude (staged kernel) + 3 warm-up + 40 timed (inline kernel), then bulk
-ncu --set full --clock-control none --import-source on -k regex:kv_ring_put -s 215 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:kv_ring_put_copy -s 5 -c 3 \
     -o gpurun_out/ringput_$TAG -f $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:kv_ring_put -s 243 -c 1 \
     -o gpurun_out/ringput_bulk_$TAG -f $CMD > gpurun_out/ncu_full_bulk_$TAG.log 2>&1
