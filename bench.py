@@ -428,7 +428,7 @@ def run_kvring(args):
     elif N == 1:
         per_launch = my_bytes / args.steps
         achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
-        tr = (traffic_ref("decode_step") if args.loop == "graph"
+        tr = (traffic_ref("decode_step", "kv_ring_put_copy_kernel") if args.loop == "graph"
               else traffic_ref("decode_step", "kv_ring_put_inl_kernel"))
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4),
