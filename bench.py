@@ -366,7 +366,8 @@ def run_kvring(args):
     # ---- floor of a decode hop: a publication with nothing dirty ("empty
     # launch + one P2P flag store"), same pools, same stream, same launch path; the
     # last leg that replicates on these pools (its step numbers are not schedule steps)
-    floor = run_floor(rt, t + 10, comp, repl, dev, world)
+    floor = run_floor(rt, t + 10, comp, repl, dev, world,
+                      "graph" if args.loop == "graph" else "streams")
 
     # ---- restore: fail stage 2 of pipeline 0, restore into a fresh pool ---------
     restore = None
@@ -847,7 +848,7 @@ def run_block_mode(args, drv, rt, t0, comp, repl, content, dev, world):
 FLOOR_REPS = 50
 
 
-def run_floor(rt, t0, comp, repl, dev, world):
+def run_floor(rt, t0, comp, repl, dev, world, loop="streams"):
     """Per-step floor of the publication on the timed loop's own path: FLOOR_REPS steps
     of kv_run_steps with no append and nothing dirty (one publish-only task per pool:
     bt / parity table / release seq, over NVLink when the successor is remote), timed
@@ -869,9 +870,14 @@ def run_floor(rt, t0, comp, repl, dev, world):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
+    if loop == "graph":
+        K.kv_run_steps_graph(prep, comp.cuda_stream, repl.cuda_stream)
+    else:
+        K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
     torch.cuda.synchronize(dev)
-    call = sorted(e[0].elapsed_time(e[2]) * 1e3 for e in evs[1:])
+    # graph loop: ev_call is not recorded (events sit around the ring-put node only)
+    i0 = 1 if loop == "graph" else 0
+    call = sorted(e[i0].elapsed_time(e[2]) * 1e3 for e in evs[1:])
     kern = sorted(e[1].elapsed_time(e[2]) * 1e3 for e in evs[1:])
     v = torch.tensor([call[len(call) // 2], kern[len(kern) // 2]], dtype=torch.float64,
                      device=dev)
@@ -879,9 +885,11 @@ def run_floor(rt, t0, comp, repl, dev, world):
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
     return {"median": round(float(v[0]), 2), "kernel_median": round(float(v[1]), 2),
             "reps": FLOOR_REPS, "pools": len(nodes),
-            "what": "kv_run_steps steps with nothing dirty (one publish-only task per pool: "
-                    "launch + bt/parity tables + release seq), timed like step_overhead_us "
-                    "(median) and kernel_us (kernel_median); the decode-step ring-put's floor"}
+            "what": "steps with nothing dirty through the timed loop's own decode loop (%s; "
+                    "one publish-only task per pool: launch / graph node + bt/parity tables + "
+                    "seq), timed like step_overhead_us (median) and kernel_us (kernel_median); "
+                    "the decode-step ring-put's floor" % ("kv_run_steps_graph" if loop == "graph"
+                                                         else "kv_run_steps")}
 
 
 SHARED_NB = 2048   # C2 primary peak is ~1.57k blocks per stage: replicas must compete
