@@ -109,23 +109,48 @@ def test_other_head_geometries_bit_exact(heads, head_dim, block):
     rt.destroy()
 
 
-def test_abort_mid_step_keeps_last_published_replica():
+@pytest.mark.parametrize("loop", ["direct", "graph"])
+def test_abort_mid_step_keeps_last_published_replica(loop):
     """A stage dying mid-replicate leaves its successor's replica at the last
-    published step (R7/R9): restore == oracle restore of the previous step."""
+    published step (R7/R9): restore == oracle restore of the previous step.  graph:
+    the steps run through kv_run_steps_graph (split publication node)."""
     from paper_2601_22438_b200 import kvring as K
     cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
                          batch_cap=6, n_requests=60, n_steps=30, fixed_prompt=None,
                          fail_node=None, fail_step=None)
     sched = _churn_sched(cfg, 11)
     rt, drv = make_gpu(cfg, schedules=sched)
+    keep = []
+
+    def graph_run(t0, t1):
+        sts = []
+        for t in range(t0, t1):
+            app = []
+            for node, e in drv.plan(t).items():
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = drv.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+            pools = [rt.handle(n) for n in rt.alive_local()]
+            sts.append(dict(append=app, repl_pools=pools if t >= 1 else [], step=t))
+        K.kv_run_steps_graph(K.PreparedSteps(sts), torch.cuda.current_stream().cuda_stream,
+                             repl.cuda_stream)
+
+    repl = torch.cuda.Stream()
     try:
         T = 20
-        for t in range(T):
-            drv.append_step(t)
-            if t >= 1:
-                if t == T - 1:
-                    K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 3)   # 3 copy tasks, no publish
-                rt.replicate_all(t)
+        if loop == "graph":
+            graph_run(0, T - 1)
+            K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 3)   # 3 copy tasks, no publish
+            graph_run(T - 1, T)
+        else:
+            for t in range(T):
+                drv.append_step(t)
+                if t >= 1:
+                    if t == T - 1:
+                        K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 3)   # no publish
+                    rt.replicate_all(t)
         torch.cuda.synchronize()
         holder = drv.coords[(0, 2)]
         meta = rt.read_meta(holder)
