@@ -2140,32 +2140,39 @@ struct GraphLoop {
       return e && atoi(e) == 1 ? 1 : 2;
     }();
     steps = graph_steps();
+    // Timing event nodes sit beside the chain (es(k) has R(k)'s dependencies, ee(k)
+    // follows R(k)); no kernel waits on them unless KVRING_GRAPH_EVENTS_IN_CHAIN=1.
+    static const bool in_chain = getenv("KVRING_GRAPH_EVENTS_IN_CHAIN") != nullptr;
     for (int k = 0; k < steps; ++k) {
       cudaKernelNodeParams kp{};
       kernel_node_params(kKindAppend, 1, args[2 * k], kp);
+      cudaGraphNode_t rprev = k > 0 ? (in_chain ? ee[k - 1] : rn[k - 1]) : wait_r1;
       cudaGraphNode_t lagdep =
-          lag == 2 ? (k >= 2 ? ee[k - 2] : (k == 0 ? wait_r2 : wait_r1))
-                   : (k >= 1 ? ee[k - 1] : wait_r1);
-      // append k also follows the LAUNCH of ring-put k-1 (its start event node): both
-      // become ready together, and the publication then gets the free CTA slots first
+          lag == 2 ? (k >= 2 ? (in_chain ? ee[k - 2] : rn[k - 2]) : (k == 0 ? wait_r2 : wait_r1))
+                   : rprev;
+      // append k also follows the LAUNCH of ring-put k-1 (the node that becomes ready with
+      // it, its start event): the publication then gets the free CTA slots first
       // (+2-10 % measured, profiles/r01/exp39.log)
       cudaGraphNode_t da[4] = {mc, k > 0 ? an[k - 1] : wait_a, lagdep,
                                k > 0 ? es[k - 1] : nullptr};
       CU(cudaGraphAddKernelNode(&an[k], g, da, k > 0 ? 4 : 3, &kp));
-      cudaGraphNode_t ds[2] = {an[k], k > 0 ? ee[k - 1] : wait_r1};
+      cudaGraphNode_t ds[2] = {an[k], rprev};
       CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
       kernel_node_params(split_pub ? kKindRingPutCopy : kKindRingPut, 1, args[2 * k + 1], kp);
-      CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
+      if (in_chain)
+        CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
+      else
+        CU(cudaGraphAddKernelNode(&rn[k], g, ds, 2, &kp));
       CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
       if (split_pub) {  // publication k after copies k and publication k-1 (seq order)
         kernel_node_params(kKindPublish, 1, args[2 * kGraphMax + k], kp);
-        cudaGraphNode_t dp[2] = {ee[k], k > 0 ? pn[k - 1] : wait_p};
+        cudaGraphNode_t dp[2] = {rn[k], k > 0 ? pn[k - 1] : wait_p};
         CU(cudaGraphAddKernelNode(&pn[k], g, dp, 2, &kp));
       }
     }
     CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[steps - 1], 1, ev_a[0]));
-    CU(cudaGraphAddEventRecordNode(&rec_r2, g, &ee[steps - 2], 1, ev_r2[0]));
-    CU(cudaGraphAddEventRecordNode(&rec_r1, g, &ee[steps - 1], 1, ev_r1[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_r2, g, &rn[steps - 2], 1, ev_r2[0]));
+    CU(cudaGraphAddEventRecordNode(&rec_r1, g, &rn[steps - 1], 1, ev_r1[0]));
     if (split_pub) CU(cudaGraphAddEventRecordNode(&rec_p, g, &pn[steps - 1], 1, ev_p[0]));
     for (auto &x : ge) CU(cudaGraphInstantiate(&x, g, 0));
     std::memset(enabled, -1, sizeof enabled);
