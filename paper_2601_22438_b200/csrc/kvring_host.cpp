@@ -345,6 +345,7 @@ struct kv_pool {
   std::vector<int> q_blocks, q_slots;
   std::vector<int64_t> slot_req;
   std::vector<int32_t> slot_len, pub_len;
+  int slot_hi = 0;  // 1 + highest live slot (slots are taken lowest first): loop bound
   std::vector<std::vector<int32_t>> slot_bt;
   SlotMap slot_of;
   std::vector<uint32_t> rel_stamp, app_stamp;  // per-slot call stamps (validation)
@@ -483,6 +484,11 @@ void unlink_holder(kv_pool *p) {
   p->holder = nullptr;
 }
 
+inline void slot_taken(kv_pool *p, int s) { p->slot_hi = std::max(p->slot_hi, s + 1); }
+inline void slot_freed(kv_pool *p) {
+  while (p->slot_hi > 0 && p->slot_req[p->slot_hi - 1] < 0) --p->slot_hi;
+}
+
 void admitted(kv_pool *p, int s) {
   p->admit_seq[s] = ++p->admit_ctr;
   p->dropped[s] = 0;
@@ -572,6 +578,7 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
     p->slot_bt[s].clear();
     p->q_slots.push_back(s);
     p->slot_req[s] = -1;
+    slot_freed(p);
     p->slot_len[s] = 0;
     p->pub_len[s] = 0;
   }
@@ -594,6 +601,7 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, TaskVec &tas
       p->pub_len[s] = 0;
       p->slot_bt[s].clear();
       admitted(p, s);
+      slot_taken(p, s);
     }
     int len = p->slot_len[s];
     int left = a.n_new[i];
@@ -626,15 +634,17 @@ inline int pub_hi(const kv_pool *p, int s) {
 void fill_pub_table(const kv_pool *p, char *dst) {
   int64_t *rq = reinterpret_cast<int64_t *>(dst);
   int32_t *ln = reinterpret_cast<int32_t *>(dst + 8 * (size_t)p->R);
-  for (int s = 0; s < p->R; ++s) {
+  for (int s = 0; s < p->slot_hi; ++s) {
     const int hi = p->slot_req[s] >= 0 ? pub_hi(p, s) : 0;
     rq[s] = hi > 0 ? p->slot_req[s] : -1;
     ln[s] = hi;
   }
+  std::fill(rq + p->slot_hi, rq + p->R, (int64_t)-1);
+  std::fill(ln + p->slot_hi, ln + p->R, 0);
 }
 
 void commit_pub_len(kv_pool *p) {
-  for (int s = 0; s < p->R; ++s) p->pub_len[s] = p->slot_req[s] >= 0 ? pub_hi(p, s) : 0;
+  for (int s = 0; s < p->slot_hi; ++s) p->pub_len[s] = p->slot_req[s] >= 0 ? pub_hi(p, s) : 0;
 }
 
 // Dirty ranges [pub_len, pub_hi) of every live slot split at block boundaries
@@ -645,7 +655,7 @@ uint64_t build_dirty_tasks(kv_pool *p, int16_t pidx, TaskVec &tasks, bool packed
   const int B = p->g.block_size;
   uint64_t bytes = 0;
   kv_pool *h = p->holder;
-  for (int s = 0; s < p->R; ++s) {
+  for (int s = 0; s < p->slot_hi; ++s) {
     if (p->slot_req[s] < 0) continue;
     int pos = p->pub_len[s];
     const int len = pub_hi(p, s);
@@ -1083,7 +1093,7 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     if (step == 0 || step <= p->last_step)
       return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
                   (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
-    for (int s = 0; s < p->R; ++s)
+    for (int s = 0; s < p->slot_hi; ++s)
       if (p->slot_req[s] >= 0) dirty += pub_hi(p, s) - p->pub_len[s];
   }
   L.reset(kKindRingPut, n_pools);
@@ -1462,6 +1472,7 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
     const int s = dst->free_slots.take_min();
     dst->slot_of.insert(e.req, s);
     dst->slot_req[s] = e.req;
+    slot_taken(dst, s);
     dst->slot_len[s] = e.len;
     dst->pub_len[s] = 0;
     dst->slot_bt[s].clear();
