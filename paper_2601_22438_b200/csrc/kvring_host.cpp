@@ -1085,7 +1085,8 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
   if (!pools[0]) return fail(KV_EINVAL, "null pool");
   int rc = check_same_device(n_pools, pools);
   if (rc) return rc;
-  long long dirty = 0;
+  const bool whole = allow_split && !legacy_task_sizing();
+  long long dirty = 0;  // only the legacy task sizing needs it before building
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = pools[k];
     if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
@@ -1093,13 +1094,13 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     if (step == 0 || step <= p->last_step)
       return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
                   (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
-    for (int s = 0; s < p->slot_hi; ++s)
-      if (p->slot_req[s] >= 0) dirty += pub_hi(p, s) - p->pub_len[s];
+    if (!whole)
+      for (int s = 0; s < p->slot_hi; ++s)
+        if (p->slot_req[s] >= 0) dirty += pub_hi(p, s) - p->pub_len[s];
   }
   L.reset(kKindRingPut, n_pools);
   L.p0 = pools[0];
   L.use_ce = use_ce;
-  const bool whole = allow_split && !legacy_task_sizing();
   const int task_segs =
       whole ? whole_item_segs(L.p0) : choose_task_segs(L.p0, dirty * L.p0->combos);
   size_t toff = 0;
