@@ -2087,7 +2087,9 @@ struct GraphLoop {
   static constexpr int kEv = 4, kSlots = 4;
   int device = -1;
   cudaGraph_t g = nullptr;
-  cudaGraphExec_t ge[2] = {};
+  cudaGraphExec_t ge[kSlots] = {};  // 2 used (parity), or one per slot in fixed mode
+  bool fixed = false;  // self-describing steps: kernel nodes never updated per step
+  KvFxArgs fx[3 * kGraphMax];
   cudaGraphNode_t mc = nullptr, wait_a = nullptr, wait_r2 = nullptr, wait_r1 = nullptr;
   cudaGraphNode_t an[kGraphMax] = {}, rn[kGraphMax] = {}, pn[kGraphMax] = {};
   cudaGraphNode_t es[kGraphMax] = {}, ee[kGraphMax] = {};
@@ -2101,13 +2103,28 @@ struct GraphLoop {
   KvNodeArgs args[3 * kGraphMax];
   int steps = 8;  // group size of this graph
   // last values set per exec instance: skip redundant update calls (each ~0.3 us)
-  signed char enabled[2][3 * kGraphMax];
-  cudaEvent_t ev_set[2][2 * kGraphMax] = {};
+  signed char enabled[kSlots][3 * kGraphMax];
+  cudaEvent_t ev_set[kSlots][2 * kGraphMax] = {};
   long long group = 0;
   std::mutex mu;  // one call at a time per device (the graph and its slots are shared)
 
   int make_event(cudaEvent_t *e) {
     CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return KV_OK;
+  }
+  // Fixed mode: point exec e's kernel nodes at slot e (once, and after a slot grows).
+  int bind_slot(int e) {
+    const int fx_grid = resident_ctas(device);
+    for (int k = 0; k < steps; ++k) {
+      cudaKernelNodeParams kp{};
+      KvFxArgs a{slot[e].dev, k};
+      fx_node_params(kKindAppend, fx_grid, a, kp);
+      CU(cudaGraphExecKernelNodeSetParams(ge[e], an[k], &kp));
+      fx_node_params(kKindRingPutCopy, fx_grid, a, kp);
+      CU(cudaGraphExecKernelNodeSetParams(ge[e], rn[k], &kp));
+      fx_node_params(kKindPublish, kFxPublishGrid, a, kp);
+      CU(cudaGraphExecKernelNodeSetParams(ge[e], pn[k], &kp));
+    }
     return KV_OK;
   }
   int build(int dev) {
@@ -2145,6 +2162,13 @@ struct GraphLoop {
       return e ? atoi(e) != 0 : true;
     }();
     if (split_pub) CU(cudaGraphAddEventWaitNode(&wait_p, g, nullptr, 0, start_r));
+    // self-describing steps (KVRING_GRAPH_FIXED=1, needs the split publication): each
+    // kernel node reads its launch from the step header in the group's slot
+    fixed = split_pub && [] {
+      const char *e = getenv("KVRING_GRAPH_FIXED");
+      return e ? atoi(e) != 0 : false;
+    }();
+    const int fx_grid = resident_ctas(dev);
     // experiment knob KVRING_GRAPH_LAG=1: append k waits for ring-put k-1 (no overlap of
     // an append with the previous publication); default 2 (reading R7's minimum)
     static const int lag = [] {
@@ -2157,7 +2181,12 @@ struct GraphLoop {
     static const bool in_chain = getenv("KVRING_GRAPH_EVENTS_IN_CHAIN") != nullptr;
     for (int k = 0; k < steps; ++k) {
       cudaKernelNodeParams kp{};
-      kernel_node_params(kKindAppend, 1, args[2 * k], kp);
+      if (fixed) {
+        fx[3 * k] = KvFxArgs{slot[0].dev, k};
+        fx_node_params(kKindAppend, fx_grid, fx[3 * k], kp);
+      } else {
+        kernel_node_params(kKindAppend, 1, args[2 * k], kp);
+      }
       cudaGraphNode_t rprev = k > 0 ? (in_chain ? ee[k - 1] : rn[k - 1]) : wait_r1;
       cudaGraphNode_t lagdep =
           lag == 2 ? (k >= 2 ? (in_chain ? ee[k - 2] : rn[k - 2]) : (k == 0 ? wait_r2 : wait_r1))
@@ -2170,14 +2199,24 @@ struct GraphLoop {
       CU(cudaGraphAddKernelNode(&an[k], g, da, k > 0 ? 4 : 3, &kp));
       cudaGraphNode_t ds[2] = {an[k], rprev};
       CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
-      kernel_node_params(split_pub ? kKindRingPutCopy : kKindRingPut, 1, args[2 * k + 1], kp);
+      if (fixed) {
+        fx[3 * k + 1] = KvFxArgs{slot[0].dev, k};
+        fx_node_params(kKindRingPutCopy, fx_grid, fx[3 * k + 1], kp);
+      } else {
+        kernel_node_params(split_pub ? kKindRingPutCopy : kKindRingPut, 1, args[2 * k + 1], kp);
+      }
       if (in_chain)
         CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
       else
         CU(cudaGraphAddKernelNode(&rn[k], g, ds, 2, &kp));
       CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
       if (split_pub) {  // publication k after copies k and publication k-1 (seq order)
-        kernel_node_params(kKindPublish, 1, args[2 * kGraphMax + k], kp);
+        if (fixed) {
+          fx[3 * k + 2] = KvFxArgs{slot[0].dev, k};
+          fx_node_params(kKindPublish, kFxPublishGrid, fx[3 * k + 2], kp);
+        } else {
+          kernel_node_params(kKindPublish, 1, args[2 * kGraphMax + k], kp);
+        }
         cudaGraphNode_t dp[2] = {rn[k], k > 0 ? pn[k - 1] : wait_p};
         CU(cudaGraphAddKernelNode(&pn[k], g, dp, 2, &kp));
       }
@@ -2186,7 +2225,13 @@ struct GraphLoop {
     CU(cudaGraphAddEventRecordNode(&rec_r2, g, &rn[steps - 2], 1, ev_r2[0]));
     CU(cudaGraphAddEventRecordNode(&rec_r1, g, &rn[steps - 1], 1, ev_r1[0]));
     if (split_pub) CU(cudaGraphAddEventRecordNode(&rec_p, g, &pn[steps - 1], 1, ev_p[0]));
-    for (auto &x : ge) CU(cudaGraphInstantiate(&x, g, 0));
+    for (int e = 0; e < (fixed ? kSlots : 2); ++e) {
+      CU(cudaGraphInstantiate(&ge[e], g, 0));
+      if (fixed) {
+        int rc = bind_slot(e);
+        if (rc) return rc;
+      }
+    }
     std::memset(enabled, -1, sizeof enabled);
     return KV_OK;
   }
@@ -2249,14 +2294,16 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
                 cudaStream_t sa, cudaStream_t sr, bool first) {
   const int N = GraphLoop::kEv;
   const long long gi = G.group++;
-  StageBuf &sl = G.slot[gi % GraphLoop::kSlots];
+  const int se = (int)(gi % GraphLoop::kSlots);
+  StageBuf &sl = G.slot[se];
+  const size_t hdr_bytes = G.fixed ? align16(sizeof(KvStepHdr) * G.steps) : 0;
   const double t0 = now_s();
   if (sl.pending) {
     CU(cudaEventSynchronize(sl.ev));
     sl.pending = false;
   }
   phase_add(kPhAcquire, now_s() - t0);
-  size_t need = 0;
+  size_t need = hdr_bytes;
   for (int i = 0; i < n; ++i) {
     if (sp[i]->has_a) need += align16(sp[i]->A.staged_bytes());
     if (sp[i]->has_p) need += align16(sp[i]->P.staged_bytes());
@@ -2268,16 +2315,37 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
     CU(cudaHostAlloc(reinterpret_cast<void **>(&sl.host), cap, cudaHostAllocDefault));
     CU(cudaMalloc(reinterpret_cast<void **>(&sl.dev), cap));
     sl.cap = cap;
+    if (G.fixed) {
+      int rc = G.bind_slot(se);
+      if (rc) return rc;
+    }
   }
   const double t1 = now_s();
-  size_t off = 0;
-  for (int i = 0; i < n; ++i) {
-    if (sp[i]->has_a && !sp[i]->A.tasks.empty()) pack_launch(sp[i]->A, sl.host, sl.dev, off);
-    if (sp[i]->has_p && !sp[i]->P.tasks.empty()) pack_launch(sp[i]->P, sl.host, sl.dev, off);
+  size_t off = hdr_bytes;
+  KvStepHdr *hdr = reinterpret_cast<KvStepHdr *>(sl.host);
+  for (int i = 0; i < (G.fixed ? G.steps : n); ++i) {
+    KvStepHdr h{};
+    if (i < n) {
+      Launch *ls2[2] = {sp[i]->has_a && !sp[i]->A.tasks.empty() ? &sp[i]->A : nullptr,
+                        sp[i]->has_p && !sp[i]->P.tasks.empty() ? &sp[i]->P : nullptr};
+      for (int w = 0; w < 2; ++w) {
+        Launch *L = ls2[w];
+        if (!L) continue;
+        pack_launch(*L, sl.host, sl.dev, off);
+        h.n_tasks[w] = (int32_t)L->tasks.size();
+        h.n_pools[w] = L->n_pools;
+        h.split[w] = L->split;
+        h.params_off[w] = (unsigned long long)(reinterpret_cast<const char *>(L->params_dev) - sl.dev);
+        h.tasks_off[w] = (unsigned long long)(reinterpret_cast<const char *>(L->tasks_dev) - sl.dev);
+        h.g = L->p0->geom_dev();
+      }
+    }
+    if (G.fixed) hdr[i] = h;
   }
   phase_add(kPhHostCopy, now_s() - t1);
   const int par = (int)(gi & 1);
-  cudaGraphExec_t ge = G.ge[par];
+  const int xi = G.fixed ? se : par;  // exec instance (and its update caches)
+  cudaGraphExec_t ge = G.ge[xi];
   cudaStream_t st = par ? sr : sa;
   CU(cudaGraphExecMemcpyNodeSetParams1D(ge, G.mc, sl.dev, sl.host, off > 0 ? off : 16,
                                         cudaMemcpyHostToDevice));
@@ -2290,27 +2358,29 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
   for (int k = 0; k < G.steps; ++k) {
     const bool on = k < n;
     StepPrep *s = on ? sp[k] : nullptr;
-    signed char *en = G.enabled[par];
-    int rc = set_kernel_node(ge, G.an[k], s ? &s->A : nullptr, on && s->has_a, G.args[2 * k],
-                             kKindAppend, en[3 * k]);
-    if (!rc)
-      rc = set_kernel_node(ge, G.rn[k], s ? &s->P : nullptr, on && s->has_p,
-                           G.args[2 * k + 1], G.split_pub ? kKindRingPutCopy : kKindRingPut,
-                           en[3 * k + 1]);
-    if (!rc && G.split_pub)
-      rc = set_kernel_node(ge, G.pn[k], s ? &s->P : nullptr, on && s->has_p,
-                           G.args[2 * kGraphMax + k], kKindPublish, en[3 * k + 2]);
-    if (rc) return rc;
+    if (!G.fixed) {  // fixed mode: the step header in the slot describes the launches
+      signed char *en = G.enabled[xi];
+      int rc = set_kernel_node(ge, G.an[k], s ? &s->A : nullptr, on && s->has_a, G.args[2 * k],
+                               kKindAppend, en[3 * k]);
+      if (!rc)
+        rc = set_kernel_node(ge, G.rn[k], s ? &s->P : nullptr, on && s->has_p,
+                             G.args[2 * k + 1], G.split_pub ? kKindRingPutCopy : kKindRingPut,
+                             en[3 * k + 1]);
+      if (!rc && G.split_pub)
+        rc = set_kernel_node(ge, G.pn[k], s ? &s->P : nullptr, on && s->has_p,
+                             G.args[2 * kGraphMax + k], kKindPublish, en[3 * k + 2]);
+      if (rc) return rc;
+    }
     cudaEvent_t e0 = G.dummy[2 * k], e1 = G.dummy[2 * k + 1];
     if (on && steps[k].ev_kernel_start) e0 = static_cast<cudaEvent_t>(steps[k].ev_kernel_start);
     if (on && steps[k].ev_kernel_end) e1 = static_cast<cudaEvent_t>(steps[k].ev_kernel_end);
-    if (G.ev_set[par][2 * k] != e0) {
+    if (G.ev_set[xi][2 * k] != e0) {
       CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.es[k], e0));
-      G.ev_set[par][2 * k] = e0;
+      G.ev_set[xi][2 * k] = e0;
     }
-    if (G.ev_set[par][2 * k + 1] != e1) {
+    if (G.ev_set[xi][2 * k + 1] != e1) {
       CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.ee[k], e1));
-      G.ev_set[par][2 * k + 1] = e1;
+      G.ev_set[xi][2 * k + 1] = e1;
     }
     if (on) {
       if (s->has_a && !s->A.tasks.empty()) {

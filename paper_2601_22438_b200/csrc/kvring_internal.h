@@ -122,6 +122,29 @@ struct KvInlineDescT {
 using KvInlineDesc = KvInlineDescT<kInlineBytes>;
 cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,
                                cudaStream_t stream, bool pdl);
+// Self-describing graph steps (kv_run_steps_graph, fixed nodes): step i of a group
+// reads its launches from this header at the start of the group's staged slot, so
+// the graph's kernel nodes keep fixed parameters (slot base, step index) and the host
+// updates nothing per step but the slot contents.  [0] = append, [1] = ring-put.
+struct alignas(16) KvStepHdr {
+  int32_t n_tasks[2];
+  int32_t n_pools[2];
+  int32_t split[2];
+  int32_t pad[2];
+  unsigned long long params_off[2];
+  unsigned long long tasks_off[2];
+  KvGeomDev g;
+};
+constexpr int kFxPublishGrid = 64;  // publication node: one CTA per pool, up to 64 pools
+// Fills kp for a fixed-node kernel (kKindAppend / kKindRingPutCopy / kKindPublish)
+// reading step `i` of the slot at `slot`; a must outlive the call consuming kp.
+struct KvFxArgs {
+  const char *slot = nullptr;
+  int step = 0;
+  void *ptrs[2] = {};
+};
+void fx_node_params(int kind, int grid, KvFxArgs &a, cudaKernelNodeParams &kp);
+
 // Arguments of a staged append / ring-put launch as a CUDA graph kernel node (the
 // graph decode loop updates them per step with cudaGraphExecKernelNodeSetParams).
 struct KvNodeArgs {

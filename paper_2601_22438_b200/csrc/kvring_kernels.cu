@@ -428,6 +428,57 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Fixed-node graph steps: the launch is described by the step header in the slot.
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_append_scatter_fx_kernel(const char *__restrict__ slot, int i) {
+  const KvStepHdr &h = reinterpret_cast<const KvStepHdr *>(slot)[i];
+  const int n = h.n_tasks[0];
+  if (n <= 0) return;
+  run_tasks<kTokMajor, kPaged, false>(reinterpret_cast<const KvTask *>(slot + h.tasks_off[0]), n,
+                                      reinterpret_cast<const KvPoolParams *>(slot + h.params_off[0]),
+                                      h.g, h.n_pools[0], nullptr, nullptr, h.split[0]);
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    kv_ring_put_copy_fx_kernel(const char *__restrict__ slot, int i) {
+  const KvStepHdr &h = reinterpret_cast<const KvStepHdr *>(slot)[i];
+  const int n = h.n_tasks[1];
+  if (n <= 0) return;
+  run_tasks<kPaged, kPaged, false>(reinterpret_cast<const KvTask *>(slot + h.tasks_off[1]), n,
+                                   reinterpret_cast<const KvPoolParams *>(slot + h.params_off[1]),
+                                   h.g, h.n_pools[1], nullptr, nullptr, h.split[1]);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    kv_publish_fx_kernel(const char *__restrict__ slot, int i) {
+  const KvStepHdr &h = reinterpret_cast<const KvStepHdr *>(slot)[i];
+  const int n_tasks = h.n_tasks[1];
+  const int q = blockIdx.x;
+  if (n_tasks <= 0 || q >= h.n_pools[1]) return;
+  const KvTask *tasks = reinterpret_cast<const KvTask *>(slot + h.tasks_off[1]);
+  const KvPoolParams &pp = reinterpret_cast<const KvPoolParams *>(slot + h.params_off[1])[q];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  int32_t *bt = reinterpret_cast<int32_t *>(pp.meta + 32 + 24 * (size_t)pp.max_reqs);
+  for (int t = threadIdx.x; t < n_tasks; t += blockDim.x) {
+    const KvTask tk = tasks[t];
+    if (tk.pool != q) continue;
+    if ((tk.flags & kFirst) && tk.slot >= 0) bt[(size_t)tk.slot * pp.max_blk + tk.j] = tk.dst_unit;
+    atomicAdd(&s_n, 1);
+  }
+  write_parity_table(pp, nullptr);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(pp.counter, (unsigned long long)s_n * (unsigned long long)h.split[1]);
+    if (pp.target != ~0ull) {
+      const bool sys = pp.sys_scope != 0;
+      fence_acquire(sys);
+      st_after_fence(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);
+    }
+  }
+}
+
 // Software-pipelined decode step (kv_run_steps_fused): ONE launch carries the
 // append of step k (tasks [0, n_append), pools params[0, n_app_pools)) and the
 // publication of step k-1 (tasks [n_append, n_tasks), pools params[n_app_pools..),
@@ -565,6 +616,19 @@ void kernel_node_params(int kind, int grid, KvNodeArgs &a, cudaKernelNodeParams 
             : kind == kKindRingPutCopy ? reinterpret_cast<void *>(kv_ring_put_copy_kernel)
             : kind == kKindPublish     ? reinterpret_cast<void *>(kv_publish_kernel)
                                        : reinterpret_cast<void *>(kv_ring_put_kernel);
+  kp.gridDim = dim3(grid > 0 ? grid : 1);
+  kp.blockDim = dim3(kThreads);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = a.ptrs;
+  kp.extra = nullptr;
+}
+
+void fx_node_params(int kind, int grid, KvFxArgs &a, cudaKernelNodeParams &kp) {
+  a.ptrs[0] = &a.slot;
+  a.ptrs[1] = &a.step;
+  kp.func = kind == kKindAppend        ? reinterpret_cast<void *>(kv_append_scatter_fx_kernel)
+            : kind == kKindPublish     ? reinterpret_cast<void *>(kv_publish_fx_kernel)
+                                       : reinterpret_cast<void *>(kv_ring_put_copy_fx_kernel);
   kp.gridDim = dim3(grid > 0 ? grid : 1);
   kp.blockDim = dim3(kThreads);
   kp.sharedMemBytes = 0;
