@@ -258,3 +258,34 @@ def test_shared_capacity_tables_match_oracle(seed, nb, mode):
     finally:
         for h in hs.values():
             K.kv_pool_destroy(h)
+
+
+def test_decode_loop_argument_errors():
+    """The native decode loops reject what they cannot run, before touching any pool:
+    the graph loop needs two distinct streams and device pools, and none of the
+    single-stream / graph loops takes shared-capacity pools (they need kv_run_steps'
+    append-after-previous-ring-put order) or, for the graph loop, host sources."""
+    cfg = configs.scaled(configs.C1, num_blocks=16, max_reqs=4, max_blocks_per_req=4)
+    a, b = _pool(cfg, 0), _pool(cfg, 1)
+    try:
+        K.kv_set_successor(a, 1, FAKE_PTR, cfg.num_blocks, FAKE_PTR)
+        step = [dict(append=[dict(pool=a, begin_step=1, release=[], req_ids=[1], n_new=[3],
+                                  src=None)], repl_pools=[a], step=1)]
+        prep = K.PreparedSteps(step)
+        with pytest.raises(K.KvError) as e:          # one stream for both roles
+            K.kv_run_steps_graph(prep, 0, 0)
+        assert e.value.code == K.KV_EINVAL
+        with pytest.raises(K.KvError) as e:          # tables-only pools launch nothing
+            K.kv_run_steps_graph(prep, 1, 2)
+        assert e.value.code == K.KV_ESTATE
+        assert _tables(a, cfg.max_reqs) == {}        # nothing applied
+        K.kv_set_successor_shared(a, b)
+        for run in (lambda p: K.kv_run_steps_graph(p, 1, 2), lambda p: K.kv_run_steps_pdl(p),
+                    lambda p: K.kv_run_steps_fused(p)):
+            with pytest.raises(K.KvError) as e:
+                run(K.PreparedSteps(step))
+            assert e.value.code == K.KV_EINVAL
+        assert _tables(a, cfg.max_reqs) == {}
+    finally:
+        K.kv_pool_destroy(a)
+        K.kv_pool_destroy(b)
