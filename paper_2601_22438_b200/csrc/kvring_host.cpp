@@ -2343,6 +2343,7 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
     if (G.fixed) hdr[i] = h;
   }
   phase_add(kPhHostCopy, now_s() - t1);
+  const double tu = now_s();
   const int par = (int)(gi & 1);
   const int xi = G.fixed ? se : par;  // exec instance (and its update caches)
   cudaGraphExec_t ge = G.ge[xi];
@@ -2398,6 +2399,7 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
   CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r1, G.ev_r1[gi % N]));
   if (G.split_pub) CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_p, G.ev_p[gi % N]));
   const double t2 = now_s();
+  phase_add(kPhEvents, t2 - tu);  // graph node updates (reported as "events")
   CU(cudaGraphLaunch(ge, st));
   CU(cudaEventRecord(sl.ev, st));
   sl.pending = true;
