@@ -262,7 +262,7 @@ def run_kvring(args):
                    for node, e in plan.items() if node in rt.local]
             pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
             st = dict(append=app, repl_pools=pools if tt >= 1 else [], step=tt)
-            every = 8 if args.loop == "pdl" else TIME_EVERY
+            every = 8 if args.loop in ("pdl", "graph") else TIME_EVERY
             if timing and (args.timeline or (tt - t0) % every == every - 1):
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
@@ -480,8 +480,9 @@ def run_kvring(args):
                                                  "overhead proper is the interference leg")
                              if args.loop == "fused" else None,
                              "what": "replication-stream device time per step (ring-put kernel incl. "
-                                     "its launch and its wait for the step's append), CUDA events by "
-                                     "kv_run_steps on every %d-th timed step" % TIME_EVERY},
+                                     "its launch and its wait for the step's append), CUDA events "
+                                     "recorded by the decode loop on every %d-th timed step"
+                                     % (8 if args.loop in ("pdl", "graph") else TIME_EVERY)},
         "kernel_us": {"kernel": "kv_step_fused_kernel" if args.loop == "fused"
                       else (RINGPUT_GRAPH if args.loop == "graph" else RINGPUT),
                       "median": round(med_kern, 2), "avg": round(avg_kern, 2),

@@ -2097,6 +2097,7 @@ struct GraphLoop {
   cudaGraphNode_t wait_p = nullptr;
   cudaEvent_t ev_a[kEv] = {}, ev_r2[kEv] = {}, ev_r1[kEv] = {}, ev_p[kEv] = {};
   bool split_pub = false;  // ring-put = copy node + separate publication node
+  bool lean = false;       // no timing event nodes (KVRING_GRAPH_LEAN=1, experiments)
   cudaEvent_t start_a = nullptr, start_r = nullptr, join = nullptr;
   cudaEvent_t dummy[2 * kGraphMax] = {};
   StageBuf slot[kSlots];
@@ -2179,6 +2180,7 @@ struct GraphLoop {
     // Timing event nodes sit beside the chain (es(k) has R(k)'s dependencies, ee(k)
     // follows R(k)); no kernel waits on them unless KVRING_GRAPH_EVENTS_IN_CHAIN=1.
     static const bool in_chain = getenv("KVRING_GRAPH_EVENTS_IN_CHAIN") != nullptr;
+    lean = !in_chain && getenv("KVRING_GRAPH_LEAN") != nullptr;  // experiment knob
     for (int k = 0; k < steps; ++k) {
       cudaKernelNodeParams kp{};
       if (fixed) {
@@ -2198,7 +2200,10 @@ struct GraphLoop {
                                k > 0 ? es[k - 1] : nullptr};
       CU(cudaGraphAddKernelNode(&an[k], g, da, k > 0 ? 4 : 3, &kp));
       cudaGraphNode_t ds[2] = {an[k], rprev};
-      CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
+      if (lean)  // experiment: no timing nodes (an empty node keeps the ordering role)
+        CU(cudaGraphAddEmptyNode(&es[k], g, ds, 2));
+      else
+        CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
       if (fixed) {
         fx[3 * k + 1] = KvFxArgs{slot[0].dev, k};
         fx_node_params(kKindRingPutCopy, fx_grid, fx[3 * k + 1], kp);
@@ -2209,7 +2214,7 @@ struct GraphLoop {
         CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
       else
         CU(cudaGraphAddKernelNode(&rn[k], g, ds, 2, &kp));
-      CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
+      if (!lean) CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
       if (split_pub) {  // publication k after copies k and publication k-1 (seq order)
         if (fixed) {
           fx[3 * k + 2] = KvFxArgs{slot[0].dev, k};
@@ -2375,11 +2380,12 @@ int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n
     cudaEvent_t e0 = G.dummy[2 * k], e1 = G.dummy[2 * k + 1];
     if (on && steps[k].ev_kernel_start) e0 = static_cast<cudaEvent_t>(steps[k].ev_kernel_start);
     if (on && steps[k].ev_kernel_end) e1 = static_cast<cudaEvent_t>(steps[k].ev_kernel_end);
-    if (G.ev_set[xi][2 * k] != e0) {
+    if (G.lean) e0 = e1 = nullptr;
+    if (e0 && G.ev_set[xi][2 * k] != e0) {
       CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.es[k], e0));
       G.ev_set[xi][2 * k] = e0;
     }
-    if (G.ev_set[xi][2 * k + 1] != e1) {
+    if (e1 && G.ev_set[xi][2 * k + 1] != e1) {
       CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.ee[k], e1));
       G.ev_set[xi][2 * k + 1] = e1;
     }
