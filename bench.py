@@ -119,6 +119,30 @@ def peaks():
 NVLINK_PEAK_GBS = 770.0   # B200_PROFILING.md measured peer copy per direction (900 nominal)
 
 
+def step_roofline(tot_bytes, ms_max, n, hbm_peak, peak_src):
+    """Whole decode step (append + ring-put + publication) against the roofline.
+
+    Over the timed run the appended bytes equal the replicated bytes D (every token
+    appended is published once, one step later).  Per GPU the step
+    moves 4·D/N through HBM: the append reads the dense source and writes the pool
+    (2·D/N), the ring-put reads the pool (D/N) and the GPU receives one link's writes
+    (D/N, its own at N = 1).  At N > 1, D/N also crosses NVLink out of each GPU.
+    """
+    sec = ms_max * 1e-3
+    hbm = 4 * tot_bytes / n / sec / 1e9
+    out = {"hbm": {"achieved": round(hbm, 1), "peak": hbm_peak, "unit": "GB/s",
+                   "frac": round(hbm / hbm_peak, 4), "peak_source": peak_src},
+           "what": "per GPU, whole timed step: algorithmic HBM bytes 4*D/N (append r+w, "
+                   "ring-put read, incoming replica writes) over ms_per_step; D = replicated "
+                   "bytes (= appended bytes over the run)"}
+    if n > 1:
+        nvl = tot_bytes / n / sec / 1e9
+        out["nvlink"] = {"achieved": round(nvl, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                         "frac": round(nvl / NVLINK_PEAK_GBS, 4),
+                         "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -488,6 +512,7 @@ def run_kvring(args):
                       "median": round(med_kern, 2), "avg": round(avg_kern, 2),
                       "sampled_launches": len(kern_us)},
         "roofline": roof,
+        "step_roofline": step_roofline(tot_bytes, ms_max, N, hbm_peak, peak_src),
         "gpu_launches": int(tot_launch),
         "wall_s_timed": round(wall, 3),
         "host_us_per_step": host_prof,
