@@ -453,15 +453,26 @@ def run_kvring(args):
     elif N == 1:
         per_launch = my_bytes / args.steps
         achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
+        pop = traffic_ref("decode_population", "kv_ring_put_copy_kernel") if args.loop == "graph" else None
         tr = (traffic_ref("decode_step", "kv_ring_put_copy_kernel") if args.loop == "graph"
               else traffic_ref("decode_step", "kv_ring_put_inl_kernel"))
+        if pop:  # per-launch average over a population of this loop's copy-node launches
+            tnote = ("ncu --set full over %d consecutive copy-node launches of this bench loop "
+                     "(profiles/traffic.json decode_population): avg DRAM bytes/launch %d (read %d, "
+                     "write %d) vs avg algorithmic r+w %d (L2 bytes the kernel requested) = %.2f; "
+                     "no re-reads, most replica writes stay in L2"
+                     % (pop["n_launches"], pop["traffic"], pop["dram_read"], pop["dram_write"],
+                        pop["algorithmic_rw"], pop["traffic_over_algorithmic"]))
+        elif tr:
+            tnote = ("ncu --set full of a decode-step launch (profiles/traffic.json): "
+                     "DRAM bytes %d vs algorithmic read %d / r+w %d; writes stay in L2"
+                     % (tr["traffic"], tr["algorithmic_read"], tr["algorithmic_rw"]))
+        else:
+            tnote = None
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4),
-                "traffic": tr["traffic"] if tr else None,
-                "traffic_note": ("ncu --set full of a decode-step launch (profiles/traffic.json): "
-                                 "DRAM bytes %d vs algorithmic read %d / r+w %d; writes stay in L2"
-                                 % (tr["traffic"], tr["algorithmic_read"], tr["algorithmic_rw"]))
-                                if tr else None,
+                "traffic": pop["traffic"] if pop else (tr["traffic"] if tr else None),
+                "traffic_note": tnote,
                 "kernel": RINGPUT_GRAPH if args.loop == "graph" else RINGPUT,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(2 * per_launch),
