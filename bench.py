@@ -161,6 +161,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a few hundred ms to start; the timed region can be shorter
+            # (C2: ~8 ms), so wait for its first sample -- the samples then bracket the region
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
