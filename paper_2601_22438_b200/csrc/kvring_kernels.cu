@@ -227,7 +227,8 @@ constexpr int kMaxPoolsPerLaunch = 64;
 // that pool's seq with a release store (last-CTA pattern, reading R9).
 __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int n_tasks,
                                           const KvPoolParams *__restrict__ params, int n_pools,
-                                          const char *tbl_base = nullptr, int split = 1) {
+                                          const char *tbl_base = nullptr, int split = 1,
+                                          int unit_off = 0) {
   __shared__ int s_cnt[kMaxPoolsPerLaunch];
   __shared__ int s_own[kMaxPoolsPerLaunch];
   for (int i = threadIdx.x; i < n_pools; i += blockDim.x) {
@@ -235,10 +236,16 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
     s_own[i] = 0;
   }
   __syncthreads();
-  // the units this CTA copied (u = blockIdx.x + i * gridDim.x), one per thread
+  // the units this CTA copied, one per thread: global unit ug = blockIdx.x + i * gridDim.x
+  // of the copy loop, of which this list holds [unit_off, unit_off + n_units) (the fused
+  // kernel's ring-put part follows its append part).  Counting exactly the CTA's own
+  // units is what makes its release cover the stores it counts.
+  const int G = (int)gridDim.x;
   const int n_units = n_tasks * split;
-  for (int u = blockIdx.x + (int)threadIdx.x * (int)gridDim.x; u < n_units;
-       u += (int)blockDim.x * (int)gridDim.x) {
+  int u0 = (int)blockIdx.x;
+  if (u0 < unit_off) u0 += (unit_off - u0 + G - 1) / G * G;
+  for (int ug = u0 + (int)threadIdx.x * G; ug < unit_off + n_units; ug += (int)blockDim.x * G) {
+    const int u = ug - unit_off;
     const KvTask tk = tasks[u / split];
     const bool lead = (u % split) == 0;  // bt entry / table ownership: once per task
     const KvPoolParams &pp = params[tk.pool];
@@ -497,7 +504,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const KvPoolParams &pp = app ? params[tk.pool] : rparams[tk.pool];
     copy_task_dyn(tk, pp.src, pp.dst, g, app);
   }
-  if (n_rep_pools > 0) publish_pass(tasks + n_append, n_tasks - n_append, rparams, n_rep_pools);
+  if (n_rep_pools > 0)
+    publish_pass(tasks + n_append, n_tasks - n_append, rparams, n_rep_pools, nullptr, 1, n_append);
 }
 
 // Receiver of the NCCL comparison: parameters come from the packed header on
