@@ -318,3 +318,75 @@ def test_block_mode_restore_resumes_at_block_boundary():
     assert t_star == 18 and all(ln % 16 == 0 for _, ln in restored)
     for (p, s), n in ring.serving.items():
         check_content(ring, n, s)          # I4: resumed stage == failure-free content
+
+
+def _brute_i1(n, holder):
+    """I1 written out independently of the oracle's link bookkeeping: every valid slot
+    of n's primary equals the holder's replica region at the same block id."""
+    B = n.g.block_size
+    for r, (s, ln, bt) in n.live().items():
+        for j, blk in enumerate(bt):
+            v = min(B, ln - j * B)
+            if not np.array_equal(holder.replica[blk, :, :, :, :v], n.primary[blk, :, :, :, :v]):
+                return False
+    return True
+
+
+def test_reprotect_applies_p227_plan_reseeds_and_freezes_excluded():
+    """OracleRing.reprotect (NEXT-1, §3.2) pinned against the paper's own example
+    rather than against the product: 4 instances x 3 stages on the paper's instance ring,
+    (0,2) fails and is promoted onto (1,2); the exclusion set
+    {(0,2),(1,2),(2,1),(3,1)} of P:227 must re-target exactly (1,1)->(0,1) and
+    (3,2)->(2,2).  Applying the plan must (a) re-seed the re-targeted links -- the new
+    holders did not hold those predecessors before, so only a full re-seed makes I1 hold at
+    the next step, (b) leave the other links untouched (no re-seed: their holders' seq
+    keeps advancing without a republication of old tokens), and (c) stop the excluded
+    nodes: (2,1)'s and (3,1)'s old holders stay frozen at the last step published before
+    the plan.  check_all (I1-I3) runs after every step."""
+    cfg = configs.scaled(configs.C1, pipelines=4, stages=3, num_blocks=128, max_reqs=16,
+                         max_blocks_per_req=12, batch_cap=3, n_requests=60, n_steps=30,
+                         fixed_prompt=None, fail_node=(0, 2), fail_step=12, ring="instance")
+    rng = np.random.default_rng(227)
+    sched = [closed_loop_schedule(rng.integers(1, 60, 60), rng.integers(1, 25, 60),
+                                  cfg.n_steps, cfg.batch_cap, pipeline=p) for p in range(4)]
+    ring = OracleRing(cfg, ring="instance", schedules=sched)
+    N = ring.nodes
+    excluded = {(0, 2), (1, 2), (2, 1), (3, 1)}
+    plan_t = 14
+    frozen = {}
+    for t in range(cfg.n_steps):
+        ring.appends(t)
+        if t == cfg.fail_step:
+            ring.fail_and_restore(t, cfg.fail_node)
+            assert ring.serving[(0, 2)] is N[(1, 2)]          # promotion onto (1,2), P:225
+        if t == plan_t:
+            before = {c: N[c].succ for c in ring.coords}
+            plan = ring.reprotect(excluded)
+            # the paper's example: exactly these two adjusted targets (P:227)
+            changed = {c for c in ring.coords if c not in excluded
+                       and plan[c] != instance_ring(c, 4, 3)}
+            assert changed == {(1, 1), (3, 2)}
+            assert plan[(1, 1)] == (0, 1) and plan[(3, 2)] == (2, 2)
+            assert N[(1, 1)].succ is N[(0, 1)] and N[(3, 2)].succ is N[(2, 2)]
+            for c in ((2, 1), (3, 1), (1, 2)):                # excluded: send nothing
+                assert N[c].succ is None
+            for c in ring.coords:                             # untouched links keep their holder
+                if c not in excluded and c not in changed:
+                    assert N[c].succ is before[c]
+            # old holders of the excluded senders freeze at the last published step
+            frozen = {(3, 1): N[(3, 1)].rseq, (0, 1): N[(0, 1)].rseq}
+            assert frozen[(3, 1)] == t - 1 and frozen[(0, 1)] == t - 1
+            # the new holders have not seen these predecessors yet
+            assert not _brute_i1(N[(1, 1)], N[(0, 1)]) or not N[(1, 1)].live()
+        if t >= 1:
+            ring.replicate(t)
+        check_all(ring)
+        if t >= plan_t:
+            assert N[(3, 1)].rseq == frozen[(3, 1)]      # (2,1) excluded: (3,1) frozen
+            assert N[(0, 1)].rseq == t                    # now written by (1,1)
+            assert N[(2, 2)].rseq == t
+            assert _brute_i1(N[(1, 1)], N[(0, 1)]) and _brute_i1(N[(3, 2)], N[(2, 2)])
+            for c in ring.coords:
+                n = N[c]
+                if c not in excluded and not n.dead and n.succ is not None:
+                    assert _brute_i1(n, n.succ), c
