@@ -133,7 +133,7 @@ int kv_set_successor(kv_pool_t *p, int32_t succ_node, void *succ_replica,
  *   - freed replica blocks are reusable AT ONCE: the entry that referenced them
  *     is withdrawn from the published table (two memsets, flushed before the
  *     next launch touching h).  Stream order needed: an append on h after the
- *     ring-put of the previous step (kv_run_steps does it; the fused / PDL loops
+ *     ring-put of the previous step (kv_run_steps does it; kv_loop_step
  *     reject shared pools, KV_EINVAL).
  * Same device, geometry, max_reqs and max_blocks_per_req; one predecessor per
  * holder (a previous one is unlinked, its replicas freed).  Re-seeds p. */
@@ -183,11 +183,14 @@ typedef struct {
 int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream);
 
 /* Publish step `step` to the successor (§8(c) step 5; R2 dirty tokens; R9).
- * For every live slot the tokens [pub_len, len) are copied from this pool to
- * the successor's replica region at the same block ids with 16-B stores (NVLink
- * P2P when the successor is remote), bt entries of the touched blocks and the
- * parity (step & 1) (req_id, len) table are written, and the last CTA stores
- * seq = step (release, system scope).  step >= 1 and strictly increasing per
+ * ONE kernel derives the work list on the device (§8(a) a3): from a snapshot of
+ * each live slot's (req_id, len, pub_len) and the pool's device-resident block
+ * table it splits the dirty tokens [pub_len, len) at block boundaries, sums them
+ * over slots, and copies them from this pool to the successor's replica region at
+ * the same block ids with 16-B stores (NVLink P2P when the successor is remote);
+ * then the bt entries of the touched blocks and the parity (step & 1)
+ * (req_id, len) table are written, and the last CTA stores seq = step (release,
+ * system scope for a peer).  Shared-capacity links use a host-built work list.  step >= 1 and strictly increasing per
  * pool; KV_EPEER if no successor is bound.  pub_len := len on return (the host
  * never waits for the peer). */
 int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream);
@@ -204,19 +207,10 @@ int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t s
 #define KV_MODE_BLOCKS 1
 int kv_set_mode(kv_pool_t *p, int32_t mode);
 
-/* Decode-loop driver: for each step, kv_append_multi(append) on append_stream,
- * then -- ordered after it by an event when the streams differ -- the
- * publication kv_replicate_step_multi(repl_pools, step) on repl_stream: the
- * paper's "separate CUDA stream ... to overlap the communication with
- * computation" (§3.2).  The append of step k also waits (event) for the
- * publication of step k-2 (steps counted across calls on the same stream pair; on
- * a new pair the first append waits for everything already on repl_stream):
- * blocks freed by a retiring request are reused
- * one step later (reading R7) and must not be overwritten while a lagging
- * publication still reads them.  Optional cudaEvent_t handles are recorded on
- * repl_stream before the publication (ev_call), around its kernel
- * (ev_kernel_start / ev_kernel_end) and after it (ev_done).  Stops at the
- * first error (steps before it stay applied). */
+/* Decode steps.  A step = the appends of step `step` (the model's KV write,
+ * kv_append_multi semantics) followed by the publication of the same step by
+ * repl_pools (kv_replicate_step_multi semantics).  The
+ * optional cudaEvent_t handles are recorded around the launches named below. */
 typedef struct {
   int32_t n_append;
   const kv_append_args_t *append;
@@ -224,46 +218,54 @@ typedef struct {
   kv_pool_t *const *repl_pools;
   uint64_t step;
   void *ev_call, *ev_kernel_start, *ev_kernel_end, *ev_done;
-  void *ev_append_start, *ev_append_end;  /* optional: around the append kernel (append_stream) */
+  void *ev_append_start, *ev_append_end;
 } kv_step_t;
-int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream, void *repl_stream);
 
-/* Single-stream, software-pipelined form of the same loop: launch k carries the
- * append of step k AND the publication of step k-1 in ONE kernel (their slots are
- * disjoint: the publication reads positions < len_{k-1} of live requests, the append
- * writes positions >= len_{k-1} or blocks quarantined >= 1 step, reading R7); one
- * more launch publishes step n-1.  Same work as kv_run_steps with half the launches
- * and no cross-stream event; each publication trails its append by one launch (the
- * overlap of replication with the next step of P:229).  ev_kernel_start/end of step
- * k bracket launch k; ev_call, ev_done, ev_append_* are ignored. */
-int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream);
+/* Two-stream decode loop, the paper's shape (§3.2: "A separate CUDA stream
+ * is used to overlap the communication with computation"): per step ONE append
+ * launch on append_stream and, ordered after it by an event, ONE publication
+ * launch on repl_stream.  The append of step k also waits (event) for the
+ * publication of step k-2 (k-1 for shared-capacity pools): blocks freed by a
+ * retiring request are reused one step later (reading R7) and must not be
+ * overwritten while a lagging publication still reads them.  Steps are counted
+ * across calls on the same stream pair; on a new pair the first append waits for
+ * everything already on repl_stream.  Equal streams: plain stream order.
+ * ev_append_start/end bracket the append launch, ev_call / ev_done the publication
+ * (stream position), ev_kernel_start/end its kernel.  Stops at the first error
+ * (steps before it stay applied). */
+int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream,
+                 void *repl_stream);
 
-/* Single-stream loop with programmatic dependent launch (PDL): per step the append
- * and the publication kernels are launched back to back on ONE stream with the
- * programmatic-serialization attribute and carry their descriptors (pool
- * parameters, publication tables, tasks; <= 28 KiB) in the kernel parameter space,
- * so no copy node sits between kernels -- a step whose descriptors do not fit is
- * staged by one H2D and launched normally (it serialises); the kernels order
- * themselves (griddepcontrol): the
- * publication of step k waits for append k, append k+1 overlaps it and waits for it
- * before exiting (seq stays monotone).  Same work and results as kv_run_steps.
- * ev_kernel_start/end and ev_append_start/end are honoured (each record is a stream
- * operation that interrupts the overlap at that step); KV_SRC_HOST appends are not
- * supported (KV_EINVAL). */
-int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream);
+/* One-launch-per-step decode loop on ONE stream (software pipelined; no lookahead:
+ * each call prepares and launches exactly the step it is given).  kv_loop_step
+ * launches ONE kernel that carries the appends of `step` AND the publication of
+ * the step previously given to this loop (the "pending" publication): the
+ * replication of step k-1 overlaps the KV write of step k inside one balanced
+ * grid -- their slots are disjoint by reading R7 -- and `step`'s publication
+ * becomes pending.  The pending publication is built from the pools' tables as
+ * they are when the next kv_loop_step / kv_loop_flush runs (the appends of the new
+ * step are applied after it), so calls made in between -- kv_fail_stage, kv_restore,
+ * kv_set_successor, a resume kv_append -- act exactly as between the append and the
+ * replicate of the sequential protocol; pending pools that died or lost their
+ * successor meanwhile publish nothing.  If the appends are rejected (KV_ENOMEM /
+ * KV_EINVAL, tables unchanged) the pending publication is still launched and the
+ * error returned.  Shared-capacity pools are not accepted (KV_EINVAL).
+ * ev_kernel_start / ev_kernel_end bracket the launch; the other events are ignored.
+ * kv_loop_flush launches the pending publication alone; kv_loop_run is n_steps
+ * kv_loop_step calls.  One host thread per loop; a pool is pending in one loop. */
+typedef struct kv_loop kv_loop_t;
+int kv_loop_create(kv_loop_t **out);
+int kv_loop_destroy(kv_loop_t *loop);
+int kv_loop_step(kv_loop_t *loop, const kv_step_t *step, void *stream);
+int kv_loop_run(kv_loop_t *loop, int32_t n_steps, const kv_step_t *steps, void *stream);
+int kv_loop_flush(kv_loop_t *loop, void *stream);
 
-/* CUDA-graph decode loop: the same work and results as kv_run_steps, issued as one
- * CUDA graph per group of 8 steps -- per step an append kernel node and a ring-put
- * kernel node whose graph edges are kv_run_steps' stream-order rules (append k
- * after append k-1 and after ring-put k-2, reading R7; ring-put k after append k
- * and after ring-put k-1), the group's descriptors staged by one H2D memcpy node.
- * Groups alternate between the two (distinct) streams and are chained by
- * event-wait nodes; on return both streams are ordered after the last group.
- * ev_kernel_start / ev_kernel_end are recorded around each ring-put node; ev_call,
- * ev_done and ev_append_* are ignored.  KV_SRC_HOST appends and shared-capacity
- * pools are not supported (KV_EINVAL). */
-int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *append_stream,
-                       void *repl_stream);
+/* Launch log of the calling thread (measurement): mode 1 clears and starts it;
+ * mode 0 stops it and copies min(count, cap) records of 5 uint64 each --
+ * [kind (1 append, 2 publication, 3 both), append payload bytes, publication
+ * payload bytes, grid, descriptor bytes] -- for every decode-step kernel launched
+ * since; returns the count. */
+int kv_launch_log(uint64_t *out, int32_t cap, int32_t mode);
 
 /* Re-protection after a failure (§8(f) NEXT-1; §3.2: "replication targets
  * will be automatically adjusted to exclude the nodes under traffic rerouting").
@@ -283,17 +285,20 @@ int kv_plan_targets(int32_t n_nodes, const int32_t *succ, const uint8_t *exclude
  * replica bytes and metadata as kv_replicate_step_multi. */
 int kv_replicate_step_ce(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, void *stream);
 
-/* Fault injection: the next replicate of p executes only its first
- * `tasks` copy tasks and never publishes -- a stage dying mid-step. -1 clears. */
-int kv_inject_abort(kv_pool_t *p, int32_t tasks);
+/* Fault injection: the next publication of p copies only the first
+ * `slices` (layer, K/V, head, token) slices of its dirty set (in the device's work
+ * order) and publishes nothing -- no tables, no seq, and p's host state stays at
+ * its previous publication: a stage dying mid-step.  -1 clears. */
+int kv_inject_abort(kv_pool_t *p, int32_t slices);
 
 /* Simulated failure (§8(a) a7): p becomes dead; its pool, replica region and
  * replica metadata are overwritten with 0xFF bytes on `stream`. */
 int kv_fail_stage(kv_pool_t *p, void *stream);
 
 /* Restore (§8(a) a8): rebuild the requests published in a holder's
- * replica region into pool dst.  Reads seq = t* (acquire) and the parity-t*
- * metadata, allocates in dst by ascending req_id then logical block j (lowest
+ * replica region into pool dst.  Reads seq = t* with a device acquire
+ * (ld.acquire.sys in a kernel on dst's device, then a fence; reading R9) and the
+ * parity-t* metadata copied after it, allocates in dst by ascending req_id then logical block j (lowest
  * free ids, R6), copies each block's valid slots [0, min(B, len - jB)) from
  * holder_replica (local HBM, or NVLink when it is a peer pointer) and rebuilds
  * dst's tables.  dst may be the holder itself (promotion, R10).  Outputs
@@ -355,15 +360,11 @@ uint64_t kv_kernel_launch_count(void);
  * Used by bench.py to time the ring-put kernel live. */
 int kv_time_next_launch(void *ev_before, void *ev_after);
 
-/* Host-side phase counters of kv_run_steps (seconds, cumulative since the last
- * reset; diagnostics, updated without synchronisation): [0] prepare (tables +
- * work lists, helper thread), [1] issue thread waiting for prepare, [2] append
- * staging + H2D call, [3] append launch, [4] publication launch, [5]
- * stream-ordering events, [6] helper waiting for the issue thread, [7] staging
- * ring waits, [8] staging host copies, [9] H2D calls, [10..12] prepare split
- * (append / replicate / commit), [13] publication staging, [14] / [15] COUNTS of
- * inline-descriptor / staged launches.  Copies min(n, count) values; returns the
- * count. */
+/* Host-side phase counters of the decode path (seconds, cumulative since the last
+ * reset; diagnostics, updated without synchronisation): [0] append preparation
+ * (validation, allocation, items), [1] publication preparation (snapshot +
+ * commit), [2] descriptor staging / host-source staging, [3] launch calls.
+ * Copies min(n, count) values; returns the count. */
 int kv_host_profile(double *out, int32_t n, int32_t reset);
 
 #ifdef __cplusplus

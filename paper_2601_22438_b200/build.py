@@ -22,7 +22,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["kvring_kernels.cu"]
+SOURCES_CU = ["kvring_kernels.cu", "kvring_step.cu"]
 SOURCES_CPP = ["kvring_host.cpp"]
 HEADERS = ["kvring_internal.h"]
 
@@ -52,7 +52,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
                    "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
-            extra = os.environ.get("KVRING_NVCC_DEFS", "")   # experiments: e.g. -DKV_UNROLL=4
+            extra = os.environ.get("KVRING_NVCC_DEFS", "")   # debug builds: -DKV_BOUNDS_CHECK
             if extra:
                 cmd[1:1] = extra.split()
             _run(cmd)

@@ -29,13 +29,10 @@
 
 #define KV_API extern "C" __attribute__((visibility("default")))
 
-// Host-side phase counters of kv_run_steps (seconds, cumulative; kv_host_profile).
+// Host-side phase counters of the decode path (seconds, cumulative; kv_host_profile).
 #include <chrono>
 namespace {
-enum { kPhPrepare = 0, kPhWaitPrep, kPhStage, kPhEnqA, kPhEnqP, kPhEvents, kPhWaitIssue,
-       kPhAcquire, kPhHostCopy, kPhH2DCall, kPhPrepAppend, kPhPrepRepl, kPhCommit,
-       kPhPubStage, kPhInlineLaunches, kPhStagedLaunches, kPhN };
-// Two threads (helper + issue) add to them: relaxed atomics, integer nanoseconds.
+enum { kPhPrepAppend = 0, kPhPrepRepl, kPhStage, kPhLaunch, kPhN };
 std::atomic<long long> g_phase_ns[kPhN];
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -264,16 +261,14 @@ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
 
 cudaError_t timed_launch(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t st,
-                         const KvPoolParams *host_params = nullptr, int split = 1) {
+                         int n_pools, const KvGeomDev &g, int grid, cudaStream_t st) {
   cudaEvent_t b = g_ev_before, a = g_ev_after;
   g_ev_before = g_ev_after = nullptr;
   if (b) {
     cudaError_t e = cudaEventRecord(b, st);
     if (e != cudaSuccess) return e;
   }
-  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st, host_params,
-                              split);
+  cudaError_t e = launch_copy(kind, tasks, n_tasks, params, n_pools, g, grid, st);
   if (e != cudaSuccess) return e;
   if (a) return cudaEventRecord(a, st);
   return cudaSuccess;
@@ -327,6 +322,8 @@ class TaskVec {
   size_t n_ = 0, cap_ = 0;
 };
 
+struct kv_loop;
+
 struct kv_pool {
   kv_geom_t g{};
   int NB = 0, R = 0, M = 0, device = -1, node_id = 0, replica_blocks = 0;
@@ -352,7 +349,6 @@ struct kv_pool {
   uint32_t call_id = 0;
   std::vector<int64_t> scratch_ids;
   std::vector<int> scratch_slot;  // slot of each append entry found by validation (-1: new)
-  TaskVec scratch_tasks;
   // shared-capacity mode (§8(f) NEXT-3, reading R17): the successor
   // `holder` keeps this pool's replicas in ITS OWN pool.  Predecessor side: per
   // slot the holder block ids of the replica, whether it was dropped, and the
@@ -375,9 +371,12 @@ struct kv_pool {
   // state
   bool dead = false;
   uint64_t last_step = 0;
-  int abort_after = -1;
-  unsigned long long *counter = nullptr;  // device, monotone
+  int abort_slices = -1;                  // fault injection (kv_inject_abort)
+  unsigned long long *counter = nullptr;  // device, monotone (host-task ring-put)
   unsigned long long issued = 0;          // host mirror of the counter target
+  unsigned long long *step_counter = nullptr;  // device, step-engine completion counter
+  int32_t *d_bt = nullptr;                // device-resident block table [R][M]
+  kv_loop *loop = nullptr;                // decode loop holding a pending publication
   uint64_t bytes_replicated = 0, tasks_launched = 0, kernels = 0, last_step_bytes = 0;
 
   KvGeomDev geom_dev() const {
@@ -584,10 +583,12 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
   }
 }
 
-// Applies the appends to the tables and emits the scatter tasks (src rows are
-// token rows of the dense source, `row_base` added).
-void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, TaskVec &tasks,
-               int task_segs) {
+// Applies the appends to the tables and emits the launch's append items (one per
+// (slot, block) piece; src rows are token rows of the pool's dense source).  Items
+// are emitted for device pools only; `slices` is the running end of the launch's
+// append space.  Returns the rows appended.
+long long do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx,
+                    std::vector<KvAppItem> &items, int32_t &slices) {
   const int B = p->g.block_size;
   int row = 0;
   for (int i = 0; i < a.n; ++i) {
@@ -609,14 +610,24 @@ void do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx, TaskVec &tas
       if (len % B == 0) p->slot_bt[s].push_back(p->free_blocks.take_min());
       const int j = len / B, lo = len % B;
       const int n = std::min(B - lo, left);
-      if (p->device >= 0)
-        push_item(tasks, pidx, row, p->slot_bt[s][j], -1, j, lo, n, p->combos, task_segs);
+      if (p->device >= 0) {
+        KvAppItem it;
+        it.off = slices;
+        it.row = row;
+        it.blk = p->slot_bt[s][j];
+        it.p0 = len;
+        it.slot = (int16_t)s;
+        it.pool = pidx;
+        items.push_back(it);
+        slices += n * p->combos;
+      }
       row += n;
       len += n;
       left -= n;
     }
     p->slot_len[s] = len;
   }
+  return row;
 }
 
 // ---- replicate --------------------------------------------------------------
@@ -774,8 +785,11 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
   if (p->device >= 0) {
     DeviceGuard dg(p->device);
     if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", p->device);
-    CU(cudaMalloc(reinterpret_cast<void **>(&p->counter), sizeof(unsigned long long)));
-    CU(cudaMemset(p->counter, 0, sizeof(unsigned long long)));
+    CU(cudaMalloc(reinterpret_cast<void **>(&p->counter), 2 * sizeof(unsigned long long)));
+    CU(cudaMemset(p->counter, 0, 2 * sizeof(unsigned long long)));
+    p->step_counter = p->counter + 1;
+    CU(cudaMalloc(reinterpret_cast<void **>(&p->d_bt), sizeof(int32_t) * (size_t)p->R * p->M));
+    CU(cudaMemset(p->d_bt, 0xFF, sizeof(int32_t) * (size_t)p->R * p->M));
     CU(launch_meta_init(p->meta, p->R, p->M, 0));
     g_launches++;
     p->kernels++;
@@ -785,6 +799,10 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
   *out = p.release();
   return KV_OK;
 }
+
+namespace {
+void loop_forget(kv_loop *L, kv_pool *p);
+}  // namespace
 
 KV_API int kv_pool_destroy(kv_pool_t *p) {
   if (!p) return KV_OK;
@@ -796,10 +814,12 @@ KV_API int kv_pool_destroy(kv_pool_t *p) {
     p->rep_src->has_succ = false;
     p->rep_src = nullptr;
   }
+  if (p->loop) loop_forget(p->loop, p);
   if (p->counter) {
     DeviceGuard dg(p->device);
     cudaDeviceSynchronize();
     cudaFree(p->counter);
+    cudaFree(p->d_bt);
   }
   delete p;
   return KV_OK;
@@ -908,12 +928,12 @@ KV_API int kv_release(kv_pool_t *p, int32_t n, const int64_t *req_ids) {
 
 namespace {
 
-// ---- launches: prepare on the host, stage descriptors with ONE H2D, enqueue ----
+// ---- host-task launches (restore, pack, shared-capacity + copy-engine ring-put) ----
 inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-// One kernel launch prepared on the host.
+// One host-task kernel launch prepared on the host.
 struct Launch {
-  int kind = kKindAppend;
+  int kind = kKindRingPut;
   int n_pools = 0;
   kv_pool *p0 = nullptr;
   std::vector<KvPoolParams> params;
@@ -922,13 +942,10 @@ struct Launch {
   TaskVec tasks;
   std::vector<int> ntask;          // replicate: tasks per pool
   std::vector<uint64_t> bytes;     // replicate: payload bytes per pool
-  std::vector<const void *> host_src;  // append: host sources (KV_SRC_HOST), per pool
-  std::vector<size_t> host_src_bytes;
   std::vector<std::vector<int>> ce_blocks;  // copy-engine variant: full blocks per pool
   bool use_ce = false;
   std::vector<kv_pool::Inval> inval;  // shared capacity: published entries to withdraw first
   int max_reqs_inval = 0;
-  int split = 1;                      // CTA units per task (whole-item tasks)
   // filled by stage()
   const KvPoolParams *params_dev = nullptr;
   const KvTask *tasks_dev = nullptr;
@@ -941,13 +958,10 @@ struct Launch {
     tasks.clear();
     ntask.assign(n, 0);
     bytes.assign(n, 0);
-    host_src.assign(n, nullptr);
-    host_src_bytes.assign(n, 0);
     if ((int)ce_blocks.size() < n) ce_blocks.resize(n);
     for (auto &v : ce_blocks) v.clear();
     use_ce = false;
     inval.clear();
-    split = 1;
     params_dev = nullptr;
     tasks_dev = nullptr;
   }
@@ -957,51 +971,20 @@ struct Launch {
   }
 };
 
-// Moves the pending published-entry invalidations of every holder this launch
-// touches (its pools, and the holders of its pools) into the launch.
-void collect_inval(Launch &L, kv_pool *const *pools, int n) {
+// Moves the pending published-entry invalidations of every holder a launch
+// touches (its pools, and the holders of its pools) into `out`.
+void collect_inval(std::vector<kv_pool::Inval> &out, int &max_reqs, kv_pool *const *pools,
+                   int n) {
   auto take = [&](kv_pool *h) {
     if (!h || h->pending_inval.empty()) return;
-    L.max_reqs_inval = h->R;
-    L.inval.insert(L.inval.end(), h->pending_inval.begin(), h->pending_inval.end());
+    max_reqs = h->R;
+    out.insert(out.end(), h->pending_inval.begin(), h->pending_inval.end());
     h->pending_inval.clear();
   };
   for (int k = 0; k < n; ++k) {
     take(pools[k]);
     take(pools[k]->holder);
   }
-}
-
-// Task size for one launch: spread the launch's slices over every resident CTA
-// (SMs x 4) so a decode-sized step runs in one wave, capped at 32 KiB per task.
-int choose_task_segs(const kv_pool *p, long long total_segs) {
-  const int maxs = std::max(1, 32768 / p->seg_bytes);
-  const long long slots = (long long)resident_ctas(p->device < 0 ? 0 : p->device);
-  static int min_segs = -1;  // experiment knob KVRING_MIN_TASK_SEGS (default 16)
-  if (min_segs < 0) {
-    const char *e = getenv("KVRING_MIN_TASK_SEGS");
-    min_segs = (e && atoi(e) > 0) ? atoi(e) : 16;
-  }
-  long long t = (total_segs + slots - 1) / std::max(1LL, slots);
-  t = (t + 15) & ~15LL;
-  t = std::max<long long>(std::min(maxs, min_segs), t);
-  return (int)std::min<long long>(maxs, t);
-}
-
-// Whole-item tasks (<= 32 KiB each, fewer descriptors to stage or carry in the
-// parameter space) split on the device into `split` CTA units so a decode step still
-// spreads over every resident CTA (KVRING_MIN_TASK_SEGS > 0: the old sizing, split 1).
-int whole_item_segs(const kv_pool *p) { return std::max(1, 32768 / p->seg_bytes); }
-
-int choose_split(const kv_pool *p, size_t n_tasks) {
-  if (n_tasks == 0) return 1;
-  const long long slots = (long long)resident_ctas(p->device < 0 ? 0 : p->device);
-  return (int)std::max(1LL, std::min(8LL, slots / (long long)n_tasks));
-}
-
-bool legacy_task_sizing() {
-  static const bool legacy = getenv("KVRING_MIN_TASK_SEGS") != nullptr;
-  return legacy;
 }
 
 int check_same_device(int n, kv_pool *const *pools) {
@@ -1017,76 +1000,14 @@ int check_same_device(int n, kv_pool *const *pools) {
   return KV_OK;
 }
 
-// Validates every pool (all-or-nothing), applies begin_step / releases / appends
-// to the host tables and builds the scatter tasks.
-int prepare_append(int n_pools, const kv_append_args_t *args, Launch &L, bool allow_split = true) {
-  if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
-  if (n_pools > kMaxPoolsPerLaunchHost)
-    return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
-  kv_pool *pools[kMaxPoolsPerLaunchHost];
-  for (int k = 0; k < n_pools; ++k) pools[k] = args[k].pool;
-  if (!pools[0]) return fail(KV_EINVAL, "null pool");
-  int rc = check_same_device(n_pools, pools);
-  if (rc) return rc;
-  long long tokens = 0;
-  {
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = args[k].pool;
-    if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
-    const bool bs = args[k].begin_step != 0;  // validation sees the released quarantine
-    rc = append_validate(p, args[k],
-                         p->free_blocks.size() + (bs ? (long long)p->q_blocks.size() : 0),
-                         p->free_slots.size() + (bs ? (long long)p->q_slots.size() : 0));
-    if (rc) return rc;
-    long long rows = 0;
-    for (int i = 0; i < args[k].n; ++i) rows += args[k].n_new[i];
-    if (p->device >= 0 && rows > 0 && !args[k].src_kv)
-      return fail(KV_EINVAL, "null src_kv with tokens to append");
-    tokens += rows;
-  }
-  }
-  L.reset(kKindAppend, n_pools);
-  L.p0 = pools[0];
-  const bool whole = allow_split && !legacy_task_sizing();
-  const int task_segs =
-      whole ? whole_item_segs(L.p0) : choose_task_segs(L.p0, tokens * L.p0->combos);
-  for (int k = 0; k < n_pools; ++k) {
-    kv_pool *p = args[k].pool;
-    if (args[k].begin_step) do_begin_step(p);
-    do_release(p, args[k].n_release, args[k].release_ids);
-    if (p->scratch_need > p->free_blocks.size()) evict_for(p, p->scratch_need);
-    const size_t before = L.tasks.size();
-    do_append(p, args[k], (int16_t)k, L.tasks, task_segs);
-    L.ntask[k] = (int)(L.tasks.size() - before);
-    long long rows = 0;
-    for (int i = 0; i < args[k].n; ++i) rows += args[k].n_new[i];
-    KvPoolParams &pp = L.params[k];
-    pp.src = static_cast<const char *>(args[k].src_kv);
-    pp.dst = p->pool;
-    pp.src_bytes = (unsigned long long)rows * p->token_bytes;
-    pp.dst_bytes = (unsigned long long)p->NB * p->block_bytes;
-    if ((args[k].flags & KV_SRC_HOST) && rows > 0) {
-      L.host_src[k] = args[k].src_kv;
-      L.host_src_bytes[k] = (size_t)rows * p->token_bytes;
-    }
-  }
-  collect_inval(L, pools, n_pools);
-  if (whole) L.split = choose_split(L.p0, L.tasks.size());
-  return KV_OK;
-}
-
-// Validates the pools and builds the dirty work list (§8(a) a3); state is
-// committed by commit_replicate once the launch is enqueued.
-int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch &L,
-                      bool use_ce = false, bool allow_split = true) {
+// Checks shared by both publication paths (state is not touched).
+int validate_replicate(int n_pools, kv_pool *const *pools, uint64_t step) {
   if (n_pools <= 0 || !pools) return fail(KV_EINVAL, "no pools");
   if (n_pools > kMaxPoolsPerLaunchHost)
     return fail(KV_EINVAL, "at most %d pools per launch", kMaxPoolsPerLaunchHost);
   if (!pools[0]) return fail(KV_EINVAL, "null pool");
   int rc = check_same_device(n_pools, pools);
   if (rc) return rc;
-  const bool whole = allow_split && !legacy_task_sizing();
-  long long dirty = 0;  // only the legacy task sizing needs it before building
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = pools[k];
     if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
@@ -1094,15 +1015,20 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     if (step == 0 || step <= p->last_step)
       return fail(KV_EINVAL, "step %llu not > last step %llu of pool %d",
                   (unsigned long long)step, (unsigned long long)p->last_step, p->node_id);
-    if (!whole)
-      for (int s = 0; s < p->slot_hi; ++s)
-        if (p->slot_req[s] >= 0) dirty += pub_hi(p, s) - p->pub_len[s];
   }
+  return KV_OK;
+}
+
+// Host-task publication (shared-capacity links: the replica's block ids come from
+// the holder's allocator; the copy-engine variant): the host builds the dirty work
+// list (build_dirty_tasks); state is committed by commit_replicate once enqueued.
+int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch &L,
+                      bool use_ce) {
+  int rc = validate_replicate(n_pools, pools, step);
+  if (rc) return rc;
   L.reset(kKindRingPut, n_pools);
   L.p0 = pools[0];
   L.use_ce = use_ce;
-  const int task_segs =
-      whole ? whole_item_segs(L.p0) : choose_task_segs(L.p0, dirty * L.p0->combos);
   size_t toff = 0;
   for (int k = 0; k < n_pools; ++k) toff += 12 * (size_t)pools[k]->R;
   L.tables.resize(toff);
@@ -1110,15 +1036,24 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
   for (int k = 0; k < n_pools; ++k) {
     kv_pool *p = pools[k];
     const size_t before = L.tasks.size();
-    L.bytes[k] = build_dirty_tasks(p, (int16_t)k, L.tasks, false, nullptr, task_segs,
+    L.bytes[k] = build_dirty_tasks(p, (int16_t)k, L.tasks, false, nullptr, p->task_segs,
                                    use_ce ? &L.ce_blocks[k] : nullptr);
     if (L.tasks.size() == before) push_publish_only(L.tasks, (int16_t)k);
     L.tasks[before].flags |= kPoolFirst;
     L.ntask[k] = (int)(L.tasks.size() - before);
-    const bool aborting = p->abort_after >= 0 && p->abort_after < L.ntask[k];
-    if (aborting) {  // fault injection: partial step, never published
-      L.tasks.resize(before + p->abort_after);
-      L.ntask[k] = p->abort_after;
+    const bool aborting = p->abort_slices >= 0;  // a stage dying mid-step: never published
+    if (aborting) {
+      // the first abort_slices slices of the step (task order) are copied
+      long long left = p->abort_slices;
+      size_t keep = before;
+      while (keep < L.tasks.size() && left > 0) {
+        KvTask &t = L.tasks[keep];
+        if (t.seg_count > left) t.seg_count = (int32_t)left;
+        left -= t.seg_count;
+        ++keep;
+      }
+      L.tasks.resize(keep);
+      L.ntask[k] = (int)(keep - before);
     }
     L.table_off[k] = toff;
     fill_pub_table(p, L.tables.data() + toff);
@@ -1130,160 +1065,93 @@ int prepare_replicate(int n_pools, kv_pool *const *pools, uint64_t step, Launch 
     pp.src_bytes = (unsigned long long)p->NB * p->block_bytes;
     pp.dst_bytes = (unsigned long long)p->succ_replica_blocks * p->block_bytes;
     pp.counter = p->counter;
-    pp.target = aborting || p->abort_after >= 0 ? ~0ull : 0ull;  // + units, set below
+    pp.target = aborting ? ~0ull : p->issued + (unsigned long long)L.ntask[k];
     pp.step = step;
     pp.max_reqs = p->R;
     pp.max_blk = p->M;
-    pp.n_table = p->R;  // staged tables carry every slot (inline launches trim them)
+    pp.n_table = p->R;
     pp.writer_node = p->node_id;
-    pp.publish = 1;
-    // KVRING_DEBUG_GPU_SCOPE=1 (experiments only: measures the cost of the system-scope
-    // publication; a remote reader could then see seq before the data)
-    static const bool dbg_gpu_scope = getenv("KVRING_DEBUG_GPU_SCOPE") != nullptr;
-    pp.sys_scope = p->succ_sys && !dbg_gpu_scope ? 1 : 0;
-    static const int sys_per_cta = getenv("KVRING_SYS_PER_CTA") ? 1 : 0;  // experiments
-    pp.pad0 = sys_per_cta;
+    pp.publish = aborting ? 0 : 1;
+    pp.sys_scope = p->succ_sys ? 1 : 0;
   }
-  collect_inval(L, pools, n_pools);
-  if (whole) L.split = choose_split(L.p0, L.tasks.size());
-  for (int k = 0; k < n_pools; ++k)  // the counter counts CTA units: tasks x split
-    if (L.params[k].target == 0ull)
-      L.params[k].target = pools[k]->issued + (unsigned long long)L.ntask[k] * L.split;
-  static const bool dbg_nocopy = getenv("KVRING_DEBUG_RINGPUT_NOCOPY") != nullptr;
-  if (dbg_nocopy)  // experiment knob: publication only (timing breakdown, breaks parity)
-    for (size_t i = 0; i < L.tasks.size(); ++i) L.tasks[i].seg_count = 0;
+  collect_inval(L.inval, L.max_reqs_inval, pools, n_pools);
   return KV_OK;
 }
 
+// Publication state after an enqueued host-task replicate (aborted pools publish
+// nothing: their host state stays at the previous publication).
 void commit_replicate(Launch &L, kv_pool *const *pools, uint64_t step) {
   for (int k = 0; k < L.n_pools; ++k) {
     kv_pool *p = pools[k];
-    p->issued += (unsigned long long)L.ntask[k] * L.split;
-    p->last_step_bytes = L.bytes[k];
-    p->bytes_replicated += L.bytes[k];
+    p->issued += (unsigned long long)L.ntask[k];
     p->tasks_launched += L.ntask[k];
-    commit_pub_len(p);
-    p->last_step = step;
-    p->abort_after = -1;
-  }
-}
-
-// Copies host-resident append sources into one device staging buffer (data,
-// not descriptors) and points the launch at it.
-int stage_host_sources(DeviceCtx *ctx, Launch &L, cudaStream_t st, StageBuf **out) {
-  *out = nullptr;
-  size_t total = 0;
-  for (int k = 0; k < L.n_pools; ++k) {
-    if (!L.host_src_bytes[k]) continue;
-    // pinned (page-locked, hence mapped under UVA) host memory: the append kernel reads
-    // it directly over PCIe -- no staging copy and no staging buffer to grow
-    cudaPointerAttributes at;
-    void *dptr = nullptr;
-    if (cudaPointerGetAttributes(&at, L.host_src[k]) == cudaSuccess &&
-        at.type == cudaMemoryTypeHost &&
-        cudaHostGetDevicePointer(&dptr, const_cast<void *>(L.host_src[k]), 0) == cudaSuccess &&
-        dptr) {
-      L.params[k].src = static_cast<const char *>(dptr);
-      L.host_src_bytes[k] = 0;
+    if (p->abort_slices >= 0) {
+      p->abort_slices = -1;
       continue;
     }
-    cudaGetLastError();
-    total += L.host_src_bytes[k];
+    p->last_step_bytes = L.bytes[k];
+    p->bytes_replicated += L.bytes[k];
+    commit_pub_len(p);
+    p->last_step = step;
   }
-  if (total == 0) return KV_OK;
-  StageBuf *sb = nullptr;
-  int rc = ctx->acquire(ctx->src, ctx->next_src, total, false, &sb);
-  if (rc) return rc;
-  size_t off = 0;
-  for (int k = 0; k < L.n_pools; ++k) {
-    if (!L.host_src_bytes[k]) continue;
-    CU(cudaMemcpyAsync(sb->dev + off, L.host_src[k], L.host_src_bytes[k], cudaMemcpyHostToDevice,
-                       st));
-    L.params[k].src = sb->dev + off;
-    off += L.host_src_bytes[k];
-  }
-  *out = sb;
-  return KV_OK;
 }
 
-// Stages the descriptors of up to two launches with ONE pinned H2D copy (launches that
-// do not carry them inline in the kernel parameter space).
-int stage(DeviceCtx *ctx, Launch *const *ls, int nl, cudaStream_t st, StageBuf **out) {
-  size_t total = 0;
-  for (int i = 0; i < nl; ++i) total += align16(ls[i]->staged_bytes());
+// Stages the descriptors of a host-task launch with ONE pinned H2D copy.
+int stage(DeviceCtx *ctx, Launch &L, cudaStream_t st, StageBuf **out) {
   StageBuf *b = nullptr;
-  const double ta = now_s();
-  int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
+  const double t0 = now_s();
+  int rc = ctx->acquire(ctx->ring, ctx->next, L.staged_bytes(), true, &b);
   if (rc) return rc;
-  const double tb = now_s();
-  phase_add(kPhAcquire, tb - ta);
-  size_t off = 0;
-  for (int i = 0; i < nl; ++i) {
-    Launch &L = *ls[i];
-    const size_t pbytes = align16(sizeof(KvPoolParams) * L.n_pools);
-    const size_t tbl = align16(L.tables.size());
-    char *h = b->host + off;
-    char *d = b->dev + off;
-    for (int k = 0; k < L.n_pools; ++k) {
-      if (L.kind == kKindRingPut) {
-        const size_t o = pbytes + L.table_off[k];
-        L.params[k].slot_req = reinterpret_cast<const int64_t *>(d + o);
-        L.params[k].slot_len = reinterpret_cast<const int32_t *>(d + o + 8 * (size_t)L.params[k].max_reqs);
-      }
+  const size_t pbytes = align16(sizeof(KvPoolParams) * L.n_pools);
+  const size_t tbl = align16(L.tables.size());
+  char *h = b->host;
+  char *d = b->dev;
+  for (int k = 0; k < L.n_pools; ++k) {
+    if (L.kind == kKindRingPut) {
+      const size_t o = pbytes + L.table_off[k];
+      L.params[k].slot_req = reinterpret_cast<const int64_t *>(d + o);
+      L.params[k].slot_len = reinterpret_cast<const int32_t *>(d + o + 8 * (size_t)L.params[k].max_reqs);
     }
-    std::memcpy(h, L.params.data(), sizeof(KvPoolParams) * L.n_pools);
-    if (!L.tables.empty()) std::memcpy(h + pbytes, L.tables.data(), L.tables.size());
-    std::memcpy(h + pbytes + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
-    L.params_dev = reinterpret_cast<const KvPoolParams *>(d);
-    L.tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
-    off += align16(L.staged_bytes());
   }
-  const double tc = now_s();
-  phase_add(kPhHostCopy, tc - tb);
-  CU(cudaMemcpyAsync(b->dev, b->host, total, cudaMemcpyHostToDevice, st));
-  phase_add(kPhH2DCall, now_s() - tc);
+  std::memcpy(h, L.params.data(), sizeof(KvPoolParams) * L.n_pools);
+  if (!L.tables.empty()) std::memcpy(h + pbytes, L.tables.data(), L.tables.size());
+  std::memcpy(h + pbytes + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
+  L.params_dev = reinterpret_cast<const KvPoolParams *>(d);
+  L.tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
+  CU(cudaMemcpyAsync(b->dev, b->host, L.staged_bytes(), cudaMemcpyHostToDevice, st));
+  phase_add(kPhStage, now_s() - t0);
   *out = b;
   return KV_OK;
 }
 
-// Grid of a copy launch: one CTA per task up to the resident CTA count (capping the
-// append's grid so the concurrent ring-put finds free CTA slots was measured: no
-// gain, profiles/r01/exp25.log).
-int launch_grid(const Launch &L) {
-  return copy_grid(L.p0->device, (int)L.tasks.size() * L.split);
-}
-
 // Shared capacity: withdraw the freed replicas' published entries (req_id -1,
-// len 0 in the published parity) before this launch may reuse their blocks.
-int flush_inval(Launch &L, cudaStream_t st) {
-  for (const auto &iv : L.inval) {
-    const int R = L.max_reqs_inval;
+// len 0 in the published parity) before a launch may reuse their blocks.
+int flush_inval(std::vector<kv_pool::Inval> &inval, int R, cudaStream_t st) {
+  for (const auto &iv : inval) {
     CU(cudaMemsetAsync(iv.meta + 32 + ((size_t)iv.par * R + iv.slot) * 8, 0xFF, 8, st));
     CU(cudaMemsetAsync(iv.meta + meta_off_len(R) + ((size_t)iv.par * R + iv.slot) * 4, 0, 4, st));
   }
-  L.inval.clear();
+  inval.clear();
   return KV_OK;
 }
 
 int enqueue(Launch &L, cudaStream_t st) {
   if (!L.inval.empty() && L.p0 && L.p0->device >= 0) {
-    int rc = flush_inval(L, st);
+    int rc = flush_inval(L.inval, L.max_reqs_inval, st);
     if (rc) return rc;
   }
   if (L.tasks.empty()) return KV_OK;
   CU(timed_launch(L.kind, L.tasks_dev, (int)L.tasks.size(), L.params_dev, L.n_pools,
-                  L.p0->geom_dev(), launch_grid(L), st, L.params.data(), L.split));
-  phase_add(kPhStagedLaunches, 1.0);
+                  L.p0->geom_dev(), copy_grid(L.p0->device, (int)L.tasks.size()), st));
   g_launches++;
   L.p0->kernels++;
   return KV_OK;
 }
 
-thread_local Launch g_append_launch, g_repl_launch;
-
 // Copy-engine runs of the full blocks of a ring-put launch (consecutive block ids
-// coalesced; the replica mirrors block ids, R5), issued before the kernel on the
-// same stream: the kernel's publication is stream-ordered after them.
+// coalesced into ONE cudaMemcpyAsync each; the replica mirrors block ids, R5), issued
+// before the kernel on the same stream: the kernel's publication is stream-ordered
+// after them.
 int issue_ce_copies(Launch &L, kv_pool *const *pools, cudaStream_t st) {
   for (int k = 0; k < L.n_pools; ++k) {
     std::vector<int> &v = L.ce_blocks[k];
@@ -1303,9 +1171,9 @@ int issue_ce_copies(Launch &L, kv_pool *const *pools, cudaStream_t st) {
   return KV_OK;
 }
 
-int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st,
-                   bool use_ce = false) {
-  Launch &L = g_repl_launch;
+int replicate_host_tasks(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream_t st,
+                         bool use_ce) {
+  thread_local Launch L;
   int rc = prepare_replicate(n_pools, pools, step, L, use_ce);
   if (rc) return rc;
   if (L.p0->device < 0) {  // tables only
@@ -1317,8 +1185,7 @@ int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream
   DeviceCtx *ctx = ctx_for(L.p0->device);
   std::lock_guard<std::mutex> lk(ctx->mu);
   StageBuf *b = nullptr;
-  Launch *ls[1] = {&L};
-  rc = stage(ctx, ls, 1, st, &b);
+  rc = stage(ctx, L, st, &b);
   if (rc) return rc;
   if (use_ce && (rc = issue_ce_copies(L, pools, st))) return rc;
   rc = enqueue(L, st);
@@ -1327,33 +1194,359 @@ int replicate_impl(int n_pools, kv_pool *const *pools, uint64_t step, cudaStream
   return ctx->done(b, st);
 }
 
+// ---- decode-step engine launches (kvring_step.cu) --------------------------------
+// One StepLaunch = one kernel: the appends of a step (items from the host allocator)
+// and/or a publication whose work list the device derives from per-slot snapshots.
+struct StepLaunch {
+  KvStepHdr h{};
+  int device = -1;
+  kv_pool *app_pool[kStepPools] = {};
+  kv_pool *rep_pool[kStepPools] = {};
+  std::vector<KvAppItem> items;
+  std::vector<int64_t> req;          // replicate snapshots, entry-major (pool, slot)
+  std::vector<int32_t> len, pub;
+  std::vector<char> blob;
+  const void *host_src[kStepPools] = {};  // KV_SRC_HOST sources
+  size_t host_src_bytes[kStepPools] = {};
+  uint64_t app_bytes = 0, rep_bytes = 0;
+  uint64_t rep_pool_bytes[kStepPools] = {};
+  uint64_t rep_step = 0;
+  std::vector<kv_pool::Inval> inval;
+  int max_reqs_inval = 0;
+  void reset() {
+    h = KvStepHdr{};
+    device = -1;
+    for (int i = 0; i < kStepPools; ++i) {
+      app_pool[i] = rep_pool[i] = nullptr;
+      host_src[i] = nullptr;
+      host_src_bytes[i] = 0;
+      rep_pool_bytes[i] = 0;
+    }
+    items.clear();
+    req.clear();
+    len.clear();
+    pub.clear();
+    app_bytes = rep_bytes = 0;
+    rep_step = 0;
+    inval.clear();
+  }
+  bool empty() const { return h.n_app == 0 && h.n_rep == 0; }
+};
+
+void set_geom(StepLaunch &S, const kv_pool *p) {
+  if (S.device >= 0 || S.h.n_app + S.h.n_rep > 0) return;
+  S.device = p->device;
+  S.h.g = p->geom_dev();
+  S.h.div_sl = kv_div((uint32_t)p->combos);
+  S.h.div_b = kv_div((uint32_t)p->g.block_size);
+}
+
+// Appends a pool's items (do_append) to the launch.  Item slices are token-major:
+// the launch's append space is the concatenation of every item's n_tok x combos.
+void step_add_append(StepLaunch &S, kv_pool *p, const kv_append_args_t &a) {
+  set_geom(S, p);
+  const int q = S.h.n_app++;
+  S.app_pool[q] = p;
+  KvStepPool &pp = S.h.app[q];
+  pp.src = static_cast<const char *>(a.src_kv);
+  pp.dst = p->pool;
+  pp.bt = p->d_bt;
+  pp.R = p->R;
+  pp.M = p->M;
+  pp.abort_slices = -1;
+  long long rows = do_append(p, a, (int16_t)q, S.items, S.h.app_slices);
+  S.app_bytes += (uint64_t)rows * p->token_bytes;
+  if ((a.flags & KV_SRC_HOST) && rows > 0) {
+    S.host_src[q] = a.src_kv;
+    S.host_src_bytes[q] = (size_t)rows * p->token_bytes;
+  }
+}
+
+// Snapshots a pool's publication (tables as they are now) into the launch and
+// commits it on the host: pub_len := the published length of every live slot.
+// The device derives the same dirty ranges from the snapshot (reading R2).
+void step_add_replicate(StepLaunch &S, kv_pool *p, uint64_t step) {
+  set_geom(S, p);
+  const int q = S.h.n_rep++;
+  S.rep_pool[q] = p;
+  S.rep_step = step;
+  KvStepPool &pp = S.h.rep[q];
+  pp.src = p->pool;
+  pp.dst = p->succ_replica;
+  pp.meta = p->succ_meta;
+  pp.bt = p->d_bt;
+  pp.step = step;
+  pp.R = p->R;
+  pp.M = p->M;
+  pp.n_slots = p->slot_hi;
+  pp.ent_off = S.h.n_ent;
+  pp.mode = p->repl_mode;
+  pp.abort_slices = p->abort_slices;
+  pp.writer_node = p->node_id;
+  pp.sys = p->succ_sys ? 1 : 0;
+  S.h.n_ent += p->slot_hi;
+  S.req.insert(S.req.end(), p->slot_req.begin(), p->slot_req.begin() + p->slot_hi);
+  S.len.insert(S.len.end(), p->slot_len.begin(), p->slot_len.begin() + p->slot_hi);
+  S.pub.insert(S.pub.end(), p->pub_len.begin(), p->pub_len.begin() + p->slot_hi);
+  uint64_t bytes = 0;
+  for (int s = 0; s < p->slot_hi; ++s)
+    if (p->slot_req[s] >= 0) bytes += (uint64_t)(pub_hi(p, s) - p->pub_len[s]);
+  bytes *= (uint64_t)p->token_bytes;
+  if (pp.abort_slices >= 0) {  // a stage dying mid-step: partial copy, never published
+    const uint64_t cut = (uint64_t)pp.abort_slices * (uint64_t)p->seg_bytes;
+    S.rep_pool_bytes[q] = 0;
+    S.rep_bytes += std::min(bytes, cut);
+    p->abort_slices = -1;
+  } else {
+    S.h.publish = 1;
+    S.h.sys_any |= pp.sys;
+    S.rep_pool_bytes[q] = bytes;
+    S.rep_bytes += bytes;
+    p->last_step_bytes = bytes;
+    p->bytes_replicated += bytes;
+    commit_pub_len(p);
+    p->last_step = step;
+  }
+  if (pp.abort_slices >= 0) S.h.any_abort = 1;
+}
+
+// Prepares the publication part: validation, then snapshot + commit of each pool.
+int step_prepare_replicate(StepLaunch &S, int n_pools, kv_pool *const *pools, uint64_t step) {
+  int rc = validate_replicate(n_pools, pools, step);
+  if (rc) return rc;
+  if (S.h.n_app > 0 && S.device != pools[0]->device)
+    return fail(KV_EINVAL, "append and publication of one launch must share a device");
+  long long ent = S.h.n_ent;
+  for (int k = 0; k < n_pools; ++k) {
+    if (pools[k]->holder) return fail(KV_EINVAL, "shared-capacity links publish through the host-task path");
+    ent += pools[k]->slot_hi;
+  }
+  if (S.h.n_rep + n_pools > kStepPools || ent > kStepMaxEnt)
+    return fail(KV_EINVAL, "too many pools / slots for one launch (%d pools, %lld slots)",
+                S.h.n_rep + n_pools, ent);
+  for (int k = 0; k < n_pools; ++k) step_add_replicate(S, pools[k], step);
+  return KV_OK;
+}
+
+// Validates every pool of an append (all-or-nothing: nothing changes on error).
+int validate_appends(int n_pools, const kv_append_args_t *args) {
+  if (n_pools <= 0 || !args) return fail(KV_EINVAL, "no pools");
+  if (n_pools > kMaxPoolsPerLaunchHost)
+    return fail(KV_EINVAL, "at most %d pools per append", kMaxPoolsPerLaunchHost);
+  kv_pool *pools[kMaxPoolsPerLaunchHost];
+  for (int k = 0; k < n_pools; ++k) pools[k] = args[k].pool;
+  if (!pools[0]) return fail(KV_EINVAL, "null pool");
+  int rc = check_same_device(n_pools, pools);
+  if (rc) return rc;
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k];
+    if (p->dead) return fail(KV_ESTATE, "pool %d is dead", p->node_id);
+    const bool bs = args[k].begin_step != 0;  // validation sees the released quarantine
+    rc = append_validate(p, args[k],
+                         p->free_blocks.size() + (bs ? (long long)p->q_blocks.size() : 0),
+                         p->free_slots.size() + (bs ? (long long)p->q_slots.size() : 0));
+    if (rc) return rc;
+    long long rows = 0;
+    for (int i = 0; i < args[k].n; ++i) rows += args[k].n_new[i];
+    if (p->device >= 0 && rows > 0 && !args[k].src_kv)
+      return fail(KV_EINVAL, "null src_kv with tokens to append");
+    if (rows * p->combos > (long long)INT32_MAX / 4)
+      return fail(KV_EINVAL, "append too large for one launch");
+  }
+  return KV_OK;
+}
+
+// Applies begin_step / releases / appends of <= kStepPools validated pools to the
+// host tables, building the launch's append items.
+void apply_appends(StepLaunch &S, int n_pools, const kv_append_args_t *args) {
+  kv_pool *pools[kStepPools];
+  for (int k = 0; k < n_pools; ++k) {
+    kv_pool *p = pools[k] = args[k].pool;
+    if (args[k].begin_step) do_begin_step(p);
+    do_release(p, args[k].n_release, args[k].release_ids);
+    if (p->scratch_need > p->free_blocks.size()) evict_for(p, p->scratch_need);
+    step_add_append(S, p, args[k]);
+  }
+  collect_inval(S.inval, S.max_reqs_inval, pools, n_pools);
+}
+
+// Pinned host sources are read by the kernel over PCIe (zero copy); pageable ones
+// are copied into a staging buffer in stream order.
+int step_stage_host_sources(DeviceCtx *ctx, StepLaunch &S, cudaStream_t st, StageBuf **out) {
+  *out = nullptr;
+  size_t total = 0;
+  for (int k = 0; k < S.h.n_app; ++k) {
+    if (!S.host_src_bytes[k]) continue;
+    cudaPointerAttributes at;
+    void *dptr = nullptr;
+    if (cudaPointerGetAttributes(&at, S.host_src[k]) == cudaSuccess &&
+        at.type == cudaMemoryTypeHost &&
+        cudaHostGetDevicePointer(&dptr, const_cast<void *>(S.host_src[k]), 0) == cudaSuccess &&
+        dptr) {
+      S.h.app[k].src = static_cast<const char *>(dptr);
+      S.host_src_bytes[k] = 0;
+      continue;
+    }
+    cudaGetLastError();
+    total += S.host_src_bytes[k];
+  }
+  if (total == 0) return KV_OK;
+  StageBuf *sb = nullptr;
+  int rc = ctx->acquire(ctx->src, ctx->next_src, total, false, &sb);
+  if (rc) return rc;
+  size_t off = 0;
+  for (int k = 0; k < S.h.n_app; ++k) {
+    if (!S.host_src_bytes[k]) continue;
+    CU(cudaMemcpyAsync(sb->dev + off, S.host_src[k], S.host_src_bytes[k], cudaMemcpyHostToDevice,
+                       st));
+    S.h.app[k].src = sb->dev + off;
+    off += S.host_src_bytes[k];
+  }
+  *out = sb;
+  return KV_OK;
+}
+
+// Per-launch record (kv_launch_log): bytes and grid of every decode-step launch.
+struct LaunchRec {
+  uint64_t kind, app_bytes, rep_bytes, grid, blob_bytes;
+};
+thread_local bool g_log_on = false;
+thread_local std::vector<LaunchRec> g_log;
+
+constexpr size_t kItemsPerLaunch = 2048;  // 48 KiB of append items per launch
+
+// Packs one launch's descriptor blob -- append items [i0, i1) and, if `with_rep`, the
+// publication part -- then launches (data inline in the parameter space when it fits,
+// else one H2D of the blob first).  Events of kv_time_next_launch honoured.
+int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCtx *ctx,
+                    cudaStream_t st) {
+  const double t0 = now_s();
+  KvStepHdr h = S.h;
+  if (!with_rep) {
+    h.n_rep = 0;
+    h.n_ent = 0;
+    h.publish = 0;
+    h.any_abort = 0;
+    h.sys_any = 0;
+  }
+  const int32_t base = i0 < S.items.size() ? S.items[i0].off : 0;
+  h.n_items = (int32_t)(i1 - i0);
+  h.app_slices = i1 < S.items.size() ? S.items[i1].off - base : S.h.app_slices - base;
+  if (h.n_items == 0) h.app_slices = 0;
+  const size_t nent = with_rep ? S.req.size() : 0;
+  size_t off = 0;
+  h.items_off = 0;
+  off = align16(sizeof(KvAppItem) * h.n_items);
+  h.req_off = (int32_t)off;
+  off += align16(8 * nent);
+  h.len_off = (int32_t)off;
+  off += align16(4 * nent);
+  h.pub_off = (int32_t)off;
+  off += align16(4 * nent);
+  h.data_bytes = (int32_t)off;
+  S.blob.resize(off);
+  char *b = S.blob.data();
+  if (h.n_items > 0) {
+    KvAppItem *it = reinterpret_cast<KvAppItem *>(b);
+    std::memcpy(it, S.items.data() + i0, sizeof(KvAppItem) * h.n_items);
+    if (base)
+      for (int k = 0; k < h.n_items; ++k) it[k].off -= base;
+  }
+  if (nent) {
+    std::memcpy(b + h.req_off, S.req.data(), 8 * nent);
+    std::memcpy(b + h.len_off, S.len.data(), 4 * nent);
+    std::memcpy(b + h.pub_off, S.pub.data(), 4 * nent);
+  }
+  if (h.publish) h.counter = S.rep_pool[0]->step_counter;
+  // grid: every resident CTA once the launch moves >= one round (256 x 6 chunks) per CTA
+  const uint64_t rep_slices = with_rep ? S.rep_bytes / (uint64_t)h.g.seg_bytes : 0;
+  const unsigned long long chunks = ((unsigned long long)h.app_slices + rep_slices)
+                                    << h.g.cps_shift;
+  const int cap = resident_ctas(S.device);
+  int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + 1535) / 1536));
+  StageBuf *db = nullptr;
+  const char *gdata = nullptr;
+  int rc = KV_OK;
+  if (h.data_bytes > kStepInline) {
+    if ((rc = ctx->acquire(ctx->ring, ctx->next, (size_t)h.data_bytes, true, &db))) return rc;
+    std::memcpy(db->host, b, (size_t)h.data_bytes);
+    CU(cudaMemcpyAsync(db->dev, db->host, (size_t)h.data_bytes, cudaMemcpyHostToDevice, st));
+    gdata = db->dev;
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_fn(), 256,
+                                                      step_smem_bytes(h)) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    cudaGetLastError();
+    grid = std::min(grid, per_sm * (cap / 4));
+  }
+  const double t1 = now_s();
+  phase_add(kPhStage, t1 - t0);
+  CU(launch_step(h, b, gdata, grid, st));
+  phase_add(kPhLaunch, now_s() - t1);
+  g_launches++;
+  if (g_log_on) {
+    uint64_t app = 0;  // payload bytes of this launch's items
+    app = (uint64_t)h.app_slices * (uint64_t)h.g.seg_bytes;
+    g_log.push_back({(uint64_t)((h.n_items > 0) | ((with_rep && h.n_rep > 0) << 1)), app,
+                     with_rep ? S.rep_bytes : 0, (uint64_t)grid, (uint64_t)h.data_bytes});
+  }
+  if (db && (rc = ctx->done(db, st))) return rc;
+  return KV_OK;
+}
+
+// Launches a prepared StepLaunch: one kernel (more only when the appends carry more
+// than kItemsPerLaunch items, e.g. a 32k-token prefill; the publication rides on the
+// first).
+int step_enqueue(StepLaunch &S, cudaStream_t st) {
+  if (S.empty() || S.device < 0) return KV_OK;
+  DeviceGuard dg(S.device);
+  if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", S.device);
+  if (!S.inval.empty()) {
+    int rc = flush_inval(S.inval, S.max_reqs_inval, st);
+    if (rc) return rc;
+  }
+  DeviceCtx *ctx = ctx_for(S.device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  StageBuf *sb = nullptr;
+  int rc = step_stage_host_sources(ctx, S, st, &sb);
+  if (rc) return rc;
+  cudaEvent_t eb = g_ev_before, ea = g_ev_after;
+  g_ev_before = g_ev_after = nullptr;
+  if (eb) CU(cudaEventRecord(eb, st));
+  const size_t n = S.items.size();
+  size_t i0 = 0;
+  bool first = true;
+  do {
+    const size_t i1 = std::min(n, i0 + kItemsPerLaunch);
+    if ((rc = step_launch_one(S, i0, i1, first, ctx, st))) return rc;
+    first = false;
+    i0 = i1;
+  } while (i0 < n);
+  if (ea) CU(cudaEventRecord(ea, st));
+  for (int q = 0; q < S.h.n_app; ++q) S.app_pool[q]->kernels++;
+  for (int q = 0; q < S.h.n_rep; ++q)
+    if (S.h.n_app == 0 || S.rep_pool[q] != S.app_pool[0]) S.rep_pool[q]->kernels++;
+  if (sb && (rc = ctx->done(sb, st))) return rc;  // the staged source outlives the kernel
+  return KV_OK;
+}
+
 }  // namespace
 
 KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream) {
-  Launch &L = g_append_launch;
-  int rc = prepare_append(n_pools, args, L);
+  thread_local StepLaunch S;
+  const double t0 = now_s();
+  int rc = validate_appends(n_pools, args);
+  phase_add(kPhPrepAppend, now_s() - t0);
   if (rc) return rc;
-  if (L.p0->device < 0) return KV_OK;
-  if (L.tasks.empty()) {
-    if (L.inval.empty()) return KV_OK;
-    DeviceGuard dg(L.p0->device);
-    return flush_inval(L, static_cast<cudaStream_t>(stream));
+  for (int k0 = 0; k0 < n_pools; k0 += kStepPools) {  // one launch per <= 8 pools
+    S.reset();
+    const double t1 = now_s();
+    apply_appends(S, std::min(kStepPools, n_pools - k0), args + k0);
+    phase_add(kPhPrepAppend, now_s() - t1);
+    if (S.device >= 0 && (rc = step_enqueue(S, static_cast<cudaStream_t>(stream)))) return rc;
   }
-  DeviceGuard dg(L.p0->device);
-  if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice failed");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DeviceCtx *ctx = ctx_for(L.p0->device);
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  StageBuf *sb = nullptr, *b = nullptr;
-  rc = stage_host_sources(ctx, L, st, &sb);
-  if (rc) return rc;
-  Launch *ls[1] = {&L};
-  rc = stage(ctx, ls, 1, st, &b);
-  if (rc) return rc;
-  rc = enqueue(L, st);
-  if (rc) return rc;
-  if (sb && (rc = ctx->done(sb, st))) return rc;  // the staged source outlives the kernel
-  return ctx->done(b, st);
+  return KV_OK;
 }
 
 KV_API int kv_append(kv_pool_t *p, int32_t n, const int64_t *req_ids, const int32_t *n_new,
@@ -1368,18 +1561,46 @@ KV_API int kv_append(kv_pool_t *p, int32_t n, const int64_t *req_ids, const int3
   return kv_append_multi(1, &a, stream);
 }
 
+namespace {
+// Publication of several pools of one device: the device-derived step engine for
+// plain links, the host-task ring-put for shared-capacity links (one launch each).
+int replicate_any(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, cudaStream_t st) {
+  int rc = validate_replicate(n_pools, pools, step);
+  if (rc) return rc;
+  kv_pool *plain[kMaxPoolsPerLaunchHost], *shared[kMaxPoolsPerLaunchHost];
+  int np = 0, ns = 0;
+  for (int k = 0; k < n_pools; ++k) (pools[k]->holder ? shared[ns++] : plain[np++]) = pools[k];
+  if (ns > 0 && (rc = replicate_host_tasks(ns, shared, step, st, false))) return rc;
+  thread_local StepLaunch S;
+  for (int k0 = 0; k0 < np;) {  // launches of <= kStepPools pools / kStepMaxEnt slots
+    S.reset();
+    int k1 = k0;
+    long long ent = 0;
+    while (k1 < np && k1 - k0 < kStepPools && ent + plain[k1]->slot_hi <= kStepMaxEnt)
+      ent += plain[k1++]->slot_hi;
+    if (k1 == k0) return fail(KV_EINVAL, "pool %d has too many slots for one launch", plain[k0]->node_id);
+    const double t0 = now_s();
+    if ((rc = step_prepare_replicate(S, k1 - k0, plain + k0, step))) return rc;
+    phase_add(kPhPrepRepl, now_s() - t0);
+    if (S.device >= 0 && (rc = step_enqueue(S, st))) return rc;
+    k0 = k1;
+  }
+  return KV_OK;
+}
+}  // namespace
+
 KV_API int kv_replicate_step(kv_pool_t *p, uint64_t step, void *stream) {
-  return replicate_impl(1, &p, step, static_cast<cudaStream_t>(stream));
+  return replicate_any(1, &p, step, static_cast<cudaStream_t>(stream));
 }
 
 KV_API int kv_replicate_step_multi(int32_t n_pools, kv_pool_t *const *pools, uint64_t step,
                                    void *stream) {
-  return replicate_impl(n_pools, pools, step, static_cast<cudaStream_t>(stream));
+  return replicate_any(n_pools, pools, step, static_cast<cudaStream_t>(stream));
 }
 
 KV_API int kv_replicate_step_ce(int32_t n_pools, kv_pool_t *const *pools, uint64_t step,
                                 void *stream) {
-  return replicate_impl(n_pools, pools, step, static_cast<cudaStream_t>(stream), true);
+  return replicate_host_tasks(n_pools, pools, step, static_cast<cudaStream_t>(stream), true);
 }
 
 KV_API int kv_set_mode(kv_pool_t *p, int32_t mode) {
@@ -1391,9 +1612,9 @@ KV_API int kv_set_mode(kv_pool_t *p, int32_t mode) {
   return KV_OK;
 }
 
-KV_API int kv_inject_abort(kv_pool_t *p, int32_t tasks) {
+KV_API int kv_inject_abort(kv_pool_t *p, int32_t slices) {
   if (!p) return fail(KV_EINVAL, "null pool");
-  p->abort_after = tasks < 0 ? -1 : tasks;
+  p->abort_slices = slices < 0 ? -1 : slices;
   return KV_OK;
 }
 
@@ -1421,12 +1642,32 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
   DeviceGuard dg(dst->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int R = dst->R, M = dst->M, B = dst->g.block_size;
-  // 1. acquire the holder's seq and the parity metadata (synchronous read).
+  {  // a holder on another GPU of this process: the kernels read it over NVLink
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, holder_meta) == cudaSuccess &&
+        at.type == cudaMemoryTypeDevice && at.device != dst->device) {
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, dst->device, at.device) == cudaSuccess && can)
+        cudaDeviceEnablePeerAccess(at.device, 0);  // already enabled: harmless error
+    }
+    cudaGetLastError();
+  }
+  // 1. acquire the holder's seq and the parity metadata (reading R9, reader side): a
+  //    kernel loads seq with ld.acquire.sys, fences, then copies header + tables into a
+  //    device scratch that is read back -- first the 32-B header (shape check), then
+  //    the whole region.  Synchronous: restore needs the tables on the host.
   std::vector<char> meta(meta_bytes(R, M));
-  CU(cudaStreamSynchronize(st));
-  CU(cudaMemcpy(meta.data(), holder_meta, 32, cudaMemcpyDefault));
+  char *scratch = nullptr;
+  CU(cudaMalloc(reinterpret_cast<void **>(&scratch), meta.size()));
+  struct Free {
+    char *p;
+    ~Free() { cudaFree(p); }
+  } free_scratch{scratch};
   uint64_t seq;
   int32_t hdr[4];
+  CU(launch_meta_acquire(static_cast<const char *>(holder_meta), scratch, 32, st));
+  CU(cudaMemcpyAsync(meta.data(), scratch, 32, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
   std::memcpy(&seq, meta.data(), 8);
   std::memcpy(hdr, meta.data() + 8, 16);
   if (hdr[3] != kMetaMagic || hdr[1] != R || hdr[2] != M)
@@ -1434,7 +1675,11 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
                 hdr[2]);
   if (seq == 0 || seq == ~0ull) return fail(KV_ENOREPLICA, "holder published nothing (seq %llu)",
                                             (unsigned long long)seq);
-  CU(cudaMemcpy(meta.data(), holder_meta, meta.size(), cudaMemcpyDefault));
+  CU(launch_meta_acquire(static_cast<const char *>(holder_meta), scratch, meta.size(), st));
+  CU(cudaMemcpyAsync(meta.data(), scratch, meta.size(), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  g_launches += 2;
+  dst->kernels += 2;
   std::memcpy(&seq, meta.data(), 8);
   const int par = (int)(seq & 1);
   const int64_t *mreq = reinterpret_cast<const int64_t *>(meta.data() + 32) + (size_t)par * R;
@@ -1485,6 +1730,15 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
       push_item(tasks, 0, mbt[(size_t)e.slot * M + j], nb, -1, j, 0, valid, dst->combos,
                 dst->task_segs);
     }
+  }
+  // the device-resident block table of dst (read by the step engine's publications)
+  {
+    std::vector<int32_t> rows((size_t)R * M, -1);
+    for (int s = 0; s < dst->slot_hi; ++s)
+      for (size_t j = 0; j < dst->slot_bt[s].size(); ++j) rows[(size_t)s * M + j] = dst->slot_bt[s][j];
+    CU(cudaMemcpyAsync(dst->d_bt, rows.data(), rows.size() * sizeof(int32_t),
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));  // `rows` is pageable host memory on the stack
   }
   // 3. copy valid slots (local HBM, or NVLink reads when the holder is remote).
   if (!tasks.empty()) {
@@ -1715,83 +1969,10 @@ KV_API int kv_sync(kv_pool_t *p) {
   return KV_OK;
 }
 
+// ---- decode loops ------------------------------------------------------------------
 namespace {
 
-// Inline descriptors (KvInlineDesc): a launch whose tables + tasks fit the kernel
-// parameter space travels with the launch itself (KVRING_INLINE=0 disables).
-// Published-table entries of pool q a ring-put launch must carry: up to the last
-// slot listed (later slots publish (-1, 0), written by the kernel).
-int table_hi(const Launch &L, int q) {
-  const int R = L.params[q].max_reqs;
-  const int64_t *rq = reinterpret_cast<const int64_t *>(L.tables.data() + L.table_off[q]);
-  int hi = R;
-  while (hi > 0 && rq[hi - 1] < 0) --hi;
-  return hi;
-}
-
-size_t inline_table_bytes(const Launch &L) {
-  if (L.kind != kKindRingPut) return 0;
-  size_t b = 0;
-  for (int q = 0; q < L.n_pools; ++q) b += align16(12 * (size_t)table_hi(L, q));
-  return b;
-}
-
-bool inline_fits(const Launch &L) {
-  static const int enabled = [] {
-    const char *e = getenv("KVRING_INLINE");
-    return e ? atoi(e) : 1;
-  }();
-  return enabled && L.n_pools <= kInlinePools &&
-         inline_table_bytes(L) + sizeof(KvTask) * L.tasks.size() <= (size_t)kInlineBytes;
-}
-
-void fill_inline(const Launch &L, KvInlineDesc &d) {
-  size_t off = 0;
-  for (int q = 0; q < L.n_pools; ++q) {
-    d.pools[q] = L.params[q];
-    if (L.kind != kKindRingPut) continue;
-    const int R = L.params[q].max_reqs, hi = table_hi(L, q);
-    const char *t = L.tables.data() + L.table_off[q];
-    std::memcpy(d.data + off, t, 8 * (size_t)hi);                       // req ids
-    std::memcpy(d.data + off + 8 * (size_t)hi, t + 8 * (size_t)R, 4 * (size_t)hi);  // lens
-    d.pools[q].slot_req = reinterpret_cast<const int64_t *>(off);
-    d.pools[q].slot_len = reinterpret_cast<const int32_t *>(off + 8 * (size_t)hi);
-    d.pools[q].n_table = hi;
-    off += align16(12 * (size_t)hi);
-  }
-  d.n_tasks = (int32_t)L.tasks.size();
-  d.n_pools = L.n_pools;
-  d.task_off = (int32_t)off;
-  d.split = L.split;
-  std::memcpy(d.data + off, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
-  d.used = (int32_t)(off + sizeof(KvTask) * L.tasks.size());
-}
-
-}  // namespace
-
-// ---- decode-loop driver -------------------------------------------------------
-// For each step: appends on the compute stream, then (after an event) the
-// publication on the replication stream -- the paper's "separate CUDA stream
-// ... to overlap the communication with computation" (§3.2).
-namespace {
-
-// Host side of one decode step, prepared ahead of its CUDA calls.
-struct StepPrep {
-  Launch A, P;
-  bool has_a = false, has_p = false;
-  bool shared = false;  // a pool of this step is in shared-capacity mode (NEXT-3)
-  // inline descriptors (kernel parameter space), filled on the helper thread
-  bool inl_a = false, inl_p = false;
-  bool no_inline = false;  // the graph loop stages every step's descriptors
-  std::unique_ptr<KvInlineDesc> da, dp;
-  int rc = KV_OK;
-  std::string err;
-};
-
-// Tables, work lists and (already) committed publication state of step k.
-// Commit happens here, before the launch: the next step's dirty ranges start
-// where this one ends; a launch error is sticky and ends the run anyway.
-bool any_shared(const kv_step_t &st) {
+bool step_has_shared(const kv_step_t &st) {
   for (int i = 0; i < st.n_append; ++i) {
     const kv_pool *p = st.append[i].pool;
     if (p && (p->holder || p->rep_src)) return true;
@@ -1803,709 +1984,270 @@ bool any_shared(const kv_step_t &st) {
   return false;
 }
 
-void prepare_step(const kv_step_t &st, StepPrep &sp) {
-  sp.has_a = st.n_append > 0;
-  sp.has_p = st.n_repl > 0;
-  sp.rc = KV_OK;
-  sp.shared = any_shared(st);
-  const double t0 = now_s();
-  if (sp.has_a && (sp.rc = prepare_append(st.n_append, st.append, sp.A))) {
-    sp.err = g_err;
-    return;
-  }
-  const double t1 = now_s();
-  phase_add(kPhPrepAppend, t1 - t0);
-  if (sp.has_p) {
-    if ((sp.rc = prepare_replicate(st.n_repl, st.repl_pools, st.step, sp.P))) {
-      sp.err = g_err;
-      return;
-    }
-    const double t2 = now_s();
-    phase_add(kPhPrepRepl, t2 - t1);
-    commit_replicate(sp.P, st.repl_pools, st.step);
-    phase_add(kPhCommit, now_s() - t2);
-  }
-  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
-  if (p0 && sp.has_a && sp.has_p && sp.P.p0->device != p0->device) {
-    sp.rc = fail(KV_EINVAL, "append and publication of one step must share a device");
-    sp.err = g_err;
-    return;
-  }
-  // descriptors that fit the kernel parameter space travel with the launch (no
-  // staging copy, no H2D, no dependent descriptor load); host-source appends and
-  // large (prefill / bulk) steps are staged
-  sp.inl_a = sp.inl_p = false;
-  if (!p0 || p0->device < 0 || sp.no_inline) return;
-  bool host_src = false;
-  if (sp.has_a)
-    for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q) host_src |= sp.A.host_src_bytes[q] != 0;
-  if (sp.has_a && !host_src && !sp.A.tasks.empty() && inline_fits(sp.A)) {
-    if (!sp.da) sp.da.reset(new KvInlineDesc());
-    fill_inline(sp.A, *sp.da);
-    sp.inl_a = true;
-  }
-  if (sp.has_p && !sp.P.tasks.empty() && inline_fits(sp.P)) {
-    if (!sp.dp) sp.dp.reset(new KvInlineDesc());
-    fill_inline(sp.P, *sp.dp);
-    sp.inl_p = true;
-  }
+int step_device(const kv_step_t &st) {
+  if (st.n_append > 0 && st.append[0].pool) return st.append[0].pool->device;
+  if (st.n_repl > 0 && st.repl_pools[0]) return st.repl_pools[0]->device;
+  return -1;
 }
 
-// Launch of a prepared inline launch (events of kv_time_next_launch honoured).
-int enqueue_inline(Launch &L, const KvInlineDesc &d, cudaStream_t st, bool pdl) {
-  if (!L.inval.empty()) {
-    int rc = flush_inval(L, st);
-    if (rc) return rc;
-  }
-  if (L.tasks.empty()) return KV_OK;
-  cudaEvent_t b = g_ev_before, a = g_ev_after;
-  g_ev_before = g_ev_after = nullptr;
-  if (b) CU(cudaEventRecord(b, st));
-  CU(launch_copy_inline(L.kind, d, L.p0->geom_dev(), launch_grid(L), st, pdl));
-  phase_add(kPhInlineLaunches, 1.0);  // a count (kv_host_profile divides like the times)
-  if (a) CU(cudaEventRecord(a, st));
-  g_launches++;
-  L.p0->kernels++;
+int record(void *ev, cudaStream_t s) {
+  if (ev) CU(cudaEventRecord(static_cast<cudaEvent_t>(ev), s));
   return KV_OK;
 }
 
-// Cross-stream order of the two-stream loop: ring-put k after append k (event
-// `ready`), and append k after ring-put k-2 -- blocks a retiring request frees in
-// step k-1 are reused from step k on (quarantine, reading R7), and the ring-put
-// that last read them is k-2's, which may otherwise still lag on its stream.
+// Cross-stream order of the two-stream loop: the publication of step k after append
+// k (event `aready`), and append k after the publication of step k-2 -- blocks a
+// retiring request frees in step k-1 are reused from step k on (quarantine, reading
+// R7), and the publication that last read them is k-2's, which may otherwise still
+// lag on its stream (k-1 with shared capacity: a freed replica block is reusable at once).
 struct StreamOrder {
   static constexpr int kN = 4;
-  cudaEvent_t aready[kN] = {};  // recorded on the append stream after append k
-  cudaEvent_t rdone[kN] = {};   // recorded on the replication stream after ring-put k
+  cudaEvent_t aready[kN] = {};
+  cudaEvent_t rdone[kN] = {};
   long long astep[kN] = {-1, -1, -1, -1};
   long long rstep[kN] = {-1, -1, -1, -1};
   long long n = 0;  // steps issued on this stream pair (continues across calls)
   cudaStream_t sa = nullptr, sr = nullptr;
   int dev = -1;
-  int ensure(int device) {
-    if (dev == device) return KV_OK;
-    for (auto &e : aready)
-      if (e) cudaEventDestroy(e);
-    for (auto &e : rdone)
-      if (e) cudaEventDestroy(e);
-    for (int i = 0; i < kN; ++i) {
-      aready[i] = rdone[i] = nullptr;
-      astep[i] = rstep[i] = -1;
+  int ensure(int device, cudaStream_t a, cudaStream_t r) {
+    if (dev != device) {
+      for (auto &e : aready)
+        if (e) cudaEventDestroy(e);
+      for (auto &e : rdone)
+        if (e) cudaEventDestroy(e);
+      for (auto &e : aready) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      for (auto &e : rdone) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      dev = device;
+      sa = sr = nullptr;
     }
-    sa = sr = nullptr;
-    for (auto &e : aready) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto &e : rdone) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    dev = device;
+    if (a != sa || r != sr) {  // a new stream pair: its first append waits for repl_stream
+      for (int i = 0; i < kN; ++i) astep[i] = rstep[i] = -1;
+      n = 0;
+      sa = a;
+      sr = r;
+      CU(cudaEventRecord(rdone[0], r));
+      CU(cudaStreamWaitEvent(a, rdone[0], 0));
+    }
     return KV_OK;
   }
 };
 
-// CUDA side of one prepared step, in two halves that may run on two host threads
-// (kv_run_steps pipelines them): the append on sa (after the ring-put of step
-// k - lag, see StreamOrder), then the publication on sr (the paper's separate
-// replication stream) after an event on sa.  Inline launches need no
-// staging; a staged launch gets its own H2D on its own stream.
-int issue_append(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa,
-                 cudaStream_t sr, StreamOrder &so) {
-  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
-  if (!p0 || p0->device < 0) return KV_OK;  // nothing to launch / tables-only pools
-  DeviceGuard dg(p0->device);
-  int rc = KV_OK;
-  if (sa != sr && (rc = so.ensure(p0->device))) return rc;
-  const int N = StreamOrder::kN;
-  if (sp.has_a && (!sp.A.tasks.empty() || !sp.A.inval.empty())) {
-    DeviceCtx *ctx = ctx_for(p0->device);
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    StageBuf *sb = nullptr, *b = nullptr;
-    const double t0 = now_s();
-    if ((rc = stage_host_sources(ctx, sp.A, sa, &sb))) return rc;
-    Launch *ls[1] = {&sp.A};
-    if (!sp.inl_a && !sp.A.tasks.empty() && (rc = stage(ctx, ls, 1, sa, &b))) return rc;
-    const double t1 = now_s();
-    phase_add(kPhStage, t1 - t0);
-    // shared capacity: a freed replica block may be reused by this very append, so
-    // the ring-put that last wrote it (k-1) must be complete
-    const int lag = sp.shared ? 1 : 2;
-    if (sa != sr && k >= lag && so.rstep[(k - lag) % N] == k - lag)
-      CU(cudaStreamWaitEvent(sa, so.rdone[(k - lag) % N], 0));
-    g_ev_before = static_cast<cudaEvent_t>(st.ev_append_start);
-    g_ev_after = static_cast<cudaEvent_t>(st.ev_append_end);
-    rc = sp.inl_a ? enqueue_inline(sp.A, *sp.da, sa, false) : enqueue(sp.A, sa);
-    g_ev_before = g_ev_after = nullptr;
-    if (rc) return rc;
-    if (sb && (rc = ctx->done(sb, sa))) return rc;  // the staged source outlives the kernel
-    if (b && (rc = ctx->done(b, sa))) return rc;
-    phase_add(kPhEnqA, now_s() - t1);
-  }
-  if (sa != sr && sp.has_p) {  // the publication of step k follows this append
-    CU(cudaEventRecord(so.aready[k % N], sa));
-    so.astep[k % N] = k;
-  }
-  return KV_OK;
-}
-
-int issue_publish(const kv_step_t &st, long long k, StepPrep &sp, cudaStream_t sa,
-                  cudaStream_t sr, StreamOrder &so) {
-  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
-  if (!p0 || p0->device < 0 || !sp.has_p) return KV_OK;
-  DeviceGuard dg(p0->device);
-  const int N = StreamOrder::kN;
-  const double t0 = now_s();
-  if (sa != sr && so.astep[k % N] == k) CU(cudaStreamWaitEvent(sr, so.aready[k % N], 0));
-  if (st.ev_call) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_call), sr));
-  const double t1 = now_s();
-  phase_add(kPhEvents, t1 - t0);
-  DeviceCtx *ctx = ctx_for(p0->device);
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  StageBuf *b = nullptr;
-  int rc = KV_OK;
-  Launch *ls[1] = {&sp.P};
-  if (!sp.inl_p && !sp.P.tasks.empty() && (rc = stage(ctx, ls, 1, sr, &b))) return rc;
-  phase_add(kPhPubStage, now_s() - t1);
-  g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
-  g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
-  rc = sp.inl_p ? enqueue_inline(sp.P, *sp.dp, sr, false) : enqueue(sp.P, sr);
-  g_ev_before = g_ev_after = nullptr;
-  if (rc) return rc;
-  if (st.ev_done) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_done), sr));
-  if (sa != sr) {
-    CU(cudaEventRecord(so.rdone[k % N], sr));
-    so.rstep[k % N] = k;
-  }
-  if (b && (rc = ctx->done(b, sr))) return rc;
-  phase_add(kPhEnqP, now_s() - t1);
-  return KV_OK;
-}
-
 }  // namespace
 
-// Decode-loop driver.  For runs of >= 8 steps a helper thread prepares step
-// k+1 (allocation, tables, work lists) while this thread issues step k's CUDA
-// calls; the two meet through a 2-deep ring of StepPrep.
 KV_API int kv_run_steps(int32_t n_steps, const kv_step_t *steps, void *append_stream,
                         void *repl_stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
   cudaStream_t sa = static_cast<cudaStream_t>(append_stream);
   cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
   thread_local StreamOrder so;
-  if (sa != sr && n_steps > 0) {
-    const kv_step_t &s0 = steps[0];
-    kv_pool *q = s0.n_append > 0 ? s0.append[0].pool : (s0.n_repl > 0 ? s0.repl_pools[0] : nullptr);
-    if (q && q->device >= 0 && (so.sa != sa || so.sr != sr || so.dev != q->device)) {
-      // a new stream pair: everything already on sr precedes this call's appends
-      DeviceGuard dg(q->device);
-      int rc = so.ensure(q->device);
-      if (rc) return rc;
-      for (int i = 0; i < StreamOrder::kN; ++i) so.rstep[i] = so.astep[i] = -1;
-      CU(cudaEventRecord(so.rdone[0], sr));
-      CU(cudaStreamWaitEvent(sa, so.rdone[0], 0));
-      so.sa = sa;
-      so.sr = sr;
-    }
-  }
-  if (n_steps < 8) {
-    thread_local StepPrep sp;
-    for (int k = 0; k < n_steps; ++k) {
-      prepare_step(steps[k], sp);
-      if (sp.rc) return sp.rc;
-      const long long kk = so.n++;
-      int rc = issue_append(steps[k], kk, sp, sa, sr, so);
-      if (!rc) rc = issue_publish(steps[k], kk, sp, sa, sr, so);
-      if (rc) return rc;
-    }
-    return KV_OK;
-  }
-  // A helper thread prepares step k+1 (allocation, tables, work lists, inline
-  // descriptors) while this thread issues step k's CUDA calls; a 2-deep ring of
-  // StepPrep.  (Issuing the appends from the helper too was measured slower:
-  // concurrent launches from two threads contend in the driver.)
-  StepPrep ring[2];  // shared with the worker (per call: reentrant across threads)
-  std::atomic<int> produced{0}, consumed{0};
-  std::atomic<bool> stop{false};
-  std::thread worker([&]() {
-    for (int k = 0; k < n_steps && !stop.load(std::memory_order_acquire); ++k) {
-      const double w0 = now_s();
-      while (k - consumed.load(std::memory_order_acquire) >= 2) {
-        if (stop.load(std::memory_order_acquire)) return;
-        std::this_thread::yield();
-      }
-      phase_add(kPhWaitIssue, now_s() - w0);
-      StepPrep &sp = ring[k & 1];
+  thread_local StepLaunch S;
+  const int N = StreamOrder::kN;
+  for (int i = 0; i < n_steps; ++i) {
+    const kv_step_t &st = steps[i];
+    const int dev = step_device(st);
+    DeviceGuard dg(dev);
+    const bool two = dev >= 0 && sa != sr;
+    int rc = KV_OK;
+    if (two && (rc = so.ensure(dev, sa, sr))) return rc;
+    const long long k = two ? so.n++ : i;
+    // the appends of step k (the model's KV write) on the append stream
+    if (st.n_append > 0) {
       const double t0 = now_s();
-      prepare_step(steps[k], sp);
-      phase_add(kPhPrepare, now_s() - t0);
-      produced.store(k + 1, std::memory_order_release);
-      if (sp.rc) return;
-    }
-  });
-  int rc = KV_OK;
-  for (int k = 0; k < n_steps; ++k) {
-    const double w0 = now_s();
-    while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
-    phase_add(kPhWaitPrep, now_s() - w0);
-    StepPrep &sp = ring[k & 1];
-    if (sp.rc) {
-      rc = sp.rc;
-      g_err = sp.err;
-      break;
-    }
-    const long long kk = so.n++;
-    rc = issue_append(steps[k], kk, sp, sa, sr, so);
-    if (!rc) rc = issue_publish(steps[k], kk, sp, sa, sr, so);
-    consumed.store(k + 1, std::memory_order_release);
-    if (rc) break;
-  }
-  stop.store(true, std::memory_order_release);
-  worker.join();
-  return rc;
-}
-
-// ---- CUDA-graph decode loop ---------------------------------------------------
-// The same work as kv_run_steps, issued as one CUDA graph per group of graph_steps() (8)
-// steps: per step an append kernel node and a ring-put kernel node with the
-// stream-order constraints of kv_run_steps as graph edges (append k after append
-// k-1 and after ring-put k-2 -- R7 --, ring-put k after append k and after ring-put
-// k-1), all descriptors of the group staged by ONE H2D memcpy node.  A kernel node
-// costs the device < 1 us instead of 2-4 us for a stream launch and the host a
-// ~0.3 us parameter update instead of a 3-6 us launch (tools/launchbench.cu).
-// Consecutive groups run on the two streams and are chained by event-wait nodes,
-// so group g+1 overlaps the tail of group g exactly like consecutive steps do.
-namespace {
-
-constexpr int kGraphMax = 32;  // node arrays; the group size itself: graph_steps()
-// Steps per graph (KVRING_GRAPH_STEPS, 2..32, default 8), read once per process.
-int graph_steps() {
-  static const int n = [] {
-    const char *e = getenv("KVRING_GRAPH_STEPS");
-    const int v = e ? atoi(e) : 8;
-    return std::max(2, std::min(kGraphMax, v));
-  }();
-  return n;
-}
-
-struct GraphLoop {
-  static constexpr int kEv = 4, kSlots = 4;
-  int device = -1;
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t ge[kSlots] = {};  // 2 used (parity), or one per slot in fixed mode
-  bool fixed = false;  // self-describing steps: kernel nodes never updated per step
-  KvFxArgs fx[3 * kGraphMax];
-  cudaGraphNode_t mc = nullptr, wait_a = nullptr, wait_r2 = nullptr, wait_r1 = nullptr;
-  cudaGraphNode_t an[kGraphMax] = {}, rn[kGraphMax] = {}, pn[kGraphMax] = {};
-  cudaGraphNode_t es[kGraphMax] = {}, ee[kGraphMax] = {};
-  cudaGraphNode_t rec_a = nullptr, rec_r2 = nullptr, rec_r1 = nullptr, rec_p = nullptr;
-  cudaGraphNode_t wait_p = nullptr;
-  cudaEvent_t ev_a[kEv] = {}, ev_r2[kEv] = {}, ev_r1[kEv] = {}, ev_p[kEv] = {};
-  bool split_pub = false;  // ring-put = copy node + separate publication node
-  bool lean = false;       // no timing event nodes (KVRING_GRAPH_LEAN=1, experiments)
-  cudaEvent_t start_a = nullptr, start_r = nullptr, join = nullptr;
-  cudaEvent_t dummy[2 * kGraphMax] = {};
-  StageBuf slot[kSlots];
-  KvNodeArgs args[3 * kGraphMax];
-  int steps = 8;  // group size of this graph
-  // last values set per exec instance: skip redundant update calls (each ~0.3 us)
-  signed char enabled[kSlots][3 * kGraphMax];
-  cudaEvent_t ev_set[kSlots][2 * kGraphMax] = {};
-  long long group = 0;
-  std::mutex mu;  // one call at a time per device (the graph and its slots are shared)
-
-  int make_event(cudaEvent_t *e) {
-    CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    return KV_OK;
-  }
-  // Fixed mode: point exec e's kernel nodes at slot e (once, and after a slot grows).
-  int bind_slot(int e) {
-    const int fx_grid = resident_ctas(device);
-    for (int k = 0; k < steps; ++k) {
-      cudaKernelNodeParams kp{};
-      KvFxArgs a{slot[e].dev, k};
-      fx_node_params(kKindAppend, fx_grid, a, kp);
-      CU(cudaGraphExecKernelNodeSetParams(ge[e], an[k], &kp));
-      fx_node_params(kKindRingPutCopy, fx_grid, a, kp);
-      CU(cudaGraphExecKernelNodeSetParams(ge[e], rn[k], &kp));
-      fx_node_params(kKindPublish, kFxPublishGrid, a, kp);
-      CU(cudaGraphExecKernelNodeSetParams(ge[e], pn[k], &kp));
-    }
-    return KV_OK;
-  }
-  int build(int dev) {
-    device = dev;
-    for (int i = 0; i < kEv; ++i) {
-      int rc = make_event(&ev_a[i]);
-      if (!rc) rc = make_event(&ev_r2[i]);
-      if (!rc) rc = make_event(&ev_r1[i]);
-      if (!rc) rc = make_event(&ev_p[i]);
+      rc = validate_appends(st.n_append, st.append);
+      phase_add(kPhPrepAppend, now_s() - t0);
       if (rc) return rc;
-    }
-    for (auto &e : dummy)
-      if (int rc = make_event(&e)) return rc;
-    if (int rc = make_event(&start_a)) return rc;
-    if (int rc = make_event(&start_r)) return rc;
-    if (int rc = make_event(&join)) return rc;
-    for (auto &sl : slot) {
-      const size_t cap = 32u << 20;
-      CU(cudaHostAlloc(reinterpret_cast<void **>(&sl.host), cap, cudaHostAllocDefault));
-      CU(cudaMalloc(reinterpret_cast<void **>(&sl.dev), cap));
-      sl.cap = cap;
-      CU(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
-    }
-    CU(cudaGraphCreate(&g, 0));
-    CU(cudaGraphAddMemcpyNode1D(&mc, g, nullptr, 0, slot[0].dev, slot[0].host, 16,
-                                cudaMemcpyHostToDevice));
-    CU(cudaGraphAddEventWaitNode(&wait_a, g, nullptr, 0, start_a));
-    CU(cudaGraphAddEventWaitNode(&wait_r2, g, nullptr, 0, start_r));
-    CU(cudaGraphAddEventWaitNode(&wait_r1, g, nullptr, 0, start_r));
-    // the publication as its own node (KVRING_GRAPH_SPLIT_PUB=0: inside the ring-put):
-    // the copies lose the per-CTA release RMW and bar.sync tail (ring-put node 10.7 vs
-    // 14.3 us median, +5 % steps/s, profiles/r01/exp43.log)
-    split_pub = [] {
-      const char *e = getenv("KVRING_GRAPH_SPLIT_PUB");
-      return e ? atoi(e) != 0 : true;
-    }();
-    if (split_pub) CU(cudaGraphAddEventWaitNode(&wait_p, g, nullptr, 0, start_r));
-    // self-describing steps (KVRING_GRAPH_FIXED=1, needs the split publication): each
-    // kernel node reads its launch from the step header in the group's slot
-    fixed = split_pub && [] {
-      const char *e = getenv("KVRING_GRAPH_FIXED");
-      return e ? atoi(e) != 0 : false;
-    }();
-    const int fx_grid = resident_ctas(dev);
-    // experiment knob KVRING_GRAPH_LAG=1: append k waits for ring-put k-1 (no overlap of
-    // an append with the previous publication); default 2 (reading R7's minimum)
-    static const int lag = [] {
-      const char *e = getenv("KVRING_GRAPH_LAG");
-      return e && atoi(e) == 1 ? 1 : 2;
-    }();
-    steps = graph_steps();
-    // Timing event nodes sit beside the chain (es(k) has R(k)'s dependencies, ee(k)
-    // follows R(k)); no kernel waits on them unless KVRING_GRAPH_EVENTS_IN_CHAIN=1.
-    static const bool in_chain = getenv("KVRING_GRAPH_EVENTS_IN_CHAIN") != nullptr;
-    lean = !in_chain && getenv("KVRING_GRAPH_LEAN") != nullptr;  // experiment knob
-    for (int k = 0; k < steps; ++k) {
-      cudaKernelNodeParams kp{};
-      if (fixed) {
-        fx[3 * k] = KvFxArgs{slot[0].dev, k};
-        fx_node_params(kKindAppend, fx_grid, fx[3 * k], kp);
-      } else {
-        kernel_node_params(kKindAppend, 1, args[2 * k], kp);
+      if (dev >= 0) {
+        const int lag = step_has_shared(st) ? 1 : 2;
+        if (two && k >= lag && so.rstep[(k - lag) % N] == k - lag)
+          CU(cudaStreamWaitEvent(sa, so.rdone[(k - lag) % N], 0));
       }
-      cudaGraphNode_t rprev = k > 0 ? (in_chain ? ee[k - 1] : rn[k - 1]) : wait_r1;
-      cudaGraphNode_t lagdep =
-          lag == 2 ? (k >= 2 ? (in_chain ? ee[k - 2] : rn[k - 2]) : (k == 0 ? wait_r2 : wait_r1))
-                   : rprev;
-      // append k also follows the LAUNCH of ring-put k-1 (the node that becomes ready with
-      // it, its start event): the publication then gets the free CTA slots first
-      // (+2-10 % measured, profiles/r01/exp39.log)
-      cudaGraphNode_t da[4] = {mc, k > 0 ? an[k - 1] : wait_a, lagdep,
-                               k > 0 ? es[k - 1] : nullptr};
-      CU(cudaGraphAddKernelNode(&an[k], g, da, k > 0 ? 4 : 3, &kp));
-      cudaGraphNode_t ds[2] = {an[k], rprev};
-      if (lean)  // experiment: no timing nodes (an empty node keeps the ordering role)
-        CU(cudaGraphAddEmptyNode(&es[k], g, ds, 2));
-      else
-        CU(cudaGraphAddEventRecordNode(&es[k], g, ds, 2, dummy[2 * k]));
-      if (fixed) {
-        fx[3 * k + 1] = KvFxArgs{slot[0].dev, k};
-        fx_node_params(kKindRingPutCopy, fx_grid, fx[3 * k + 1], kp);
-      } else {
-        kernel_node_params(split_pub ? kKindRingPutCopy : kKindRingPut, 1, args[2 * k + 1], kp);
-      }
-      if (in_chain)
-        CU(cudaGraphAddKernelNode(&rn[k], g, &es[k], 1, &kp));
-      else
-        CU(cudaGraphAddKernelNode(&rn[k], g, ds, 2, &kp));
-      if (!lean) CU(cudaGraphAddEventRecordNode(&ee[k], g, &rn[k], 1, dummy[2 * k + 1]));
-      if (split_pub) {  // publication k after copies k and publication k-1 (seq order)
-        if (fixed) {
-          fx[3 * k + 2] = KvFxArgs{slot[0].dev, k};
-          fx_node_params(kKindPublish, kFxPublishGrid, fx[3 * k + 2], kp);
-        } else {
-          kernel_node_params(kKindPublish, 1, args[2 * kGraphMax + k], kp);
-        }
-        cudaGraphNode_t dp[2] = {rn[k], k > 0 ? pn[k - 1] : wait_p};
-        CU(cudaGraphAddKernelNode(&pn[k], g, dp, 2, &kp));
-      }
-    }
-    CU(cudaGraphAddEventRecordNode(&rec_a, g, &an[steps - 1], 1, ev_a[0]));
-    CU(cudaGraphAddEventRecordNode(&rec_r2, g, &rn[steps - 2], 1, ev_r2[0]));
-    CU(cudaGraphAddEventRecordNode(&rec_r1, g, &rn[steps - 1], 1, ev_r1[0]));
-    if (split_pub) CU(cudaGraphAddEventRecordNode(&rec_p, g, &pn[steps - 1], 1, ev_p[0]));
-    for (int e = 0; e < (fixed ? kSlots : 2); ++e) {
-      CU(cudaGraphInstantiate(&ge[e], g, 0));
-      if (fixed) {
-        int rc = bind_slot(e);
+      for (int k0 = 0; k0 < st.n_append; k0 += kStepPools) {
+        S.reset();
+        const double t1 = now_s();
+        const int n = std::min(kStepPools, st.n_append - k0);
+        apply_appends(S, n, st.append + k0);
+        phase_add(kPhPrepAppend, now_s() - t1);
+        if (dev < 0) continue;
+        g_ev_before = k0 == 0 ? static_cast<cudaEvent_t>(st.ev_append_start) : nullptr;
+        g_ev_after = k0 + n == st.n_append ? static_cast<cudaEvent_t>(st.ev_append_end) : nullptr;
+        rc = step_enqueue(S, sa);
+        g_ev_before = g_ev_after = nullptr;
         if (rc) return rc;
       }
     }
-    std::memset(enabled, -1, sizeof enabled);
-    return KV_OK;
+    // the publication of step k on the replication stream (§3.2)
+    if (st.n_repl > 0) {
+      if (two) {
+        CU(cudaEventRecord(so.aready[k % N], sa));
+        so.astep[k % N] = k;
+        CU(cudaStreamWaitEvent(sr, so.aready[k % N], 0));
+      }
+      if (dev >= 0 && (rc = record(st.ev_call, sr))) return rc;
+      g_ev_before = static_cast<cudaEvent_t>(st.ev_kernel_start);
+      g_ev_after = static_cast<cudaEvent_t>(st.ev_kernel_end);
+      rc = replicate_any(st.n_repl, st.repl_pools, st.step, sr);
+      g_ev_before = g_ev_after = nullptr;
+      if (rc) return rc;
+      if (dev >= 0 && (rc = record(st.ev_done, sr))) return rc;
+      if (two) {
+        CU(cudaEventRecord(so.rdone[k % N], sr));
+        so.rstep[k % N] = k;
+      }
+    }
+  }
+  return KV_OK;
+}
+
+// ---- one launch per decode step (software pipelined) -------------------------------
+struct kv_loop {
+  std::vector<kv_pool *> pend;  // pools whose publication of pend_step is pending
+  uint64_t pend_step = 0;
+  std::vector<std::unique_ptr<StepLaunch>> S;  // launches of one step (<= 8 pools each)
+  StepLaunch &at(size_t i) {
+    while (S.size() <= i) S.emplace_back(new StepLaunch());
+    return *S[i];
   }
 };
 
-std::mutex g_graph_mu;
-std::map<int, std::unique_ptr<GraphLoop>> g_graph;
-
-// Packs one launch's descriptors (params, publication tables, tasks) into a group
-// slot at `off` and points the launch at the device copy.
-void pack_launch(Launch &L, char *h, char *d, size_t &off) {
-  const size_t pbytes = align16(sizeof(KvPoolParams) * L.n_pools);
-  const size_t tbl = align16(L.tables.size());
-  for (int k = 0; k < L.n_pools; ++k)
-    if (L.kind == kKindRingPut) {
-      const size_t o = off + pbytes + L.table_off[k];
-      L.params[k].slot_req = reinterpret_cast<const int64_t *>(d + o);
-      L.params[k].slot_len = reinterpret_cast<const int32_t *>(d + o + 8 * (size_t)L.params[k].max_reqs);
-    }
-  std::memcpy(h + off, L.params.data(), sizeof(KvPoolParams) * L.n_pools);
-  if (!L.tables.empty()) std::memcpy(h + off + pbytes, L.tables.data(), L.tables.size());
-  std::memcpy(h + off + pbytes + tbl, L.tasks.data(), sizeof(KvTask) * L.tasks.size());
-  L.params_dev = reinterpret_cast<const KvPoolParams *>(d + off);
-  L.tasks_dev = reinterpret_cast<const KvTask *>(d + off + pbytes + tbl);
-  off += align16(L.staged_bytes());
+namespace {
+void loop_forget(kv_loop *L, kv_pool *p) {
+  auto &v = L->pend;
+  v.erase(std::remove(v.begin(), v.end(), p), v.end());
 }
 
-int set_kernel_node(cudaGraphExec_t ge, cudaGraphNode_t node, Launch *L, bool present,
-                    KvNodeArgs &a, int kind, signed char &enabled) {
-  cudaKernelNodeParams kp{};
-  a = KvNodeArgs{};
-  int grid = 1;
-  if (present && L && !L->tasks.empty()) {
-    a.tasks = L->tasks_dev;
-    a.n_tasks = (int)L->tasks.size();
-    a.params = L->params_dev;
-    a.g = L->p0->geom_dev();
-    a.n_pools = L->n_pools;
-    a.split = L->split;
-    if (L->n_pools <= kInlinePools) {
-      a.pk.n = L->n_pools;
-      for (int q = 0; q < L->n_pools; ++q) {
-        a.pk.src[q] = L->params[q].src;
-        a.pk.dst[q] = L->params[q].dst;
-      }
-    }
-    grid = kind == kKindPublish ? L->n_pools : launch_grid(*L);  // publication: CTA per pool
+// The pending publication, built from the pools' CURRENT tables: everything the
+// harness did since the previous step (a failure, a restore, a relink, a resume
+// re-append) is reflected exactly as in the sequential protocol (append t, then
+// replicate t).  Pools that died or lost their successor meanwhile publish nothing.
+// Fills launches 0..(*n_out - 1) (<= kStepPools pools / kStepMaxEnt slots each).
+int loop_take_pending(kv_loop *L, int *n_out) {
+  *n_out = 0;
+  if (L->pend.empty()) return KV_OK;
+  kv_pool *ps[kMaxPoolsPerLaunchHost];
+  int n = 0;
+  for (kv_pool *p : L->pend) {
+    p->loop = nullptr;
+    if (!p->dead && p->has_succ) ps[n++] = p;
   }
-  kernel_node_params(kind, grid, a, kp);
-  CU(cudaGraphExecKernelNodeSetParams(ge, node, &kp));
-  if (enabled != (present ? 1 : 0)) {
-    CU(cudaGraphNodeSetEnabled(ge, node, present ? 1 : 0));
-    enabled = present ? 1 : 0;
-  }
-  return KV_OK;
-}
-
-// Issues group [k0, k0 + n) of prepared steps (n <= G.steps).
-int issue_group(GraphLoop &G, const kv_step_t *steps, StepPrep *const *sp, int n,
-                cudaStream_t sa, cudaStream_t sr, bool first) {
-  const int N = GraphLoop::kEv;
-  const long long gi = G.group++;
-  const int se = (int)(gi % GraphLoop::kSlots);
-  StageBuf &sl = G.slot[se];
-  const size_t hdr_bytes = G.fixed ? align16(sizeof(KvStepHdr) * G.steps) : 0;
+  L->pend.clear();
+  if (n == 0) return KV_OK;
   const double t0 = now_s();
-  if (sl.pending) {
-    CU(cudaEventSynchronize(sl.ev));
-    sl.pending = false;
+  int rc = validate_replicate(n, ps, L->pend_step);
+  int nl = 0;
+  for (int k0 = 0; !rc && k0 < n; ++nl) {
+    int k1 = k0;
+    long long ent = 0;
+    while (k1 < n && k1 - k0 < kStepPools && ent + ps[k1]->slot_hi <= kStepMaxEnt)
+      ent += ps[k1++]->slot_hi;
+    if (k1 == k0) return fail(KV_EINVAL, "pool %d has too many slots for one launch", ps[k0]->node_id);
+    StepLaunch &S = L->at(nl);
+    S.reset();
+    rc = step_prepare_replicate(S, k1 - k0, ps + k0, L->pend_step);
+    k0 = k1;
   }
-  phase_add(kPhAcquire, now_s() - t0);
-  size_t need = hdr_bytes;
-  for (int i = 0; i < n; ++i) {
-    if (sp[i]->has_a) need += align16(sp[i]->A.staged_bytes());
-    if (sp[i]->has_p) need += align16(sp[i]->P.staged_bytes());
-  }
-  if (need > sl.cap) {  // rare (bulk steps): grow this slot
-    if (sl.host) cudaFreeHost(sl.host);
-    if (sl.dev) cudaFree(sl.dev);
-    const size_t cap = std::max(need * 2, sl.cap);
-    CU(cudaHostAlloc(reinterpret_cast<void **>(&sl.host), cap, cudaHostAllocDefault));
-    CU(cudaMalloc(reinterpret_cast<void **>(&sl.dev), cap));
-    sl.cap = cap;
-    if (G.fixed) {
-      int rc = G.bind_slot(se);
-      if (rc) return rc;
-    }
-  }
-  const double t1 = now_s();
-  size_t off = hdr_bytes;
-  KvStepHdr *hdr = reinterpret_cast<KvStepHdr *>(sl.host);
-  for (int i = 0; i < (G.fixed ? G.steps : n); ++i) {
-    KvStepHdr h{};
-    if (i < n) {
-      Launch *ls2[2] = {sp[i]->has_a && !sp[i]->A.tasks.empty() ? &sp[i]->A : nullptr,
-                        sp[i]->has_p && !sp[i]->P.tasks.empty() ? &sp[i]->P : nullptr};
-      for (int w = 0; w < 2; ++w) {
-        Launch *L = ls2[w];
-        if (!L) continue;
-        pack_launch(*L, sl.host, sl.dev, off);
-        h.n_tasks[w] = (int32_t)L->tasks.size();
-        h.n_pools[w] = L->n_pools;
-        h.split[w] = L->split;
-        h.params_off[w] = (unsigned long long)(reinterpret_cast<const char *>(L->params_dev) - sl.dev);
-        h.tasks_off[w] = (unsigned long long)(reinterpret_cast<const char *>(L->tasks_dev) - sl.dev);
-        h.g = L->p0->geom_dev();
-      }
-    }
-    if (G.fixed) hdr[i] = h;
-  }
-  phase_add(kPhHostCopy, now_s() - t1);
-  const double tu = now_s();
-  const int par = (int)(gi & 1);
-  const int xi = G.fixed ? se : par;  // exec instance (and its update caches)
-  cudaGraphExec_t ge = G.ge[xi];
-  cudaStream_t st = par ? sr : sa;
-  CU(cudaGraphExecMemcpyNodeSetParams1D(ge, G.mc, sl.dev, sl.host, off > 0 ? off : 16,
-                                        cudaMemcpyHostToDevice));
-  const int pe = (int)((gi + N - 1) % N);
-  CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_a, first ? G.start_a : G.ev_a[pe]));
-  CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r2, first ? G.start_r : G.ev_r2[pe]));
-  CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_r1, first ? G.start_r : G.ev_r1[pe]));
-  if (G.split_pub)
-    CU(cudaGraphExecEventWaitNodeSetEvent(ge, G.wait_p, first ? G.start_r : G.ev_p[pe]));
-  for (int k = 0; k < G.steps; ++k) {
-    const bool on = k < n;
-    StepPrep *s = on ? sp[k] : nullptr;
-    if (!G.fixed) {  // fixed mode: the step header in the slot describes the launches
-      signed char *en = G.enabled[xi];
-      int rc = set_kernel_node(ge, G.an[k], s ? &s->A : nullptr, on && s->has_a, G.args[2 * k],
-                               kKindAppend, en[3 * k]);
-      if (!rc)
-        rc = set_kernel_node(ge, G.rn[k], s ? &s->P : nullptr, on && s->has_p,
-                             G.args[2 * k + 1], G.split_pub ? kKindRingPutCopy : kKindRingPut,
-                             en[3 * k + 1]);
-      if (!rc && G.split_pub)
-        rc = set_kernel_node(ge, G.pn[k], s ? &s->P : nullptr, on && s->has_p,
-                             G.args[2 * kGraphMax + k], kKindPublish, en[3 * k + 2]);
-      if (rc) return rc;
-    }
-    cudaEvent_t e0 = G.dummy[2 * k], e1 = G.dummy[2 * k + 1];
-    if (on && steps[k].ev_kernel_start) e0 = static_cast<cudaEvent_t>(steps[k].ev_kernel_start);
-    if (on && steps[k].ev_kernel_end) e1 = static_cast<cudaEvent_t>(steps[k].ev_kernel_end);
-    if (G.lean) e0 = e1 = nullptr;
-    if (e0 && G.ev_set[xi][2 * k] != e0) {
-      CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.es[k], e0));
-      G.ev_set[xi][2 * k] = e0;
-    }
-    if (e1 && G.ev_set[xi][2 * k + 1] != e1) {
-      CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.ee[k], e1));
-      G.ev_set[xi][2 * k + 1] = e1;
-    }
-    if (on) {
-      if (s->has_a && !s->A.tasks.empty()) {
-        g_launches++;
-        s->A.p0->kernels++;
-      }
-      if (s->has_p && !s->P.tasks.empty()) {
-        g_launches++;
-        s->P.p0->kernels++;
-      }
-    }
-  }
-  CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_a, G.ev_a[gi % N]));
-  CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r2, G.ev_r2[gi % N]));
-  CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_r1, G.ev_r1[gi % N]));
-  if (G.split_pub) CU(cudaGraphExecEventRecordNodeSetEvent(ge, G.rec_p, G.ev_p[gi % N]));
-  const double t2 = now_s();
-  phase_add(kPhEvents, t2 - tu);  // graph node updates (reported as "events")
-  CU(cudaGraphLaunch(ge, st));
-  CU(cudaEventRecord(sl.ev, st));
-  sl.pending = true;
-  phase_add(kPhEnqP, now_s() - t2);
-  return KV_OK;
+  phase_add(kPhPrepRepl, now_s() - t0);
+  *n_out = nl;
+  return rc;
 }
-
 }  // namespace
 
-KV_API int kv_run_steps_graph(int32_t n_steps, const kv_step_t *steps, void *append_stream,
-                              void *repl_stream) {
+KV_API int kv_loop_create(kv_loop_t **out) {
+  if (!out) return fail(KV_EINVAL, "null argument");
+  *out = new kv_loop();
+  return KV_OK;
+}
+
+KV_API int kv_loop_destroy(kv_loop_t *L) {
+  if (!L) return KV_OK;
+  for (kv_pool *p : L->pend) p->loop = nullptr;
+  delete L;
+  return KV_OK;
+}
+
+KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
+  if (!L || !st) return fail(KV_EINVAL, "null argument");
+  if (st->n_repl > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "too many pools");
+  for (int i = 0; i < st->n_repl; ++i) {
+    kv_pool *p = st->repl_pools[i];
+    if (!p) return fail(KV_EINVAL, "null pool");
+    if (p->holder || p->rep_src)
+      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps (two streams)");
+    if (p->loop && p->loop != L) return fail(KV_ESTATE, "pool %d is pending in another loop", p->node_id);
+  }
+  for (int i = 0; i < st->n_append; ++i)
+    if (st->append[i].pool && (st->append[i].pool->holder || st->append[i].pool->rep_src))
+      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps (two streams)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // 1. the previous step's publication (snapshots + host commit, before any append)
+  int n_rep = 0;
+  int rc = loop_take_pending(L, &n_rep);
+  if (rc) return rc;
+  for (int i = n_rep; i < (int)L->S.size(); ++i) L->S[i]->reset();
+  // 2. this step's appends; if they are rejected the publication still launches
+  int rc_app = KV_OK, n_app = 0;
+  if (st->n_append > 0) {
+    const double t0 = now_s();
+    rc_app = validate_appends(st->n_append, st->append);
+    if (!rc_app)
+      for (int k0 = 0; k0 < st->n_append; k0 += kStepPools, ++n_app)
+        apply_appends(L->at(n_app), std::min(kStepPools, st->n_append - k0), st->append + k0);
+    phase_add(kPhPrepAppend, now_s() - t0);
+  }
+  // 3. one launch (more only beyond 8 pools per role)
+  const int nl = std::max(n_rep, n_app);
+  for (int i = 0; i < nl; ++i) {
+    g_ev_before = i == 0 ? static_cast<cudaEvent_t>(st->ev_kernel_start) : nullptr;
+    g_ev_after = i == nl - 1 ? static_cast<cudaEvent_t>(st->ev_kernel_end) : nullptr;
+    rc = step_enqueue(*L->S[i], s);
+    g_ev_before = g_ev_after = nullptr;
+    if (rc) return rc;
+  }
+  if (rc_app) return rc_app;
+  // 4. this step's publication rides on the next launch
+  if (st->n_repl > 0) {
+    L->pend.assign(st->repl_pools, st->repl_pools + st->n_repl);
+    L->pend_step = st->step;
+    for (kv_pool *p : L->pend) p->loop = L;
+  }
+  return KV_OK;
+}
+
+KV_API int kv_loop_run(kv_loop_t *L, int32_t n_steps, const kv_step_t *steps, void *stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
-  if (n_steps == 0) return KV_OK;
-  cudaStream_t sa = static_cast<cudaStream_t>(append_stream);
-  cudaStream_t sr = static_cast<cudaStream_t>(repl_stream);
-  if (sa == sr) return fail(KV_EINVAL, "kv_run_steps_graph needs two distinct streams");
-  kv_pool *p0 = nullptr;
-  for (int k = 0; k < n_steps; ++k) {
-    if (any_shared(steps[k]))
-      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps");
-    for (int i = 0; i < steps[k].n_append; ++i) {
-      if (steps[k].append[i].flags & KV_SRC_HOST)
-        return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_graph");
-      if (!p0) p0 = steps[k].append[i].pool;
-    }
-    if (!p0 && steps[k].n_repl > 0) p0 = steps[k].repl_pools[0];
+  for (int i = 0; i < n_steps; ++i) {
+    int rc = kv_loop_step(L, &steps[i], stream);
+    if (rc) return rc;
   }
-  if (!p0) return fail(KV_EINVAL, "no pools");
-  if (p0->device < 0) return fail(KV_ESTATE, "kv_run_steps_graph needs device pools");
-  DeviceGuard dg(p0->device);
-  GraphLoop *G;
-  {
-    std::lock_guard<std::mutex> lk(g_graph_mu);
-    auto &up = g_graph[p0->device];
-    if (!up) {
-      up.reset(new GraphLoop());
-      if (int rc = up->build(p0->device)) {
-        up.reset();
-        return rc;
-      }
-    }
-    G = up.get();
+  return KV_OK;
+}
+
+KV_API int kv_loop_flush(kv_loop_t *L, void *stream) {
+  if (!L) return fail(KV_EINVAL, "null loop");
+  int n = 0;
+  int rc = loop_take_pending(L, &n);
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i)
+    if ((rc = step_enqueue(*L->S[i], static_cast<cudaStream_t>(stream)))) return rc;
+  return KV_OK;
+}
+
+KV_API int kv_launch_log(uint64_t *out, int32_t cap, int32_t mode) {
+  if (mode == 1) {
+    g_log.clear();
+    g_log_on = true;
+    return 0;
   }
-  std::lock_guard<std::mutex> call_lock(G->mu);
-  // earlier work on both streams precedes the first group
-  CU(cudaEventRecord(G->start_a, sa));
-  CU(cudaEventRecord(G->start_r, sr));
-  const int GS = G->steps;
-  const int R = 2 * GS;  // prepared-step ring shared with the helper
-  std::vector<StepPrep> ring(R);
-  for (auto &x : ring) x.no_inline = true;
-  std::atomic<int> produced{0}, consumed{0};
-  std::atomic<bool> stop{false};
-  std::thread worker([&]() {
-    for (int k = 0; k < n_steps && !stop.load(std::memory_order_acquire); ++k) {
-      const double w0 = now_s();
-      while (k - consumed.load(std::memory_order_acquire) >= R) {
-        if (stop.load(std::memory_order_acquire)) return;
-        std::this_thread::yield();
-      }
-      phase_add(kPhWaitIssue, now_s() - w0);
-      const double t0 = now_s();
-      prepare_step(steps[k], ring[k % R]);
-      phase_add(kPhPrepare, now_s() - t0);
-      produced.store(k + 1, std::memory_order_release);
-      if (ring[k % R].rc) return;
+  g_log_on = false;
+  const int n = (int)g_log.size();
+  if (out)
+    for (int i = 0; i < n && i < cap; ++i) {
+      out[5 * i + 0] = g_log[i].kind;
+      out[5 * i + 1] = g_log[i].app_bytes;
+      out[5 * i + 2] = g_log[i].rep_bytes;
+      out[5 * i + 3] = g_log[i].grid;
+      out[5 * i + 4] = g_log[i].blob_bytes;
     }
-  });
-  int rc = KV_OK;
-  cudaStream_t last = sa;
-  for (int k0 = 0; k0 < n_steps && !rc; k0 += GS) {
-    const int n = std::min(GS, n_steps - k0);
-    const double w0 = now_s();
-    while (produced.load(std::memory_order_acquire) < k0 + n) {
-      if (ring[(produced.load() + R - 1) % R].rc && produced.load() > 0) break;
-      std::this_thread::yield();
-    }
-    phase_add(kPhWaitPrep, now_s() - w0);
-    StepPrep *sp[kGraphMax];
-    for (int i = 0; i < n; ++i) {
-      sp[i] = &ring[(k0 + i) % R];
-      if (produced.load(std::memory_order_acquire) <= k0 + i || sp[i]->rc) {
-        rc = sp[i]->rc ? sp[i]->rc : KV_EINVAL;
-        g_err = sp[i]->err;
-        break;
-      }
-    }
-    if (rc) break;
-    rc = issue_group(*G, steps + k0, sp, n, sa, sr, k0 == 0);
-    last = (G->group - 1) & 1 ? sr : sa;
-    consumed.store(k0 + n, std::memory_order_release);
-  }
-  stop.store(true, std::memory_order_release);
-  worker.join();
-  if (!rc) {  // both streams end after the last group
-    cudaStream_t other = last == sa ? sr : sa;
-    CU(cudaEventRecord(G->join, last));
-    CU(cudaStreamWaitEvent(other, G->join, 0));
-  }
-  return rc;
+  return n;
 }
 
 // ---- re-protection (§8(f) NEXT-1; §3.2) --------------------
@@ -2530,278 +2272,4 @@ KV_API int kv_plan_targets(int32_t n_nodes, const int32_t *succ, const uint8_t *
     }
   }
   return KV_OK;
-}
-
-// ---- software-pipelined decode loop (single stream) --------------------------
-namespace {
-
-struct FusedPrep {
-  Launch A, P;        // append of step k, publication of step k-1
-  bool has_a = false, has_p = false;
-  int rc = KV_OK;
-  std::string err;
-};
-
-// Prepare launch k: the publication of step k-1 FIRST (its dirty ranges end at
-// len_{k-1}), then the append of step k (which moves len on).
-void prepare_fused(const kv_step_t *steps, int n_steps, int k, FusedPrep &fp) {
-  fp.rc = KV_OK;
-  fp.has_p = k >= 1 && steps[k - 1].n_repl > 0;
-  fp.has_a = k < n_steps && steps[k].n_append > 0;
-  if (fp.has_p) {
-    const kv_step_t &pv = steps[k - 1];
-    if ((fp.rc = prepare_replicate(pv.n_repl, pv.repl_pools, pv.step, fp.P, false, false))) {
-      fp.err = g_err;
-      return;
-    }
-    commit_replicate(fp.P, pv.repl_pools, pv.step);
-  }
-  if (fp.has_a && (fp.rc = prepare_append(steps[k].n_append, steps[k].append, fp.A, false))) {
-    fp.err = g_err;
-    return;
-  }
-  if (fp.has_a && fp.has_p && fp.A.p0->device != fp.P.p0->device) {
-    fp.rc = fail(KV_EINVAL, "append and publication of one launch must share a device");
-    fp.err = g_err;
-  }
-}
-
-// One H2D: [A params | P params] [P tables] [A tasks | P tasks]; P tasks keep
-// pool indices local to P (the kernel offsets its params pointer).
-int stage_fused(DeviceCtx *ctx, FusedPrep &fp, cudaStream_t st, StageBuf **out,
-                const KvPoolParams **params_dev, const KvTask **tasks_dev) {
-  Launch &A = fp.A, &P = fp.P;
-  const int na = fp.has_a ? A.n_pools : 0, np = fp.has_p ? P.n_pools : 0;
-  const size_t pbytes = align16(sizeof(KvPoolParams) * (size_t)(na + np));
-  const size_t tbl = fp.has_p ? align16(P.tables.size()) : 0;
-  const size_t nta = fp.has_a ? A.tasks.size() : 0, ntp = fp.has_p ? P.tasks.size() : 0;
-  const size_t total = pbytes + tbl + sizeof(KvTask) * (nta + ntp);
-  StageBuf *b = nullptr;
-  const double ta = now_s();
-  int rc = ctx->acquire(ctx->ring, ctx->next, total, true, &b);
-  if (rc) return rc;
-  const double tb = now_s();
-  phase_add(kPhAcquire, tb - ta);
-  char *h = b->host, *d = b->dev;
-  for (int k = 0; k < np; ++k) {
-    P.params[k].slot_req = reinterpret_cast<const int64_t *>(d + pbytes + P.table_off[k]);
-    P.params[k].slot_len =
-        reinterpret_cast<const int32_t *>(d + pbytes + P.table_off[k] + 8 * (size_t)P.params[k].max_reqs);
-  }
-  if (na) std::memcpy(h, A.params.data(), sizeof(KvPoolParams) * na);
-  if (np) std::memcpy(h + sizeof(KvPoolParams) * na, P.params.data(), sizeof(KvPoolParams) * np);
-  if (tbl) std::memcpy(h + pbytes, P.tables.data(), P.tables.size());
-  if (nta) std::memcpy(h + pbytes + tbl, A.tasks.data(), sizeof(KvTask) * nta);
-  if (ntp) std::memcpy(h + pbytes + tbl + sizeof(KvTask) * nta, P.tasks.data(), sizeof(KvTask) * ntp);
-  const double tc = now_s();
-  phase_add(kPhHostCopy, tc - tb);
-  CU(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, st));
-  phase_add(kPhH2DCall, now_s() - tc);
-  *params_dev = reinterpret_cast<const KvPoolParams *>(d);
-  *tasks_dev = reinterpret_cast<const KvTask *>(d + pbytes + tbl);
-  *out = b;
-  return KV_OK;
-}
-
-int issue_fused(const kv_step_t *ev_step, FusedPrep &fp, cudaStream_t st) {
-  kv_pool *p0 = fp.has_a ? fp.A.p0 : (fp.has_p ? fp.P.p0 : nullptr);
-  if (!p0 || p0->device < 0) return KV_OK;
-  DeviceGuard dg(p0->device);
-  DeviceCtx *ctx = ctx_for(p0->device);
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  StageBuf *sb = nullptr, *b = nullptr;
-  int rc = KV_OK;
-  double t0 = now_s();
-  if (fp.has_a && (rc = stage_host_sources(ctx, fp.A, st, &sb))) return rc;
-  const KvPoolParams *pd = nullptr;
-  const KvTask *td = nullptr;
-  if ((rc = stage_fused(ctx, fp, st, &b, &pd, &td))) return rc;
-  double t1 = now_s();
-  phase_add(kPhStage, t1 - t0);
-  const int na = fp.has_a ? fp.A.n_pools : 0, np = fp.has_p ? fp.P.n_pools : 0;
-  const int nta = fp.has_a ? (int)fp.A.tasks.size() : 0;
-  const int ntot = nta + (fp.has_p ? (int)fp.P.tasks.size() : 0);
-  if (ntot > 0) {
-    if (ev_step && ev_step->ev_kernel_start)
-      CU(cudaEventRecord(static_cast<cudaEvent_t>(ev_step->ev_kernel_start), st));
-    CU(launch_fused(td, nta, ntot, pd, na, np, p0->geom_dev(), copy_grid(p0->device, ntot), st));
-    if (ev_step && ev_step->ev_kernel_end)
-      CU(cudaEventRecord(static_cast<cudaEvent_t>(ev_step->ev_kernel_end), st));
-    g_launches++;
-    p0->kernels++;
-  }
-  if (sb && (rc = ctx->done(sb, st))) return rc;
-  rc = ctx->done(b, st);
-  phase_add(kPhEnqA, now_s() - t1);
-  return rc;
-}
-
-}  // namespace
-
-// Single-stream, software-pipelined decode loop: launch k carries the append of
-// step k AND the publication of step k-1 (disjoint slots, see kv_step_fused_kernel),
-// a last launch publishes step n-1.  Same work as kv_run_steps, half the launches,
-// no cross-stream event; the publication of a step trails its append by one launch
-// -- the overlap of replication with the next step's compute of P:229.
-KV_API int kv_run_steps_fused(int32_t n_steps, const kv_step_t *steps, void *stream) {
-  for (int k = 0; k < n_steps && steps; ++k)
-    if (any_shared(steps[k]))
-      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps (append after ring-put k-1)");
-  if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int n_launch = n_steps + 1;  // + the flush of the last publication
-  if (n_steps < 8) {
-    thread_local FusedPrep fp;
-    for (int k = 0; k < n_launch; ++k) {
-      prepare_fused(steps, n_steps, k, fp);
-      if (fp.rc) return fp.rc;
-      int rc = issue_fused(k < n_steps ? &steps[k] : nullptr, fp, st);
-      if (rc) return rc;
-    }
-    return KV_OK;
-  }
-  FusedPrep ring[2];
-  std::atomic<int> produced{0}, consumed{0};
-  std::atomic<bool> stop{false};
-  std::thread worker([&]() {
-    for (int k = 0; k < n_launch && !stop.load(std::memory_order_acquire); ++k) {
-      const double w0 = now_s();
-      while (k - consumed.load(std::memory_order_acquire) >= 2) {
-        if (stop.load(std::memory_order_acquire)) return;
-        std::this_thread::yield();
-      }
-      phase_add(kPhWaitIssue, now_s() - w0);
-      const double t0 = now_s();
-      prepare_fused(steps, n_steps, k, ring[k & 1]);
-      phase_add(kPhPrepare, now_s() - t0);
-      produced.store(k + 1, std::memory_order_release);
-      if (ring[k & 1].rc) return;
-    }
-  });
-  int rc = KV_OK;
-  for (int k = 0; k < n_launch; ++k) {
-    const double w0 = now_s();
-    while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
-    phase_add(kPhWaitPrep, now_s() - w0);
-    FusedPrep &fp = ring[k & 1];
-    if (fp.rc) {
-      rc = fp.rc;
-      g_err = fp.err;
-      break;
-    }
-    rc = issue_fused(k < n_steps ? &steps[k] : nullptr, fp, st);
-    consumed.store(k + 1, std::memory_order_release);
-    if (rc) break;
-  }
-  stop.store(true, std::memory_order_release);
-  worker.join();
-  return rc;
-}
-
-// ---- single-stream decode loop with programmatic dependent launch ----------------
-namespace {
-
-// One step of the PDL loop: launches whose descriptors fit the parameter space go
-// inline with the PDL attribute (no copy node between kernels); larger ones (bulk
-// prefill steps) are staged by one H2D and launched normally -- that step
-// serialises, the kernels' griddepcontrol calls are then no-ops.
-int issue_step_pdl(const kv_step_t &st, int k, StepPrep &sp, cudaStream_t s) {
-  (void)k;
-  kv_pool *p0 = sp.has_a ? sp.A.p0 : (sp.has_p ? sp.P.p0 : nullptr);
-  if (!p0 || p0->device < 0) return KV_OK;
-  DeviceGuard dg(p0->device);
-  const bool has_a = sp.has_a && !sp.A.tasks.empty(), has_p = sp.has_p && !sp.P.tasks.empty();
-  if (sp.has_a)
-    for (size_t q = 0; q < sp.A.host_src_bytes.size(); ++q)
-      if (sp.A.host_src_bytes[q])
-        return fail(KV_EINVAL, "KV_SRC_HOST is not supported by kv_run_steps_pdl");
-  const bool inl_a = has_a && sp.inl_a, inl_p = has_p && sp.inl_p;  // filled by prepare_step
-  const double t0 = now_s();
-  DeviceCtx *ctx = ctx_for(p0->device);
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  Launch *ls[2];
-  int nl = 0;
-  if (has_a && !inl_a) ls[nl++] = &sp.A;
-  if (has_p && !inl_p) ls[nl++] = &sp.P;
-  StageBuf *b = nullptr;
-  int rc = KV_OK;
-  if (nl && (rc = stage(ctx, ls, nl, s, &b))) return rc;
-  const double t1 = now_s();
-  phase_add(kPhStage, t1 - t0);
-  if (has_a) {
-    if (st.ev_append_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_start), s));
-    if (inl_a) {
-      if ((rc = enqueue_inline(sp.A, *sp.da, s, true))) return rc;
-    } else if ((rc = enqueue(sp.A, s))) {
-      return rc;
-    }
-    if (st.ev_append_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_append_end), s));
-  }
-  const double t2 = now_s();
-  phase_add(kPhEnqA, t2 - t1);
-  if (has_p) {
-    if (st.ev_kernel_start) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_start), s));
-    if (inl_p) {
-      if ((rc = enqueue_inline(sp.P, *sp.dp, s, true))) return rc;
-    } else if ((rc = enqueue(sp.P, s))) {
-      return rc;
-    }
-    if (st.ev_kernel_end) CU(cudaEventRecord(static_cast<cudaEvent_t>(st.ev_kernel_end), s));
-  }
-  if (b && (rc = ctx->done(b, s))) return rc;
-  phase_add(kPhEnqP, now_s() - t2);
-  return KV_OK;
-}
-
-}  // namespace
-
-// Single-stream decode loop with programmatic dependent launch: per step the
-// append and the publication are launched back to back on ONE stream with the
-// PDL attribute, descriptors travel in the kernel parameter space (inline), and the
-// kernels order themselves with griddepcontrol (see kvring_kernels.cu): the
-// publication of step k starts as soon as append k completes and runs while append
-// k+1 copies -- the overlap the paper gets from a separate stream, without
-// a cross-stream event per step.  A helper thread prepares step k+1 meanwhile.
-KV_API int kv_run_steps_pdl(int32_t n_steps, const kv_step_t *steps, void *stream) {
-  if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
-  for (int k = 0; k < n_steps; ++k)
-    if (any_shared(steps[k]))
-      return fail(KV_EINVAL, "shared-capacity pools need kv_run_steps (append after ring-put k-1)");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  StepPrep ring[2];
-  std::atomic<int> produced{0}, consumed{0};
-  std::atomic<bool> stop{false};
-  std::thread worker([&]() {
-    for (int k = 0; k < n_steps && !stop.load(std::memory_order_acquire); ++k) {
-      const double w0 = now_s();
-      while (k - consumed.load(std::memory_order_acquire) >= 2) {
-        if (stop.load(std::memory_order_acquire)) return;
-        std::this_thread::yield();
-      }
-      phase_add(kPhWaitIssue, now_s() - w0);
-      const double t0 = now_s();
-      prepare_step(steps[k], ring[k & 1]);
-      phase_add(kPhPrepare, now_s() - t0);
-      produced.store(k + 1, std::memory_order_release);
-      if (ring[k & 1].rc) return;
-    }
-  });
-  int rc = KV_OK;
-  for (int k = 0; k < n_steps; ++k) {
-    const double w0 = now_s();
-    while (produced.load(std::memory_order_acquire) <= k) std::this_thread::yield();
-    phase_add(kPhWaitPrep, now_s() - w0);
-    StepPrep &sp = ring[k & 1];
-    if (sp.rc) {
-      rc = sp.rc;
-      g_err = sp.err;
-      break;
-    }
-    rc = issue_step_pdl(steps[k], k, sp, s);
-    consumed.store(k + 1, std::memory_order_release);
-    if (rc) break;
-  }
-  stop.store(true, std::memory_order_release);
-  worker.join();
-  return rc;
 }

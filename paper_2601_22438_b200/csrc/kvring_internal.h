@@ -1,5 +1,5 @@
 // Internal types shared by the host core (kvring_host.cpp) and the sm_100a
-// kernels (kvring_kernels.cu).  Not part of the ABI.
+// kernels (kvring_kernels.cu, kvring_step.cu).  Not part of the ABI.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -82,89 +82,111 @@ struct alignas(16) KvPackedHeader {
 };
 constexpr int kPackedMagic = 0x4B565042;
 
-// Launch wrappers (kvring_kernels.cu).  All return the cudaError_t of the launch.
-enum KernelKind : int { kKindAppend = 0, kKindRingPut = 1, kKindRestore = 2, kKindPack = 3,
-                        kKindRingPutCopy = 4, kKindPublish = 5 };
+// Launch wrappers of the host-task kernels (kvring_kernels.cu): restore-remap, the
+// NCCL-variant gather-pack, and the host-task ring-put that the shared-capacity
+// (holder-allocated replica ids) and copy-engine links use.  All return the
+// cudaError_t of the launch.
+enum KernelKind : int { kKindRingPut = 1, kKindRestore = 2, kKindPack = 3 };
 constexpr int kMaxPoolsPerLaunchHost = 64;
-// Per-pool source / destination bases passed by value in the kernel parameter
-// space (hot kernels): the only parameters on the path to a CTA's first data load.
-constexpr int kInlinePools = 8;
-struct KvParamPack {
-  const char *src[kInlinePools];
-  char *dst[kInlinePools];
-  int n;  // 0: read them from the staged global copy
-};
-// split: each task is processed as `split` CTA units (a contiguous share of its
-// slices each), so the host emits whole-item tasks (<= 32 KiB) and the device still
-// spreads a decode step over every resident CTA; the publication counts units.
 cudaError_t launch_copy(int kind, const KvTask *tasks, int n_tasks, const KvPoolParams *params,
-                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream,
-                        const KvPoolParams *host_params = nullptr, int split = 1);
-cudaError_t launch_fused(const KvTask *tasks, int n_append, int n_tasks, const KvPoolParams *params,
-                         int n_app_pools, int n_rep_pools, const KvGeomDev &g, int grid,
-                         cudaStream_t stream);
-// A launch carried entirely in the kernel's parameter space (<= 32 KiB since
-// CUDA 12.1): per-pool parameters, the ring-put's publication tables and the task
-// list.  No H2D staging copy and no dependent global load before a CTA's first
-// data load; ring-put pools carry their table offsets (into `data`) in
-// slot_req / slot_len.
-// Size classes: the launch copies the whole parameter block (the driver's copy
-// costs ~0.2 us per KiB on the host), so a launch pays for the smallest class its
-// tables + tasks fit: 4, 8, 16 or 28 KiB.
-constexpr int kInlineBytes = 28 * 1024;
-template <int CAP>
-struct KvInlineDescT {
-  int32_t n_tasks, n_pools, task_off, used;  // used: bytes of data in use
-  int32_t split, pad0, pad1, pad2;           // CTA units per task (see launch_copy)
-  KvPoolParams pools[kInlinePools];
-  alignas(16) char data[CAP];
-};
-using KvInlineDesc = KvInlineDescT<kInlineBytes>;
-cudaError_t launch_copy_inline(int kind, const KvInlineDesc &d, const KvGeomDev &g, int grid,
-                               cudaStream_t stream, bool pdl);
-// Self-describing graph steps (kv_run_steps_graph, fixed nodes): step i of a group
-// reads its launches from this header at the start of the group's staged slot, so
-// the graph's kernel nodes keep fixed parameters (slot base, step index) and the host
-// updates nothing per step but the slot contents.  [0] = append, [1] = ring-put.
-struct alignas(16) KvStepHdr {
-  int32_t n_tasks[2];
-  int32_t n_pools[2];
-  int32_t split[2];
-  int32_t pad[2];
-  unsigned long long params_off[2];
-  unsigned long long tasks_off[2];
-  KvGeomDev g;
-};
-constexpr int kFxPublishGrid = 64;  // publication node: one CTA per pool, up to 64 pools
-// Fills kp for a fixed-node kernel (kKindAppend / kKindRingPutCopy / kKindPublish)
-// reading step `i` of the slot at `slot`; a must outlive the call consuming kp.
-struct KvFxArgs {
-  const char *slot = nullptr;
-  int step = 0;
-  void *ptrs[2] = {};
-};
-void fx_node_params(int kind, int grid, KvFxArgs &a, cudaKernelNodeParams &kp);
-
-// Arguments of a staged append / ring-put launch as a CUDA graph kernel node (the
-// graph decode loop updates them per step with cudaGraphExecKernelNodeSetParams).
-struct KvNodeArgs {
-  const KvTask *tasks = nullptr;
-  int n_tasks = 0;
-  const KvPoolParams *params = nullptr;
-  KvGeomDev g{};
-  int n_pools = 0;
-  KvParamPack pk{};
-  int split = 1;
-  void *ptrs[7] = {};
-};
-// Fills kp (function, grid, block, argument pointers into a) for kind
-// kKindAppend / kKindRingPut; a must outlive the call that consumes kp.
-void kernel_node_params(int kind, int grid, KvNodeArgs &a, cudaKernelNodeParams &kp);
+                        int n_pools, const KvGeomDev &g, int grid, cudaStream_t stream);
 cudaError_t launch_unpack(const char *packed, char *replica, char *meta,
                           unsigned long long *counter, const KvGeomDev &g, int grid,
                           cudaStream_t stream);
 cudaError_t launch_meta_init(char *meta, int R, int M, cudaStream_t stream);
+// 1-CTA acquire of a holder's metadata (kv_restore): ld.acquire.sys of seq, then a copy
+// of header + tables into `out` (device scratch).
+cudaError_t launch_meta_acquire(const char *meta, char *out, size_t bytes, cudaStream_t stream);
 int copy_grid(int device, int n_tasks);
 int resident_ctas(int device);
+
+// ---------------------------------------------------------------------------
+// Decode-step engine (kvring_step.cu): ONE launch carries the appends of a step
+// (host-built items: the allocator is the host's) and/or the publication of a
+// step whose work list the DEVICE derives (§8(a) a3) from per-slot
+// (req_id, len, pub_len) snapshots and the pool's device-resident block table.
+// Every byte moved by the launch is one flat space of 16-B chunks split evenly
+// over the CTAs (append chunks and replication chunks each), so the launch is
+// balanced however the step mixes prefill, decode and publication.
+
+// Unsigned 32-bit division by an invariant d >= 1 (Granlund-Montgomery, Hacker's
+// Delight 10-8): l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1,
+// t = umulhi(m, x), q = (t + ((x - t) >> sh1)) >> sh2, sh1 = min(l, 1), sh2 = max(l - 1, 0).
+struct KvDiv {
+  uint32_t d, m, sh1, sh2;
+};
+inline KvDiv kv_div(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  KvDiv r;
+  r.d = d;
+  r.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1ull);
+  r.sh1 = l < 1 ? l : 1;
+  r.sh2 = l > 1 ? l - 1 : 0;
+  return r;
+}
+
+// One append item: n tokens of one request slot that land in ONE block.  Its slices
+// occupy the flat range [off, next item's off) in token-major order (slice x of the
+// item = token x / combos, (layer, K/V, head) x % combos).
+struct alignas(8) KvAppItem {
+  int32_t off;    // first slice (flat, over every item of the launch)
+  int32_t row;    // first token row in the pool's dense source
+  int32_t blk;    // destination block id (host allocator)
+  int32_t p0;     // position of the item's first token (j = p0 / B, slot in block = p0 % B)
+  int16_t slot;   // request slot: the item writes bt[slot][j] = blk on the device
+  int16_t pool;   // index into KvStepHdr::app
+};
+static_assert(sizeof(KvAppItem) == 24, "KvAppItem must be 24 B");
+
+struct alignas(16) KvStepPool {
+  const char *src;        // append: dense source; replicate: this pool
+  char *dst;              // append: this pool; replicate: successor replica region
+  char *meta;             // replicate: successor metadata (include/kvring.h layout)
+  int32_t *bt;            // device block table [R][M] of the pool (append writes, replicate reads)
+  unsigned long long step;  // replicate: seq to publish
+  int32_t R, M;
+  int32_t n_slots;        // replicate: table entries (slots >= n_slots publish (-1, 0))
+  int32_t ent_off;        // replicate: index of the pool's first entry
+  int32_t mode;           // KV_MODE_TOKENS / KV_MODE_BLOCKS
+  int32_t abort_slices;   // replicate: -1, or copy only the first N slices and never publish
+  int32_t writer_node;
+  int32_t sys;            // successor is not this GPU's HBM: system-scope publication
+};
+
+constexpr int kStepPools = 8;      // pools per launch (each role)
+constexpr int kStepMaxEnt = 4096;  // replicate table entries per launch (sum of n_slots)
+
+struct alignas(16) KvStepHdr {
+  int32_t n_app, n_rep;             // pools per role
+  int32_t n_items, n_ent;           // append items; replicate entries
+  int32_t items_off, req_off, len_off, pub_off;  // byte offsets into the data blob
+  int32_t data_bytes;               // bytes of the data blob (a multiple of 16)
+  int32_t app_slices;               // total append slices (end of the last item)
+  int32_t publish;                  // some replicate pool publishes this launch
+  int32_t any_abort;
+  int32_t sys_any;
+  int32_t pad0;
+  unsigned long long *counter;      // completion counter (the last CTA resets it to 0)
+  KvGeomDev g;
+  KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)
+  KvDiv div_b;                      // block size
+  KvStepPool app[kStepPools];
+  KvStepPool rep[kStepPools];
+};
+
+// Data blob carried in the kernel parameter space for small launches.
+constexpr int kStepInline = 24 * 1024;
+template <int CAP>
+struct alignas(16) KvStepInlT {
+  KvStepHdr h;
+  alignas(16) char data[CAP];
+};
+// Launches the step kernel: data in the parameter space when data_bytes <= kStepInline
+// (4/8/16/24 KiB classes), else read from `gdata` (device copy of the blob).
+cudaError_t launch_step(const KvStepHdr &h, const char *host_data, const char *gdata, int grid,
+                        cudaStream_t stream);
+int step_smem_bytes(const KvStepHdr &h);
+const void *step_kernel_fn();
 
 }  // namespace kvring

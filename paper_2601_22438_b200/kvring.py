@@ -27,9 +27,9 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_pool_destroy", "kv_query", "kv_release", "kv_replicate_step",
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
-            "kv_plan_targets", "kv_set_mode", "kv_run_steps_fused", "kv_run_steps_pdl",
-            "kv_replicate_step_ce", "kv_set_successor_shared", "kv_drop_replicas",
-            "kv_run_steps_graph"]
+            "kv_plan_targets", "kv_set_mode", "kv_replicate_step_ce",
+            "kv_set_successor_shared", "kv_drop_replicas", "kv_loop_create", "kv_loop_destroy",
+            "kv_loop_step", "kv_loop_run", "kv_loop_flush", "kv_launch_log"]
 
 
 class KvError(RuntimeError):
@@ -127,11 +127,14 @@ def lib() -> ctypes.CDLL:
             "kv_sync": (ctypes.c_int, [_P]),
             "kv_time_next_launch": (ctypes.c_int, [_P, _P]),
             "kv_run_steps": (ctypes.c_int, [_I32, _P, _P, _P]),
-            "kv_run_steps_fused": (ctypes.c_int, [_I32, _P, _P]),
-            "kv_run_steps_pdl": (ctypes.c_int, [_I32, _P, _P]),
+            "kv_loop_create": (ctypes.c_int, [ctypes.POINTER(_P)]),
+            "kv_loop_destroy": (ctypes.c_int, [_P]),
+            "kv_loop_step": (ctypes.c_int, [_P, _P, _P]),
+            "kv_loop_run": (ctypes.c_int, [_P, _I32, _P, _P]),
+            "kv_loop_flush": (ctypes.c_int, [_P, _P]),
+            "kv_launch_log": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_replicate_step_ce": (ctypes.c_int, [_I32, _P, _U64, _P]),
             "kv_set_successor_shared": (ctypes.c_int, [_P, _P]),
-            "kv_run_steps_graph": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_drop_replicas": (ctypes.c_int, [_P]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
@@ -274,17 +277,41 @@ def kv_run_steps(prepared: "PreparedSteps", append_stream: int = 0, repl_stream:
                               repl_stream))
 
 
-def kv_run_steps_graph(prepared: "PreparedSteps", append_stream: int, repl_stream: int) -> None:
-    _check(lib().kv_run_steps_graph(prepared.n, ctypes.addressof(prepared.arr), append_stream,
-                                    repl_stream))
+class KvLoop:
+    """One-launch-per-step decode loop (kv_loop_*): each step's launch carries its
+    appends and the previous step's publication."""
+
+    def __init__(self):
+        h = _P()
+        _check(lib().kv_loop_create(ctypes.byref(h)))
+        self.h = h.value
+
+    def step(self, prepared: "PreparedSteps", k: int = 0, stream: int = 0) -> None:
+        _check(lib().kv_loop_step(self.h, ctypes.addressof(prepared.arr) +
+                                  k * ctypes.sizeof(kv_step_t), stream))
+
+    def run(self, prepared: "PreparedSteps", stream: int = 0) -> None:
+        _check(lib().kv_loop_run(self.h, prepared.n, ctypes.addressof(prepared.arr), stream))
+
+    def flush(self, stream: int = 0) -> None:
+        _check(lib().kv_loop_flush(self.h, stream))
+
+    def destroy(self) -> None:
+        if self.h:
+            _check(lib().kv_loop_destroy(self.h))
+            self.h = None
 
 
-def kv_run_steps_fused(prepared: "PreparedSteps", stream: int = 0) -> None:
-    _check(lib().kv_run_steps_fused(prepared.n, ctypes.addressof(prepared.arr), stream))
-
-
-def kv_run_steps_pdl(prepared: "PreparedSteps", stream: int = 0) -> None:
-    _check(lib().kv_run_steps_pdl(prepared.n, ctypes.addressof(prepared.arr), stream))
+def kv_launch_log(start: bool, cap: int = 1 << 16):
+    """start=True clears and starts the calling thread's launch log; start=False stops
+    it and returns a list of dicts (kind, app_bytes, rep_bytes, grid, blob_bytes)."""
+    if start:
+        lib().kv_launch_log(None, 0, 1)
+        return []
+    out = np.zeros(5 * cap, dtype=np.uint64)
+    n = lib().kv_launch_log(_ptr(out), cap, 0)
+    keys = ("kind", "app_bytes", "rep_bytes", "grid", "blob_bytes")
+    return [dict(zip(keys, (int(x) for x in out[5 * i:5 * i + 5]))) for i in range(min(n, cap))]
 
 
 def kv_replicate_step(p: int, step: int, stream: int = 0) -> None:
@@ -313,8 +340,8 @@ def kv_replicate_step_ce(pools, step: int, stream: int = 0) -> None:
     _check(lib().kv_replicate_step_ce(len(pools), ctypes.addressof(arr), step, stream))
 
 
-def kv_inject_abort(p: int, tasks: int) -> None:
-    _check(lib().kv_inject_abort(p, tasks))
+def kv_inject_abort(p: int, slices: int) -> None:
+    _check(lib().kv_inject_abort(p, slices))
 
 
 def kv_fail_stage(p: int, stream: int = 0) -> None:
@@ -392,15 +419,12 @@ def kv_plan_targets(succ, excluded=None):
     return [int(x) for x in out]
 
 
-HOST_PHASES = ["prepare", "wait_prepare", "stage_h2d", "launch_append", "launch_publish",
-               "events", "worker_wait_issue", "stage.acquire_wait", "stage.host_copy",
-               "stage.h2d_call", "prepare.append", "prepare.replicate", "prepare.commit",
-               "publish.stage", "n_inline_launches", "n_staged_launches"]
+HOST_PHASES = ["prepare.append", "prepare.replicate", "stage", "launch"]
 
 
 def kv_host_profile(reset: bool = True) -> dict:
-    out = np.zeros(16, dtype=np.float64)
-    n = lib().kv_host_profile(_ptr(out), 16, 1 if reset else 0)
+    out = np.zeros(len(HOST_PHASES), dtype=np.float64)
+    n = lib().kv_host_profile(_ptr(out), len(HOST_PHASES), 1 if reset else 0)
     return {HOST_PHASES[i] if i < len(HOST_PHASES) else str(i): float(out[i]) for i in range(n)}
 
 

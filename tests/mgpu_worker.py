@@ -61,12 +61,13 @@ def main():
     if transport == "nccl":
         from paper_2601_22438_b200.nccl_compare import NcclRing
         nccl = NcclRing(rt, 64 << 20)
-    if transport in ("runsteps", "graph"):
+    if transport in ("runsteps", "loop"):
         # the bench's launch path: kv_run_steps on two streams (helper-thread prepare,
         # inline descriptors, system-scope publication over NVLink), in chunks around
         # the failure step
         comp = torch.cuda.current_stream(dev)
         repl = torch.cuda.Stream(dev)
+        kl = K.KvLoop()
         keep = []
 
         def chunk(t0, t1):
@@ -86,8 +87,11 @@ def main():
                 oring.appends(tt)
                 if tt >= 1:
                     oring.replicate(tt)
-            run = K.kv_run_steps_graph if transport == "graph" else K.kv_run_steps
-            run(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+            if transport == "loop":
+                kl.run(K.PreparedSteps(sts), comp.cuda_stream)
+                kl.flush(comp.cuda_stream)
+            else:
+                K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
             torch.cuda.synchronize(dev)
             dist.barrier()
             compare_state(rt, drv, oring, tag=f"rank {rank} run_steps {t0}..{t1 - 1}")
@@ -104,7 +108,7 @@ def main():
         torch.cuda.synchronize(dev)
         dist.barrier()
         chunk(cfg.fail_step + 1, cfg.n_steps)
-    for t in range(cfg.n_steps if transport not in ("runsteps", "graph") else 0):
+    for t in range(cfg.n_steps if transport not in ("runsteps", "loop") else 0):
         drv.append_step(t)
         oring.appends(t)
         if t == cfg.fail_step:

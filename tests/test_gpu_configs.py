@@ -141,11 +141,11 @@ def test_c5_bulk_replication_and_restore(copy_engine):
         rt.destroy()
 
 
-@pytest.mark.parametrize("loop", ["graph", "streams"])
+@pytest.mark.parametrize("loop", ["loop", "streams"])
 def test_c2_full_geometry_whole_arrays(loop):
     """C2 at BASELINE's full geometry in the bench's launch configurations (4 pools of
-    12,288 x 512 KiB blocks on one GPU; kv_run_steps_graph -- the bench default on one
-    GPU -- and kv_run_steps with two streams), 160 steps:
+    12,288 x 512 KiB blocks on one GPU; the one-launch-per-step kv_loop -- the bench
+    default -- and kv_run_steps with two streams), 160 steps:
     whole pools, whole replica regions and metadata == the oracle in content mode.
     The oracle holds the first 2,048 blocks (lowest-free-id allocation gives the same
     block ids while use stays below that; asserted) and every GPU block beyond them
@@ -176,16 +176,20 @@ def test_c2_full_geometry_whole_arrays(loop):
         for n in oring.nodes.values():
             assert max([b for s in range(n.R) for b in n.slot_bt[s]] + [0]) < 2048
         K.kv_host_profile(reset=True)
-        if loop == "graph":
-            K.kv_run_steps_graph(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+        K.kv_launch_log(True)
+        if loop == "loop":
+            kl = K.KvLoop()
+            kl.run(K.PreparedSteps(sts), comp.cuda_stream)
+            kl.flush(comp.cuda_stream)
+            kl.destroy()
         else:
             K.kv_run_steps(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
         torch.cuda.synchronize()
-        prof = K.kv_host_profile(reset=True)
-        if loop == "streams":
-            # both launch paths ran: decode steps with descriptors in the kernel parameter
-            # space, prefill-heavy steps staged in global memory
-            assert prof["n_inline_launches"] > 0 and prof["n_staged_launches"] > 0, prof
+        log = K.kv_launch_log(False)
+        # both descriptor paths ran: decode steps in the kernel parameter space,
+        # prefill-heavy steps (the admissions of step 0) from a device copy
+        assert any(r["blob_bytes"] <= 24576 for r in log) and \
+            any(r["blob_bytes"] > 24576 for r in log), [r["blob_bytes"] for r in log[:4]]
         sentinel = np.int16(np.uint16(0x5A5A).view(np.int16))
         for c, gid in drv.coords.items():
             on = oring.nodes[c]

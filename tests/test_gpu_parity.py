@@ -109,11 +109,12 @@ def test_other_head_geometries_bit_exact(heads, head_dim, block):
     rt.destroy()
 
 
-@pytest.mark.parametrize("loop", ["direct", "graph"])
+@pytest.mark.parametrize("loop", ["direct", "loop"])
 def test_abort_mid_step_keeps_last_published_replica(loop):
     """A stage dying mid-replicate leaves its successor's replica at the last
-    published step (R7/R9): restore == oracle restore of the previous step.  graph:
-    the steps run through kv_run_steps_graph (split publication node)."""
+    published step (R7/R9): restore == oracle restore of the previous step.  loop:
+    the steps run through the one-launch-per-step loop (kv_loop_*), the aborted
+    publication being the pending one launched by kv_loop_flush."""
     from paper_2601_22438_b200 import kvring as K
     cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
                          batch_cap=6, n_requests=60, n_steps=30, fixed_prompt=None,
@@ -122,7 +123,7 @@ def test_abort_mid_step_keeps_last_published_replica(loop):
     rt, drv = make_gpu(cfg, schedules=sched)
     keep = []
 
-    def graph_run(t0, t1):
+    def loop_run(kl, t0, t1):
         sts = []
         for t in range(t0, t1):
             app = []
@@ -134,22 +135,22 @@ def test_abort_mid_step_keeps_last_published_replica(loop):
                                 req_ids=e["req_ids"], n_new=e["n_new"], src=src))
             pools = [rt.handle(n) for n in rt.alive_local()]
             sts.append(dict(append=app, repl_pools=pools if t >= 1 else [], step=t))
-        K.kv_run_steps_graph(K.PreparedSteps(sts), torch.cuda.current_stream().cuda_stream,
-                             repl.cuda_stream)
+        kl.run(K.PreparedSteps(sts), torch.cuda.current_stream().cuda_stream)
 
-    repl = torch.cuda.Stream()
     try:
         T = 20
-        if loop == "graph":
-            graph_run(0, T - 1)
-            K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 3)   # 3 copy tasks, no publish
-            graph_run(T - 1, T)
+        if loop == "loop":
+            kl = K.KvLoop()
+            loop_run(kl, 0, T)                                    # step T-1 pending
+            K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 300)  # 300 slices, no publish
+            kl.flush(torch.cuda.current_stream().cuda_stream)
+            kl.destroy()
         else:
             for t in range(T):
                 drv.append_step(t)
                 if t >= 1:
                     if t == T - 1:
-                        K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 3)   # no publish
+                        K.kv_inject_abort(rt.handle(drv.coords[(0, 1)]), 300)   # no publish
                     rt.replicate_all(t)
         torch.cuda.synchronize()
         holder = drv.coords[(0, 2)]
@@ -321,8 +322,10 @@ def test_run_steps_two_streams_bit_exact(shared):
         if shared:
             assert sum(n.evictions for n in oring.nodes.values()) > 0
             assert sum(n.drops for n in oring.nodes.values()) > 0
-            with pytest.raises(K.KvError):     # the PDL / fused loops refuse shared pools
-                K.kv_run_steps_pdl(K.PreparedSteps(steps[:1]), comp.cuda_stream)
+            kl = K.KvLoop()
+            with pytest.raises(K.KvError):     # the one-launch loop refuses shared pools
+                kl.run(K.PreparedSteps(steps[:1]), comp.cuda_stream)
+            kl.destroy()
     finally:
         rt.destroy()
 
@@ -458,47 +461,34 @@ def test_restore_errors_and_edge_cases():
         rt.destroy()
 
 
-@pytest.mark.parametrize("n_steps", [6, 30])
-def test_run_steps_fused_bit_exact(n_steps):
-    """kv_run_steps_fused (append of step k + publication of step k-1 in one launch,
-    final flush): whole arrays == oracle after the run (6 steps: inline path, 30:
-    helper-thread path)."""
+def _loop_steps(rt, drv, t0, t1, keep):
     from paper_2601_22438_b200 import kvring as K
-    cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
-                         batch_cap=6, n_requests=60, n_steps=n_steps, fixed_prompt=None,
-                         fail_node=None, fail_step=None)
-    sched = _churn_sched(cfg, 31)
-    rt, drv = make_gpu(cfg, schedules=sched)
-    oring = OracleRing(cfg, schedules=sched)
-    try:
-        steps, keep = [], []
-        for t in range(cfg.n_steps):
-            app = []
-            for node, e in drv.plan(t).items():
-                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
-                src = drv.content(e["stage"], ids, pos) if ids else None
-                keep.append(src)
-                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
-                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
-            pools = [rt.handle(n) for n in rt.alive_local()] if t >= 1 else []
-            steps.append(dict(append=app, repl_pools=pools, step=t))
-            oring.appends(t)
-            if t >= 1:
-                oring.replicate(t)
-        prep = K.PreparedSteps(steps)
-        torch.cuda.synchronize()
-        K.kv_run_steps_fused(prep, torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        compare_state(rt, drv, oring, tag="fused")
-    finally:
-        rt.destroy()
+    sts = []
+    for t in range(t0, t1):
+        app = []
+        for node, e in drv.plan(t).items():
+            if node not in rt.local:
+                continue
+            ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+            src = drv.content(e["stage"], ids, pos) if ids else None
+            keep.append(src)
+            app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                            req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+        pools = [rt.handle(n) for n in rt.alive_local() if rt.succ.get(n) is not None]
+        sts.append(dict(append=app, repl_pools=pools if t >= 1 else [], step=t))
+    return K.PreparedSteps(sts)
 
 
-@pytest.mark.parametrize("n_steps,fail", [(5, False), (30, False), (41, True)])
-def test_run_steps_graph_bit_exact(n_steps, fail):
-    """kv_run_steps_graph (one CUDA graph per 8 steps, two streams, event-chained
-    groups; partial last group) == oracle, whole arrays, churn; with `fail` a stage fails
-    mid-run (restore through the C ABI between two graph runs)."""
+@pytest.mark.parametrize("n_steps,fail,every", [(6, False, 0), (40, False, 7), (41, True, 0),
+                                                (33, True, 5)])
+def test_loop_bit_exact(n_steps, fail, every):
+    """The one-launch-per-step loop (kv_loop_step: appends of step k + the publication
+    of step k-1 in ONE kernel, per-step calls, no lookahead) == oracle, whole arrays,
+    churn.  `every`: flush and compare every few steps.  With `fail` a stage fails after
+    the appends of step 19 while step 19's publication is pending: fail, restore and
+    relink run between two kv_loop_step calls and the pending publication follows the
+    sequential protocol (dead pool dropped, predecessor re-seeded into the fresh pool,
+    which publishes step 19 itself)."""
     from paper_2601_22438_b200 import kvring as K
     cfg = configs.scaled(configs.C1, num_blocks=96, max_reqs=12, max_blocks_per_req=12,
                          batch_cap=6, n_requests=60, n_steps=n_steps, fixed_prompt=None,
@@ -506,53 +496,38 @@ def test_run_steps_graph_bit_exact(n_steps, fail):
     sched = _churn_sched(cfg, 33)
     rt, drv = make_gpu(cfg, schedules=sched)
     oring = OracleRing(cfg, schedules=sched)
-    comp = torch.cuda.current_stream()
-    repl = torch.cuda.Stream()
+    st = torch.cuda.current_stream().cuda_stream
+    kl = K.KvLoop()
     keep = []
-
-    def run(t0, t1):
-        sts = []
-        for t in range(t0, t1):
-            app = []
-            for node, e in drv.plan(t).items():
-                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
-                src = drv.content(e["stage"], ids, pos) if ids else None
-                keep.append(src)
-                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
-                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
-            pools = [rt.handle(n) for n in rt.alive_local() if rt.succ.get(n) is not None]
-            sts.append(dict(append=app, repl_pools=pools if t >= 1 else [], step=t))
+    try:
+        for t in range(n_steps):
+            prep = _loop_steps(rt, drv, t, t + 1, keep)
+            kl.step(prep, 0, st)
             oring.appends(t)
+            if fail and t == cfg.fail_step:
+                dst, _ = drv.fail_and_restore(t, cfg.fail_node)
+                oring.fail_and_restore(t, cfg.fail_node)
+                # the fresh pool is not in the loop's pending list: it publishes step t
+                # directly, like every alive linked node of the sequential protocol
+                rt.replicate_all(t, nodes=[dst])
             if t >= 1:
                 oring.replicate(t)
-        K.kv_run_steps_graph(K.PreparedSteps(sts), comp.cuda_stream, repl.cuda_stream)
+            if every and t % every == every - 1:
+                kl.flush(st)
+                torch.cuda.synchronize()
+                compare_state(rt, drv, oring, tag=f"loop step {t}")
+        kl.flush(st)
         torch.cuda.synchronize()
-        compare_state(rt, drv, oring, tag=f"graph {t0}..{t1 - 1}")
-
-    try:
-        if not fail:
-            run(0, n_steps)
-        else:
-            run(0, cfg.fail_step)
-            t = cfg.fail_step
-            drv.append_step(t)
-            oring.appends(t)
-            drv.fail_and_restore(t, cfg.fail_node)
-            oring.fail_and_restore(t, cfg.fail_node)
-            rt.replicate_all(t)
-            oring.replicate(t)
-            torch.cuda.synchronize()
-            compare_state(rt, drv, oring, tag="after restore")
-            run(t + 1, n_steps)
+        compare_state(rt, drv, oring, tag="loop end")
     finally:
+        kl.destroy()
         rt.destroy()
 
 
 @pytest.mark.parametrize("n_steps", [12, 90])
-def test_run_steps_pdl_bit_exact(n_steps):
-    """kv_run_steps_pdl (one stream, programmatic dependent launch, zero-copy
-    descriptors; append k+1 overlaps the publication of step k): whole arrays ==
-    oracle; 90 steps wrap the 64-slot descriptor ring."""
+def test_loop_batched_run_bit_exact(n_steps):
+    """kv_loop_run (the bench's native loop over marshalled steps) == oracle; the
+    pending publication survives between two calls."""
     from paper_2601_22438_b200 import kvring as K
     cfg = configs.scaled(configs.C1, num_blocks=160, max_reqs=16, max_blocks_per_req=12,
                          batch_cap=8, n_requests=200, n_steps=n_steps, fixed_prompt=None,
@@ -560,28 +535,22 @@ def test_run_steps_pdl_bit_exact(n_steps):
     sched = _churn_sched(cfg, 41)
     rt, drv = make_gpu(cfg, schedules=sched)
     oring = OracleRing(cfg, schedules=sched)
+    kl = K.KvLoop()
+    keep = []
     try:
-        steps, keep = [], []
-        for t in range(cfg.n_steps):
-            app = []
-            for node, e in drv.plan(t).items():
-                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
-                src = drv.content(e["stage"], ids, pos) if ids else None
-                keep.append(src)
-                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
-                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
-            pools = [rt.handle(n) for n in rt.alive_local()] if t >= 1 else []
-            steps.append(dict(append=app, repl_pools=pools, step=t))
+        for t in range(n_steps):
             oring.appends(t)
             if t >= 1:
                 oring.replicate(t)
+        half = n_steps // 2
+        st = torch.cuda.current_stream().cuda_stream
+        kl.run(_loop_steps(rt, drv, 0, half, keep), st)
+        kl.run(_loop_steps(rt, drv, half, n_steps, keep), st)
+        kl.flush(st)
         torch.cuda.synchronize()
-        half = n_steps // 2            # two calls: the ring is drained between them
-        K.kv_run_steps_pdl(K.PreparedSteps(steps[:half]), torch.cuda.current_stream().cuda_stream)
-        K.kv_run_steps_pdl(K.PreparedSteps(steps[half:]), torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        compare_state(rt, drv, oring, tag="pdl")
+        compare_state(rt, drv, oring, tag="loop run")
     finally:
+        kl.destroy()
         rt.destroy()
 
 

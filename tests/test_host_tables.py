@@ -178,8 +178,8 @@ def test_plan_targets_matches_oracle_ring_walk():
     assert got[idx[(1, 1)]] == idx[(0, 1)] and got[idx[(3, 2)]] == idx[(2, 2)]
 
 
-def test_run_steps_fused_tables_match_oracle():
-    """The software-pipelined loop's host side (tables-only pools): after the final
+def test_loop_tables_match_oracle():
+    """The one-launch-per-step loop's host side (tables-only pools): after the final
     flush every table and the payload byte count equal the oracle's at C2 size."""
     cfg = configs.C2
     ring = OracleRing(cfg, content=False)
@@ -187,6 +187,7 @@ def test_run_steps_fused_tables_match_oracle():
     hs = {c: _pool(cfg, k) for k, c in enumerate(ring.coords)}
     for c in ring.coords:
         K.kv_set_successor(hs[c], 0, FAKE_PTR, cfg.num_blocks, FAKE_PTR)
+    loop = K.KvLoop()
     try:
         steps = []
         for t in range(150):
@@ -200,14 +201,51 @@ def test_run_steps_fused_tables_match_oracle():
                    for c in ring.coords]
             steps.append(dict(append=app, repl_pools=[hs[c] for c in ring.coords] if t >= 1 else [],
                               step=t))
-        K.kv_run_steps_fused(K.PreparedSteps(steps))
+        loop.run(K.PreparedSteps(steps))
+        for c in ring.coords:               # step 149's publication is still pending
+            assert K.kv_stats(hs[c])["last_step"] == 148
+        loop.flush()
         for c in ring.coords:
             assert _tables(hs[c], cfg.max_reqs) == ring.nodes[c].live()
             assert K.kv_stats(hs[c])["last_step"] == 149
+            req, ln, pub, nb = K.kv_dump_slots(hs[c], cfg.max_reqs)
+            assert (pub == ln).all()
         assert sum(K.kv_stats(hs[c])["bytes_replicated"] for c in ring.coords) == ring.moved
     finally:
+        loop.destroy()
         for h in hs.values():
             K.kv_pool_destroy(h)
+
+
+def test_loop_rejected_append_still_publishes_pending_step():
+    """when the appends of step k are rejected (KV_ENOMEM, all-or-nothing),
+    the publication of step k-1 that rides on the same launch still goes out, and the
+    host state matches the sequential protocol (publish k-1, append k rejected)."""
+    cfg = configs.scaled(configs.C1, num_blocks=6, max_reqs=4, max_blocks_per_req=8)
+    a = _pool(cfg, 0)
+    K.kv_set_successor(a, 1, FAKE_PTR, cfg.num_blocks, FAKE_PTR)
+    loop = K.KvLoop()
+    try:
+        ok = [dict(append=[dict(pool=a, begin_step=1, release=[], req_ids=[7], n_new=[40],
+                                src=None)], repl_pools=[a], step=1)]
+        loop.run(K.PreparedSteps(ok))                      # 3 blocks; step 1 pending
+        assert K.kv_stats(a)["last_step"] == 0
+        big = [dict(append=[dict(pool=a, begin_step=1, release=[], req_ids=[8], n_new=[60],
+                                 src=None)], repl_pools=[a], step=2)]
+        with pytest.raises(K.KvError) as e:                # needs 4 blocks, 3 free
+            loop.run(K.PreparedSteps(big))
+        assert e.value.code == K.KV_ENOMEM
+        st = K.kv_stats(a)
+        assert st["last_step"] == 1                        # step 1 was published anyway
+        assert st["bytes_replicated"] == 40 * 2 * 2 * 8 * 128 * 2
+        assert _tables(a, cfg.max_reqs) == {7: (0, 40, [0, 1, 2])}
+        req, ln, pub, nb = K.kv_dump_slots(a, cfg.max_reqs)
+        assert pub[0] == 40
+        loop.flush()                                       # nothing pending: no-op
+        assert K.kv_stats(a)["last_step"] == 1
+    finally:
+        loop.destroy()
+        K.kv_pool_destroy(a)
 
 
 @pytest.mark.parametrize("seed,nb,mode", [(0, 32, "tokens"), (1, 28, "tokens"), (3, 24, "tokens"),
@@ -261,31 +299,32 @@ def test_shared_capacity_tables_match_oracle(seed, nb, mode):
 
 
 def test_decode_loop_argument_errors():
-    """The native decode loops reject what they cannot run, before touching any pool:
-    the graph loop needs two distinct streams and device pools, and none of the
-    single-stream / graph loops takes shared-capacity pools (they need kv_run_steps'
-    append-after-previous-ring-put order) or, for the graph loop, host sources."""
+    """The one-launch loop rejects shared-capacity pools (they need kv_run_steps'
+    append-after-previous-publication order) before touching any pool; a pool can be
+    pending in one loop only."""
     cfg = configs.scaled(configs.C1, num_blocks=16, max_reqs=4, max_blocks_per_req=4)
     a, b = _pool(cfg, 0), _pool(cfg, 1)
+    l1, l2 = K.KvLoop(), K.KvLoop()
     try:
         K.kv_set_successor(a, 1, FAKE_PTR, cfg.num_blocks, FAKE_PTR)
         step = [dict(append=[dict(pool=a, begin_step=1, release=[], req_ids=[1], n_new=[3],
                                   src=None)], repl_pools=[a], step=1)]
-        prep = K.PreparedSteps(step)
-        with pytest.raises(K.KvError) as e:          # one stream for both roles
-            K.kv_run_steps_graph(prep, 0, 0)
-        assert e.value.code == K.KV_EINVAL
-        with pytest.raises(K.KvError) as e:          # tables-only pools launch nothing
-            K.kv_run_steps_graph(prep, 1, 2)
+        l1.run(K.PreparedSteps(step))
+        step2 = [dict(append=[], repl_pools=[a], step=2)]
+        with pytest.raises(K.KvError) as e:
+            l2.run(K.PreparedSteps(step2))
         assert e.value.code == K.KV_ESTATE
-        assert _tables(a, cfg.max_reqs) == {}        # nothing applied
+        l1.flush()
+        assert K.kv_stats(a)["last_step"] == 1
         K.kv_set_successor_shared(a, b)
-        for run in (lambda p: K.kv_run_steps_graph(p, 1, 2), lambda p: K.kv_run_steps_pdl(p),
-                    lambda p: K.kv_run_steps_fused(p)):
-            with pytest.raises(K.KvError) as e:
-                run(K.PreparedSteps(step))
-            assert e.value.code == K.KV_EINVAL
-        assert _tables(a, cfg.max_reqs) == {}
+        with pytest.raises(K.KvError) as e:
+            l1.run(K.PreparedSteps([dict(append=[dict(pool=a, begin_step=1, release=[],
+                                                      req_ids=[2], n_new=[3], src=None)],
+                                         repl_pools=[a], step=2)]))
+        assert e.value.code == K.KV_EINVAL
+        assert set(_tables(a, cfg.max_reqs)) == {1}
     finally:
+        l1.destroy()
+        l2.destroy()
         K.kv_pool_destroy(a)
         K.kv_pool_destroy(b)

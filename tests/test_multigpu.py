@@ -15,12 +15,13 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("n,transport", [(2, "p2p"), (2, "nccl"), (2, "runsteps"), (2, "graph"),
-                                         (4, "p2p"), (4, "nccl"), (4, "runsteps"), (4, "graph"),
+@pytest.mark.parametrize("n,transport", [(2, "p2p"), (2, "nccl"), (2, "runsteps"), (2, "loop"),
+                                         (4, "p2p"), (4, "nccl"), (4, "runsteps"), (4, "loop"),
                                          (8, "p2p")])
 def test_ring_over_nvlink_parity(n, transport):
     """p2p: fused ring-put over NVLink; nccl: the comparison transport (bit-exact too);
-    runsteps / graph: the native decode loops (kv_run_steps, kv_run_steps_graph) over
+    runsteps / loop: the native decode loops (kv_run_steps on two streams, the
+    one-launch-per-step kv_loop) over
     NVLink."""
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
