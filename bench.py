@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-restore", action="store_true")
-    ap.add_argument("--bulk-reps", type=int, default=5, help="C5 bulk re-seed reps (0: skip)")
+    ap.add_argument("--bulk-reps", type=int, default=20, help="C5 bulk re-seed reps (0: skip)")
+    ap.add_argument("--c4-restores", type=int, default=10,
+                    help="C4 failover restores (configs[3]; 0: skip)")
     ap.add_argument("--interference-steps", type=int, default=100,
                     help="steps with a Llama-3.1-8B stage decode proxy on the compute stream, "
                          "replication on vs off (0: skip)")
@@ -62,17 +64,8 @@ def parse():
                     help="steps replicated through the NCCL send/recv comparison (0: skip)")
     ap.add_argument("--shared-steps", type=int, default=100,
                     help="timed steps of the shared-capacity leg (NEXT-3; N = 1 only; 0: skip)")
-    ap.add_argument("--timeline", action="store_true",
-                    help="diagnostic: time every step and print the replication-stream timeline")
-    ap.add_argument("--loop", default="auto", choices=["auto", "fused", "streams", "pdl", "graph"],
-                    help="streams: kv_run_steps (append stream + replication stream); graph: "
-                         "kv_run_steps_graph (the same steps as CUDA graphs of 8 steps); pdl: "
-                         "one stream with programmatic dependent launch; fused: append k + "
-                         "publication k-1 per launch; auto (default): graph (measured +7-13 %% "
-                         "on 1 GPU, +2.5-3.5 %% on 2 and 4 GPUs over the two-stream loop, "
-                         "profiles/r01/exp37.log, exp39-41.log)")
-    ap.add_argument("--single-stream", action="store_true",
-                    help="append and replicate on one stream (default: replication stream)")
+    ap.add_argument("--no-survey-layout", dest="survey_layout", action="store_false",
+                    help="skip the SURVEY §8(e) one-stage-per-GPU layout leg at N > 1")
     return ap.parse_args()
 
 
@@ -100,11 +93,6 @@ def traffic_ref(kind, kernel="kv_ring_put_kernel"):
         return None
 
 
-# the timed decode steps launch the inline-descriptor ring-put (descriptors in the
-# kernel parameter space); steps whose descriptors exceed 28 KiB use the staged one
-RINGPUT = "kv_ring_put_inl_kernel (staged kv_ring_put_kernel for large steps)"
-RINGPUT_GRAPH = ("kv_ring_put_copy_kernel (CUDA-graph copy nodes of kv_run_steps_graph; the "
-                 "publication is a separate kv_publish_kernel node)")
 
 
 def peaks():
@@ -198,6 +186,145 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- GPU arm
+def layout_map(kind, N, S):
+    """Logical nodes -> GPUs.  weak (default): N pipelines of S stages, node (p, s) on GPU
+    (p + s) mod N -- every GPU hosts S stages and, for N > 1, every ring hop crosses
+    NVLink (per-GPU work fixed).  survey: C2 with ONE stage per GPU --
+    one pipeline up to N = 4 (stage s on GPU s mod N), N / 4 pipelines beyond (C3's two
+    4-stage pipelines on 8 GPUs); total work fixed up to N = 4."""
+    P = N if kind == "weak" else max(1, N // S)
+    coords = {(p, s): p * S + s for p in range(P) for s in range(S)}
+    if kind == "weak":
+        placement = {coords[(p, s)]: (p + s) % N for (p, s) in coords}
+    else:
+        placement = {coords[(p, s)]: (p * S + s) % N for (p, s) in coords}
+    succ = {coords[(p, s)]: coords[(p, (s + 1) % S)] for (p, s) in coords}
+    return P, coords, placement, succ
+
+
+def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every, publish=True):
+    """Runs W warm-up and K timed decode steps of the schedule from step t through the
+    one-launch-per-step loop (kv_loop_run: each step prepared and launched in order, no
+    lookahead).  Sources are pre-generated in HBM (> L2).  Returns the timing record."""
+    import torch
+    import torch.distributed as dist
+
+    def gen_sources(t0, n):
+        out = {}
+        for tt in range(t0, t0 + n):
+            out[tt] = {}
+            for node, e in drv.plan(tt).items():
+                if node in rt.local:
+                    ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                    out[tt][node] = content(e["stage"], ids, pos) if ids else None
+        return out
+
+    src = gen_sources(t, args.warmup + args.steps)
+    src_bytes = sum(x.numel() * 2 for d in src.values() for x in d.values() if x is not None)
+
+    def prepare(t0, n, timing):
+        steps, evs = [], []
+        for k, tt in enumerate(range(t0, t0 + n)):
+            app = [dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                        req_ids=e["req_ids"], n_new=e["n_new"], src=src[tt].get(node))
+                   for node, e in drv.plan(tt).items() if node in rt.local]
+            pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
+            st = dict(append=app, repl_pools=pools if (tt >= 1 and publish) else [], step=tt)
+            if timing and k % every == 0:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                st.update(ev_kernel_start=ev[0], ev_kernel_end=ev[1])
+                evs.append((k, ev))
+            steps.append(st)
+        return K.PreparedSteps(steps), evs
+
+    warm, _ = prepare(t, args.warmup, False)
+    timed, evs = prepare(t + args.warmup, args.steps, True)
+    torch.cuda.synchronize(dev)
+    kl.run(warm, comp.cuda_stream)
+    torch.cuda.synchronize(dev)
+    nodes = rt.alive_local()
+    bytes0 = {n: K.kv_stats(rt.handle(n))["bytes_replicated"] for n in nodes}
+    l0 = K.kv_kernel_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K.kv_host_profile(reset=True)
+    K.kv_launch_log(True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        torch.cuda.synchronize(dev)
+        w0 = time.perf_counter()
+        start.record(comp)
+        kl.run(timed, comp.cuda_stream)
+        end.record(comp)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - w0
+    log = K.kv_launch_log(False)
+    launches = K.kv_kernel_launch_count() - l0
+    host = {k: round(v / args.steps * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}
+    kl.flush(comp.cuda_stream)         # the last timed step's publication (untimed)
+    torch.cuda.synchronize(dev)
+    by = float(sum(K.kv_stats(rt.handle(n))["bytes_replicated"] - bytes0[n] for n in nodes))
+    del src
+    return {"ms": start.elapsed_time(end), "bytes": by, "launches": launches, "wall": wall,
+            "log": log, "evs": evs, "host": host, "clocks": clk.summary(),
+            "src_gib": src_bytes / 2**30}
+
+
+def paired_roofline(rec, steps, N, hbm_peak, peak_src):
+    """Roofline of the decode-step kernel from the SAME launches: every timed launch
+    that carries CUDA events (all of them when steps <= 64) is paired with its own
+    algorithmic bytes from the launch log; achieved = sum(bytes) / sum(durations).
+    N = 1: HBM bytes = append (read dense source + write pool) + publication (read
+    pool + write the local replica) = 2 (app + rep).  N > 1: the publication's bytes
+    cross NVLink (its stores go to the peer), reported against the NVLink peak; the
+    HBM figure (2 app + rep, this GPU's own traffic) beside it."""
+    log = rec["log"]
+    if len(log) != steps:
+        return {"paired": False, "note": "launch log has %d records for %d steps" % (len(log), steps)}
+    durs, hb, nb, ab, rb = [], 0.0, 0.0, 0.0, 0.0
+    for k, ev in rec["evs"]:
+        d = ev[0].elapsed_time(ev[1]) * 1e-3
+        r = log[k]
+        durs.append(d)
+        ab += r["app_bytes"]
+        rb += r["rep_bytes"]
+        hb += 2 * r["app_bytes"] + (2 if N == 1 else 1) * r["rep_bytes"]
+        nb += r["rep_bytes"]
+    T = sum(durs)
+    kname = "kv_step_inl_kernel (one launch per step: append k + publication k-1)"
+    out = {"kernel": kname, "launches_paired": len(durs), "avg_launch_us": round(T / len(durs) * 1e6, 2),
+           "median_launch_us": round(statistics.median(durs) * 1e6, 2),
+           "algorithmic_bytes_per_launch": int(hb / len(durs)),
+           "append_bytes_per_launch": int(ab / len(durs)),
+           "replicate_bytes_per_launch": int(rb / len(durs)), "paired": True}
+    hbm = hb / T / 1e9
+    if N == 1:
+        out.update(bound="hbm", achieved=round(hbm, 1), peak=hbm_peak, unit="GB/s",
+                   frac=round(hbm / hbm_peak, 4), peak_source=peak_src)
+    else:
+        nvl = nb / T / 1e9
+        out.update(bound="nvlink", achieved=round(nvl, 1), peak=NVLINK_PEAK_GBS, unit="GB/s",
+                   frac=round(nvl / NVLINK_PEAK_GBS, 4),
+                   peak_source="B200_PROFILING.md measured peer copy 770 GB/s/direction",
+                   hbm={"achieved": round(hbm, 1), "peak": hbm_peak,
+                        "frac": round(hbm / hbm_peak, 4)})
+    return out
+
+
+def reduce_max_sum(vals, dev, world):
+    """[max..., sum...] of a float vector over ranks."""
+    import torch
+    import torch.distributed as dist
+    v = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if world == 1:
+        return [float(x) for x in v], [float(x) for x in v]
+    mx, sm = v.clone(), v.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return [float(x) for x in mx], [float(x) for x in sm]
+
+
 def run_kvring(args):
     import torch
     import torch.distributed as dist
@@ -205,14 +332,12 @@ def run_kvring(args):
     from kvgen.content import CONTENT_SEED
     from kvgen.cuda import content_tokens_cuda
     from paper_2601_22438_b200 import kvring as K
-    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver, StreamOrder
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     N = args.gpus
-    if args.loop == "auto":
-        args.loop = "graph"
     if world != N:
         raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}; launch N>1 with torch.distributed.run")
     torch.cuda.set_device(local_rank)
@@ -221,157 +346,77 @@ def run_kvring(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
+    hbm_peak, peak_src = peaks()
+    every = 1 if args.steps <= 64 else 8
 
-    base = configs.C2
-    S = base.stages
-    cfg = configs.scaled(base, pipelines=N)
-    g = cfg.geom
-    coords = {(p, s): p * S + s for p in range(N) for s in range(S)}
-    placement = {coords[(p, s)]: (p + s) % N for (p, s) in coords}
-    succ = {coords[(p, s)]: coords[(p, (s + 1) % S)] for (p, s) in coords}
-    n_total = (args.prelude + args.warmup + args.steps + args.e2e_steps + args.nccl_steps
-               + 2 * args.interference_steps + args.block_steps + 3)
-    scheds = configs.build_schedules(cfg, n_steps=n_total)
-    rt = RingRuntime(g, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement, succ,
-                     rank=rank, world=world, device=local_rank, spares=1, group=group,
-                     sentinel=None)
+    def build(kind, n_extra):
+        base = configs.C2
+        S = base.stages
+        P, coords, placement, succ = layout_map(kind, N, S)
+        cfg = configs.scaled(base, pipelines=P)
+        scheds = configs.build_schedules(cfg, n_steps=args.prelude + args.warmup + args.steps
+                                         + n_extra + 3)
+        rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req,
+                         placement, succ, rank=rank, world=world, device=local_rank, spares=1,
+                         group=group, sentinel=None)
+        g = cfg.geom
 
-    def content(stage, ids, pos):
-        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
-                                   g.kv_heads, g.head_dim, device=local_rank)
+        def content(stage, ids, pos):
+            return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                       g.kv_heads, g.head_dim, device=local_rank)
 
-    drv = ScheduleDriver(rt, scheds, coords, content)
+        return cfg, rt, ScheduleDriver(rt, scheds, coords, content), content
+
     comp = torch.cuda.current_stream(dev)
-    repl = comp if args.single_stream else torch.cuda.Stream(dev)
+    repl = torch.cuda.Stream(dev)
+    # legs after the headline: appends-only (W + K), two-stream (K), e2e, NCCL,
+    # interference (2x), block mode (+1 re-seed), slack
+    n_extra = (args.e2e_steps + args.nccl_steps + 2 * args.interference_steps + args.block_steps
+               + 2 * (args.warmup + args.steps) + 40)
+    cfg, rt, drv, content = build("weak", n_extra)
 
-    order = StreamOrder(comp, repl)
-
-    def step(t):
-        order.before_append()
-        drv.append_step(t, stream=comp)
-        if t >= 1:
-            order.before_publish()
-            rt.replicate_all(t, stream=repl)
-            order.after_publish()
-
-    # ---- prelude: reach steady state (untimed) --------------------------------
+    # ---- prelude: reach steady state (untimed; sequential protocol on one stream) ----
     t = 0
     for _ in range(args.prelude):
-        step(t)
+        drv.append_step(t, stream=comp)
+        if t >= 1:
+            rt.replicate_all(t, stream=comp)
         t += 1
     torch.cuda.synchronize(dev)
 
-    # ---- pre-generate the sources of the warm-up + timed steps (inputs resident in HBM)
-    def gen_sources(t0, n):
-        out = {}
-        for tt in range(t0, t0 + n):
-            plan = drv.plan(tt)
-            out[tt] = {}
-            for node, e in plan.items():
-                if node in rt.local:
-                    ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
-                    out[tt][node] = content(e["stage"], ids, pos) if ids else None
-        return out
+    # ---- headline: one launch per decode step (kv_loop), W warm-up + K timed ----------
+    kl = K.KvLoop()
+    t_timed0 = t + args.warmup
+    rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every)
+    t += args.warmup + args.steps
+    mx, sm = reduce_max_sum([rec["ms"], rec["bytes"], float(rec["launches"])], dev, world)
+    ms_max, tot_bytes, tot_launch = mx[0], sm[1], sm[2]
+    roof = paired_roofline(rec, args.steps, N, hbm_peak, peak_src)
+    traffic = traffic_ref("decode_population", "kv_step_inl_kernel")
+    roof["traffic"] = traffic["traffic"] if traffic else None
+    if traffic:
+        roof["traffic_note"] = traffic.get("note")
+    kern_us = sorted(ev[0].elapsed_time(ev[1]) * 1e3 for _, ev in rec["evs"])
 
-    src = gen_sources(t, args.warmup + args.steps)
-    src_bytes = sum(x.numel() * 2 for d in src.values() for x in d.values() if x is not None)
-    # The per-step request events (which requests grow by how many tokens) are the
-    # workload's input, planned and marshalled ahead like the sources; allocation,
-    # work lists, H2D staging and launches all run inside the timed region
-    # (kv_run_steps: the native decode loop, append on the compute stream, publish
-    # on the replication stream).
-    def prepare(t0, n, timing):
-        # kernel-timing events on every TIME_EVERY-th step (each record is a host API
-        # call inside the timed region; sampling keeps the host loop lean)
-        steps, evs = [], []
-        for tt in range(t0, t0 + n):
-            plan = drv.plan(tt)
-            app = [dict(pool=rt.handle(node), begin_step=1, release=e["release"],
-                        req_ids=e["req_ids"], n_new=e["n_new"], src=src[tt].get(node))
-                   for node, e in plan.items() if node in rt.local]
-            pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
-            st = dict(append=app, repl_pools=pools if tt >= 1 else [], step=tt)
-            every = 8 if args.loop in ("pdl", "graph") else TIME_EVERY
-            if timing and (args.timeline or (tt - t0) % every == every - 1):
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-                st.update(ev_call=ev[0], ev_kernel_start=ev[1], ev_kernel_end=ev[2])
-                if args.timeline:
-                    ea = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                    st.update(ev_append_start=ea[0], ev_append_end=ea[1])
-                    ev = ev + ea
-                evs.append(ev)
-            steps.append(st)
-        return K.PreparedSteps(steps), evs
+    # ---- the same steps' appends alone: the per-step cost of replication --------------
+    base_rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every,
+                          publish=False)
+    t += args.warmup + args.steps
+    ms_app = reduce_max_sum([base_rec["ms"]], dev, world)[0][0]
+    # re-seed the backlog the append-only steps left (untimed)
+    drv.append_step(t, stream=comp)
+    rt.replicate_all(t, stream=comp)
+    t += 1
+    torch.cuda.synchronize(dev)
 
-    warm, _ = prepare(t, args.warmup, False)
-    timed, evs = prepare(t + args.warmup, args.steps, True)
-    torch.cuda.synchronize(dev)
-    if args.loop == "fused":
-        K.kv_run_steps_fused(warm, comp.cuda_stream)
-    elif args.loop == "pdl":
-        K.kv_run_steps_pdl(warm, comp.cuda_stream)
-    elif args.loop == "graph":
-        K.kv_run_steps_graph(warm, comp.cuda_stream, repl.cuda_stream)
-    else:
-        K.kv_run_steps(warm, comp.cuda_stream, repl.cuda_stream)
-    t += args.warmup
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-
-    # ---- timed region -----------------------------------------------------------
-    local_nodes = rt.alive_local()
-    bytes0 = {n: K.kv_stats(rt.handle(n))["bytes_replicated"] for n in local_nodes}
-    l0 = K.kv_kernel_launch_count()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_timed0 = t
-    K.kv_host_profile(reset=True)
-    with ClockSampler(local_rank) as clk:
-        torch.cuda.synchronize(dev)
-        w0 = time.perf_counter()
-        start.record(comp)
-        if args.loop == "fused":
-            K.kv_run_steps_fused(timed, comp.cuda_stream)
-        elif args.loop == "pdl":
-            K.kv_run_steps_pdl(timed, comp.cuda_stream)
-        elif args.loop == "graph":
-            K.kv_run_steps_graph(timed, comp.cuda_stream, repl.cuda_stream)
-        else:
-            K.kv_run_steps(timed, comp.cuda_stream, repl.cuda_stream)
-        fin = torch.cuda.Event()
-        fin.record(repl)
-        comp.wait_event(fin)
-        end.record(comp)
-        torch.cuda.synchronize(dev)
-        wall = time.perf_counter() - w0
+    # ---- two-stream loop (P:229's shape): append stream + replication stream ----------
+    two = run_two_stream(args, K, drv, rt, t, comp, repl, content, dev, world)
     t += args.steps
-    del src
-    launches = K.kv_kernel_launch_count() - l0
-    host_prof = {k: round(v / args.steps * (1.0 if k.startswith("n_") else 1e6), 2)
-                 for k, v in K.kv_host_profile(reset=True).items()}
-    ms = start.elapsed_time(end)
-    kern_us = [e[1].elapsed_time(e[2]) * 1e3 for e in evs]
-    rep_us = kern_us if args.loop in ("fused", "pdl", "graph") else [e[0].elapsed_time(e[2]) * 1e3
-                                                           for e in evs]
-    if args.timeline and rank == 0:
-        T = lambda e: start.elapsed_time(e) * 1e3
-        print("TIMELINE us: append [start,end] (compute stream) | ring-put [start,end] "
-              "(replication stream); host wall %.1f us/step" % (wall / args.steps * 1e6),
-              file=sys.stderr)
-        for k, e in enumerate(evs[:80]):
-            a0, a1 = (T(e[3]), T(e[4])) if len(e) > 3 else (0, 0)
-            print("  step %3d  append %8.1f %8.1f (%5.1f)  ringput %8.1f %8.1f (%5.1f)"
-                  % (k, a0, a1, a1 - a0, T(e[1]), T(e[2]), T(e[2]) - T(e[1])), file=sys.stderr)
-    step_bytes = {n: K.kv_stats(rt.handle(n))["bytes_replicated"] - bytes0[n] for n in local_nodes}
-    my_bytes = float(sum(step_bytes.values()))
 
     # ---- e2e: host-resident inputs (pinned), H2D + D2H inside the timed region ---
     e2e = None
     if args.e2e_steps > 0:
-        e2e = run_e2e(args, drv, rt, t, comp, repl, content, dev, world)
+        e2e = run_e2e(args, K, kl, drv, rt, t, comp, content, dev, world)
         t += args.e2e_steps
 
     # ---- NCCL comparison (a6): same workload, pack -> count -> send/recv -> unpack ---
@@ -392,22 +437,33 @@ def run_kvring(args):
         block = run_block_mode(args, drv, rt, t, comp, repl, content, dev, world)
         t += args.block_steps + 1
 
-    # ---- floor of a decode hop: a publication with nothing dirty ("empty
-    # launch + one P2P flag store"), same pools, same stream, same launch path; the
-    # last leg that replicates on these pools (its step numbers are not schedule steps)
-    floor = run_floor(rt, t + 10, comp, repl, dev, world,
-                      "graph" if args.loop == "graph" else "streams")
+    # ---- floor of a decode hop: a publication with nothing dirty ----------------------
+    floor = run_floor(K, kl, rt, t + 10, comp, dev, world)
 
     # ---- restore: fail stage 2 of pipeline 0, restore into a fresh pool ---------
     restore = None
     if not args.no_restore:
         restore = run_restore(drv, rt, t, dev, comp, world)
 
-    # ---- bulk leg (C5: 32k-token prefill per stage, full-block re-seed) -----------
     pool_gib = rt.n_slots * 2 * rt.replica_bytes / 2**30
+    kl.destroy()
     rt.destroy()
     del rt, drv
     torch.cuda.empty_cache()
+
+    # ---- SURVEY §8(e) layout at N > 1: one C2 stage per GPU ----------------------------
+    survey = None
+    if N > 1 and args.survey_layout:
+        survey = run_survey_layout(args, build, dev, world, comp, every)
+        torch.cuda.empty_cache()
+
+    # ---- C4 failover (configs[3]): 16 logical nodes, batch 128, kill (0,2) at step 300 --
+    c4 = None
+    if args.c4_restores > 0:
+        c4 = run_c4(args, rank, world, local_rank, dev, group)
+        torch.cuda.empty_cache()
+
+    # ---- bulk leg (C5: 32k-token prefill per stage, full-block re-seed) -----------
     bulk = run_bulk(args, rank, world, local_rank, dev, group) if args.bulk_reps > 0 else None
 
     # ---- shared capacity (NEXT-3): replicas in the holder's own pool, under pressure -
@@ -416,139 +472,49 @@ def run_kvring(args):
         shared = (run_shared(args, local_rank, dev) if world == 1 else
                   {"skipped": "shared capacity needs the holder on the same GPU (N = 1)"})
 
-    # ---- reduce over ranks --------------------------------------------------------
-    vec = torch.tensor([ms, my_bytes, float(launches), wall], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = vec.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vec.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, tot_bytes, tot_launch = float(mx[0]), float(sm[1]), int(sm[2])
-    else:
-        ms_max, tot_bytes, tot_launch = ms, my_bytes, launches
-
-    hbm_peak, peak_src = peaks()
-    med_kern = statistics.median(kern_us)
-    avg_kern = sum(kern_us) / len(kern_us)
-    if args.loop == "fused":
-        # kv_step_fused_kernel: append of step k (D_k read from the dense source + D_k
-        # written into the pool) and publication of step k-1 (D_{k-1} read + written);
-        # over the timed run appended bytes == published bytes == my_bytes, in K+1 launches
-        n_launch = args.steps + 1
-        kname = "kv_step_fused_kernel"
-        if N == 1:
-            per = 4 * my_bytes / n_launch
-            achieved = per / (avg_kern * 1e-6) / 1e9
-            roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                    "frac": round(achieved / hbm_peak, 4), "traffic": None, "kernel": kname,
-                    "peak_source": peak_src, "algorithmic_bytes_per_launch": int(per),
-                    "avg_launch_us": round(avg_kern, 2),
-                    "what": "append k (D r+w) + publication k-1 (D r+w) per launch, HBM"}
-        else:
-            per = my_bytes / n_launch
-            achieved = per / (avg_kern * 1e-6) / 1e9
-            roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
-                    "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
-                    "kernel": kname,
-                    "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
-                    "algorithmic_bytes_per_launch": int(per), "avg_launch_us": round(avg_kern, 2),
-                    "what": "NVLink bytes of the publication part per launch"}
-    # ring-put algorithmic bytes per launch: D read + D written (HBM at N=1; at N>1
-    # the write crosses NVLink -- reported against the NVLink per-direction peak)
-    elif N == 1:
-        per_launch = my_bytes / args.steps
-        achieved = 2 * per_launch / (avg_kern * 1e-6) / 1e9
-        pop = traffic_ref("decode_population", "kv_ring_put_copy_kernel") if args.loop == "graph" else None
-        tr = (traffic_ref("decode_step", "kv_ring_put_copy_kernel") if args.loop == "graph"
-              else traffic_ref("decode_step", "kv_ring_put_inl_kernel"))
-        if pop:  # per-launch average over a population of this loop's copy-node launches
-            tnote = ("ncu --set full over %d consecutive copy-node launches of this bench loop "
-                     "(profiles/traffic.json decode_population): avg DRAM bytes/launch %d (read %d, "
-                     "write %d) vs avg algorithmic r+w %d (L2 bytes the kernel requested) = %.2f; "
-                     "no re-reads, most replica writes stay in L2"
-                     % (pop["n_launches"], pop["traffic"], pop["dram_read"], pop["dram_write"],
-                        pop["algorithmic_rw"], pop["traffic_over_algorithmic"]))
-        elif tr:
-            tnote = ("ncu --set full of a decode-step launch (profiles/traffic.json): "
-                     "DRAM bytes %d vs algorithmic read %d / r+w %d; writes stay in L2"
-                     % (tr["traffic"], tr["algorithmic_read"], tr["algorithmic_rw"]))
-        else:
-            tnote = None
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4),
-                "traffic": pop["traffic"] if pop else (tr["traffic"] if tr else None),
-                "traffic_note": tnote,
-                "kernel": RINGPUT_GRAPH if args.loop == "graph" else RINGPUT,
-                "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": int(2 * per_launch),
-                "avg_launch_us": round(avg_kern, 2)}
-    else:
-        per_launch = my_bytes / args.steps
-        achieved = per_launch / (avg_kern * 1e-6) / 1e9
-        tr = traffic_ref("decode_step_nvlink", "kv_ring_put_inl_kernel")
-        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
-                "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
-                "traffic": (tr["dram_read"] if tr else None),
-                "nvlink_traffic_note": ("ncu of a decode-only launch (tools/nvlink_profile.py, "
-                                        "profiles/traffic.json): nvltx user bytes %d / wire "
-                                        "bytes %d vs algorithmic %d"
-                                        % (tr["nvltx_bytes_data_user"], tr["nvltx_bytes"],
-                                           tr["algorithmic_nvlink"])) if tr else None,
-                "kernel": RINGPUT,
-                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
-                "algorithmic_bytes_per_launch": int(per_launch), "avg_launch_us": round(avg_kern, 2)}
     value = tot_bytes / (ms_max * 1e-3) / 1e9
+    ms_step = ms_max / args.steps
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": N,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (ShareGPT-shaped lognormal trace, closed-form KV words)",
         "config": bench_config(N),
         "dtype_note": "bf16 KV words moved bit-exactly as 16-bit data (no arithmetic)",
-        "run": {"timed_steps": [t_timed0, t_timed0 + args.steps - 1], "loop": args.loop,
-                "inputs_gib": {"pre_generated_sources": round(src_bytes / 2**30, 2),
-                               "pools_and_replicas_per_gpu": round(pool_gib, 1)},
-                "streams": "single" if args.single_stream else "compute+replication"},
+        "run": {"timed_steps": [t_timed0, t_timed0 + args.steps - 1],
+                "loop": "kv_loop_run: per step ONE launch = appends of step k + publication of "
+                        "step k-1; each step prepared and launched in order (no lookahead)",
+                "inputs_gib": {"pre_generated_sources": round(rec["src_gib"], 2),
+                               "pools_and_replicas_per_gpu": round(pool_gib, 1)}},
         "gb_s_per_gpu": round(value / N, 2),
         "replicated_bytes": int(tot_bytes),
-        "loop": args.loop,
-        "step_overhead_us": {"median": round(statistics.median(rep_us), 2),
-                             "p99": round(float(np.percentile(rep_us, 99)), 2),
-                             "budget_us": 400.0, "tpot_ms": 20.0,
-                             "fused_loop_note": ("with the fused loop this is the whole fused "
-                                                 "launch (append + publication); the replication "
-                                                 "overhead proper is the interference leg")
-                             if args.loop == "fused" else None,
-                             "what": "replication-stream device time per step (ring-put kernel incl. "
-                                     "its launch and its wait for the step's append), CUDA events "
-                                     "recorded by the decode loop on every %d-th timed step"
-                                     % (8 if args.loop in ("pdl", "graph") else TIME_EVERY)},
-        "kernel_us": {"kernel": "kv_step_fused_kernel" if args.loop == "fused"
-                      else (RINGPUT_GRAPH if args.loop == "graph" else RINGPUT),
-                      "median": round(med_kern, 2), "avg": round(avg_kern, 2),
-                      "sampled_launches": len(kern_us)},
+        "step_overhead_us": {
+            "median": round((ms_max - ms_app) / args.steps * 1e3, 2),
+            "step_us_with_replication": round(ms_step * 1e3, 2),
+            "step_us_appends_only": round(ms_app / args.steps * 1e3, 2),
+            "budget_us": 400.0, "tpot_ms": 20.0,
+            "what": "per decode step: the same loop with and without the publications (K steps "
+                    "each, max over ranks); the harness has no model compute, so this is the "
+                    "whole device cost replication adds to a step (interference: with a model)"},
+        "kernel_us": {"kernel": roof.get("kernel"), "median": round(statistics.median(kern_us), 2),
+                      "avg": round(sum(kern_us) / len(kern_us), 2),
+                      "timed_launches": len(kern_us)},
         "roofline": roof,
         "step_roofline": step_roofline(tot_bytes, ms_max, N, hbm_peak, peak_src),
         "gpu_launches": int(tot_launch),
-        "wall_s_timed": round(wall, 3),
-        "host_us_per_step": host_prof,
-        "clocks": clk.summary(),
+        "wall_s_timed": round(rec["wall"], 4),
+        "host_us_per_step": rec["host"],
+        "clocks": rec["clocks"],
+        "two_stream": two,
+        "step_floor_us": floor,
     }
     if e2e is not None:
         line["e2e"] = e2e
-    line["step_floor_us"] = floor
-    if restore is not None:
-        line["restore"] = restore
-    if bulk is not None:
-        line["bulk"] = bulk
-    if nccl is not None:
-        line["nccl_compare"] = nccl
-    if interference is not None:
-        line["interference"] = interference
-    if block is not None:
-        line["block_mode"] = block
-    if shared is not None:
-        line["shared_capacity"] = shared
+    for k, v in (("restore", restore), ("c4_failover", c4), ("bulk", bulk), ("nccl_compare", nccl),
+                 ("interference", interference), ("block_mode", block),
+                 ("shared_capacity", shared), ("survey_layout", survey)):
+        if v is not None:
+            line[k] = v
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, t_timed0, min(args.steps, 60))
     if rank == 0:
@@ -556,6 +522,238 @@ def run_kvring(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_two_stream(args, K, drv, rt, t0, comp, repl, content, dev, world):
+    """The same workload through kv_run_steps: per step one append launch on the compute
+    stream and one publication launch on a separate replication stream after an event
+    ("A separate CUDA stream is used to overlap the communication with
+    computation"); append k waits for the publication of k-2 (R7)."""
+    import torch
+    import torch.distributed as dist
+    n = args.steps
+    steps, keep = [], []
+    for tt in range(t0, t0 + n):
+        app = []
+        for node, e in drv.plan(tt).items():
+            if node in rt.local:
+                ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                src = content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=src))
+        pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
+        steps.append(dict(append=app, repl_pools=pools, step=tt))
+    prep = K.PreparedSteps(steps)
+    nodes = rt.alive_local()
+    b0 = {nd: K.kv_stats(rt.handle(nd))["bytes_replicated"] for nd in nodes}
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(comp)
+    K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
+    fin = torch.cuda.Event()
+    fin.record(repl)
+    comp.wait_event(fin)
+    b.record(comp)
+    torch.cuda.synchronize(dev)
+    by = float(sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in nodes))
+    mx, sm = reduce_max_sum([a.elapsed_time(b), by], dev, world)
+    ms, tot = mx[0], sm[1]
+    return {"value": round(tot / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "steps": n,
+            "ms_per_step": round(ms / n, 4),
+            "what": "kv_run_steps: append launch on the compute stream, publication launch on a "
+                    "replication stream after an event (2 launches per step)"}
+
+
+def run_survey_layout(args, build, dev, world, comp, every):
+    """C2 with one stage per GPU (1 pipeline at N <= 4, N / 4 pipelines
+    beyond); same loop, warm-up and timing as the headline."""
+    import torch
+    from paper_2601_22438_b200 import kvring as K
+    cfg, rt, drv, content = build("survey", 0)
+    t = 0
+    for _ in range(args.prelude):
+        drv.append_step(t, stream=comp)
+        if t >= 1:
+            rt.replicate_all(t, stream=comp)
+        t += 1
+    torch.cuda.synchronize(dev)
+    kl = K.KvLoop()
+    rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every)
+    mx, sm = reduce_max_sum([rec["ms"], rec["bytes"]], dev, world)
+    ms, tot = mx[0], sm[1]
+    hbm_peak, peak_src = peaks()
+    roof = paired_roofline(rec, args.steps, world, hbm_peak, peak_src)
+    stages = len(rt.alive_local())
+    kl.destroy()
+    rt.destroy()
+    return {"layout": "one C2 stage per GPU (%d pipeline(s) x %d stages, stage s of pipeline p on "
+                      "GPU (4p + s) mod N)" % (cfg.pipelines, cfg.stages),
+            "stages_per_gpu": stages, "value": round(tot / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "ms_per_step": round(ms / args.steps, 4), "roofline": roof,
+            "scaling": "strong (C2's total work fixed)" if world <= 4 else "C3 layout (2 pipelines)"}
+
+
+C4_NB = 4096   # C4's resident peak is ~3.2k blocks per node (batch 128): pools sized to it
+
+
+def run_c4(args, rank, world, local_rank, dev, group):
+    """BASELINE configs[3] / SURVEY §8(d) C4: 16 logical nodes (4 pipelines x 4 stages,
+    north_star's stage ring), node (i, s) on GPU (4i + s) mod N, closed-loop batch 128 per
+    pipeline.  Steps 0..299 run the sequential protocol; at step 300 node (0,2) fails
+    after its append (before its publication: t* = 299).  Its pool and block table are
+    then restored from its successor's replica `c4_restores` times into a fresh pool
+    (re-created each time; local HBM at N = 1, over NVLink from the next GPU at N > 1);
+    promotion onto the holder runs the same kernel and is covered by the parity tests
+    (the paper's instance ring, tests/test_gpu_configs.py).  Kernel time by
+    CUDA events around the restore kernel, wall time around the whole kv_restore call
+    (metadata acquire + read-back + allocation + kernel)."""
+    import torch
+    import torch.distributed as dist
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED
+    from kvgen.cuda import content_tokens_cuda
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    cfg = configs.scaled(configs.C4, num_blocks=C4_NB)
+    I, S = cfg.pipelines, cfg.stages
+    coords = {(i, s): i * S + s for i in range(I) for s in range(S)}
+    placement = {coords[(i, s)]: (4 * i + s) % world for (i, s) in coords}
+    succ = {coords[(i, s)]: coords[(i, (s + 1) % S)] for (i, s) in coords}
+    scheds = configs.build_schedules(cfg, n_steps=cfg.fail_step + 2)
+    rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement,
+                     succ, rank=rank, world=world, device=local_rank, spares=1, group=group,
+                     sentinel=None)
+    g = cfg.geom
+
+    def content(stage, ids, pos):
+        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim, device=local_rank)
+
+    drv = ScheduleDriver(rt, scheds, coords, content)
+    comp = torch.cuda.current_stream(dev)
+    T = cfg.fail_step
+    for t in range(T):
+        drv.append_step(t, stream=comp)
+        if t >= 1:
+            rt.replicate_all(t, stream=comp)
+    drv.append_step(T, stream=comp)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    f = coords[cfg.fail_node]
+    holder = succ[f]
+    rt.fail(f, comp)
+    dst = drv.next_node
+    drv.next_node += 1
+    dst_rank = rt.placement[holder] if world == 1 else (rt.placement[holder] + 1) % world
+    rt.new_node(dst, dst_rank)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    kern, wall, info = [], [], [0.0, 0.0, 0.0]
+    for rep in range(args.c4_restores + 1):
+        if rank == dst_rank:
+            slot = rt.local[dst]
+            K.kv_pool_destroy(slot.handle)
+            rt._create(dst, slot)                     # a fresh pool on the same memory
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            K.kv_time_next_launch(a, b)
+            w0 = time.perf_counter()
+            t_star, restored = rt.restore(dst, holder, comp)
+            torch.cuda.synchronize(dev)
+            w = (time.perf_counter() - w0) * 1e3
+            if rep > 0:
+                kern.append(a.elapsed_time(b))
+                wall.append(w)
+            tok = sum(ln for _, ln in restored)
+            info = [float(t_star), float(len(restored)), float(tok * g.token_bytes)]
+    res = torch.tensor([statistics.median(kern) if kern else 0.0,
+                        statistics.median(wall) if wall else 0.0,
+                        float(np.percentile(kern, 99)) if kern else 0.0] + info,
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(res, op=dist.ReduceOp.SUM)      # one rank contributes
+    rt.destroy()
+    kms, wms, k99, t_star, nreq, R = [float(x) for x in res.tolist()]
+    hbm_peak, peak_src = peaks()
+    out = {"workload": "c4_failover_16 (16 logical nodes, batch 128 per pipeline, stage ring, "
+                       "node (i,s) on GPU (4i+s) mod N, pools of %d blocks)" % C4_NB,
+           "failed": list(cfg.fail_node), "fail_step": T, "t_star": int(t_star),
+           "requests": int(nreq), "restored_bytes": int(R), "restores": args.c4_restores,
+           "kernel_ms_median": round(kms, 4), "kernel_ms_p99": round(k99, 4),
+           "wall_ms_median": round(wms, 3)}
+    if world == 1:
+        gbs = 2 * R / (kms * 1e-3) / 1e9
+        out["roofline"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
+                           "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
+                           "peak_source": peak_src, "algorithmic_bytes_per_launch": int(2 * R),
+                           "path": "local HBM: fresh pool on the holder's GPU"}
+    else:
+        gbs = R / (kms * 1e-3) / 1e9
+        out["roofline"] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": NVLINK_PEAK_GBS,
+                           "unit": "GB/s", "frac": round(gbs / NVLINK_PEAK_GBS, 4),
+                           "algorithmic_bytes_per_launch": int(R),
+                           "path": "remote: fresh pool on GPU %d reads GPU %d's replica over "
+                                   "NVLink" % (dst_rank, rt.placement[holder])}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["oracle"] = oracle_c4_restore(cfg, scheds)
+    return out
+
+
+def oracle_c4_restore(cfg, scheds):
+    """The oracle's restore of the same failure, as it stands, on ONE core: the ring runs
+    to step 300 in metadata mode; the holder's published replica slots are filled with
+    their closed-form words (setup, untimed); then OracleNode.restore_from copies them
+    into a fresh node (timed).  Peak RSS of the process reported beside it."""
+    import resource
+    from kvgen.content import CONTENT_SEED, content_tokens
+    from oracle.kvring_oracle import OracleNode
+    from oracle.simulate import OracleRing
+    aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    try:
+        if aff:
+            os.sched_setaffinity(0, {min(aff)})
+        ring = OracleRing(cfg, content=False, schedules=scheds)
+        T = cfg.fail_step
+        for t in range(T + 1):
+            ring.appends(t)
+            if t < T and t >= 1:
+                ring.replicate(t)
+        f = ring.serving[cfg.fail_node]
+        holder = f.succ
+        f.fail()
+        g = cfg.geom
+        shape = (cfg.num_blocks, g.layers, 2, g.kv_heads, g.block_size, g.head_dim)
+        holder.content = True
+        holder.replica = np.zeros(shape, dtype=np.uint16)
+        stage = cfg.fail_node[1]
+        B = g.block_size
+        for r, (s, ln, bt) in holder.published().items():
+            words = content_tokens(CONTENT_SEED, [r] * ln, range(ln), stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim)
+            for j, blk in enumerate(bt):
+                v = min(B, ln - j * B)
+                holder.replica[blk, :, :, :, :v] = words[j * B:j * B + v].transpose(1, 2, 3, 0, 4)
+        dst = OracleNode(g, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, node_id=99,
+                         content=True)
+        t0 = time.perf_counter()
+        t_star, restored = dst.restore_from(holder)
+        dt = time.perf_counter() - t0
+        tok = sum(ln for _, ln in restored)
+        return {"restore_ms": round(dt * 1e3, 1), "t_star": int(t_star), "requests": len(restored),
+                "restored_bytes": int(tok * g.token_bytes), "cores": 1,
+                "peak_rss_gib": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20, 2),
+                "what": "OracleNode.restore_from (numpy, one core) of the same failure; peak RSS "
+                        "of the bench process (GPU arm + oracle)"}
+    except Exception as e:
+        return {"restore_ms": None, "error": str(e)[:200]}
+    finally:
+        if aff:
+            os.sched_setaffinity(0, aff)
 
 
 def run_bulk(args, rank, world, local_rank, dev, group):
@@ -890,48 +1088,36 @@ def run_block_mode(args, drv, rt, t0, comp, repl, content, dev, world):
 FLOOR_REPS = 50
 
 
-def run_floor(rt, t0, comp, repl, dev, world, loop="streams"):
-    """Per-step floor of the publication on the timed loop's own path: FLOOR_REPS steps
-    of kv_run_steps with no append and nothing dirty (one publish-only task per pool:
-    bt / parity table / release seq, over NVLink when the successor is remote), timed
-    exactly like step_overhead_us (events from before the publication to after its
-    kernel, on the replication stream; max over ranks).  The decode-step ring-put is
-    compared with it."""
+def run_floor(K, kl, rt, t0, comp, dev, world):
+    """Per-step floor of the publication on the timed loop's own path: FLOOR_REPS loop
+    steps with no append and nothing dirty (a launch that only writes the parity table
+    and the seq flag of every pool, over NVLink when the successor is remote), each
+    launch bracketed by CUDA events like the headline's kernel_us; max over ranks."""
     import torch
     import torch.distributed as dist
-    from paper_2601_22438_b200 import kvring as K
     nodes = [n for n in rt.alive_local() if rt.succ.get(n) is not None]
     handles = [rt.handle(n) for n in nodes]
     sts, evs = [], []
-    for k in range(FLOOR_REPS + 1):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for k in range(FLOOR_REPS + 2):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         evs.append(ev)
-        sts.append(dict(append=[], repl_pools=handles, step=t0 + k, ev_call=ev[0],
-                        ev_kernel_start=ev[1], ev_kernel_end=ev[2]))
+        sts.append(dict(append=[], repl_pools=handles, step=t0 + k, ev_kernel_start=ev[0],
+                        ev_kernel_end=ev[1]))
     prep = K.PreparedSteps(sts)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    if loop == "graph":
-        K.kv_run_steps_graph(prep, comp.cuda_stream, repl.cuda_stream)
-    else:
-        K.kv_run_steps(prep, comp.cuda_stream, repl.cuda_stream)
+    kl.run(prep, comp.cuda_stream)
+    kl.flush(comp.cuda_stream)
     torch.cuda.synchronize(dev)
-    # graph loop: ev_call is not recorded (events sit around the ring-put node only)
-    i0 = 1 if loop == "graph" else 0
-    call = sorted(e[i0].elapsed_time(e[2]) * 1e3 for e in evs[1:])
-    kern = sorted(e[1].elapsed_time(e[2]) * 1e3 for e in evs[1:])
-    v = torch.tensor([call[len(call) // 2], kern[len(kern) // 2]], dtype=torch.float64,
-                     device=dev)
+    kern = sorted(e[0].elapsed_time(e[1]) * 1e3 for e in evs[2:])   # launches 2.. publish
+    v = torch.tensor([kern[len(kern) // 2]], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-    return {"median": round(float(v[0]), 2), "kernel_median": round(float(v[1]), 2),
-            "reps": FLOOR_REPS, "pools": len(nodes),
-            "what": "steps with nothing dirty through the timed loop's own decode loop (%s; "
-                    "one publish-only task per pool: launch / graph node + bt/parity tables + "
-                    "seq), timed like step_overhead_us (median) and kernel_us (kernel_median); "
-                    "the decode-step ring-put's floor" % ("kv_run_steps_graph" if loop == "graph"
-                                                         else "kv_run_steps")}
+    return {"kernel_median": round(float(v[0]), 2), "reps": FLOOR_REPS, "pools": len(nodes),
+            "what": "loop steps with nothing dirty (kv_loop_step: one launch writing every "
+                    "pool's parity table and seq), CUDA events around each launch; the "
+                    "decode-step launch's floor"}
 
 
 SHARED_NB = 2048   # C2 primary peak is ~1.57k blocks per stage: replicas must compete
@@ -1084,45 +1270,35 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
                                       "p99": round(float(np.percentile(us, 99)), 2)}}
 
 
-def _append_host(drv, t, host_sources, stream):
-    """kv_append_multi with KV_SRC_HOST: the library copies the pinned host KV."""
-    from paper_2601_22438_b200 import kvring as K
-    entries = []
-    for node, e in drv.plan(t).items():
-        if node not in drv.rt.local:
-            continue
-        src = host_sources.get(node) if host_sources else None
-        entries.append(dict(node=node, begin_step=1, release=e["release"], req_ids=e["req_ids"],
-                            n_new=e["n_new"], src=src, flags=K.KV_SRC_HOST))
-    drv.rt.append_all(entries, stream)
-
-
-def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
-    """Same metric through the C ABI with HOST buffers: per step the new-token KV is
-    copied from pinned host memory by kv_append (KV_SRC_HOST) and the published seq
-    flags of the successors are read back to pinned host memory."""
+def run_e2e(args, K, kl, drv, rt, t0, comp, content, dev, world):
+    """Same metric through the public API with HOST buffers: per step one kv_loop_step
+    (the Python binding's call) whose appends read the step's new-token KV from pinned
+    host memory (KV_SRC_HOST: the kernel reads it over PCIe), and a D2H read-back of
+    the seq flags the predecessors published into this GPU's replica metadata."""
     import torch
     import torch.distributed as dist
-    from paper_2601_22438_b200 import kvring as K
-    from paper_2601_22438_b200.runtime import StreamOrder
     n = args.e2e_steps
-    host = {}
+    host, preps = {}, []
     h2d = 0
     for tt in range(t0, t0 + n):
-        host[tt] = {}
+        app = []
         for node, e in drv.plan(tt).items():
             if node in rt.local:
                 ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+                hbuf = None
                 if ids:
                     d = content(e["stage"], ids, pos)
                     hbuf = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
                     hbuf.copy_(d)
-                    host[tt][node] = hbuf
                     h2d += d.numel() * 2
+                host[(tt, node)] = hbuf
+                app.append(dict(pool=rt.handle(node), begin_step=1, release=e["release"],
+                                req_ids=e["req_ids"], n_new=e["n_new"], src=hbuf,
+                                flags=K.KV_SRC_HOST))
+        pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
+        preps.append(K.PreparedSteps([dict(append=app, repl_pools=pools, step=tt)]))
     torch.cuda.synchronize(dev)
     nodes = rt.alive_local()
-    # the step's result on this GPU: the seq flags its nodes' predecessors published into
-    # this GPU's replica metadata (local memory whatever the ring placement)
     seq_dev = [rt.local[nd].meta[:8] for nd in nodes]
     seq_host = torch.empty((n, len(nodes), 8), dtype=torch.uint8, pin_memory=True)
     d2h = 0
@@ -1133,36 +1309,18 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     st.record(comp)
-    order = StreamOrder(comp, repl)
     for k in range(n):
-        tt = t0 + k
-        order.before_append()
-        _append_host(drv, tt, host[tt], comp)
-        order.before_publish()
-        rt.replicate_all(tt, stream=repl)
-        order.after_publish()
-        with torch.cuda.stream(repl):
-            for i, sd in enumerate(seq_dev):
-                if sd is not None:
-                    seq_host[k, i].copy_(sd, non_blocking=True)
-                    d2h += 8
-    fin = torch.cuda.Event()
-    fin.record(repl)
-    comp.wait_event(fin)
+        kl.step(preps[k], 0, comp.cuda_stream)
+        for i, sd in enumerate(seq_dev):
+            seq_host[k, i].copy_(sd, non_blocking=True)
+            d2h += 8
+    kl.flush(comp.cuda_stream)
     en.record(comp)
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - w0
-    ms = st.elapsed_time(en)
-    by = sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in nodes)
-    vec = torch.tensor([ms, float(by)], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = vec.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vec.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms, by = float(mx[0]), float(sm[1])
-    # per-step read-backs are not synchronised with the remote writers (one-sided
-    # publication); after a barrier every local replica must hold the last step
+    by = float(sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in nodes))
+    mx, sm = reduce_max_sum([st.elapsed_time(en), by, wall], dev, world)
+    ms, by, wall = mx[0], sm[1], mx[2]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -1173,9 +1331,9 @@ def run_e2e(args, drv, rt, t0, comp, repl, content, dev, world):
             "h2d_bytes_per_step": int(h2d // n), "d2h_bytes_per_step": int(d2h // n),
             "steps": n, "ms_per_step": round(ms / n, 4), "wall_s": round(wall, 3),
             "seq_readback_ok": ok,
-            "path": "kv_append_multi(KV_SRC_HOST) on pinned host tensors (the scatter kernel "
-                    "reads them over PCIe, zero copy) + kv_replicate_step_multi; per step a "
-                    "D2H read-back of the published seq flags"}
+            "path": "per step one kv_loop_step call from Python (appends read pinned host KV "
+                    "over PCIe, zero copy; the previous step's publication in the same launch) "
+                    "+ a D2H read-back of the published seq flags"}
 
 
 def run_restore(drv, rt, t, dev, stream, world=1):

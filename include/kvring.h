@@ -75,7 +75,7 @@ typedef struct kv_pool kv_pool_t; /* opaque; one per logical node (instance, sta
 typedef struct {
   int32_t layers;      /* L_s, layers of this pipeline stage                         */
   int32_t kv_heads;    /* H (Llama-3.1-8B: 8)                                         */
-  int32_t head_dim;    /* d (128); head_dim * elem_bytes must be a power of 2 >= 16   */
+  int32_t head_dim;    /* d (128); head_dim * elem_bytes: a power of 2 in [16, 512]    */
   int32_t block_size;  /* B tokens per block (16)                                     */
   int32_t elem_bytes;  /* must be 2 (16-bit words)                                    */
 } kv_geom_t;

@@ -181,19 +181,26 @@ struct StageBuf {
   char *host = nullptr;
   char *dev = nullptr;
   size_t cap = 0;
-  cudaEvent_t ev = nullptr;
+  cudaEvent_t ev = nullptr;   // recorded on the consuming stream after the last use
+  cudaEvent_t up = nullptr;   // recorded on the upload stream after the H2D copy
   bool pending = false;
 };
 
 struct DeviceCtx {
   int device = 0;
   std::mutex mu;
-  static constexpr int kRing = 8;
+  static constexpr int kRing = 16;
   StageBuf ring[kRing];
   int next = 0;
   StageBuf src[kRing];  // device copies of host-resident append sources (KV_SRC_HOST)
   int next_src = 0;
   unsigned long long *unpack_counter = nullptr;
+  cudaStream_t upload = nullptr;  // descriptor uploads of the decode-step engine
+  int ensure_upload() {
+    if (upload) return KV_OK;
+    CU(cudaStreamCreateWithFlags(&upload, cudaStreamNonBlocking));
+    return KV_OK;
+  }
   size_t cap_hint = 8u << 20;       // descriptor slots: 8 MiB (growth never hits a hot loop)
   size_t src_cap_hint = 64u << 20;  // host-source slots: 64 MiB (a 2k-token prefill per stage)
 
@@ -230,6 +237,7 @@ struct DeviceCtx {
       }
     }
     if (!b.ev) CU(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+    if (!b.up) CU(cudaEventCreateWithFlags(&b.up, cudaEventDisableTiming));
     *out = &b;
     return KV_OK;
   }
@@ -403,8 +411,10 @@ int validate_geom(const kv_geom_t *g) {
     return fail(KV_EINVAL, "geometry fields must be positive (block_size <= 4096)");
   if (g->elem_bytes != 2) return fail(KV_EINVAL, "elem_bytes must be 2 (16-bit words)");
   const int seg = g->head_dim * g->elem_bytes;
-  if (seg < 16 || (seg & (seg - 1)) != 0)
-    return fail(KV_EINVAL, "head_dim * elem_bytes = %d must be a power of two >= 16", seg);
+  if (seg < 16 || seg > 512 || (seg & (seg - 1)) != 0)
+    return fail(KV_EINVAL, "head_dim * elem_bytes = %d must be a power of two in [16, 512]", seg);
+  if ((long long)g->block_size * g->layers * 2 * g->kv_heads >= (1LL << 24))
+    return fail(KV_EINVAL, "a block must hold fewer than 2^24 (layer, K/V, head, token) slices");
   return KV_OK;
 }
 
@@ -1239,6 +1249,7 @@ void set_geom(StepLaunch &S, const kv_pool *p) {
   S.h.g = p->geom_dev();
   S.h.div_sl = kv_div((uint32_t)p->combos);
   S.h.div_b = kv_div((uint32_t)p->g.block_size);
+  S.h.div_bs = kv_div((uint32_t)(p->g.block_size * p->combos));
 }
 
 // Appends a pool's items (do_append) to the launch.  Item slices are token-major:
@@ -1458,31 +1469,26 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCt
     std::memcpy(b + h.pub_off, S.pub.data(), 4 * nent);
   }
   if (h.publish) h.counter = S.rep_pool[0]->step_counter;
-  // grid: every resident CTA once the launch moves >= one round (256 x 6 chunks) per CTA
+  // grid: enough CTAs for ~1024 16-B chunks each, at most every resident CTA
   const uint64_t rep_slices = with_rep ? S.rep_bytes / (uint64_t)h.g.seg_bytes : 0;
   const unsigned long long chunks = ((unsigned long long)h.app_slices + rep_slices)
                                     << h.g.cps_shift;
-  const int cap = resident_ctas(S.device);
-  int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + 1535) / 1536));
+  const int cap = step_resident_ctas(S.device, step_smem_bytes(h));
+  int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + 1023) / 1024));
+  // the blob goes to the device on the context's upload stream, ordered before the
+  // launch by an event: the copy overlaps whatever the launch stream is still running
   StageBuf *db = nullptr;
-  const char *gdata = nullptr;
-  int rc = KV_OK;
-  if (h.data_bytes > kStepInline) {
-    if ((rc = ctx->acquire(ctx->ring, ctx->next, (size_t)h.data_bytes, true, &db))) return rc;
-    std::memcpy(db->host, b, (size_t)h.data_bytes);
-    CU(cudaMemcpyAsync(db->dev, db->host, (size_t)h.data_bytes, cudaMemcpyHostToDevice, st));
-    gdata = db->dev;
-    int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_fn(), 256,
-                                                      step_smem_bytes(h)) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-    cudaGetLastError();
-    grid = std::min(grid, per_sm * (cap / 4));
-  }
+  int rc = ctx->acquire(ctx->ring, ctx->next, (size_t)h.data_bytes, true, &db);
+  if (rc) return rc;
+  if ((rc = ctx->ensure_upload())) return rc;
+  std::memcpy(db->host, b, (size_t)h.data_bytes);
+  CU(cudaMemcpyAsync(db->dev, db->host, (size_t)h.data_bytes, cudaMemcpyHostToDevice, ctx->upload));
+  CU(cudaEventRecord(db->up, ctx->upload));
+  CU(cudaStreamWaitEvent(st, db->up, 0));
+  const char *gdata = db->dev;
   const double t1 = now_s();
   phase_add(kPhStage, t1 - t0);
-  CU(launch_step(h, b, gdata, grid, st));
+  CU(launch_step(h, gdata, grid, st));
   phase_add(kPhLaunch, now_s() - t1);
   g_launches++;
   if (g_log_on) {

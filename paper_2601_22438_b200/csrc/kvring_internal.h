@@ -171,22 +171,15 @@ struct alignas(16) KvStepHdr {
   KvGeomDev g;
   KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)
   KvDiv div_b;                      // block size
+  KvDiv div_bs;                     // slices per block (block size x slices per token)
   KvStepPool app[kStepPools];
   KvStepPool rep[kStepPools];
 };
 
-// Data blob carried in the kernel parameter space for small launches.
-constexpr int kStepInline = 24 * 1024;
-template <int CAP>
-struct alignas(16) KvStepInlT {
-  KvStepHdr h;
-  alignas(16) char data[CAP];
-};
-// Launches the step kernel: data in the parameter space when data_bytes <= kStepInline
-// (4/8/16/24 KiB classes), else read from `gdata` (device copy of the blob).
-cudaError_t launch_step(const KvStepHdr &h, const char *host_data, const char *gdata, int grid,
-                        cudaStream_t stream);
+// Launches the step kernel over a device copy of the descriptor blob.
+cudaError_t launch_step(const KvStepHdr &h, const char *gdata, int grid, cudaStream_t stream);
 int step_smem_bytes(const KvStepHdr &h);
 const void *step_kernel_fn();
+int step_resident_ctas(int device, int smem);
 
 }  // namespace kvring

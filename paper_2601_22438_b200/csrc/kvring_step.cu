@@ -20,10 +20,10 @@
 // loop puts append k and the publication of k-1 in one launch; their slots are
 // disjoint by reading R7, so they need no ordering inside the kernel).
 //
-// Pure data movement, HBM / NVLink bound: no tensor cores.  Descriptors (items and
-// per-slot tables, <= 24 KiB) travel in the kernel parameter space; each CTA copies
-// them to shared memory with warp-uniform loads (the constant bank broadcasts),
-// larger launches read a device copy.
+// Pure data movement, HBM / NVLink bound: no tensor cores.  The per-launch header
+// (pool bases, step, divisors) travels in the kernel parameter space; the descriptor
+// blob (items and per-slot tables) is uploaded by the host on a side stream, ahead of
+// the launch, and each CTA copies it to shared memory with coalesced loads.
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -35,8 +35,12 @@ namespace kvring {
 namespace {
 
 constexpr int kThreads = 256;
+// 4 resident 256-thread CTAs per SM (32 warps: the address arithmetic of one warp hides
+// behind the others) with 8 independent 16-B loads in flight per thread (<= 64
+// registers): 128 KB in flight per SM; a decode step's share of a lane (~7 chunks at C2)
+// is one round of loads.
 constexpr int kMinBlocks = 4;
-constexpr int kU = 6;  // 16-B chunks in flight per thread (96 KB per SM at 4 CTAs / SM; 56 registers)
+constexpr int kU = 8;
 constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t x, const KvDiv &d) {
@@ -77,6 +81,7 @@ struct StepSmem {
   const int32_t *lo;
   int32_t *pref;
   int32_t *blk0;
+  int32_t *bpref;  // prefix over entries of the blocks each publication touches
 };
 
 __device__ __forceinline__ StepSmem step_smem(const KvStepHdr &h, char *sm) {
@@ -87,6 +92,7 @@ __device__ __forceinline__ StepSmem step_smem(const KvStepHdr &h, char *sm) {
   s.lo = reinterpret_cast<const int32_t *>(sm + h.pub_off);
   s.pref = reinterpret_cast<int32_t *>(sm + h.data_bytes);
   s.blk0 = s.pref + h.n_ent + 1;
+  s.bpref = s.blk0 + h.n_ent;
   return s;
 }
 
@@ -97,118 +103,198 @@ __device__ __forceinline__ int rep_pool_of(const KvStepHdr &h, int e) {
   return q;
 }
 
-// Append item walker: slice x (flat, append space) -> source / destination addresses.
-struct AppLoc {
-  const KvStepHdr &h;
-  const KvAppItem *items;
-  int i = -1, lo = 0, hi = 0;
-  __device__ AppLoc(const KvStepHdr &h_, const KvAppItem *it) : h(h_), items(it) {}
-  __device__ __forceinline__ void seek(int x) {
-    int a = 0, b = h.n_items - 1;  // last item with off <= x
-    while (a < b) {
-      const int m = (a + b + 1) >> 1;
-      if (items[m].off <= x) a = m; else b = m - 1;
-    }
-    i = a;
-    lo = items[a].off;
-    hi = a + 1 < h.n_items ? items[a + 1].off : h.app_slices;
-  }
-  __device__ __forceinline__ bool at(int x, const char *&sp, char *&dp) {
-    if (i < 0 || x < lo) seek(x);
-    while (x >= hi) {
-      ++i;
-      lo = hi;
-      hi = i + 1 < h.n_items ? items[i + 1].off : h.app_slices;
-    }
-    const KvAppItem &it = items[i];
-    const KvStepPool &pp = h.app[it.pool];
-    const uint32_t r = (uint32_t)(x - lo);
-    const uint32_t t = fdiv(r, h.div_sl);          // token inside the item
-    const uint32_t c = r - t * h.div_sl.d;         // (layer, K/V, head)
-    const uint32_t j = fdiv((uint32_t)it.p0, h.div_b);
-    const uint32_t tok = (uint32_t)it.p0 - j * (uint32_t)h.g.block_size + t;
-    sp = pp.src + (long long)(it.row + (int)t) * h.g.token_bytes + (long long)c * h.g.seg_bytes;
-    dp = pp.dst + (long long)it.blk * h.g.block_bytes +
-         (long long)(c * (uint32_t)h.g.block_size + tok) * h.g.seg_bytes;
-    return true;
-  }
-};
+// q / n for a small divisor n and q < 2^24: float reciprocal estimate, then an exact
+// integer correction (the estimate is within one of the quotient).
+__device__ __forceinline__ uint32_t div_small(uint32_t q, uint32_t n, float rn) {
+  uint32_t d = (uint32_t)((float)q * rn);
+  if (d * n > q) --d;
+  if ((d + 1) * n <= q) ++d;
+  return d;
+}
 
-// Replicate entry walker: slice x (flat, replicate space) -> addresses at the same
-// block id in this pool and in the successor's replica region (reading R5).
-struct RepLoc {
+// Work cursor over the launch's ONE flat space of slices: [0, A) are the append
+// items' slices, [A, A + P) the publication's.  A warp round moves kU consecutive warp
+// iterations; lane l handles 16-B chunk (l mod cps) of slice x + l / cps and each
+// iteration advances every lane by d = 32 / cps slices (16 lanes per 256-B slice:
+// coalesced).  Appends and publication share the space, so a lane issues its loads of
+// both in the same rounds (a decode step is one round of loads in flight per lane).
+//
+// Inside a piece (an append item, or one block of a publication entry) a slice is an
+// (inner, outer) pair; source offset = inner * s_in + outer * s_out, destination offset
+// = inner * d_in + outer * d_out, inner runs fastest:
+//   append  (token-major: the dense source row is read contiguously)
+//           inner = (layer, K/V, head) c < SL, outer = token t:
+//           src = row base + t * token_bytes + c * seg; dst = block + (c * B + t0 + t) * seg
+//   publish ((layer, K/V, head)-major within a block piece of n tokens: a full block is
+//           ONE contiguous run, read from this pool and written at the same offsets of
+//           the successor's replica region, reading R5)
+//           inner = token t < n, outer = combo c: off = block + (c * B + t0 + t) * seg
+// so stepping d slices is pointer += d * stride plus a rare carry; only a piece boundary
+// (or the round's end, or a fault-injection cut) starts a new sub-round with a locate.
+struct Cursor {
   const KvStepHdr &h;
   const StepSmem &s;
-  int e = -1, lo = 0, hi = 0, q = 0, slot = 0, plo = 0;
-  int cj = -1, cblk = 0;  // cached (j, block id) of the current entry
-  __device__ RepLoc(const KvStepHdr &h_, const StepSmem &s_) : h(h_), s(s_) {}
-  __device__ __forceinline__ void enter(int ee) {
-    e = ee;
-    lo = s.pref[e];
-    hi = s.pref[e + 1];
-    q = rep_pool_of(h, e);
-    slot = e - h.rep[q].ent_off;
-    plo = s.lo[e];
-    cj = -1;
-  }
-  __device__ __forceinline__ void seek(int x) {
-    int a = 0, b = h.n_ent - 1;  // last entry with pref <= x and a non-empty range
-    while (a < b) {
-      const int m = (a + b + 1) >> 1;
-      if (s.pref[m] <= x) a = m; else b = m - 1;
+  const char *sp = nullptr;   // current slice's source address
+  char *dp = nullptr;         // current slice's destination address
+  uint32_t in = 0, nin = 1;
+  int ds_in = 0, dd_in = 0;   // d * s_in, d * d_in
+  int s_wrap = 0, d_wrap = 0; // s_out - nin * s_in, d_out - nin * d_in
+  int idx = -1;               // item / entry of the current piece
+  int pb = -1;                // end of the piece (flat slice)
+  int lim = 0x7fffffff;       // publication cut short by fault injection (flat slice)
+  bool in_rep = false;        // idx is a publication entry
+  __device__ Cursor(const KvStepHdr &h_, const StepSmem &s_) : h(h_), s(s_) {}
+
+  __device__ __forceinline__ void locate(int x, uint32_t d) {
+    uint32_t out, s_in, s_out, d_in, d_out;
+    const uint32_t B = (uint32_t)h.g.block_size, seg = (uint32_t)h.g.seg_bytes;
+    if (x < h.app_slices) {
+      const KvAppItem *items = s.items;
+      int a = !in_rep && idx >= 0 && items[idx].off <= x ? idx : 0, b = h.n_items - 1;
+      while (a < b) {                  // last item with off <= x
+        const int m = (a + b + 1) >> 1;
+        if (items[m].off <= x) a = m; else b = m - 1;
+      }
+      idx = a;
+      in_rep = false;
+      const KvAppItem &it = items[a];
+      pb = a + 1 < h.n_items ? items[a + 1].off : h.app_slices;
+      lim = 0x7fffffff;
+      const uint32_t r = (uint32_t)(x - it.off);
+      out = fdiv(r, h.div_sl);
+      in = r - out * h.div_sl.d;
+      nin = h.div_sl.d;
+      const KvStepPool &pp = h.app[it.pool];
+      const uint32_t j = fdiv((uint32_t)it.p0, h.div_b);
+      s_in = seg;
+      s_out = (uint32_t)h.g.token_bytes;
+      d_in = B * seg;
+      d_out = seg;
+      sp = pp.src + (long long)it.row * h.g.token_bytes + (long long)(in * s_in) +
+           (long long)out * s_out;
+      dp = pp.dst + (long long)it.blk * h.g.block_bytes +
+           (long long)(it.p0 - j * B) * seg + (long long)(in * d_in) + (long long)out * d_out;
+    } else {
+      const int xr = x - h.app_slices;
+      if (!in_rep || xr < s.pref[idx] || xr >= s.pref[idx + 1]) {
+        int a = in_rep && xr >= s.pref[idx] ? idx : 0, b = h.n_ent - 1;
+        while (a < b) {                // last entry with pref <= xr
+          const int m = (a + b + 1) >> 1;
+          if (s.pref[m] <= xr) a = m; else b = m - 1;
+        }
+        idx = a;
+        in_rep = true;
+      }
+      const int e = idx;
+      const int q = rep_pool_of(h, e);
+      const KvStepPool &pp = h.rep[q];
+      const int slot = e - pp.ent_off;
+      lim = (h.any_abort && pp.abort_slices >= 0)
+                ? h.app_slices + s.pref[pp.ent_off] + pp.abort_slices : 0x7fffffff;
+      const uint32_t SL = h.div_sl.d;
+      const uint32_t plo = (uint32_t)s.lo[e], phi = (uint32_t)s.hi[e];
+      const uint32_t j0 = fdiv(plo, h.div_b), t0 = plo - j0 * B;
+      const uint32_t n0 = min(B - t0, phi - plo);
+      const uint32_t r = (uint32_t)(xr - s.pref[e]);
+      uint32_t j, tok0, rr, pa;
+      if (r < n0 * SL) {               // the entry's first (possibly partial) block
+        j = j0;
+        nin = n0;
+        tok0 = t0;
+        rr = r;
+        pa = 0;
+      } else {                         // full blocks, the last one possibly partial
+        const uint32_t r2 = r - n0 * SL;
+        const uint32_t jj = fdiv(r2, h.div_bs);
+        j = j0 + 1 + jj;
+        nin = min(B, phi - j * B);
+        tok0 = 0;
+        rr = r2 - jj * h.div_bs.d;
+        pa = n0 * SL + jj * h.div_bs.d;
+      }
+      pb = h.app_slices + s.pref[e] + (int)(pa + nin * SL);
+      out = div_small(rr, nin, __frcp_rn((float)nin));
+      in = rr - out * nin;
+      const int blk = j == j0 ? s.blk0[e] : pp.bt[(size_t)slot * pp.M + j];
+      const long long off = (long long)blk * h.g.block_bytes + (long long)tok0 * seg +
+                            (long long)in * seg + (long long)out * (B * seg);
+      s_in = d_in = seg;
+      s_out = d_out = B * seg;
+      sp = pp.src + off;
+      dp = pp.dst + off;
     }
-    enter(a);
+    ds_in = (int)(d * s_in);
+    dd_in = (int)(d * d_in);
+    s_wrap = (int)s_out - (int)(nin * s_in);
+    d_wrap = (int)d_out - (int)(nin * d_in);
   }
-  // false: the chunk is not copied (fault injection cut the pool's step short)
-  __device__ __forceinline__ bool at(int x, const char *&sp, char *&dp) {
-    if (e < 0 || x < lo) seek(x);
-    while (x >= hi) enter(e + 1);
-    const KvStepPool &pp = h.rep[q];
-    if (h.any_abort && pp.abort_slices >= 0 && x - s.pref[pp.ent_off] >= pp.abort_slices)
-      return false;
-    const uint32_t r = (uint32_t)(x - lo);
-    const uint32_t t = fdiv(r, h.div_sl);
-    const uint32_t c = r - t * h.div_sl.d;
-    const uint32_t p = (uint32_t)plo + t;           // token position in the request
-    const uint32_t j = fdiv(p, h.div_b);
-    const uint32_t tok = p - j * (uint32_t)h.g.block_size;
-    if ((int)j != cj) {
-      cj = (int)j;
-      cblk = j == fdiv((uint32_t)plo, h.div_b) ? s.blk0[e] : pp.bt[(size_t)slot * pp.M + j];
+
+  __device__ __forceinline__ void carry_src() {
+    while (in >= nin) {
+      in -= nin;
+      sp += s_wrap;
     }
-    const long long off = (long long)cblk * h.g.block_bytes +
-                          (long long)(c * (uint32_t)h.g.block_size + tok) * h.g.seg_bytes;
-    sp = pp.src + off;
-    dp = pp.dst + off;
-    return true;
   }
 };
 
-// Copies the chunks [c0, c1) of one flat space: thread t takes chunks c0 + t,
-// c0 + t + 256, ... (16 consecutive lanes cover one 256-B slice: coalesced); all
-// kU loads of a round are issued before its stores.
-template <class Loc>
-__device__ __forceinline__ void copy_range(uint32_t c0, uint32_t c1, Loc &loc,
-                                           const KvGeomDev &g) {
-  const uint32_t cmask = (1u << g.cps_shift) - 1u;
-  for (uint32_t base = c0; base < c1; base += (uint32_t)kThreads * kU) {
-    uint4 v[kU];
-    char *dp[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t y = base + (uint32_t)(u * kThreads) + threadIdx.x;
-      dp[u] = nullptr;
-      const char *sp;
-      char *d;
-      if (y < c1 && loc.at((int)(y >> g.cps_shift), sp, d)) {
-        const uint32_t lc = (y & cmask) << 4;
-        v[u] = ld_stream(sp + lc);
-        dp[u] = d + lc;
+// Copies the flat space [0, T) with every warp of the grid: rounds of kU warp
+// iterations (32 x kU chunks of consecutive slices: 4 KiB at 256-B slices) are dealt
+// grid-stride, so the whole grid works inside one window of ~(warps x 4 KiB) at a time.
+// A lane locates its piece once per (sub-)round and then only adds strides; a round is
+// split where a lane's slices leave the piece (rare: pieces are >= 128 slices at C2).
+// All loads of a (sub-)round are issued before its stores; the stores replay the
+// destination stepping instead of keeping kU pointers live.
+__device__ __forceinline__ void copy_all(int T, Cursor &cur, const KvGeomDev &g) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)blockIdx.x * kWarps + (int)(threadIdx.x >> 5);
+  const int W = (int)gridDim.x * kWarps;
+  const int cs = g.cps_shift;
+  const uint32_t d = 32u >> cs;                 // slices per warp iteration
+  const int span = (int)d * kU;                 // slices per warp round
+  const uint32_t lc = ((uint32_t)lane & ((1u << cs) - 1u)) << 4;
+  for (long long base = (long long)gw * span; base < T; base += (long long)W * span) {
+    const int rend = (int)min((long long)T, base + span);
+    int x = (int)base + (lane >> cs);           // this lane's slice
+    while (__any_sync(0xffffffffu, x < rend)) {
+      int n = 0;
+      if (x < rend) {
+        cur.locate(x, d);
+        const bool skip = x >= cur.lim;
+        const int end = min(min(rend, cur.pb), skip ? cur.pb : cur.lim);
+        n = min(kU, (end - x + (int)d - 1) / (int)d);
+        if (skip) {                             // fault injection: this stretch is not copied
+          x += n * (int)d;
+          n = 0;
+        }
       }
-    }
+      char *const dp0 = cur.dp;
+      const uint32_t in0 = cur.in;
+      uint4 v[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (dp[u]) st_stream(dp[u], v[u]);
+      for (int u = 0; u < kU; ++u) {
+        if (u < n) {
+          v[u] = ld_stream(cur.sp + lc);
+          cur.sp += cur.ds_in;
+          cur.in += d;
+          cur.carry_src();
+        }
+      }
+      char *dq = dp0;
+      uint32_t in = in0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (u < n) {
+          st_stream(dq + lc, v[u]);
+          dq += cur.dd_in;
+          in += d;
+          while (in >= cur.nin) {
+            in -= cur.nin;
+            dq += cur.d_wrap;
+          }
+        }
+      }
+      x += n * (int)d;
+    }
   }
 }
 
@@ -236,23 +322,14 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *total) {
   return wbase + x - v;
 }
 
-template <bool INL>
 __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__restrict__ data) {
   extern __shared__ __align__(16) char sm[];
-  // 1. descriptor blob -> shared memory
+  // 1. descriptor blob (device copy, uploaded ahead on a side stream) -> shared memory:
+  //    coalesced 16-B loads, one round trip (every CTA reads the same bytes: L2 hits)
   {
     const int n16 = h.data_bytes >> 4;
-    if (INL) {
-      // parameter space: warp-uniform 16-B loads (constant-bank broadcast)
-      const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int k = w; k < n16; k += kWarps) {
-        const uint4 x = reinterpret_cast<const uint4 *>(data)[k];
-        if (lane == 0) reinterpret_cast<uint4 *>(sm)[k] = x;
-      }
-    } else {
-      for (int k = threadIdx.x; k < n16; k += kThreads)
-        reinterpret_cast<uint4 *>(sm)[k] = reinterpret_cast<const uint4 *>(data)[k];
-    }
+    for (int k = threadIdx.x; k < n16; k += kThreads)
+      reinterpret_cast<uint4 *>(sm)[k] = __ldg(reinterpret_cast<const uint4 *>(data) + k);
   }
   __syncthreads();
   StepSmem s = step_smem(h, sm);
@@ -263,7 +340,7 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
   if (h.n_rep > 0) {
     const int per = (h.n_ent + kThreads - 1) / kThreads;
     const int e0 = min((int)threadIdx.x * per, h.n_ent), e1 = min(e0 + per, h.n_ent);
-    int local = 0;
+    int local = 0, blocal = 0;
     int q = e0 < h.n_ent ? rep_pool_of(h, e0) : 0;
     for (int e = e0; e < e1; ++e) {
       while (q + 1 < h.n_rep && e >= h.rep[q + 1].ent_off) ++q;
@@ -279,34 +356,38 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
       const int cnt = (hi - lo) * (int)SL;
       s.pref[e] = cnt;
       local += cnt;
+      const int nb = hi > lo ? (hi + B - 1) / B - lo / B : 0;  // blocks touched (bt entries)
+      s.bpref[e] = nb;
+      blocal += nb;
       if (hi > lo) {
         const int slot = e - pp.ent_off;
         s.blk0[e] = pp.bt[(size_t)slot * pp.M + (lo / B)];
       }
     }
-    int total;
+    int total, btotal;
     int base = block_exclusive_scan(local, &total);
+    __syncthreads();  // the scan's shared scratch is reused below
+    int bbase = block_exclusive_scan(blocal, &btotal);
     for (int e = e0; e < e1; ++e) {
       const int c = s.pref[e];
       s.pref[e] = base;
       base += c;
+      const int cb = s.bpref[e];
+      s.bpref[e] = bbase;
+      bbase += cb;
     }
-    if (threadIdx.x == 0) s.pref[h.n_ent] = total;
+    if (threadIdx.x == 0) {
+      s.pref[h.n_ent] = total;
+      s.bpref[h.n_ent] = btotal;
+    }
     P = total;
     __syncthreads();
   }
   // 3. copies: this CTA's share of each flat space
   const uint32_t G = gridDim.x, b = blockIdx.x;
-  const int cs = h.g.cps_shift;
-  if (h.n_items > 0) {
-    const unsigned long long T = (unsigned long long)h.app_slices << cs;
-    AppLoc loc(h, s.items);
-    copy_range((uint32_t)(T * b / G), (uint32_t)(T * (b + 1) / G), loc, h.g);
-  }
-  if (P > 0) {
-    const unsigned long long T = (unsigned long long)P << cs;
-    RepLoc loc(h, s);
-    copy_range((uint32_t)(T * b / G), (uint32_t)(T * (b + 1) / G), loc, h.g);
+  {
+    Cursor cur(h, s);
+    copy_all(h.app_slices + P, cur, h.g);
   }
   // 4. tables: the appended items' device bt entries; the publication's parity
   //    (req_id, len) table and the bt entries of the blocks it touched.  Readers trust
@@ -328,16 +409,28 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
       for (uint32_t sl = gt; sl < (uint32_t)R; sl += stride) {
         if ((int)sl < pp.n_slots) {
           const int e = pp.ent_off + (int)sl;
-          const int lo = s.lo[e], hi = s.hi[e];
+          const int hi = s.hi[e];
           mreq[sl] = hi > 0 ? s.req[e] : -1;
           mlen[sl] = hi;
-          if (hi > lo)
-            for (int j = lo / B; j * B < hi; ++j)
-              mbt[(size_t)sl * pp.M + j] = j == lo / B ? s.blk0[e] : pp.bt[(size_t)sl * pp.M + j];
         } else {
           mreq[sl] = -1;
           mlen[sl] = 0;
         }
+      }
+      // bt entries of every touched block, one per thread over the whole pool (a bulk
+      // re-seed touches thousands of blocks per request)
+      const int e_lo = pp.ent_off, e_hi = pp.ent_off + pp.n_slots;
+      const int nb_lo = s.bpref[e_lo], nb_hi = s.bpref[e_hi];
+      for (uint32_t k = gt; k < (uint32_t)(nb_hi - nb_lo); k += stride) {
+        const int gk = nb_lo + (int)k;
+        int a = e_lo, z = e_hi - 1;      // last entry with bpref <= gk
+        while (a < z) {
+          const int m = (a + z + 1) >> 1;
+          if (s.bpref[m] <= gk) a = m; else z = m - 1;
+        }
+        const int sl = a - pp.ent_off;
+        const int j = s.lo[a] / B + (gk - s.bpref[a]);
+        mbt[(size_t)sl * pp.M + j] = gk == s.bpref[a] ? s.blk0[a] : pp.bt[(size_t)sl * pp.M + j];
       }
       if (gt == 0) *reinterpret_cast<int32_t *>(pp.meta + 8) = pp.writer_node;
     }
@@ -371,53 +464,48 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
 
 }  // namespace
 
-// Descriptors in the kernel parameter space (<= kStepInline bytes of data).
-template <int CAP>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-    kv_step_inl_kernel(const __grid_constant__ KvStepInlT<CAP> d) {
-  step_body<true>(d.h, d.data);
-}
-
-// Larger launches: the blob is a device copy (staged H2D by the host).
+// The decode-step kernel: header by value in the parameter space, descriptor blob in
+// device memory.
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     kv_step_kernel(const __grid_constant__ KvStepHdr h, const char *__restrict__ gdata) {
-  step_body<false>(h, gdata);
+  step_body(h, gdata);
 }
 
 const void *step_kernel_fn() { return reinterpret_cast<const void *>(kv_step_kernel); }
 
+// Resident CTAs of the step kernel on `device` for a launch's shared memory.
+int step_resident_ctas(int device, int smem) {
+  static int cache_dev = -1, cache_smem = -1, cache_val = 0;
+  if (device == cache_dev && smem == cache_smem) return cache_val;
+  int sms = 148, per = kMinBlocks;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    sms = 148;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kv_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kv_step_kernel, kThreads, smem) !=
+          cudaSuccess || per < 1)
+    per = 1;
+  cudaGetLastError();
+  cache_dev = device;
+  cache_smem = smem;
+  cache_val = sms * per;
+  return cache_val;
+}
+
 int step_smem_bytes(const KvStepHdr &h) {
-  return h.data_bytes + 4 * (2 * h.n_ent + 1) + 16;
+  return h.data_bytes + 4 * (3 * h.n_ent + 2) + 16;
 }
 
 namespace {
-template <int CAP>
-cudaError_t launch_inl(const KvStepHdr &h, const char *host_data, int grid, int smem,
-                       cudaStream_t st) {
-  static thread_local KvStepInlT<CAP> d;  // argument block (copied by the launch)
-  d.h = h;
-  memcpy(d.data, host_data, (size_t)h.data_bytes);
-  kv_step_inl_kernel<CAP><<<grid, kThreads, smem, st>>>(d);
-  return cudaGetLastError();
-}
-
 bool g_attr_set = false;
 }  // namespace
 
-cudaError_t launch_step(const KvStepHdr &h, const char *host_data, const char *gdata, int grid,
-                        cudaStream_t st) {
+cudaError_t launch_step(const KvStepHdr &h, const char *gdata, int grid, cudaStream_t st) {
   const int smem = step_smem_bytes(h);
   if (!g_attr_set) {
-    // staged launches may carry up to ~200 KiB of descriptors in shared memory
+    // large launches may carry up to ~200 KiB of descriptors in shared memory
     cudaFuncSetAttribute(kv_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     g_attr_set = true;
-  }
-  if (gdata == nullptr) {
-    if (h.data_bytes <= 4096) return launch_inl<4096>(h, host_data, grid, smem, st);
-    if (h.data_bytes <= 8192) return launch_inl<8192>(h, host_data, grid, smem, st);
-    if (h.data_bytes <= 16384) return launch_inl<16384>(h, host_data, grid, smem, st);
-    if (h.data_bytes <= kStepInline) return launch_inl<kStepInline>(h, host_data, grid, smem, st);
-    return cudaErrorInvalidValue;
   }
   kv_step_kernel<<<grid, kThreads, smem, st>>>(h, gdata);
   return cudaGetLastError();
