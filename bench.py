@@ -202,10 +202,14 @@ def layout_map(kind, N, S):
     return P, coords, placement, succ
 
 
-def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every, publish=True):
+def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, instrument=False,
+               publish=True):
     """Runs W warm-up and K timed decode steps of the schedule from step t through the
     one-launch-per-step loop (kv_loop_run: each step prepared and launched in order, no
-    lookahead).  Sources are pre-generated in HBM (> L2).  Returns the timing record."""
+    lookahead).  Sources are pre-generated in HBM (> L2).  Not instrumented, consecutive
+    launches overlap (programmatic dependent launch: a launch's prologue runs while the
+    previous step's grid drains); `instrument` brackets every launch with CUDA events
+    (which serialises them) to time each kernel alone.  Returns the timing record."""
     import torch
     import torch.distributed as dist
 
@@ -230,7 +234,7 @@ def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every, publis
                    for node, e in drv.plan(tt).items() if node in rt.local]
             pools = [rt.handle(nd) for nd in rt.alive_local() if rt.succ.get(nd) is not None]
             st = dict(append=app, repl_pools=pools if (tt >= 1 and publish) else [], step=tt)
-            if timing and k % every == 0:
+            if timing:
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
                 st.update(ev_kernel_start=ev[0], ev_kernel_end=ev[1])
                 evs.append((k, ev))
@@ -238,7 +242,7 @@ def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every, publis
         return K.PreparedSteps(steps), evs
 
     warm, _ = prepare(t, args.warmup, False)
-    timed, evs = prepare(t + args.warmup, args.steps, True)
+    timed, evs = prepare(t + args.warmup, args.steps, instrument)
     torch.cuda.synchronize(dev)
     kl.run(warm, comp.cuda_stream)
     torch.cuda.synchronize(dev)
@@ -271,33 +275,36 @@ def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every, publis
             "src_gib": src_bytes / 2**30}
 
 
-def paired_roofline(rec, steps, N, hbm_peak, peak_src):
-    """Roofline of the decode-step kernel from the SAME launches: every timed launch
-    that carries CUDA events (all of them when steps <= 64) is paired with its own
-    algorithmic bytes from the launch log; achieved = sum(bytes) / sum(durations).
-    N = 1: HBM bytes = append (read dense source + write pool) + publication (read
-    pool + write the local replica) = 2 (app + rep).  N > 1: the publication's bytes
-    cross NVLink (its stores go to the peer), reported against the NVLink peak; the
-    HBM figure (2 app + rep, this GPU's own traffic) beside it."""
+def launch_bytes(r, N):
+    """Algorithmic bytes of one decode-step launch: (HBM, NVLink).  N = 1: append (read the
+    dense source + write the pool) + publication (read the pool + write the local replica)
+    = 2 (app + rep) through HBM.  N > 1: the publication's writes go to the peer over
+    NVLink, so HBM carries 2 app + rep and NVLink rep."""
+    if N == 1:
+        return 2 * r["app_bytes"] + 2 * r["rep_bytes"], 0
+    return 2 * r["app_bytes"] + r["rep_bytes"], r["rep_bytes"]
+
+
+def timed_roofline(rec, N, hbm_peak, peak_src):
+    """Roofline of the decode-step kernel over the timed region: every launch in it (the
+    launch log of the same region) with its algorithmic bytes, divided by the region's
+    CUDA-event duration -- the kernel's average launch duration in the pipelined loop is
+    region / launches.  N = 1: HBM-bound; N > 1: the NVLink hop (publication bytes) against
+    the NVLink peak, the HBM figure beside it."""
     log = rec["log"]
-    if len(log) != steps:
-        return {"paired": False, "note": "launch log has %d records for %d steps" % (len(log), steps)}
-    durs, hb, nb, ab, rb = [], 0.0, 0.0, 0.0, 0.0
-    for k, ev in rec["evs"]:
-        d = ev[0].elapsed_time(ev[1]) * 1e-3
-        r = log[k]
-        durs.append(d)
-        ab += r["app_bytes"]
-        rb += r["rep_bytes"]
-        hb += 2 * r["app_bytes"] + (2 if N == 1 else 1) * r["rep_bytes"]
-        nb += r["rep_bytes"]
-    T = sum(durs)
-    kname = "kv_step_inl_kernel (one launch per step: append k + publication k-1)"
-    out = {"kernel": kname, "launches_paired": len(durs), "avg_launch_us": round(T / len(durs) * 1e6, 2),
-           "median_launch_us": round(statistics.median(durs) * 1e6, 2),
-           "algorithmic_bytes_per_launch": int(hb / len(durs)),
-           "append_bytes_per_launch": int(ab / len(durs)),
-           "replicate_bytes_per_launch": int(rb / len(durs)), "paired": True}
+    T = rec["ms"] * 1e-3
+    hb = sum(launch_bytes(r, N)[0] for r in log)
+    nb = sum(launch_bytes(r, N)[1] for r in log)
+    n = max(1, len(log))
+    out = {"kernel": "kv_step_kernel (one launch per step: append k + publication k-1)",
+           "launches": len(log), "avg_launch_us": round(T / n * 1e6, 2),
+           "algorithmic_bytes_per_launch": int((hb if N == 1 else nb) / n),
+           "hbm_bytes_per_launch": int(hb / n),
+           "append_bytes_per_launch": int(sum(r["app_bytes"] for r in log) / n),
+           "replicate_bytes_per_launch": int(sum(r["rep_bytes"] for r in log) / n),
+           "what": "sum over the timed region's launches (kv_launch_log) of their algorithmic "
+                   "bytes / the region's CUDA-event duration (= bytes per launch / average "
+                   "launch duration; launches overlap by programmatic dependent launch)"}
     hbm = hb / T / 1e9
     if N == 1:
         out.update(bound="hbm", achieved=round(hbm, 1), peak=hbm_peak, unit="GB/s",
@@ -309,6 +316,28 @@ def paired_roofline(rec, steps, N, hbm_peak, peak_src):
                    peak_source="B200_PROFILING.md measured peer copy 770 GB/s/direction",
                    hbm={"achieved": round(hbm, 1), "peak": hbm_peak,
                         "frac": round(hbm / hbm_peak, 4)})
+    return out
+
+
+def isolated_launches(rec, N, hbm_peak):
+    """The instrumented pass: each launch bracketed by its own CUDA events (serialised, no
+    overlap), paired with its own bytes from the launch log."""
+    log, evs = rec["log"], rec["evs"]
+    if len(log) != len(evs):
+        return {"paired": False, "note": "launch log has %d records for %d timed steps"
+                                         % (len(log), len(evs))}
+    durs = [ev[0].elapsed_time(ev[1]) * 1e-3 for _, ev in evs]
+    hb = sum(launch_bytes(r, N)[0] for r in log)
+    nb = sum(launch_bytes(r, N)[1] for r in log)
+    T = sum(durs)
+    out = {"launches": len(durs), "median_us": round(statistics.median(durs) * 1e6, 2),
+           "avg_us": round(T / len(durs) * 1e6, 2),
+           "p99_us": round(float(np.percentile(durs, 99)) * 1e6, 2),
+           "hbm_gb_s": round(hb / T / 1e9, 1), "hbm_frac": round(hb / T / 1e9 / hbm_peak, 4),
+           "what": "each launch alone between its own CUDA events (no overlap), paired with "
+                   "its own algorithmic bytes"}
+    if N > 1:
+        out["nvlink_gb_s"] = round(nb / T / 1e9, 1)
     return out
 
 
@@ -347,7 +376,6 @@ def run_kvring(args):
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     hbm_peak, peak_src = peaks()
-    every = 1 if args.steps <= 64 else 8
 
     def build(kind, n_extra):
         base = configs.C2
@@ -372,7 +400,7 @@ def run_kvring(args):
     # legs after the headline: appends-only (W + K), two-stream (K), e2e, NCCL,
     # interference (2x), block mode (+1 re-seed), slack
     n_extra = (args.e2e_steps + args.nccl_steps + 2 * args.interference_steps + args.block_steps
-               + 2 * (args.warmup + args.steps) + 40)
+               + 4 * (args.warmup + args.steps) + 40)
     cfg, rt, drv, content = build("weak", n_extra)
 
     # ---- prelude: reach steady state (untimed; sequential protocol on one stream) ----
@@ -387,20 +415,23 @@ def run_kvring(args):
     # ---- headline: one launch per decode step (kv_loop), W warm-up + K timed ----------
     kl = K.KvLoop()
     t_timed0 = t + args.warmup
-    rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every)
+    rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world)
     t += args.warmup + args.steps
     mx, sm = reduce_max_sum([rec["ms"], rec["bytes"], float(rec["launches"])], dev, world)
     ms_max, tot_bytes, tot_launch = mx[0], sm[1], sm[2]
-    roof = paired_roofline(rec, args.steps, N, hbm_peak, peak_src)
-    traffic = traffic_ref("decode_population", "kv_step_inl_kernel")
+    roof = timed_roofline(rec, N, hbm_peak, peak_src)
+    traffic = traffic_ref("decode_population", "kv_step_kernel")
     roof["traffic"] = traffic["traffic"] if traffic else None
     if traffic:
         roof["traffic_note"] = traffic.get("note")
-    kern_us = sorted(ev[0].elapsed_time(ev[1]) * 1e3 for _, ev in rec["evs"])
+
+    # ---- the same loop, every launch timed alone (events serialise the launches) -------
+    inst = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, instrument=True)
+    t += args.warmup + args.steps
+    iso = isolated_launches(inst, N, hbm_peak)
 
     # ---- the same steps' appends alone: the per-step cost of replication --------------
-    base_rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every,
-                          publish=False)
+    base_rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, publish=False)
     t += args.warmup + args.steps
     ms_app = reduce_max_sum([base_rec["ms"]], dev, world)[0][0]
     # re-seed the backlog the append-only steps left (untimed)
@@ -454,7 +485,7 @@ def run_kvring(args):
     # ---- SURVEY §8(e) layout at N > 1: one C2 stage per GPU ----------------------------
     survey = None
     if N > 1 and args.survey_layout:
-        survey = run_survey_layout(args, build, dev, world, comp, every)
+        survey = run_survey_layout(args, build, dev, world, comp)
         torch.cuda.empty_cache()
 
     # ---- C4 failover (configs[3]): 16 logical nodes, batch 128, kill (0,2) at step 300 --
@@ -496,9 +527,7 @@ def run_kvring(args):
             "what": "per decode step: the same loop with and without the publications (K steps "
                     "each, max over ranks); the harness has no model compute, so this is the "
                     "whole device cost replication adds to a step (interference: with a model)"},
-        "kernel_us": {"kernel": roof.get("kernel"), "median": round(statistics.median(kern_us), 2),
-                      "avg": round(sum(kern_us) / len(kern_us), 2),
-                      "timed_launches": len(kern_us)},
+        "kernel_us": iso,
         "roofline": roof,
         "step_roofline": step_roofline(tot_bytes, ms_max, N, hbm_peak, peak_src),
         "gpu_launches": int(tot_launch),
@@ -567,7 +596,7 @@ def run_two_stream(args, K, drv, rt, t0, comp, repl, content, dev, world):
                     "replication stream after an event (2 launches per step)"}
 
 
-def run_survey_layout(args, build, dev, world, comp, every):
+def run_survey_layout(args, build, dev, world, comp):
     """C2 with one stage per GPU (1 pipeline at N <= 4, N / 4 pipelines
     beyond); same loop, warm-up and timing as the headline."""
     import torch
@@ -581,11 +610,11 @@ def run_survey_layout(args, build, dev, world, comp, every):
         t += 1
     torch.cuda.synchronize(dev)
     kl = K.KvLoop()
-    rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, every)
+    rec = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world)
     mx, sm = reduce_max_sum([rec["ms"], rec["bytes"]], dev, world)
     ms, tot = mx[0], sm[1]
     hbm_peak, peak_src = peaks()
-    roof = paired_roofline(rec, args.steps, world, hbm_peak, peak_src)
+    roof = timed_roofline(rec, world, hbm_peak, peak_src)
     stages = len(rt.alive_local())
     kl.destroy()
     rt.destroy()

@@ -363,7 +363,8 @@ int kv_time_next_launch(void *ev_before, void *ev_after);
 /* Host-side phase counters of the decode path (seconds, cumulative since the last
  * reset; diagnostics, updated without synchronisation): [0] append preparation
  * (validation, allocation, items), [1] publication preparation (snapshot +
- * commit), [2] descriptor staging / host-source staging, [3] launch calls.
+ * commit), [2] descriptor staging / host-source staging, [3] launch calls; [4..7] split
+ * [2]: packing the descriptor blob, acquiring a staging slot, the H2D call, events.
  * Copies min(n, count) values; returns the count. */
 int kv_host_profile(double *out, int32_t n, int32_t reset);
 

@@ -32,7 +32,8 @@
 // Host-side phase counters of the decode path (seconds, cumulative; kv_host_profile).
 #include <chrono>
 namespace {
-enum { kPhPrepAppend = 0, kPhPrepRepl, kPhStage, kPhLaunch, kPhN };
+enum { kPhPrepAppend = 0, kPhPrepRepl, kPhStage, kPhLaunch, kPhPack, kPhAcquire, kPhH2D,
+       kPhEvents, kPhN };
 std::atomic<long long> g_phase_ns[kPhN];
 inline double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -179,10 +180,10 @@ class SlotMap {
 // Pinned-host + device staging buffer ring, per device (shared by its pools).
 struct StageBuf {
   char *host = nullptr;
+  char *hmapped = nullptr;    // device-side address of `host` (zero-copy reads)
   char *dev = nullptr;
   size_t cap = 0;
   cudaEvent_t ev = nullptr;   // recorded on the consuming stream after the last use
-  cudaEvent_t up = nullptr;   // recorded on the upload stream after the H2D copy
   bool pending = false;
 };
 
@@ -195,10 +196,60 @@ struct DeviceCtx {
   StageBuf src[kRing];  // device copies of host-resident append sources (KV_SRC_HOST)
   int next_src = 0;
   unsigned long long *unpack_counter = nullptr;
-  cudaStream_t upload = nullptr;  // descriptor uploads of the decode-step engine
-  int ensure_upload() {
-    if (upload) return KV_OK;
-    CU(cudaStreamCreateWithFlags(&upload, cudaStreamNonBlocking));
+  // Descriptor slots of the decode-step engine.  A slot is reused once the pinned word
+  // done[slot] (written by the launch's last CTA) shows the nonce of its last launch: the
+  // host polls memory instead of recording an event per launch, so nothing but kernels
+  // sits between two steps on the stream (a programmatic launch overlaps them).
+  static constexpr int kBlobRing = 32;
+  struct BlobSlot {
+    char *host = nullptr, *hmapped = nullptr, *dev = nullptr;
+    size_t cap = 0;
+    unsigned long long used = 0;  // nonce of the last launch that read this slot
+  };
+  BlobSlot blob[kBlobRing];
+  int next_blob = 0;
+  unsigned long long *flags = nullptr;     // device: per slot, nonce of the blob its buffer holds
+  unsigned long long *counters = nullptr;  // device: per slot, completion counter
+  volatile unsigned long long *done_host = nullptr;  // pinned host: per slot, last completed nonce
+  unsigned long long *done_dev = nullptr;       // its device-side address
+  int acquire_blob(size_t bytes, BlobSlot **out, int *index) {
+    if (!flags) {
+      CU(cudaMalloc(reinterpret_cast<void **>(&flags), 128 * (size_t)kBlobRing));
+      CU(cudaMemset(flags, 0, 128 * (size_t)kBlobRing));
+      CU(cudaMalloc(reinterpret_cast<void **>(&counters), 128 * (size_t)kBlobRing));
+      CU(cudaMemset(counters, 0, 128 * (size_t)kBlobRing));
+      void *h = nullptr;
+      CU(cudaHostAlloc(&h, 64 * (size_t)kBlobRing, cudaHostAllocMapped));
+      std::memset(h, 0, 64 * (size_t)kBlobRing);
+      done_host = static_cast<volatile unsigned long long *>(h);
+      CU(cudaHostGetDevicePointer(reinterpret_cast<void **>(&done_dev), h, 0));
+    }
+    const int i = next_blob;
+    next_blob = (next_blob + 1) % kBlobRing;
+    BlobSlot &b = blob[i];
+    // wait for the slot's previous launch (bounded: a launch that never completes is a
+    // sticky CUDA error, surfaced instead of spinning forever)
+    const double t0 = now_s();
+    for (long long k = 0; done_host[8 * i] < b.used; ++k) {
+      if ((k & 1023) == 1023) {
+        const cudaError_t e = cudaStreamQuery(nullptr);
+        if (e != cudaSuccess && e != cudaErrorNotReady)
+          return fail(KV_ECUDA, "decode-step launch failed: %s", cudaGetErrorString(e));
+        if (now_s() - t0 > 30.0) return fail(KV_ECUDA, "descriptor slot %d never released", i);
+      }
+    }
+    if (b.cap < bytes) {
+      const size_t cap = std::max<size_t>((bytes + 4095) & ~(size_t)4095, 64 << 10);
+      if (b.host) cudaFreeHost(b.host);
+      if (b.dev) cudaFree(b.dev);
+      b.host = b.dev = nullptr;
+      CU(cudaHostAlloc(reinterpret_cast<void **>(&b.host), cap, cudaHostAllocMapped));
+      CU(cudaHostGetDevicePointer(reinterpret_cast<void **>(&b.hmapped), b.host, 0));
+      CU(cudaMalloc(reinterpret_cast<void **>(&b.dev), cap));
+      b.cap = cap;
+    }
+    *out = &b;
+    *index = i;
     return KV_OK;
   }
   size_t cap_hint = 8u << 20;       // descriptor slots: 8 MiB (growth never hits a hot loop)
@@ -231,13 +282,15 @@ struct DeviceCtx {
         r.host = nullptr;
         r.dev = nullptr;
         r.cap = 0;
-        if (want_host) CU(cudaHostAlloc(reinterpret_cast<void **>(&r.host), cap, cudaHostAllocDefault));
+        if (want_host) {
+          CU(cudaHostAlloc(reinterpret_cast<void **>(&r.host), cap, cudaHostAllocMapped));
+          CU(cudaHostGetDevicePointer(reinterpret_cast<void **>(&r.hmapped), r.host, 0));
+        }
         CU(cudaMalloc(reinterpret_cast<void **>(&r.dev), cap));
         r.cap = cap;
       }
     }
     if (!b.ev) CU(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
-    if (!b.up) CU(cudaEventCreateWithFlags(&b.up, cudaEventDisableTiming));
     *out = &b;
     return KV_OK;
   }
@@ -382,7 +435,6 @@ struct kv_pool {
   int abort_slices = -1;                  // fault injection (kv_inject_abort)
   unsigned long long *counter = nullptr;  // device, monotone (host-task ring-put)
   unsigned long long issued = 0;          // host mirror of the counter target
-  unsigned long long *step_counter = nullptr;  // device, step-engine completion counter
   int32_t *d_bt = nullptr;                // device-resident block table [R][M]
   kv_loop *loop = nullptr;                // decode loop holding a pending publication
   uint64_t bytes_replicated = 0, tasks_launched = 0, kernels = 0, last_step_bytes = 0;
@@ -797,7 +849,6 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
     if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", p->device);
     CU(cudaMalloc(reinterpret_cast<void **>(&p->counter), 2 * sizeof(unsigned long long)));
     CU(cudaMemset(p->counter, 0, 2 * sizeof(unsigned long long)));
-    p->step_counter = p->counter + 1;
     CU(cudaMalloc(reinterpret_cast<void **>(&p->d_bt), sizeof(int32_t) * (size_t)p->R * p->M));
     CU(cudaMemset(p->d_bt, 0xFF, sizeof(int32_t) * (size_t)p->R * p->M));
     CU(launch_meta_init(p->meta, p->R, p->M, 0));
@@ -1214,7 +1265,8 @@ struct StepLaunch {
   kv_pool *rep_pool[kStepPools] = {};
   std::vector<KvAppItem> items;
   std::vector<int64_t> req;          // replicate snapshots, entry-major (pool, slot)
-  std::vector<int32_t> len, pub;
+  std::vector<int32_t> len, pub, blk0;
+  bool pdl = false;  // launched as a programmatic dependent of the previous step's grid
   std::vector<char> blob;
   const void *host_src[kStepPools] = {};  // KV_SRC_HOST sources
   size_t host_src_bytes[kStepPools] = {};
@@ -1236,6 +1288,8 @@ struct StepLaunch {
     req.clear();
     len.clear();
     pub.clear();
+    blk0.clear();
+    pdl = false;
     app_bytes = rep_bytes = 0;
     rep_step = 0;
     inval.clear();
@@ -1300,8 +1354,16 @@ void step_add_replicate(StepLaunch &S, kv_pool *p, uint64_t step) {
   S.len.insert(S.len.end(), p->slot_len.begin(), p->slot_len.begin() + p->slot_hi);
   S.pub.insert(S.pub.end(), p->pub_len.begin(), p->pub_len.begin() + p->slot_hi);
   uint64_t bytes = 0;
-  for (int s = 0; s < p->slot_hi; ++s)
-    if (p->slot_req[s] >= 0) bytes += (uint64_t)(pub_hi(p, s) - p->pub_len[s]);
+  const int B = p->g.block_size;
+  for (int s = 0; s < p->slot_hi; ++s) {
+    int b0 = -1;
+    if (p->slot_req[s] >= 0) {
+      const int lo = p->pub_len[s], hi = pub_hi(p, s);
+      bytes += (uint64_t)(hi - lo);
+      if (hi > lo) b0 = p->slot_bt[s][lo / B];  // the block of the first dirty token
+    }
+    S.blk0.push_back(b0);
+  }
   bytes *= (uint64_t)p->token_bytes;
   if (pp.abort_slices >= 0) {  // a stage dying mid-step: partial copy, never published
     const uint64_t cut = (uint64_t)pp.abort_slices * (uint64_t)p->seg_bytes;
@@ -1417,6 +1479,8 @@ int step_stage_host_sources(DeviceCtx *ctx, StepLaunch &S, cudaStream_t st, Stag
   return KV_OK;
 }
 
+std::atomic<unsigned long long> g_blob_nonce{0};
+
 // Per-launch record (kv_launch_log): bytes and grid of every decode-step launch.
 struct LaunchRec {
   uint64_t kind, app_bytes, rep_bytes, grid, blob_bytes;
@@ -1445,20 +1509,25 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCt
   h.app_slices = i1 < S.items.size() ? S.items[i1].off - base : S.h.app_slices - base;
   if (h.n_items == 0) h.app_slices = 0;
   const size_t nent = with_rep ? S.req.size() : 0;
-  size_t off = 0;
-  h.items_off = 0;
-  off = align16(sizeof(KvAppItem) * h.n_items);
+  // blob: [16-B header: launch nonce] [items] [req_id] [len] [pub_len] [blk0]
+  size_t off = 16;
+  h.items_off = (int32_t)off;
+  off += align16(sizeof(KvAppItem) * h.n_items);
   h.req_off = (int32_t)off;
   off += align16(8 * nent);
   h.len_off = (int32_t)off;
   off += align16(4 * nent);
   h.pub_off = (int32_t)off;
   off += align16(4 * nent);
+  h.blk0_off = (int32_t)off;
+  off += align16(4 * nent);
   h.data_bytes = (int32_t)off;
-  S.blob.resize(off);
+  S.blob.assign(off, 0);
   char *b = S.blob.data();
+  const unsigned long long nonce = ++g_blob_nonce;
+  std::memcpy(b, &nonce, 8);
   if (h.n_items > 0) {
-    KvAppItem *it = reinterpret_cast<KvAppItem *>(b);
+    KvAppItem *it = reinterpret_cast<KvAppItem *>(b + h.items_off);
     std::memcpy(it, S.items.data() + i0, sizeof(KvAppItem) * h.n_items);
     if (base)
       for (int k = 0; k < h.n_items; ++k) it[k].off -= base;
@@ -1467,28 +1536,36 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCt
     std::memcpy(b + h.req_off, S.req.data(), 8 * nent);
     std::memcpy(b + h.len_off, S.len.data(), 4 * nent);
     std::memcpy(b + h.pub_off, S.pub.data(), 4 * nent);
+    std::memcpy(b + h.blk0_off, S.blk0.data(), 4 * nent);
   }
-  if (h.publish) h.counter = S.rep_pool[0]->step_counter;
+  h.pdl = S.pdl ? 1 : 0;
   // grid: enough CTAs for ~1024 16-B chunks each, at most every resident CTA
   const uint64_t rep_slices = with_rep ? S.rep_bytes / (uint64_t)h.g.seg_bytes : 0;
   const unsigned long long chunks = ((unsigned long long)h.app_slices + rep_slices)
                                     << h.g.cps_shift;
   const int cap = step_resident_ctas(S.device, step_smem_bytes(h));
   int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + 1023) / 1024));
-  // the blob goes to the device on the context's upload stream, ordered before the
-  // launch by an event: the copy overlaps whatever the launch stream is still running
-  StageBuf *db = nullptr;
-  int rc = ctx->acquire(ctx->ring, ctx->next, (size_t)h.data_bytes, true, &db);
+  // the blob goes into a pinned host slot; CTA 0 of the kernel pulls it across PCIe and
+  // shares it through the slot's device buffer and flag (no copy-engine call, no event)
+  DeviceCtx::BlobSlot *db = nullptr;
+  int slot = 0;
+  const double ta = now_s();
+  phase_add(kPhPack, ta - t0);
+  int rc = ctx->acquire_blob((size_t)h.data_bytes, &db, &slot);
   if (rc) return rc;
-  if ((rc = ctx->ensure_upload())) return rc;
   std::memcpy(db->host, b, (size_t)h.data_bytes);
-  CU(cudaMemcpyAsync(db->dev, db->host, (size_t)h.data_bytes, cudaMemcpyHostToDevice, ctx->upload));
-  CU(cudaEventRecord(db->up, ctx->upload));
-  CU(cudaStreamWaitEvent(st, db->up, 0));
-  const char *gdata = db->dev;
+  phase_add(kPhAcquire, now_s() - ta);
+  h.hblob = db->hmapped;
+  h.gblob = db->dev;
+  h.flag = ctx->flags + 16 * slot;        // one 128-B line per slot
+  h.counter = ctx->counters + 16 * slot;
+  h.done = ctx->done_dev + 8 * slot;      // 64-B apart in pinned memory
+  h.nonce = nonce;
+  db->used = nonce;
   const double t1 = now_s();
   phase_add(kPhStage, t1 - t0);
-  CU(launch_step(h, gdata, grid, st));
+  h.pad0 = (int32_t)(nonce & 0x7fffffff);  // launch nonce (debug timelines)
+  CU(launch_step(h, grid, st, S.pdl));
   phase_add(kPhLaunch, now_s() - t1);
   g_launches++;
   if (g_log_on) {
@@ -1497,7 +1574,6 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCt
     g_log.push_back({(uint64_t)((h.n_items > 0) | ((with_rep && h.n_rep > 0) << 1)), app,
                      with_rep ? S.rep_bytes : 0, (uint64_t)grid, (uint64_t)h.data_bytes});
   }
-  if (db && (rc = ctx->done(db, st))) return rc;
   return KV_OK;
 }
 
@@ -2204,6 +2280,9 @@ KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
   for (int i = 0; i < nl; ++i) {
     g_ev_before = i == 0 ? static_cast<cudaEvent_t>(st->ev_kernel_start) : nullptr;
     g_ev_after = i == nl - 1 ? static_cast<cudaEvent_t>(st->ev_kernel_end) : nullptr;
+    // consecutive steps of the loop overlap: a launch's prologue (descriptor, work list)
+    // runs while the previous step's grid drains (timed launches are serialised)
+    L->S[i]->pdl = !st->ev_kernel_start && !st->ev_kernel_end;
     rc = step_enqueue(*L->S[i], s);
     g_ev_before = g_ev_after = nullptr;
     if (rc) return rc;
@@ -2232,8 +2311,10 @@ KV_API int kv_loop_flush(kv_loop_t *L, void *stream) {
   int n = 0;
   int rc = loop_take_pending(L, &n);
   if (rc) return rc;
-  for (int i = 0; i < n; ++i)
+  for (int i = 0; i < n; ++i) {
+    L->S[i]->pdl = true;
     if ((rc = step_enqueue(*L->S[i], static_cast<cudaStream_t>(stream)))) return rc;
+  }
   return KV_OK;
 }
 

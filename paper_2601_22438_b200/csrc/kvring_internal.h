@@ -161,13 +161,21 @@ struct alignas(16) KvStepHdr {
   int32_t n_app, n_rep;             // pools per role
   int32_t n_items, n_ent;           // append items; replicate entries
   int32_t items_off, req_off, len_off, pub_off;  // byte offsets into the data blob
+  int32_t blk0_off;                 // per entry: block holding the first dirty token
   int32_t data_bytes;               // bytes of the data blob (a multiple of 16)
   int32_t app_slices;               // total append slices (end of the last item)
   int32_t publish;                  // some replicate pool publishes this launch
   int32_t any_abort;
   int32_t sys_any;
-  int32_t pad0;
-  unsigned long long *counter;      // completion counter (the last CTA resets it to 0)
+  int32_t pad0;                     // launch nonce (debug timelines)
+  int32_t pdl;                      // launched as a programmatic dependent of the previous kernel
+  int32_t pad1;
+  const char *hblob;                // the descriptor blob in pinned host memory (device-mapped)
+  char *gblob;                      // its device copy (written by CTA 0)
+  unsigned long long *flag;         // = nonce once gblob holds this launch's blob
+  unsigned long long nonce;         // launch nonce (monotone per process)
+  unsigned long long *counter;      // completion counter of the slot (the last CTA resets it)
+  unsigned long long *done;         // pinned host word: = nonce once the launch completed
   KvGeomDev g;
   KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)
   KvDiv div_b;                      // block size
@@ -176,8 +184,9 @@ struct alignas(16) KvStepHdr {
   KvStepPool rep[kStepPools];
 };
 
-// Launches the step kernel over a device copy of the descriptor blob.
-cudaError_t launch_step(const KvStepHdr &h, const char *gdata, int grid, cudaStream_t stream);
+// Launches the step kernel (blob, flag and nonce in the header).  pdl: programmatic
+// dependent launch (the previous kernel on the stream may still be draining).
+cudaError_t launch_step(const KvStepHdr &h, int grid, cudaStream_t stream, bool pdl);
 int step_smem_bytes(const KvStepHdr &h);
 const void *step_kernel_fn();
 int step_resident_ctas(int device, int smem);

@@ -22,8 +22,9 @@
 //
 // Pure data movement, HBM / NVLink bound: no tensor cores.  The per-launch header
 // (pool bases, step, divisors) travels in the kernel parameter space; the descriptor
-// blob (items and per-slot tables) is uploaded by the host on a side stream, ahead of
-// the launch, and each CTA copies it to shared memory with coalesced loads.
+// blob (items and per-slot tables) is written by the host into pinned memory, pulled
+// across PCIe once by CTA 0 and shared with the other CTAs through device memory and a
+// release/acquire flag -- the per-step host cost is one launch.
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -91,8 +92,8 @@ __device__ __forceinline__ StepSmem step_smem(const KvStepHdr &h, char *sm) {
   s.hi = reinterpret_cast<int32_t *>(sm + h.len_off);
   s.lo = reinterpret_cast<const int32_t *>(sm + h.pub_off);
   s.pref = reinterpret_cast<int32_t *>(sm + h.data_bytes);
-  s.blk0 = s.pref + h.n_ent + 1;
-  s.bpref = s.blk0 + h.n_ent;
+  s.blk0 = reinterpret_cast<int32_t *>(sm + h.blk0_off);
+  s.bpref = s.pref + h.n_ent + 1;
   return s;
 }
 
@@ -322,16 +323,79 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *total) {
   return wbase + x - v;
 }
 
-__device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__restrict__ data) {
+#ifdef KV_TIMELINE
+// Debug builds (-DKV_TIMELINE, tools/step_timeline.py): thread 0 of every CTA stamps
+// %globaltimer at each phase boundary of the latest launch.
+__device__ unsigned long long g_kv_timeline[4 * 1024 * 8];  // the last 4 launches
+#define KV_STAMP(k)                                                                   \
+  do {                                                                                \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                      \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_kv_timeline[((unsigned)h.pad0 & 3u) * 8192 + blockIdx.x * 8 + (k)] = t_;     \
+    }                                                                                 \
+  } while (0)
+#else
+#define KV_STAMP(k) \
+  do {              \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void step_body(const KvStepHdr &h) {
   extern __shared__ __align__(16) char sm[];
-  // 1. descriptor blob (device copy, uploaded ahead on a side stream) -> shared memory:
-  //    coalesced 16-B loads, one round trip (every CTA reads the same bytes: L2 hits)
+  KV_STAMP(0);
+#ifdef KV_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x < 1024)
+    g_kv_timeline[((unsigned)h.pad0 & 3u) * 8192 + blockIdx.x * 8 + 7] = (unsigned)h.pad0;
+#endif
+  // programmatic dependent launch: the next step's grid may start its prologue as soon
+  // as this grid's CTAs leave (a no-op for a normally serialised launch)
+  if (h.pdl) asm volatile("griddepcontrol.launch_dependents;" :::);
+  // 1. descriptor blob -> shared memory.  The host writes it into pinned host memory and
+  //    launches -- no copy-engine call and no event per step.  CTA 0 pulls it across
+  //    PCIe once (zero copy) into a device buffer and releases a per-buffer flag carrying
+  //    the launch nonce; every other CTA acquires the flag (bounded wait: a timeout traps)
+  //    and copies the buffer from L2.  (CTA 0 is not waited on by anything it waits for:
+  //    the other CTAs only spin, so it always gets a slot.)
   {
     const int n16 = h.data_bytes >> 4;
-    for (int k = threadIdx.x; k < n16; k += kThreads)
-      reinterpret_cast<uint4 *>(sm)[k] = __ldg(reinterpret_cast<const uint4 *>(data) + k);
+    uint4 *smv = reinterpret_cast<uint4 *>(sm);
+    if (blockIdx.x == 0) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(h.hblob);
+      uint4 *dst = reinterpret_cast<uint4 *>(h.gblob);
+      for (int k = threadIdx.x; k < n16; k += kThreads) {
+        uint4 x;
+        asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(src + k));
+        smv[k] = x;
+        asm volatile("st.global.cg.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + k), "r"(x.x),
+                     "r"(x.y), "r"(x.z), "r"(x.w) : "memory");
+      }
+      __syncthreads();  // every thread's stores precede the single release below
+      if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(h.flag), "l"(h.nonce) : "memory");
+    } else {
+      if (threadIdx.x == 0) {
+        unsigned long long v;
+        for (long long spin = 0;; ++spin) {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.flag) : "memory");
+          if (v == h.nonce) break;
+          if (spin > (1ll << 22)) __trap();  // ~1 s: CTA 0 never published the descriptor
+          __nanosleep(64);
+        }
+      }
+      __syncthreads();
+      const uint4 *gsrc = reinterpret_cast<const uint4 *>(h.gblob);
+      for (int k = threadIdx.x; k < n16; k += kThreads) {
+        uint4 x;
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(gsrc + k));
+        smv[k] = x;
+      }
+    }
   }
   __syncthreads();
+  KV_STAMP(1);
   StepSmem s = step_smem(h, sm);
   const uint32_t SL = h.div_sl.d;
   const int B = h.g.block_size;
@@ -359,10 +423,6 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
       const int nb = hi > lo ? (hi + B - 1) / B - lo / B : 0;  // blocks touched (bt entries)
       s.bpref[e] = nb;
       blocal += nb;
-      if (hi > lo) {
-        const int slot = e - pp.ent_off;
-        s.blk0[e] = pp.bt[(size_t)slot * pp.M + (lo / B)];
-      }
     }
     int total, btotal;
     int base = block_exclusive_scan(local, &total);
@@ -383,12 +443,17 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
     P = total;
     __syncthreads();
   }
-  // 3. copies: this CTA's share of each flat space
+  // every read below may touch data the previous step's grid wrote (its appends, its
+  // device block-table entries): wait for it to complete (programmatic launch)
+  if (h.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // 3. copies: the grid's flat space, dealt in warp rounds
+  KV_STAMP(2);
   const uint32_t G = gridDim.x, b = blockIdx.x;
   {
     Cursor cur(h, s);
     copy_all(h.app_slices + P, cur, h.g);
   }
+  KV_STAMP(3);
   // 4. tables: the appended items' device bt entries; the publication's parity
   //    (req_id, len) table and the bt entries of the blocks it touched.  Readers trust
   //    none of it before seq = step (written below, after every CTA's release).
@@ -435,18 +500,21 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
       if (gt == 0) *reinterpret_cast<int32_t *>(pp.meta + 8) = pp.writer_node;
     }
   }
-  // 5. completion: bar.sync + one release RMW per CTA; the last CTA issues one
-  //    acquire-release fence (system scope if a successor is a peer) and stores every
-  //    publishing pool's seq (release pattern), then rearms the counter.
-  if (h.publish) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned long long old = atom_add_release_gpu(h.counter, 1ull);
-      if (old == (unsigned long long)G - 1ull) {
-        if (h.sys_any)
-          asm volatile("fence.acq_rel.sys;" ::: "memory");
-        else
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  KV_STAMP(4);
+  // 5. completion: bar.sync + one release RMW per CTA on the launch's counter; the last
+  //    CTA issues one acquire-release fence (system scope if a successor is a peer) and
+  //    stores every publishing pool's seq (release pattern; reading R9), then tells the
+  //    host the descriptor slot is free (nonce into pinned memory: every CTA read the
+  //    slot long before it arrived here) and rearms the counter for the slot's next launch.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long old = atom_add_release_gpu(h.counter, 1ull);
+    if (old == (unsigned long long)G - 1ull) {
+      if (h.sys_any)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+      else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (h.publish)
         for (int q = 0; q < h.n_rep; ++q) {
           const KvStepPool &pp = h.rep[q];
           if (pp.abort_slices >= 0) continue;
@@ -456,22 +524,31 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h, const char *__rest
           else
             asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
         }
-        *h.counter = 0ull;  // the next launch on this counter is stream-ordered after this one
-      }
+      *h.counter = 0ull;  // the slot's next launch starts after the host saw `done`
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.done), "l"(h.nonce) : "memory");
     }
   }
+  KV_STAMP(5);
 }
 
 }  // namespace
 
 // The decode-step kernel: header by value in the parameter space, descriptor blob in
-// device memory.
+// pinned host memory (pulled in by CTA 0, see step_body).
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
-    kv_step_kernel(const __grid_constant__ KvStepHdr h, const char *__restrict__ gdata) {
-  step_body(h, gdata);
+    kv_step_kernel(const __grid_constant__ KvStepHdr h) {
+  step_body(h);
 }
 
 const void *step_kernel_fn() { return reinterpret_cast<const void *>(kv_step_kernel); }
+
+#ifdef KV_TIMELINE
+extern "C" __attribute__((visibility("default"))) int kv_debug_timeline(unsigned long long *out,
+                                                                       int n) {
+  return cudaMemcpyFromSymbol(out, g_kv_timeline, sizeof(unsigned long long) * (size_t)n) ==
+                 cudaSuccess ? 0 : -3;
+}
+#endif
 
 // Resident CTAs of the step kernel on `device` for a launch's shared memory.
 int step_resident_ctas(int device, int smem) {
@@ -493,22 +570,31 @@ int step_resident_ctas(int device, int smem) {
 }
 
 int step_smem_bytes(const KvStepHdr &h) {
-  return h.data_bytes + 4 * (3 * h.n_ent + 2) + 16;
+  return h.data_bytes + 4 * (2 * h.n_ent + 2) + 16;
 }
 
 namespace {
 bool g_attr_set = false;
 }  // namespace
 
-cudaError_t launch_step(const KvStepHdr &h, const char *gdata, int grid, cudaStream_t st) {
+cudaError_t launch_step(const KvStepHdr &h, int grid, cudaStream_t st, bool pdl) {
   const int smem = step_smem_bytes(h);
   if (!g_attr_set) {
     // large launches may carry up to ~200 KiB of descriptors in shared memory
     cudaFuncSetAttribute(kv_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     g_attr_set = true;
   }
-  kv_step_kernel<<<grid, kThreads, smem, st>>>(h, gdata);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kv_step_kernel, h);
 }
 
 }  // namespace kvring

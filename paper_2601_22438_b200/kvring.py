@@ -419,7 +419,8 @@ def kv_plan_targets(succ, excluded=None):
     return [int(x) for x in out]
 
 
-HOST_PHASES = ["prepare.append", "prepare.replicate", "stage", "launch"]
+HOST_PHASES = ["prepare.append", "prepare.replicate", "stage", "launch", "stage.pack",
+               "stage.acquire", "stage.h2d_call", "stage.events"]
 
 
 def kv_host_profile(reset: bool = True) -> dict:

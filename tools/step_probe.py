@@ -88,24 +88,46 @@ def main():
                             req_ids=e["req_ids"], n_new=e["n_new"], src=src))
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         evs.append(ev)
-        steps.append(dict(append=app, repl_pools=[rt.handle(s) for s in range(S)], step=t,
-                          ev_kernel_start=ev[0], ev_kernel_end=ev[1]))
+        st = dict(append=app, repl_pools=[rt.handle(s) for s in range(S)], step=t)
+        if os.environ.get("STEP_PROBE_NOEVENTS") is None:
+            st.update(ev_kernel_start=ev[0], ev_kernel_end=ev[1])
+        steps.append(st)
     kl = K.KvLoop()
     torch.cuda.synchronize()
     K.kv_launch_log(True)
-    kl.run(K.PreparedSteps(steps), comp.cuda_stream)
+    prep = K.PreparedSteps(steps)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
+    K.kv_host_profile(reset=True)
+    t0.record(comp)
+    w0 = time.perf_counter()
+    kl.run(prep, comp.cuda_stream)
+    wall_us = (time.perf_counter() - w0) * 1e6
+    t1.record(comp)
     torch.cuda.synchronize()
+    loop_us = t0.elapsed_time(t1) * 1e3
     log = K.kv_launch_log(False)
-    kl.flush(comp.cuda_stream)
+    if os.environ.get("STEP_PROBE_NOFLUSH") is None:
+        kl.flush(comp.cuda_stream)
     torch.cuda.synchronize()
     out = []
-    for r, ev in zip(log, evs):
+    prev = None
+    noev = os.environ.get("STEP_PROBE_NOEVENTS") is not None
+    for r, ev in zip(log, evs if not noev else []):
         us = ev[0].elapsed_time(ev[1]) * 1e3
+        gap = prev[1].elapsed_time(ev[0]) * 1e3 if prev is not None else None
+        prev = ev
         by = 2 * (r["app_bytes"] + r["rep_bytes"])
-        out.append({"us": round(us, 2), "rw_mb": round(by / 1e6, 2),
+        out.append({"us": round(us, 2), "gap_us": None if gap is None else round(gap, 2),
+                    "rw_mb": round(by / 1e6, 2),
                     "gb_s": round(by / (us * 1e-6) / 1e9, 1), "grid": r["grid"],
                     "blob": r["blob_bytes"]})
-    print(json.dumps({"probe": "decode", "launches": out}))
+    rw = sum(2 * (r["app_bytes"] + r["rep_bytes"]) for r in log)
+    host = {k: round(v / n * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}
+    print(json.dumps({"probe": "decode", "launches": out, "loop_us": round(loop_us, 1),
+                      "host_wall_us_per_step": round(wall_us / n, 2), "host": host,
+                      "us_per_step": round(loop_us / n, 2),
+                      "gb_s_rw": round(rw / (loop_us * 1e-6) / 1e9, 1)}))
     kl.destroy()
     rt.destroy()
 
