@@ -73,3 +73,82 @@ extern "C" __attribute__((visibility("default"))) int kvgen_content(
       seed_mix, salt_mix, req_dev, pos_dev, n, layer0, L, H, d, out_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+
+// ---- test support: concurrent reader of a replica's publication (reading R9) ----------
+// One CTA spins on a replica metadata's seq with ld.acquire.sys while the predecessor
+// (another GPU) keeps publishing.  For every new seq it snapshots the parity (seq & 1)
+// (req_id, len) table and, for each listed slot, the first 256-B slice of its last valid
+// token (layer 0, K, head 0), then re-reads seq (acquire) so the host can drop snapshots
+// whose parity buffer was overwritten meanwhile (seq advanced by >= 2).  Records:
+//   out[k] = { u64 seq, u64 seq_after, i64 req[R], i32 len[R], u16 slice[R][d] }
+// Bounded: gives up after `max_spin` polls without a new seq.  Test infrastructure.
+namespace {
+__global__ void r9_observe_kernel(const char *meta, const char *replica, int R, int M, int B,
+                                  long long block_bytes, int seg_bytes, int n_obs,
+                                  long long max_spin, char *out, long long rec_bytes,
+                                  int *n_done) {
+  __shared__ unsigned long long s_seq;
+  __shared__ int s_stop;
+  unsigned long long last = 0;
+  int k = 0;
+  while (k < n_obs) {
+    if (threadIdx.x == 0) {
+      unsigned long long v = last;
+      long long spin = 0;
+      while (v == last && spin < max_spin) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(meta) : "memory");
+        ++spin;
+      }
+      s_seq = v;
+      s_stop = (v == last);
+    }
+    __syncthreads();
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (s_stop) break;
+    const unsigned long long seq = s_seq;
+    last = seq;
+    char *rec = out + (long long)k * rec_bytes;
+    const int par = (int)(seq & 1ull);
+    const long long *mreq = reinterpret_cast<const long long *>(meta + 32) + (long long)par * R;
+    const int *mlen = reinterpret_cast<const int *>(meta + 32 + 16LL * R) + (long long)par * R;
+    const int *mbt = reinterpret_cast<const int *>(meta + 32 + 24LL * R);
+    long long *oreq = reinterpret_cast<long long *>(rec + 16);
+    int *olen = reinterpret_cast<int *>(rec + 16 + 8LL * R);
+    char *oslice = rec + 16 + 12LL * R;
+    for (int s = threadIdx.x; s < R; s += blockDim.x) {
+      const long long r = *(volatile const long long *)(mreq + s);
+      const int ln = *(volatile const int *)(mlen + s);
+      oreq[s] = r;
+      olen[s] = ln;
+      if (r >= 0 && ln > 0) {
+        const int pos = ln - 1;
+        const int blk = *(volatile const int *)(mbt + (long long)s * M + pos / B);
+        const char *src = replica + (long long)blk * block_bytes + (long long)(pos % B) * seg_bytes;
+        for (int b = 0; b < seg_bytes; b += 4)
+          *reinterpret_cast<int *>(oslice + (long long)s * seg_bytes + b) =
+              *(volatile const int *)(src + b);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(meta) : "memory");
+      reinterpret_cast<unsigned long long *>(rec)[0] = seq;
+      reinterpret_cast<unsigned long long *>(rec)[1] = v;
+    }
+    __syncthreads();
+    ++k;
+  }
+  if (threadIdx.x == 0) *n_done = k;
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int kvgen_r9_observe(
+    const void *meta, const void *replica, int R, int M, int B, long long block_bytes,
+    int seg_bytes, int n_obs, long long max_spin, void *out, long long rec_bytes, int *n_done,
+    void *stream) {
+  r9_observe_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char *>(meta), static_cast<const char *>(replica), R, M, B, block_bytes,
+      seg_bytes, n_obs, max_spin, static_cast<char *>(out), rec_bytes, n_done);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}

@@ -46,3 +46,27 @@ def content_tokens_cuda(seed: int, req_ids, positions, layer0: int, layers: int,
         raise RuntimeError(f"kvgen_content failed ({rc})")
     out._kvgen_keepalive = (req, pos)  # inputs must outlive the async kernel
     return out
+
+
+def r9_observe(meta_ptr: int, replica_ptr: int, R: int, M: int, B: int, block_bytes: int,
+               seg_bytes: int, n_obs: int, max_spin: int = 1 << 26, device=None, stream=None):
+    """Launch the concurrent R9 reader (test support, see kvgen.cu); returns
+    (records tensor [n_obs][rec_bytes] uint8, n_done tensor, rec_bytes) -- read after sync."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    rec = 16 + 12 * R + R * seg_bytes
+    rec = (rec + 15) // 16 * 16
+    out = torch.zeros((n_obs, rec), dtype=torch.uint8, device=dev)
+    n_done = torch.zeros(1, dtype=torch.int32, device=dev)
+    L = lib()
+    L.kvgen_r9_observe.restype = ctypes.c_int
+    L.kvgen_r9_observe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_longlong, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_longlong, ctypes.c_void_p, ctypes.c_longlong,
+                                   ctypes.c_void_p, ctypes.c_void_p]
+    s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+    rc = L.kvgen_r9_observe(meta_ptr, replica_ptr, R, M, B, block_bytes, seg_bytes, n_obs,
+                            max_spin, out.data_ptr(), rec, n_done.data_ptr(), s)
+    if rc != 0:
+        raise RuntimeError("kvgen_r9_observe failed")
+    return out, n_done, rec

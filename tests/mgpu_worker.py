@@ -36,6 +36,8 @@ def main():
     dev = torch.device("cuda", lr)
     from datetime import timedelta
     dist.init_process_group("nccl", device_id=dev, timeout=timedelta(seconds=120))
+    if os.environ.get("KV_TRANSPORT") == "r9":
+        return r9_main(rank, world, lr, dev)
     N, S = world, 4
     cfg = configs.scaled(configs.C1, pipelines=N, num_blocks=96, max_reqs=12,
                          max_blocks_per_req=12, batch_cap=6, n_requests=60, n_steps=30,
@@ -156,6 +158,120 @@ def main():
             if not np.array_equal(got, want):
                 print(f"rank {rank}: remote restore content mismatch for {r}", flush=True)
                 ok = 0
+    okt = torch.tensor([ok], device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    rt.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_PARITY_OK" if int(okt) == 1 else "MGPU_PARITY_FAIL", flush=True)
+    sys.exit(0 if int(okt) == 1 else 1)
+
+
+def r9_main(rank, world, lr, dev):
+    """Reading R9 observed concurrently: node A (rank 0) publishes every step over NVLink
+    into node B's replica region (rank 1) through the one-launch loop, with no barrier or
+    synchronize between steps; meanwhile a reader kernel on rank 1 acquires B's seq and,
+    for every new value t, snapshots the parity-t table and the newest token slice of every
+    listed request.  Each snapshot not overwritten meanwhile must equal the oracle's
+    published table of step t and the closed-form words of those tokens: a reader that
+    acquires seq = t sees all of step t."""
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED, content_tokens
+    from kvgen.cuda import content_tokens_cuda, r9_observe
+    from kvgen.schedule import closed_loop_schedule
+    from oracle.simulate import OracleRing
+    from paper_2601_22438_b200 import kvring as K
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    assert world >= 2
+    T = 400
+    cfg = configs.scaled(configs.C1, stages=2, num_blocks=256, max_reqs=32,
+                         max_blocks_per_req=16, batch_cap=12, n_requests=400, n_steps=T,
+                         fixed_prompt=None, fail_node=None, fail_step=None)
+    rng = np.random.default_rng(909)
+    sched = [closed_loop_schedule(rng.integers(1, 90, size=400), rng.integers(1, 60, size=400),
+                                  T, cfg.batch_cap)]
+    coords = {(0, 0): 0, (0, 1): 1}
+    placement = {0: 0, 1: 1 % world}
+    succ = {0: 1, 1: None}
+    rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement,
+                     succ, rank=rank, world=world, device=lr, spares=0, group=dist.group.WORLD)
+    g = cfg.geom
+
+    def content(stage, ids, pos):
+        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim, device=lr)
+
+    drv = ScheduleDriver(rt, sched, coords, content)
+    # expected published tables of A, step by step (oracle, metadata mode)
+    oring = OracleRing(cfg, content=False, schedules=sched)
+    expect = {}
+    for t in range(T):
+        oring.appends(t)
+        if t >= 1:
+            oring.replicate(t)
+            expect[t] = oring.nodes[(0, 1)].published()
+    ok = 1
+    if rank == 0:
+        keep, sts = [], []
+        for t in range(T):
+            e = drv.plan(t).get(0)
+            ids, pos = drv.tokens(e["req_ids"], e["n_new"], e["start"])
+            src = content(0, ids, pos) if ids else None
+            keep.append(src)
+            sts.append(dict(append=[dict(pool=rt.handle(0), begin_step=1, release=e["release"],
+                                         req_ids=e["req_ids"], n_new=e["n_new"], src=src)],
+                            repl_pools=[rt.handle(0)] if t >= 1 else [], step=t))
+        prep = K.PreparedSteps(sts)
+        kl = K.KvLoop()
+        torch.cuda.synchronize(dev)
+        dist.barrier()                       # the reader is running
+        kl.run(prep, torch.cuda.current_stream(dev).cuda_stream)
+        kl.flush(torch.cuda.current_stream(dev).cuda_stream)
+        torch.cuda.synchronize(dev)
+        kl.destroy()
+    elif rank == 1:
+        side = torch.cuda.Stream(dev)
+        R, M, B = cfg.max_reqs, cfg.max_blocks_per_req, g.block_size
+        with torch.cuda.stream(side):
+            recs, n_done, rec_bytes = r9_observe(rt.meta_ptr(1), rt.replica_ptr(1), R, M, B,
+                                                 rt.block_bytes, g.head_dim * 2, 256,
+                                                 max_spin=1 << 22, device=lr,
+                                                 stream=side.cuda_stream)
+        dist.barrier()
+        side.synchronize()
+        n = int(n_done.item())
+        raw = recs.cpu().numpy()
+        valid = 0
+        for k in range(n):
+            rec = raw[k]
+            seq, after = (int(x) for x in rec[:16].view(np.uint64))
+            if after > seq + 1:              # parity buffer reused while copying
+                continue
+            req = rec[16:16 + 8 * R].view(np.int64)
+            ln = rec[16 + 8 * R:16 + 12 * R].view(np.int32)
+            sl = rec[16 + 12 * R:16 + 12 * R + R * g.head_dim * 2].view(np.uint16).reshape(R, -1)
+            pub = expect[seq]
+            got = {int(req[s]): (s, int(ln[s])) for s in range(R) if req[s] >= 0}
+            want = {r: (s, l) for r, (s, l, bt) in pub.items()}
+            if got != want:
+                print(f"r9: seq {seq}: table {got} != {want}", flush=True)
+                ok = 0
+                continue
+            for r, (s, l) in got.items():
+                w = content_tokens(CONTENT_SEED, [r], [l - 1], 0, g.layers, g.kv_heads,
+                                   g.head_dim)[0, 0, 0, 0]
+                if not np.array_equal(sl[s], w):
+                    print(f"r9: seq {seq}: request {r} token {l - 1} not visible", flush=True)
+                    ok = 0
+            valid += 1
+        print(f"r9: {n} observations, {valid} checked (distinct seqs seen while publishing)",
+              flush=True)
+        if valid < 5:
+            print("r9: too few concurrent observations", flush=True)
+            ok = 0
+    else:
+        dist.barrier()
     okt = torch.tensor([ok], device=dev)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     rt.destroy()

@@ -3,9 +3,10 @@ C3 (Poisson arrivals, two pipelines), C4 (16 logical nodes, batch 128, failure
 of (0,2) at step 300 and restore -- stage ring into a fresh pool, and the
 paper's instance ring with promotion onto the holder), C5 (32k-token prefill
 per stage: bulk full-block replication and a bulk restore).  Tables and device
-metadata are compared with the oracle in metadata mode; valid KV slots are
-checked on samples against the closed form (the full arrays do not fit the
-oracle's host memory).  Pools are sized to the workload's peak block use
+metadata are compared with the oracle in metadata mode; EVERY valid KV slot of every
+primary and replica is checked against the closed form on the GPU (the full arrays do
+not fit the oracle's host memory), and blocks above the run's high-water id must still
+hold the sentinel.  Pools are sized to the workload's peak block use
 (measured with the oracle), not the 6-12 GiB worst case."""
 import numpy as np
 import pytest
@@ -20,38 +21,66 @@ from gpu_harness import compare_state, make_gpu, node_map
 pytestmark = pytest.mark.gpu
 
 
-def _sample_check(rt, drv, oring, rng, per_node=3):
-    """Sampled valid slots of every live node's primary (and its successor's
-    replica when published) equal the closed-form content."""
+def _gather_positions(arr, bt_of_pos, B, items, dev):
+    """arr[bt[pos // B], :, :, :, pos % B, :] for items (req, pos) -> [n][L][2][H][d]."""
+    blk = torch.tensor([bt_of_pos[i] for i in range(len(items))], device=dev)
+    slot = torch.tensor([p % B for _, p in items], device=dev)
+    return arr[blk, :, :, :, slot]
+
+
+def _full_check(rt, drv, oring, hw, chunk=1 << 16):
+    """Every valid slot of every live node's primary AND of its successor's replica (at
+    the published length) equals the closed-form content (I2, I1 through the closed form;
+    the expected words come from kvgen's CUDA twin of the numpy generator, pinned byte for
+    byte by tests/test_kvgen_cuda.py); every block at or above the run's high-water block
+    id still holds the sentinel in every pool and replica region (I5: no stray writes).
+    Tables come from the oracle (metadata mode), independent of the GPU path."""
+    from kvgen.cuda import content_tokens_cuda
+    from paper_2601_22438_b200.runtime import SENTINEL_WORD
     torch.cuda.synchronize()
     g = rt.g
     B = g.block_size
     nm = node_map(rt, drv, oring)
     inv = {n: c for c, n in drv.serving.items()}
+    checked = 0
     for gid, on in nm.items():
-        if on.dead or gid not in inv:
+        if on.dead or gid not in inv or gid not in rt.local:
             continue
         stage = inv[gid][1]
-        live = on.live()
-        if not live:
-            continue
-        items = []
-        for r, (s, ln, bt) in live.items():
-            for pos in rng.choice(ln, size=min(ln, per_node), replace=False):
-                items.append((r, int(pos), bt[int(pos) // B]))
-        want = content_tokens(CONTENT_SEED, [i[0] for i in items], [i[1] for i in items],
-                              stage * g.layers, g.layers, g.kv_heads, g.head_dim)
-        idx = torch.tensor([i[2] for i in items], device=rt.dev)
-        slot = torch.tensor([i[1] % B for i in items], device=rt.dev)
-        prim = rt.local[gid].pool[idx, :, :, :, slot].cpu().numpy().view(np.uint16)
-        assert np.array_equal(prim, want), f"node {gid} primary"
+        targets = [("primary", rt.local[gid].pool, on.live())]
         succ = rt.succ.get(gid)
-        if succ is not None and succ in rt.local and on.succ is not None:
+        if succ is not None and succ in rt.local and on.succ is not None and not on.succ.dead:
             pub = on.succ.published()
-            keep = [k for k, it in enumerate(items) if it[0] in pub and it[1] < pub[it[0]][1]]
-            if keep:
-                rep = rt.local[succ].replica[idx[keep], :, :, :, slot[keep]].cpu().numpy()
-                assert np.array_equal(rep.view(np.uint16), want[keep]), f"replica of node {gid}"
+            targets.append(("replica", rt.local[succ].replica, pub))
+        for name, arr, table in targets:
+            items, bts = [], []
+            for r, (s, ln, bt) in sorted(table.items()):
+                for pos in range(ln):
+                    items.append((r, pos))
+                    bts.append(bt[pos // B])
+            for c0 in range(0, len(items), chunk):
+                it = items[c0:c0 + chunk]
+                want = content_tokens_cuda(CONTENT_SEED, [x[0] for x in it], [x[1] for x in it],
+                                           stage * g.layers, g.layers, g.kv_heads, g.head_dim,
+                                           device=rt.device)
+                got = _gather_positions(arr, bts[c0:c0 + chunk], B, it, rt.dev)
+                if not torch.equal(got, want):
+                    bad = (got != want).reshape(len(it), -1).any(1).nonzero()[:3].flatten().tolist()
+                    raise AssertionError(f"node {gid} {name}: slots {[it[k] for k in bad]} differ")
+                checked += len(it)
+    w = SENTINEL_WORD if SENTINEL_WORD < 0x8000 else SENTINEL_WORD - 0x10000
+    for gid, slot in rt.local.items():
+        if gid in rt.dead:            # a failed node's memory is poisoned (a7)
+            continue
+        for name, arr in (("pool", slot.pool), ("replica", slot.replica)):
+            if hw < arr.shape[0]:
+                assert bool((arr[hw:] == w).all().item()), f"node {gid} {name}: stray write above block {hw}"
+    return checked
+
+
+def _high_water(oring):
+    return max([b for n in oring.all_nodes() if not n.dead for s in range(n.R) for b in n.slot_bt[s]]
+               + [-1]) + 1
 
 
 def _run(cfg, steps, ring="stage", check_every=50, restore_mode=None, copy_engine=False):
@@ -59,7 +88,7 @@ def _run(cfg, steps, ring="stage", check_every=50, restore_mode=None, copy_engin
     rt.copy_engine = copy_engine
     oring = OracleRing(cfg, content=False, ring=ring, schedules=drv.sched,
                        restore_mode=restore_mode)
-    rng = np.random.default_rng(3)
+    hw = 0
     try:
         for t in range(steps):
             drv.append_step(t)
@@ -73,7 +102,11 @@ def _run(cfg, steps, ring="stage", check_every=50, restore_mode=None, copy_engin
                 oring.replicate(t)
             if t % check_every == 0 or t == steps - 1:
                 compare_state(rt, drv, oring, content=False, tag=f"step {t}")
-        _sample_check(rt, drv, oring, rng)
+            hw = max(hw, _high_water(oring))
+            if cfg.fail_step == t:
+                _full_check(rt, drv, oring, hw)      # right after the restore (I4)
+        n = _full_check(rt, drv, oring, hw)          # the end of the run
+        assert n > 0
         return rt, drv, oring
     except Exception:
         rt.destroy()
