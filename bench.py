@@ -1246,9 +1246,10 @@ def run_shared(args, local_rank, dev):
 
 def run_nccl(args, drv, rt, t0, comp, content, dev, world):
     """The paper's transport (NCCL send/recv, P:8 §3.3) on the same workload, as the
-    measured comparison: per step append, then gather-pack, 8-B count exchange,
-    grouped send/recv, unpack + publish.  One stream; per-step transport time by
-    CUDA events around pack..unpack."""
+    measured comparison: per step append, then gather-pack, the packed sizes exchanged on
+    the host (gloo; no GPU sync), ONE grouped ncclSend/ncclRecv (libkvnccl; at N = 1 the
+    single rank sends to itself), unpack + publish.  One stream; CUDA events around
+    pack..unpack and around the NCCL group."""
     import torch
     import torch.distributed as dist
     from paper_2601_22438_b200 import kvring as K
@@ -1268,6 +1269,8 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
         dist.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(n)]
+    evn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n)]
     b0 = {nd: K.kv_stats(rt.handle(nd))["bytes_replicated"] for nd in rt.alive_local()}
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
@@ -1276,7 +1279,7 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
         tt = t0 + k
         drv.append_step(tt, stream=comp, sources=srcs[tt], plan=plans[tt])
         evs[k][0].record(comp)
-        ring.step(tt, comp)
+        ring.step(tt, comp, events=evn[k])
         evs[k][1].record(comp)
     en.record(comp)
     torch.cuda.synchronize(dev)
@@ -1284,19 +1287,21 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
     ms = st.elapsed_time(en)
     by = sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in rt.alive_local())
     us = [a.elapsed_time(b) * 1e3 for a, b in evs]
-    vec = torch.tensor([ms, float(by), wall], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = vec.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vec.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms, by, wall = float(mx[0]), float(sm[1]), float(mx[2])
-    return {"transport": "nccl send/recv (pack, count exchange, send/recv, unpack)" if world > 1
-            else "loopback pack -> unpack (no NCCL at N=1)",
+    us_n = [a.elapsed_time(b) * 1e3 for a, b in evn]
+    ring.destroy()
+    mx, sm = reduce_max_sum([ms, float(by), wall], dev, world)
+    ms, by, wall = mx[0], sm[1], mx[2]
+    return {"transport": "NCCL 2.28 grouped ncclSend/ncclRecv (libkvnccl): pack, host count "
+                         "exchange (gloo, N > 1), send/recv, unpack"
+                         + (" -- one rank sending to itself" if world == 1 else ""),
             "value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "steps": n,
             "ms_per_step": round(ms / n, 4), "wall_ms_per_step": round(wall / n * 1e3, 4),
-            "transport_us_per_step": {"median": round(statistics.median(us), 2),
-                                      "p99": round(float(np.percentile(us, 99)), 2)}}
+            "step_us": {"median": round(statistics.median(us), 2),
+                        "p99": round(float(np.percentile(us, 99)), 2),
+                        "what": "pack + count exchange + NCCL group + unpack"},
+            "nccl_group_us": {"median": round(statistics.median(us_n), 2),
+                              "p99": round(float(np.percentile(us_n, 99)), 2),
+                              "what": "the ncclSend/ncclRecv group alone"}}
 
 
 def run_e2e(args, K, kl, drv, rt, t0, comp, content, dev, world):

@@ -73,5 +73,33 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     return LIB
 
 
+NCCL_HOME = None
+try:  # the NCCL that ships with the torch venv (2.28; not the system /usr/include copy)
+    import nvidia.nccl as _nv_nccl
+    NCCL_HOME = list(_nv_nccl.__path__)[0]
+except Exception:
+    pass
+LIB_NCCL = os.path.join(HERE, "libkvnccl.so")
+
+
+def build_nccl(force: bool = False) -> str | None:
+    """libkvnccl.so: the NCCL comparison transport's native driver (a6)."""
+    if NCCL_HOME is None:
+        return None
+    src = os.path.join(CSRC, "kvnccl.cpp")
+    deps = [src, os.path.join(INCLUDE, "kvnccl.h")]
+    if force or _stale(LIB_NCCL, deps):
+        lib = os.path.join(NCCL_HOME, "lib")
+        tmp = LIB_NCCL + ".tmp"
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-fvisibility=hidden", "-Wall",
+              "-I", INCLUDE, "-I", os.path.join(NCCL_HOME, "include"),
+              "-I", os.path.join(CUDA_HOME, "include"), src, "-o", tmp,
+              "-L", lib, "-l:libnccl.so.2", f"-Wl,-rpath,{lib}",
+              "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart"])
+        shutil.move(tmp, LIB_NCCL)
+    return LIB_NCCL
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)
+    build_nccl(force="--force" in sys.argv)

@@ -204,7 +204,8 @@ struct DeviceCtx {
   struct BlobSlot {
     char *host = nullptr, *hmapped = nullptr, *dev = nullptr;
     size_t cap = 0;
-    unsigned long long used = 0;  // nonce of the last launch that read this slot
+    unsigned long long used = 0;      // nonce of the last launch that read this slot
+    unsigned long long arrivals = 0;  // CTAs counted so far on the slot's device counter
   };
   BlobSlot blob[kBlobRing];
   int next_blob = 0;
@@ -1559,6 +1560,8 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCt
   h.gblob = db->dev;
   h.flag = ctx->flags + 16 * slot;        // one 128-B line per slot
   h.counter = ctx->counters + 16 * slot;
+  h.target = db->arrivals + (unsigned long long)grid;
+  db->arrivals = h.target;
   h.done = ctx->done_dev + 8 * slot;      // 64-B apart in pinned memory
   h.nonce = nonce;
   db->used = nonce;

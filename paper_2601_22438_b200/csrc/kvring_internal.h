@@ -174,7 +174,8 @@ struct alignas(16) KvStepHdr {
   char *gblob;                      // its device copy (written by CTA 0)
   unsigned long long *flag;         // = nonce once gblob holds this launch's blob
   unsigned long long nonce;         // launch nonce (monotone per process)
-  unsigned long long *counter;      // completion counter of the slot (the last CTA resets it)
+  unsigned long long *counter;      // completion counter of the slot (monotone)
+  unsigned long long target;        // its value once every CTA of this launch arrived
   unsigned long long *done;         // pinned host word: = nonce once the launch completed
   KvGeomDev g;
   KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)

@@ -505,11 +505,12 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   //    CTA issues one acquire-release fence (system scope if a successor is a peer) and
   //    stores every publishing pool's seq (release pattern; reading R9), then tells the
   //    host the descriptor slot is free (nonce into pinned memory: every CTA read the
-  //    slot long before it arrived here) and rearms the counter for the slot's next launch.
+  //    slot long before it arrived here).  The slot's counter is monotone: the host passes
+  //    the value the last arrival of this launch makes it reach.
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned long long old = atom_add_release_gpu(h.counter, 1ull);
-    if (old == (unsigned long long)G - 1ull) {
+    if (old + 1ull == h.target) {
       if (h.sys_any)
         asm volatile("fence.acq_rel.sys;" ::: "memory");
       else
@@ -524,7 +525,6 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
           else
             asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
         }
-      *h.counter = 0ull;  // the slot's next launch starts after the host saw `done`
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.done), "l"(h.nonce) : "memory");
     }
   }

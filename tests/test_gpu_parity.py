@@ -212,6 +212,7 @@ def test_pack_unpack_equals_ring_put():
     try:
         # node 0 -> node 1 by ring-put; a shadow copy of node 0's stream via pack/unpack
         shadow = rt.slots[4]
+        shadow.meta.fill_(255)   # a spare slot has no pool handle: its bt rows start at -1
         buf = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
         n0 = rt.handle(0)
         for t in range(cfg.n_steps):
