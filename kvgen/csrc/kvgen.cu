@@ -79,14 +79,15 @@ extern "C" __attribute__((visibility("default"))) int kvgen_content(
 // (another GPU) keeps publishing.  For every new seq it snapshots the parity (seq & 1)
 // (req_id, len) table and, for each listed slot, the first 256-B slice of its last valid
 // token (layer 0, K, head 0), then re-reads seq (acquire) so the host can drop snapshots
-// whose parity buffer was overwritten meanwhile (seq advanced by >= 2).  Records:
+// whose parity buffer was overwritten meanwhile (seq advanced by >= 2); stops at
+// `last_seq` (the writer's final step) or after `max_spin` polls without news.  Records:
 //   out[k] = { u64 seq, u64 seq_after, i64 req[R], i32 len[R], u16 slice[R][d] }
 // Bounded: gives up after `max_spin` polls without a new seq.  Test infrastructure.
 namespace {
 __global__ void r9_observe_kernel(const char *meta, const char *replica, int R, int M, int B,
                                   long long block_bytes, int seg_bytes, int n_obs,
-                                  long long max_spin, char *out, long long rec_bytes,
-                                  int *n_done) {
+                                  long long max_spin, unsigned long long last_seq, char *out,
+                                  long long rec_bytes, int *n_done) {
   __shared__ unsigned long long s_seq;
   __shared__ int s_stop;
   unsigned long long last = 0;
@@ -138,6 +139,7 @@ __global__ void r9_observe_kernel(const char *meta, const char *replica, int R, 
     }
     __syncthreads();
     ++k;
+    if (seq >= last_seq) break;  // the writer's final step
   }
   if (threadIdx.x == 0) *n_done = k;
 }
@@ -145,10 +147,10 @@ __global__ void r9_observe_kernel(const char *meta, const char *replica, int R, 
 
 extern "C" __attribute__((visibility("default"))) int kvgen_r9_observe(
     const void *meta, const void *replica, int R, int M, int B, long long block_bytes,
-    int seg_bytes, int n_obs, long long max_spin, void *out, long long rec_bytes, int *n_done,
-    void *stream) {
+    int seg_bytes, int n_obs, long long max_spin, unsigned long long last_seq, void *out,
+    long long rec_bytes, int *n_done, void *stream) {
   r9_observe_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char *>(meta), static_cast<const char *>(replica), R, M, B, block_bytes,
-      seg_bytes, n_obs, max_spin, static_cast<char *>(out), rec_bytes, n_done);
+      seg_bytes, n_obs, max_spin, last_seq, static_cast<char *>(out), rec_bytes, n_done);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

@@ -49,7 +49,8 @@ def content_tokens_cuda(seed: int, req_ids, positions, layer0: int, layers: int,
 
 
 def r9_observe(meta_ptr: int, replica_ptr: int, R: int, M: int, B: int, block_bytes: int,
-               seg_bytes: int, n_obs: int, max_spin: int = 1 << 26, device=None, stream=None):
+               seg_bytes: int, n_obs: int, last_seq: int, max_spin: int = 1 << 28, device=None,
+               stream=None):
     """Launch the concurrent R9 reader (test support, see kvgen.cu); returns
     (records tensor [n_obs][rec_bytes] uint8, n_done tensor, rec_bytes) -- read after sync."""
     import torch
@@ -62,11 +63,11 @@ def r9_observe(meta_ptr: int, replica_ptr: int, R: int, M: int, B: int, block_by
     L.kvgen_r9_observe.restype = ctypes.c_int
     L.kvgen_r9_observe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_longlong, ctypes.c_int, ctypes.c_int,
-                                   ctypes.c_longlong, ctypes.c_void_p, ctypes.c_longlong,
-                                   ctypes.c_void_p, ctypes.c_void_p]
+                                   ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_void_p,
+                                   ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]
     s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
     rc = L.kvgen_r9_observe(meta_ptr, replica_ptr, R, M, B, block_bytes, seg_bytes, n_obs,
-                            max_spin, out.data_ptr(), rec, n_done.data_ptr(), s)
+                            max_spin, last_seq, out.data_ptr(), rec, n_done.data_ptr(), s)
     if rc != 0:
         raise RuntimeError("kvgen_r9_observe failed")
     return out, n_done, rec

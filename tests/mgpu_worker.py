@@ -236,7 +236,7 @@ def r9_main(rank, world, lr, dev):
         with torch.cuda.stream(side):
             recs, n_done, rec_bytes = r9_observe(rt.meta_ptr(1), rt.replica_ptr(1), R, M, B,
                                                  rt.block_bytes, g.head_dim * 2, 256,
-                                                 max_spin=1 << 22, device=lr,
+                                                 last_seq=T - 1, device=lr,
                                                  stream=side.cuda_stream)
         dist.barrier()
         side.synchronize()

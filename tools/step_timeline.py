@@ -51,4 +51,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    finally:  # back to the product build
+        subprocess.run([sys.executable, "-m", "paper_2601_22438_b200.build", "--force"],
+                       cwd=ROOT, stdout=subprocess.DEVNULL)
