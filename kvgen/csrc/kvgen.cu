@@ -154,3 +154,82 @@ extern "C" __attribute__((visibility("default"))) int kvgen_r9_observe(
       seg_bytes, n_obs, max_spin, last_seq, static_cast<char *>(out), rec_bytes, n_done);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+
+// ---- workload proxy: paged decode attention over the live KV (bench interference leg) --
+// The model-side consumer replication competes with for HBM: for
+// every (request, layer, KV head) one warp streams the request's K and V slices out of the
+// paged pool (layout [blk][L][2][H][B][d], bf16) and computes softmax(q.K / sqrt(d)) V for
+// the GQA group's `qpk` query heads with an online softmax.  Reads every valid KV slot once
+// per step, as a decode step's attention does.  Workload proxy, not part of the method.
+namespace {
+__device__ __forceinline__ float bf16f(uint16_t x) { return __uint_as_float((uint32_t)x << 16); }
+
+__global__ void attn_proxy_kernel(const char *const *pools, const int *req_pool,
+                                  const int *req_len, const int *req_bt_off, const int *bt,
+                                  int n_req, int L, int H, int B, int d, int qpk,
+                                  const float *q, float *out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int per_req = L * H;
+  if (warp >= n_req * per_req) return;
+  const int r = warp / per_req, lh = warp % per_req, l = lh / H, h = lh % H;
+  const char *pool = pools[req_pool[r]];
+  const long long blk_bytes = (long long)L * 2 * H * B * d * 2;
+  const int dv = d / 32;  // dims per lane (d = 128: 4)
+  float qv[4][4], acc[4][4], m[4], ssum[4];
+  for (int g = 0; g < qpk && g < 4; ++g) {
+    for (int k = 0; k < dv && k < 4; ++k) {
+      qv[g][k] = q[((long long)(lh * qpk + g)) * d + lane * dv + k];
+      acc[g][k] = 0.f;
+    }
+    m[g] = -1e30f;
+    ssum[g] = 0.f;
+  }
+  const float scale = rsqrtf((float)d);
+  const int len = req_len[r];
+  for (int t = 0; t < len; ++t) {
+    const int blk = bt[req_bt_off[r] + t / B];
+    const char *base = pool + (long long)blk * blk_bytes;
+    const uint16_t *kp = reinterpret_cast<const uint16_t *>(
+        base + ((((long long)l * 2 + 0) * H + h) * B + (t % B)) * d * 2);
+    const uint16_t *vp = reinterpret_cast<const uint16_t *>(
+        base + ((((long long)l * 2 + 1) * H + h) * B + (t % B)) * d * 2);
+    float kf[4], vf[4];
+    for (int k = 0; k < dv && k < 4; ++k) {
+      kf[k] = bf16f(kp[lane * dv + k]);
+      vf[k] = bf16f(vp[lane * dv + k]);
+    }
+    for (int g = 0; g < qpk && g < 4; ++g) {
+      float s = 0.f;
+      for (int k = 0; k < dv && k < 4; ++k) s += qv[g][k] * kf[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      s *= scale;
+      if (!(s == s) || s > 1e30f || s < -1e30f) s = 0.f;  // the words are arbitrary bits
+      const float mn = fmaxf(m[g], s), c = __expf(m[g] - mn), p = __expf(s - mn);
+      ssum[g] = ssum[g] * c + p;
+      for (int k = 0; k < dv && k < 4; ++k) {
+        const float v = (vf[k] == vf[k] && fabsf(vf[k]) < 1e30f) ? vf[k] : 0.f;
+        acc[g][k] = acc[g][k] * c + p * v;
+      }
+      m[g] = mn;
+    }
+  }
+  for (int g = 0; g < qpk && g < 4; ++g)
+    for (int k = 0; k < dv && k < 4; ++k)
+      out[((long long)(warp * qpk + g)) * d + lane * dv + k] = acc[g][k] / fmaxf(ssum[g], 1e-30f);
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int kvgen_attn_proxy(
+    const void *pools_dev, const int *req_pool, const int *req_len, const int *req_bt_off,
+    const int *bt, int n_req, int L, int H, int B, int d, int qpk, const float *q, float *out,
+    void *stream) {
+  if (d % 32 != 0 || d > 128 || qpk > 4) return -1;
+  const long long warps = (long long)n_req * L * H;
+  const int threads = 256;
+  const long long grid = (warps * 32 + threads - 1) / threads;
+  attn_proxy_kernel<<<(int)grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char *const *>(pools_dev), req_pool, req_len, req_bt_off, bt, n_req, L,
+      H, B, d, qpk, q, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}

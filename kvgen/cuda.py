@@ -71,3 +71,43 @@ def r9_observe(meta_ptr: int, replica_ptr: int, R: int, M: int, B: int, block_by
     if rc != 0:
         raise RuntimeError("kvgen_r9_observe failed")
     return out, n_done, rec
+
+
+class AttnProxy:
+    """Paged decode attention over a fixed set of live requests (bench interference
+    workload proxy, NEXT-4): tables = [(pool_tensor_index, len, block_ids)], pools = the
+    stage pools (torch int16 tensors).  run(stream) launches one kernel."""
+
+    def __init__(self, pools, tables, L, H, B, d, qpk=4, device=None):
+        import torch
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        ptrs = np.array([p.data_ptr() for p in pools], dtype=np.uint64)
+        self.pools = torch.as_tensor(ptrs.view(np.int64)).to(self.dev)
+        self.keep = pools
+        rp, rl, ro, bts = [], [], [], []
+        for pi, ln, blocks in tables:
+            rp.append(pi)
+            rl.append(ln)
+            ro.append(len(bts))
+            bts.extend(blocks)
+        i32 = lambda x: torch.as_tensor(np.asarray(x, dtype=np.int32)).to(self.dev)
+        self.rp, self.rl, self.ro, self.bt = i32(rp), i32(rl), i32(ro), i32(bts or [0])
+        self.n, self.L, self.H, self.B, self.d, self.qpk = len(rp), L, H, B, d, qpk
+        g = torch.Generator(device=self.dev).manual_seed(7)
+        self.q = torch.randn(max(1, self.n * L * H * qpk * d), device=self.dev, generator=g)
+        self.out = torch.empty_like(self.q)
+        self.tokens = sum(rl)
+        L_ = lib()
+        L_.kvgen_attn_proxy.restype = ctypes.c_int
+        L_.kvgen_attn_proxy.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int] * 6 + \
+            [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+
+    def run(self, stream: int) -> None:
+        if self.n == 0:
+            return
+        rc = lib().kvgen_attn_proxy(self.pools.data_ptr(), self.rp.data_ptr(), self.rl.data_ptr(),
+                                    self.ro.data_ptr(), self.bt.data_ptr(), self.n, self.L,
+                                    self.H, self.B, self.d, self.qpk, self.q.data_ptr(),
+                                    self.out.data_ptr(), stream)
+        if rc != 0:
+            raise RuntimeError("kvgen_attn_proxy failed")

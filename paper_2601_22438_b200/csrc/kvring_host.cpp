@@ -23,6 +23,7 @@
 #include <vector>
 
 #include <cuda_runtime_api.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (ranges show up under nsys / ncu)
 
 #include "kvring.h"
 #include "kvring_internal.h"
@@ -50,6 +51,14 @@ KV_API int kv_host_profile(double *out, int32_t n, int32_t reset) {
 }
 
 using namespace kvring;
+
+namespace {
+// NVTX phase range (SURVEY §5 tracing): append / replicate / decode-loop step / restore.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -1619,6 +1628,7 @@ int step_enqueue(StepLaunch &S, cudaStream_t st) {
 }  // namespace
 
 KV_API int kv_append_multi(int32_t n_pools, const kv_append_args_t *args, void *stream) {
+  NvtxRange nv("kv_append");
   thread_local StepLaunch S;
   const double t0 = now_s();
   int rc = validate_appends(n_pools, args);
@@ -1650,6 +1660,7 @@ namespace {
 // Publication of several pools of one device: the device-derived step engine for
 // plain links, the host-task ring-put for shared-capacity links (one launch each).
 int replicate_any(int32_t n_pools, kv_pool_t *const *pools, uint64_t step, cudaStream_t st) {
+  NvtxRange nv("kv_replicate_step");
   int rc = validate_replicate(n_pools, pools, step);
   if (rc) return rc;
   kv_pool *plain[kMaxPoolsPerLaunchHost], *shared[kMaxPoolsPerLaunchHost];
@@ -1704,6 +1715,7 @@ KV_API int kv_inject_abort(kv_pool_t *p, int32_t slices) {
 }
 
 KV_API int kv_fail_stage(kv_pool_t *p, void *stream) {
+  NvtxRange nv("kv_fail_stage");
   if (!p) return fail(KV_EINVAL, "null pool");
   if (p->dead) return fail(KV_ESTATE, "pool %d already dead", p->node_id);
   p->dead = true;
@@ -1721,6 +1733,7 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
                       const void *holder_meta, void *stream, uint64_t *t_star,
                       int64_t *req_ids_out, int32_t *resume_len_out, int32_t cap,
                       int32_t *n_out) {
+  NvtxRange nv("kv_restore");
   if (!dst || !holder_replica || !holder_meta) return fail(KV_EINVAL, "null argument");
   if (dst->dead) return fail(KV_ESTATE, "restore target %d is dead", dst->node_id);
   if (dst->device < 0) return fail(KV_ESTATE, "restore needs a device pool");
@@ -2250,6 +2263,7 @@ KV_API int kv_loop_destroy(kv_loop_t *L) {
 }
 
 KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
+  NvtxRange nv("kv_loop_step");
   if (!L || !st) return fail(KV_EINVAL, "null argument");
   if (st->n_repl > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "too many pools");
   for (int i = 0; i < st->n_repl; ++i) {
