@@ -208,14 +208,12 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
       if (s_cnt[i] == 0) continue;
       const KvPoolParams &pp = params[i];
       const bool sys = pp.sys_scope != 0;
-      // Every CTA of this launch runs on this GPU, so the count RMW only needs GPU
-      // scope even when the stores went to an NVLink peer; the completing CTA then
-      // issues ONE system-scope acquire-release fence before its (relaxed) store of
-      // seq.  Causality order is transitive (release.gpu -> fence.acq_rel.sys, which
-      // acquires the count and releases the seq store that follows it), so a peer that
-      // acquires seq = t sees every CTA's stores.
+      // The count RMW is a release at SYSTEM scope when the successor is an NVLink peer:
+      // a GPU-scope release does not wait for this CTA's stores into peer memory (the
+      // concurrent reader test caught seq = t ahead of step t's slices with it); the
+      // completing CTA then issues one acquire-release fence before its store of seq.
       const unsigned long long old =
-          atom_add_release(pp.counter, (unsigned long long)s_cnt[i], false);
+          atom_add_release(pp.counter, (unsigned long long)s_cnt[i], sys);
       if (old + (unsigned long long)s_cnt[i] == pp.target) {
         fence_acquire(sys);
         st_after_fence(reinterpret_cast<unsigned long long *>(pp.meta), pp.step, sys);

@@ -63,13 +63,19 @@ __device__ __forceinline__ void st_stream(void *p, const uint4 &v) {
                : "memory");
 }
 
-__device__ __forceinline__ unsigned long long atom_add_release_gpu(unsigned long long *p,
-                                                                   unsigned long long v) {
+__device__ __forceinline__ unsigned long long atom_add_release(unsigned long long *p,
+                                                               unsigned long long v, bool sys) {
   unsigned long long old;
-  asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;"
-               : "=l"(old)
-               : "l"(p), "l"(v)
-               : "memory");
+  if (sys)
+    asm volatile("atom.add.release.sys.global.u64 %0, [%1], %2;"
+                 : "=l"(old)
+                 : "l"(p), "l"(v)
+                 : "memory");
+  else
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;"
+                 : "=l"(old)
+                 : "l"(p), "l"(v)
+                 : "memory");
   return old;
 }
 
@@ -501,15 +507,18 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
     }
   }
   KV_STAMP(4);
-  // 5. completion: bar.sync + one release RMW per CTA on the launch's counter; the last
-  //    CTA issues one acquire-release fence (system scope if a successor is a peer) and
+  // 5. completion: bar.sync + one release RMW per CTA on the launch's counter -- at SYSTEM
+  //    scope when a successor is an NVLink peer: a GPU-scope release does not wait for the
+  //    CTA's stores into peer memory, and the concurrent reader test (tests/mgpu_worker.py
+  //    r9) saw seq = t before step t's slices with it -- then the last CTA issues one
+  //    acquire-release fence (system scope if a successor is a peer) and
   //    stores every publishing pool's seq (release pattern; reading R9), then tells the
   //    host the descriptor slot is free (nonce into pinned memory: every CTA read the
   //    slot long before it arrived here).  The slot's counter is monotone: the host passes
   //    the value the last arrival of this launch makes it reach.
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned long long old = atom_add_release_gpu(h.counter, 1ull);
+    const unsigned long long old = atom_add_release(h.counter, 1ull, h.sys_any != 0);
     if (old + 1ull == h.target) {
       if (h.sys_any)
         asm volatile("fence.acq_rel.sys;" ::: "memory");

@@ -190,7 +190,7 @@ def r9_main(rank, world, lr, dev):
                          fixed_prompt=None, fail_node=None, fail_step=None)
     rng = np.random.default_rng(909)
     sched = [closed_loop_schedule(rng.integers(1, 90, size=400), rng.integers(1, 60, size=400),
-                                  T, cfg.batch_cap)]
+                                  T + 1, cfg.batch_cap)]
     coords = {(0, 0): 0, (0, 1): 1}
     placement = {0: 0, 1: 1 % world}
     succ = {0: 1, 1: None}
@@ -206,7 +206,7 @@ def r9_main(rank, world, lr, dev):
     # expected published tables of A, step by step (oracle, metadata mode)
     oring = OracleRing(cfg, content=False, schedules=sched)
     expect = {}
-    for t in range(T):
+    for t in range(T + 1):
         oring.appends(t)
         if t >= 1:
             oring.replicate(t)
@@ -258,7 +258,13 @@ def r9_main(rank, world, lr, dev):
                 print(f"r9: seq {seq}: table {got} != {want}", flush=True)
                 ok = 0
                 continue
+            # a request that retires at t+1 frees its blocks, and step t+2's copies may
+            # refill them before seq moves past t+1: check the requests still published at
+            # t+1 (their blocks stay theirs until step t+2's retirement, R7)
+            nxt = expect.get(seq + 1, {})
             for r, (s, l) in got.items():
+                if r not in nxt:
+                    continue
                 w = content_tokens(CONTENT_SEED, [r], [l - 1], 0, g.layers, g.kv_heads,
                                    g.head_dim)[0, 0, 0, 0]
                 if not np.array_equal(sl[s], w):
