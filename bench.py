@@ -158,6 +158,17 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def align(self, timeout: float = 0.5):
+        """Returns right after the next sample arrives: a sub-ms timed region then starts
+        just after nvidia-smi's query and ends long before the next one (-lms 100), so
+        the query's driver work never lands inside it (samples still bracket it)."""
+        if self.proc is None:
+            return
+        n = len(self.samples)
+        t0 = time.perf_counter()
+        while len(self.samples) == n and time.perf_counter() - t0 < timeout:
+            time.sleep(0.0005)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -255,14 +266,24 @@ def timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, instrument=Fa
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     K.kv_host_profile(reset=True)
     K.kv_launch_log(True)
+    heat = torch.empty(2, 256 << 20, dtype=torch.uint8, device=dev)
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         torch.cuda.synchronize(dev)
+        clk.align()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+        # the GPU idled while the sampler started: ~4 ms of HBM copies right before the
+        # region (same stream, no sync) so it starts at full clocks, not on a ramp
+        for _ in range(24):
+            heat[1].copy_(heat[0])
         w0 = time.perf_counter()
         start.record(comp)
         kl.run(timed, comp.cuda_stream)
         end.record(comp)
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - w0
+    del heat
     log = K.kv_launch_log(False)
     launches = K.kv_kernel_launch_count() - l0
     host = {k: round(v / args.steps * 1e6, 2) for k, v in K.kv_host_profile(reset=True).items()}

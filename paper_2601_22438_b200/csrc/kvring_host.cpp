@@ -220,14 +220,23 @@ struct DeviceCtx {
   int next_blob = 0;
   unsigned long long *flags = nullptr;     // device: per slot, nonce of the blob its buffer holds
   unsigned long long *counters = nullptr;  // device: per slot, completion counter
+  unsigned int *work = nullptr;            // device: per slot, 8 dynamic round counters (512 B)
   volatile unsigned long long *done_host = nullptr;  // pinned host: per slot, last completed nonce
   unsigned long long *done_dev = nullptr;       // its device-side address
+  // the last decode-step launch on this device: a chained launch (kvring_step.cu) on the
+  // same stream acquires its final count
+  cudaStream_t last_stream = nullptr;
+  unsigned long long *last_counter = nullptr;
+  unsigned long long last_final = 0;
   int acquire_blob(size_t bytes, BlobSlot **out, int *index) {
     if (!flags) {
       CU(cudaMalloc(reinterpret_cast<void **>(&flags), 128 * (size_t)kBlobRing));
       CU(cudaMemset(flags, 0, 128 * (size_t)kBlobRing));
       CU(cudaMalloc(reinterpret_cast<void **>(&counters), 128 * (size_t)kBlobRing));
       CU(cudaMemset(counters, 0, 128 * (size_t)kBlobRing));
+      CU(cudaMalloc(reinterpret_cast<void **>(&work), 512 * (size_t)kBlobRing));
+      CU(cudaMemset(work, 0, 512 * (size_t)kBlobRing));
+      CU(cudaDeviceSynchronize());  // once: the zeroed words precede any launch on any stream
       void *h = nullptr;
       CU(cudaHostAlloc(&h, 64 * (size_t)kBlobRing, cudaHostAllocMapped));
       std::memset(h, 0, 64 * (size_t)kBlobRing);
@@ -1277,6 +1286,7 @@ struct StepLaunch {
   std::vector<int64_t> req;          // replicate snapshots, entry-major (pool, slot)
   std::vector<int32_t> len, pub, blk0;
   bool pdl = false;  // launched as a programmatic dependent of the previous step's grid
+  bool chain_ok = false;  // the previous kernel on the stream is this library's step launch
   std::vector<char> blob;
   const void *host_src[kStepPools] = {};  // KV_SRC_HOST sources
   size_t host_src_bytes[kStepPools] = {};
@@ -1300,6 +1310,7 @@ struct StepLaunch {
     pub.clear();
     blk0.clear();
     pdl = false;
+    chain_ok = false;
     app_bytes = rep_bytes = 0;
     rep_step = 0;
     inval.clear();
@@ -1503,8 +1514,8 @@ constexpr size_t kItemsPerLaunch = 2048;  // 48 KiB of append items per launch
 // Packs one launch's descriptor blob -- append items [i0, i1) and, if `with_rep`, the
 // publication part -- then launches (data inline in the parameter space when it fits,
 // else one H2D of the blob first).  Events of kv_time_next_launch honoured.
-int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCtx *ctx,
-                    cudaStream_t st) {
+int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool chain,
+                    DeviceCtx *ctx, cudaStream_t st) {
   const double t0 = now_s();
   KvStepHdr h = S.h;
   if (!with_rep) {
@@ -1569,8 +1580,18 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, DeviceCt
   h.gblob = db->dev;
   h.flag = ctx->flags + 16 * slot;        // one 128-B line per slot
   h.counter = ctx->counters + 16 * slot;
+  h.work = ctx->work + 128 * slot;
   h.target = db->arrivals + (unsigned long long)grid;
-  db->arrivals = h.target;
+  db->arrivals = h.target + 1;            // + the final count after the seq stores
+  h.chain = 0;
+  if (chain && S.pdl && ctx->last_counter && ctx->last_stream == st) {
+    h.chain = 1;
+    h.prev_counter = ctx->last_counter;
+    h.prev_target = ctx->last_final;
+  }
+  ctx->last_stream = st;
+  ctx->last_counter = h.counter;
+  ctx->last_final = h.target + 1;
   h.done = ctx->done_dev + 8 * slot;      // 64-B apart in pinned memory
   h.nonce = nonce;
   db->used = nonce;
@@ -1613,7 +1634,8 @@ int step_enqueue(StepLaunch &S, cudaStream_t st) {
   bool first = true;
   do {
     const size_t i1 = std::min(n, i0 + kItemsPerLaunch);
-    if ((rc = step_launch_one(S, i0, i1, first, ctx, st))) return rc;
+    // a later chunk follows this enqueue's previous launch directly on the stream
+    if ((rc = step_launch_one(S, i0, i1, first, first ? S.chain_ok : true, ctx, st))) return rc;
     first = false;
     i0 = i1;
   } while (i0 < n);
@@ -2262,7 +2284,10 @@ KV_API int kv_loop_destroy(kv_loop_t *L) {
   return KV_OK;
 }
 
-KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
+namespace {
+// chain_first: the previous kernel on `stream` is this loop's previous launch (inside
+// kv_loop_run, which enqueues nothing else between its steps)
+int loop_step(kv_loop_t *L, const kv_step_t *st, void *stream, bool chain_first) {
   NvtxRange nv("kv_loop_step");
   if (!L || !st) return fail(KV_EINVAL, "null argument");
   if (st->n_repl > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "too many pools");
@@ -2300,6 +2325,7 @@ KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
     // consecutive steps of the loop overlap: a launch's prologue (descriptor, work list)
     // runs while the previous step's grid drains (timed launches are serialised)
     L->S[i]->pdl = !st->ev_kernel_start && !st->ev_kernel_end;
+    L->S[i]->chain_ok = i > 0 || chain_first;
     rc = step_enqueue(*L->S[i], s);
     g_ev_before = g_ev_after = nullptr;
     if (rc) return rc;
@@ -2314,10 +2340,16 @@ KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
   return KV_OK;
 }
 
+}  // namespace
+
+KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
+  return loop_step(L, st, stream, false);
+}
+
 KV_API int kv_loop_run(kv_loop_t *L, int32_t n_steps, const kv_step_t *steps, void *stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
   for (int i = 0; i < n_steps; ++i) {
-    int rc = kv_loop_step(L, &steps[i], stream);
+    int rc = loop_step(L, &steps[i], stream, i > 0);
     if (rc) return rc;
   }
   return KV_OK;

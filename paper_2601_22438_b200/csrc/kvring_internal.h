@@ -169,7 +169,8 @@ struct alignas(16) KvStepHdr {
   int32_t sys_any;
   int32_t pad0;                     // launch nonce (debug timelines)
   int32_t pdl;                      // launched as a programmatic dependent of the previous kernel
-  int32_t pad1;
+  int32_t chain;                    // the previous kernel on the stream is this library's step
+                                    // launch: acquire its final count instead of griddepcontrol.wait
   const char *hblob;                // the descriptor blob in pinned host memory (device-mapped)
   char *gblob;                      // its device copy (written by CTA 0)
   unsigned long long *flag;         // = nonce once gblob holds this launch's blob
@@ -177,6 +178,9 @@ struct alignas(16) KvStepHdr {
   unsigned long long *counter;      // completion counter of the slot (monotone)
   unsigned long long target;        // its value once every CTA of this launch arrived
   unsigned long long *done;         // pinned host word: = nonce once the launch completed
+  unsigned int *work;               // dynamic round counters of the slot (8 x 64 B, zero at rest)
+  unsigned long long *prev_counter; // chain: the previous launch's counter ...
+  unsigned long long prev_target;   // ... and its final value (every CTA arrived, seq stored)
   KvGeomDev g;
   KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)
   KvDiv div_b;                      // block size

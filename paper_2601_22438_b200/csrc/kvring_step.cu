@@ -251,17 +251,21 @@ struct Cursor {
 // split where a lane's slices leave the piece (rare: pieces are >= 128 slices at C2).
 // All loads of a (sub-)round are issued before its stores; the stores replay the
 // destination stepping instead of keeping kU pointers live.
-__device__ __forceinline__ void copy_all(int T, Cursor &cur, const KvGeomDev &g) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (int)blockIdx.x * kWarps + (int)(threadIdx.x >> 5);
-  const int W = (int)gridDim.x * kWarps;
-  const int cs = g.cps_shift;
-  const uint32_t d = 32u >> cs;                 // slices per warp iteration
-  const int span = (int)d * kU;                 // slices per warp round
-  const uint32_t lc = ((uint32_t)lane & ((1u << cs) - 1u)) << 4;
-  for (long long base = (long long)gw * span; base < T; base += (long long)W * span) {
-    const int rend = (int)min((long long)T, base + span);
-    int x = (int)base + (lane >> cs);           // this lane's slice
+//
+// Rounds [0, st * W) are dealt statically (round r to warp r mod W); the rest are
+// handed out dynamically through kWorkCtrs counters (warp w draws from counter w mod
+// kWorkCtrs the rounds st*W + c, st*W + c + kWorkCtrs, ...): SMs do not all move bytes
+// at the same rate (GPCs differ in SM count, the two dies), so a static split leaves
+// the slowest warps finishing alone.  st = 3/4 of the rounds per warp (at least 1):
+// a decode step (fewer rounds than warps) never touches the counters.
+constexpr int kWorkCtrs = 8;
+constexpr int kBlobBatch = 8;  // descriptor loads in flight per thread
+constexpr int kWorkStride = 16;  // u32 words between counters (64 B)
+
+__device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs, uint32_t d,
+                                           uint32_t lc, Cursor &cur) {
+  {
+    int x = base + (lane >> cs);                // this lane's slice
     while (__any_sync(0xffffffffu, x < rend)) {
       int n = 0;
       if (x < rend) {
@@ -305,6 +309,51 @@ __device__ __forceinline__ void copy_all(int T, Cursor &cur, const KvGeomDev &g)
   }
 }
 
+__device__ __forceinline__ void copy_all(int T, Cursor &cur, const KvGeomDev &g,
+                                         unsigned int *work) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)blockIdx.x * kWarps + (int)(threadIdx.x >> 5);
+  const int W = (int)gridDim.x * kWarps;
+  const int cs = g.cps_shift;
+  const uint32_t d = 32u >> cs;                 // slices per warp iteration
+  const int span = (int)d * kU;                 // slices per warp round
+  const uint32_t lc = ((uint32_t)lane & ((1u << cs) - 1u)) << 4;
+  const int R = (int)(((long long)T + span - 1) / span);
+#ifdef KV_AB_STATIC  // A/B builds (tools/ab_bench.sh): every round dealt statically
+  const int st = R;
+#elif defined(KV_AB_DYN4)
+  const int st = R / W >= 4 ? (R / W) * 3 / 4 : R;
+#else
+  const int st = max(1, (R / W) * 3 / 4);
+#endif
+  const int Rs = (int)min((long long)R, (long long)st * W);
+  const int c = gw % kWorkCtrs;
+  unsigned int *const ctr = work + c * kWorkStride;
+  // one call site for both phases (two inlined copies of the round spill registers); the
+  // draw of the next dynamic round is issued before the current round's copies, so its
+  // latency hides behind them
+  unsigned int next = 0;
+  bool drawn = false;                           // `next` holds a draw (warp-uniform)
+  for (int r = gw;;) {
+    if (r >= Rs) {                              // static share done: take a drawn round
+      if (Rs >= R) break;
+      if (!drawn && lane == 0) next = atomicAdd(ctr, 1u);
+      const unsigned int k = __shfl_sync(0xffffffffu, next, 0);
+      drawn = false;
+      const long long rd = (long long)Rs + c + (long long)k * kWorkCtrs;
+      if (rd >= R) break;
+      r = (int)rd;
+    }
+    if (Rs < R && (r >= Rs || r + W >= Rs)) {   // the next round is dynamic: draw it now
+      if (lane == 0) next = atomicAdd(ctr, 1u);
+      drawn = true;
+    }
+    const long long base = (long long)r * span;
+    copy_round((int)base, (int)min((long long)T, base + span), lane, cs, d, lc, cur);
+    r = r < Rs ? r + W : 0x7fffffff;
+  }
+}
+
 // Block-wide exclusive scan of one int per thread; returns the exclusive prefix and
 // the total in *total.
 __device__ __forceinline__ int block_exclusive_scan(int v, int *total) {
@@ -332,13 +381,13 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *total) {
 #ifdef KV_TIMELINE
 // Debug builds (-DKV_TIMELINE, tools/step_timeline.py): thread 0 of every CTA stamps
 // %globaltimer at each phase boundary of the latest launch.
-__device__ unsigned long long g_kv_timeline[4 * 1024 * 8];  // the last 4 launches
+__device__ unsigned long long g_kv_timeline[32 * 1024 * 8];  // the last 32 launches
 #define KV_STAMP(k)                                                                   \
   do {                                                                                \
     if (threadIdx.x == 0 && blockIdx.x < 1024) {                                      \
       unsigned long long t_;                                                          \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
-      g_kv_timeline[((unsigned)h.pad0 & 3u) * 8192 + blockIdx.x * 8 + (k)] = t_;     \
+      g_kv_timeline[((unsigned)h.pad0 & 31u) * 8192 + blockIdx.x * 8 + (k)] = t_;     \
     }                                                                                 \
   } while (0)
 #else
@@ -352,7 +401,7 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   KV_STAMP(0);
 #ifdef KV_TIMELINE
   if (threadIdx.x == 0 && blockIdx.x < 1024)
-    g_kv_timeline[((unsigned)h.pad0 & 3u) * 8192 + blockIdx.x * 8 + 7] = (unsigned)h.pad0;
+    g_kv_timeline[((unsigned)h.pad0 & 31u) * 8192 + blockIdx.x * 8 + 7] = (unsigned)h.pad0;
 #endif
   // programmatic dependent launch: the next step's grid may start its prologue as soon
   // as this grid's CTAs leave (a no-op for a normally serialised launch)
@@ -369,13 +418,27 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
     if (blockIdx.x == 0) {
       const uint4 *src = reinterpret_cast<const uint4 *>(h.hblob);
       uint4 *dst = reinterpret_cast<uint4 *>(h.gblob);
-      for (int k = threadIdx.x; k < n16; k += kThreads) {
-        uint4 x;
-        asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(src + k));
-        smv[k] = x;
-        asm volatile("st.global.cg.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + k), "r"(x.x),
-                     "r"(x.y), "r"(x.z), "r"(x.w) : "memory");
+      // kBlobBatch loads in flight per thread before any store: one PCIe round trip per
+      // 32 KiB instead of one per 4 KiB
+      for (int k0 = 0; k0 < n16; k0 += kThreads * kBlobBatch) {
+        uint4 x[kBlobBatch];
+#pragma unroll
+        for (int u = 0; u < kBlobBatch; ++u) {
+          const int k = k0 + u * kThreads + (int)threadIdx.x;
+          if (k < n16)
+            asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(x[u].x), "=r"(x[u].y), "=r"(x[u].z), "=r"(x[u].w)
+                         : "l"(src + k));
+        }
+#pragma unroll
+        for (int u = 0; u < kBlobBatch; ++u) {
+          const int k = k0 + u * kThreads + (int)threadIdx.x;
+          if (k < n16) {
+            smv[k] = x[u];
+            asm volatile("st.global.cg.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + k), "r"(x[u].x),
+                         "r"(x[u].y), "r"(x[u].z), "r"(x[u].w) : "memory");
+          }
+        }
       }
       __syncthreads();  // every thread's stores precede the single release below
       if (threadIdx.x == 0)
@@ -392,11 +455,21 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
       }
       __syncthreads();
       const uint4 *gsrc = reinterpret_cast<const uint4 *>(h.gblob);
-      for (int k = threadIdx.x; k < n16; k += kThreads) {
-        uint4 x;
-        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(gsrc + k));
-        smv[k] = x;
+      for (int k0 = 0; k0 < n16; k0 += kThreads * kBlobBatch) {
+        uint4 x[kBlobBatch];
+#pragma unroll
+        for (int u = 0; u < kBlobBatch; ++u) {
+          const int k = k0 + u * kThreads + (int)threadIdx.x;
+          if (k < n16)
+            asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(x[u].x), "=r"(x[u].y), "=r"(x[u].z), "=r"(x[u].w)
+                         : "l"(gsrc + k));
+        }
+#pragma unroll
+        for (int u = 0; u < kBlobBatch; ++u) {
+          const int k = k0 + u * kThreads + (int)threadIdx.x;
+          if (k < n16) smv[k] = x[u];
+        }
       }
     }
   }
@@ -450,14 +523,36 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
     __syncthreads();
   }
   // every read below may touch data the previous step's grid wrote (its appends, its
-  // device block-table entries): wait for it to complete (programmatic launch)
-  if (h.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // device block-table entries, its seq): wait for it.  A chained launch (the previous
+  // kernel on the stream is this library's previous step launch, nothing else between)
+  // acquires that launch's final count -- reached once every CTA arrived and its seq
+  // stores were made -- which returns ~2-3 us before griddepcontrol.wait would (that
+  // waits for the whole grid to retire and flush).  No deadlock: a programmatic
+  // dependent grid starts only after every CTA of the previous grid has started.
+#ifdef KV_AB_NOCHAIN  // A/B builds (tools/ab_bench.sh): always griddepcontrol.wait
+  if (false) {
+#else
+  if (h.chain) {
+#endif
+    if (threadIdx.x == 0) {
+      unsigned long long v;
+      for (long long spin = 0;; ++spin) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.prev_counter) : "memory");
+        if (v >= h.prev_target) break;
+        if (spin > (1ll << 24)) __trap();  // the previous launch never completed
+        if (spin > 64) __nanosleep(32);
+      }
+    }
+    __syncthreads();
+  } else if (h.pdl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   // 3. copies: the grid's flat space, dealt in warp rounds
   KV_STAMP(2);
   const uint32_t G = gridDim.x, b = blockIdx.x;
   {
     Cursor cur(h, s);
-    copy_all(h.app_slices + P, cur, h.g);
+    copy_all(h.app_slices + P, cur, h.g, h.work);
   }
   KV_STAMP(3);
   // 4. tables: the appended items' device bt entries; the publication's parity
@@ -534,6 +629,10 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
           else
             asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
         }
+      // the dynamic round counters are free again (every warp drew its last round)
+      for (int c = 0; c < kWorkCtrs; ++c) h.work[c * kWorkStride] = 0u;
+      // final count: the next chained launch acquires it (its seq stores follow these)
+      atom_add_release(h.counter, 1ull, h.sys_any != 0);
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.done), "l"(h.nonce) : "memory");
     }
   }
@@ -571,6 +670,9 @@ int step_resident_ctas(int device, int smem) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kv_step_kernel, kThreads, smem) !=
           cudaSuccess || per < 1)
     per = 1;
+#ifdef KV_AB_CTAS_PER_SM  // A/B builds (tools/ab_bench.sh): a smaller grid cap
+  per = per < KV_AB_CTAS_PER_SM ? per : KV_AB_CTAS_PER_SM;
+#endif
   cudaGetLastError();
   cache_dev = device;
   cache_smem = smem;

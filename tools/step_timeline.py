@@ -31,23 +31,37 @@ def main():
     from paper_2601_22438_b200 import kvring as K
     f = K.lib().kv_debug_timeline
     f.restype = ctypes.c_int
-    buf = np.zeros(4 * 1024 * 8, dtype=np.uint64)
+    NL = 32
+    buf = np.zeros(NL * 1024 * 8, dtype=np.uint64)
     f(buf.ctypes.data, buf.size)
-    t = buf.reshape(4, 1024, 8)
+    t = buf.reshape(NL, 1024, 8)
     launches = []
-    for k in range(4):
+    for k in range(NL):
         nz = t[k][:, 7] != 0
         if nz.any():
             launches.append((int(t[k][nz][0, 7]), t[k][nz].astype(np.float64)))
     launches.sort()
-    t0 = min(x[:, 0].min() for _, x in launches)
     names = ["start", "blob", "wait", "copies", "tables", "done"]
-    for nonce, x in launches:
+    t0 = min(x[:, 0].min() for _, x in launches[-4:])
+    for nonce, x in launches[-4:]:     # the last 4 in full
         print("launch %d (%d CTAs):" % (nonce, len(x)))
         for k, name in enumerate(names):
             col = (x[:, k] - t0) / 1e3
             print("   %-7s min %8.2f  median %8.2f  max %8.2f us" % (name, col.min(),
                                                                      np.median(col), col.max()))
+    # every kept launch, relative to its own first CTA start (copies = warp 0 of each CTA)
+    print("\nlaunch  CTAs  period | blob.med wait.med wait.max | copies.med copies.max | "
+          "done.med done.max | prev.done.max->wait.min")
+    prev = None
+    for nonce, x in launches:
+        s0 = x[:, 0].min()
+        r = lambda k, fn: (fn(x[:, k]) - s0) / 1e3
+        period = (s0 - prev[:, 0].min()) / 1e3 if prev is not None else float("nan")
+        gap = (x[:, 2].min() - prev[:, 5].max()) / 1e3 if prev is not None else float("nan")
+        print("%6d %5d %7.2f | %8.2f %8.2f %8.2f | %10.2f %10.2f | %8.2f %8.2f | %6.2f" % (
+            nonce, len(x), period, r(1, np.median), r(2, np.median), r(2, np.max),
+            r(3, np.median), r(3, np.max), r(5, np.median), r(5, np.max), gap))
+        prev = x
 
 
 if __name__ == "__main__":
