@@ -228,6 +228,13 @@ struct DeviceCtx {
   cudaStream_t last_stream = nullptr;
   unsigned long long *last_counter = nullptr;
   unsigned long long last_final = 0;
+  // seqs of the last launch if it deferred its publication (kvring_internal.h): the next
+  // launch on pend_stream stores them from its publisher CTA
+  int n_pend_pub = 0;
+  unsigned long long *pend_seq[kStepPools] = {};
+  unsigned long long pend_step[kStepPools] = {};
+  int pend_sys = 0;
+  cudaStream_t pend_stream = nullptr;
   int acquire_blob(size_t bytes, BlobSlot **out, int *index) {
     if (!flags) {
       CU(cudaMalloc(reinterpret_cast<void **>(&flags), 128 * (size_t)kBlobRing));
@@ -1287,6 +1294,7 @@ struct StepLaunch {
   std::vector<int32_t> len, pub, blk0;
   bool pdl = false;  // launched as a programmatic dependent of the previous step's grid
   bool chain_ok = false;  // the previous kernel on the stream is this library's step launch
+  bool defer_next = false;  // the next launch on the stream is chained (it may publish ours)
   std::vector<char> blob;
   const void *host_src[kStepPools] = {};  // KV_SRC_HOST sources
   size_t host_src_bytes[kStepPools] = {};
@@ -1311,6 +1319,7 @@ struct StepLaunch {
     blk0.clear();
     pdl = false;
     chain_ok = false;
+    defer_next = false;
     app_bytes = rep_bytes = 0;
     rep_step = 0;
     inval.clear();
@@ -1566,6 +1575,36 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
                                     << h.g.cps_shift;
   const int cap = step_resident_ctas(S.device, step_smem_bytes(h));
   int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + 1023) / 1024));
+  // a deferred publication of the previous launch: one more CTA stores its seqs
+  h.n_prev = 0;
+  if (ctx->n_pend_pub > 0) {
+    if (ctx->pend_stream != st)
+      return fail(KV_ESTATE, "a deferred publication is pending on another stream");
+    h.n_prev = ctx->n_pend_pub;
+    h.prev_sys = ctx->pend_sys;
+    for (int q = 0; q < h.n_prev; ++q) {
+      h.prev_seq[q] = ctx->pend_seq[q];
+      h.prev_step[q] = ctx->pend_step[q];
+    }
+    grid = std::min(grid, std::max(1, cap - 1)) + 1;
+  }
+  // defer this launch's own seqs when a chained launch follows on the stream (a later
+  // chunk of this step, or the next step of kv_loop_run) and a successor is a peer: the
+  // CTAs then leave without waiting for their NVLink stores' acknowledgements
+  h.defer = 0;
+  int n_def = 0, def_sys = 0;
+  unsigned long long *def_seq[kStepPools];
+  unsigned long long def_step[kStepPools];
+  if (with_rep && h.publish && h.sys_any && S.pdl && (i1 < S.items.size() || S.defer_next)) {
+    for (int q = 0; q < h.n_rep; ++q) {
+      if (h.rep[q].abort_slices >= 0) continue;
+      def_seq[n_def] = reinterpret_cast<unsigned long long *>(h.rep[q].meta);
+      def_step[n_def] = h.rep[q].step;
+      if (h.rep[q].sys) def_sys |= 1 << n_def;
+      ++n_def;
+    }
+    h.defer = n_def > 0;
+  }
   // the blob goes into a pinned host slot; CTA 0 of the kernel pulls it across PCIe and
   // shares it through the slot's device buffer and flag (no copy-engine call, no event)
   DeviceCtx::BlobSlot *db = nullptr;
@@ -1600,6 +1639,16 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
   h.pad0 = (int32_t)(nonce & 0x7fffffff);  // launch nonce (debug timelines)
   CU(launch_step(h, grid, st, S.pdl));
   phase_add(kPhLaunch, now_s() - t1);
+  // launched: the previous deferred publication is this launch's; this one's is pending
+  ctx->n_pend_pub = n_def;
+  if (n_def > 0) {
+    for (int q = 0; q < n_def; ++q) {
+      ctx->pend_seq[q] = def_seq[q];
+      ctx->pend_step[q] = def_step[q];
+    }
+    ctx->pend_sys = def_sys;
+    ctx->pend_stream = st;
+  }
   g_launches++;
   if (g_log_on) {
     uint64_t app = 0;  // payload bytes of this launch's items
@@ -2287,7 +2336,10 @@ KV_API int kv_loop_destroy(kv_loop_t *L) {
 namespace {
 // chain_first: the previous kernel on `stream` is this loop's previous launch (inside
 // kv_loop_run, which enqueues nothing else between its steps)
-int loop_step(kv_loop_t *L, const kv_step_t *st, void *stream, bool chain_first) {
+// defer_last: a chained launch follows this step's last launch on the stream (the next
+// step of kv_loop_run), so a publication over NVLink may hand its seq stores to it
+int loop_step(kv_loop_t *L, const kv_step_t *st, void *stream, bool chain_first,
+              bool defer_last) {
   NvtxRange nv("kv_loop_step");
   if (!L || !st) return fail(KV_EINVAL, "null argument");
   if (st->n_repl > kMaxPoolsPerLaunchHost) return fail(KV_EINVAL, "too many pools");
@@ -2326,6 +2378,7 @@ int loop_step(kv_loop_t *L, const kv_step_t *st, void *stream, bool chain_first)
     // runs while the previous step's grid drains (timed launches are serialised)
     L->S[i]->pdl = !st->ev_kernel_start && !st->ev_kernel_end;
     L->S[i]->chain_ok = i > 0 || chain_first;
+    L->S[i]->defer_next = i < nl - 1 || defer_last;
     rc = step_enqueue(*L->S[i], s);
     g_ev_before = g_ev_after = nullptr;
     if (rc) return rc;
@@ -2343,16 +2396,46 @@ int loop_step(kv_loop_t *L, const kv_step_t *st, void *stream, bool chain_first)
 }  // namespace
 
 KV_API int kv_loop_step(kv_loop_t *L, const kv_step_t *st, void *stream) {
-  return loop_step(L, st, stream, false);
+  return loop_step(L, st, stream, false, false);
 }
+
+namespace {
+// A launch deferred its seq stores but no launch followed on `stream` (an error stopped
+// the loop): one launch with nothing to move but the publisher CTA stores them.
+int flush_deferred(void *stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<DeviceCtx *> ctxs;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (auto &kv : g_ctx) ctxs.push_back(kv.second.get());
+  }
+  for (DeviceCtx *ctx : ctxs) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->n_pend_pub == 0 || ctx->pend_stream != st) continue;
+    DeviceGuard dg(ctx->device);
+    if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", ctx->device);
+    StepLaunch S;
+    S.device = ctx->device;
+    S.pdl = true;
+    int rc = step_launch_one(S, 0, 0, false, true, ctx, st);
+    if (rc) return rc;
+  }
+  return KV_OK;
+}
+}  // namespace
 
 KV_API int kv_loop_run(kv_loop_t *L, int32_t n_steps, const kv_step_t *steps, void *stream) {
   if (n_steps < 0 || (n_steps > 0 && !steps)) return fail(KV_EINVAL, "bad steps");
   for (int i = 0; i < n_steps; ++i) {
-    int rc = loop_step(L, &steps[i], stream, i > 0);
-    if (rc) return rc;
+    // the next step launches (its appends, or this step's publication) and is chained
+    const bool next = i + 1 < n_steps && (steps[i + 1].n_append > 0 || steps[i].n_repl > 0);
+    int rc = loop_step(L, &steps[i], stream, i > 0, next);
+    if (rc) {
+      flush_deferred(stream);
+      return rc;
+    }
   }
-  return KV_OK;
+  return flush_deferred(stream);
 }
 
 KV_API int kv_loop_flush(kv_loop_t *L, void *stream) {

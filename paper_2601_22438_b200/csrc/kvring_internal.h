@@ -179,6 +179,17 @@ struct alignas(16) KvStepHdr {
   unsigned long long target;        // its value once every CTA of this launch arrived
   unsigned long long *done;         // pinned host word: = nonce once the launch completed
   unsigned int *work;               // dynamic round counters of the slot (8 x 64 B, zero at rest)
+  // deferred publication over NVLink: a launch with `defer` does not wait for its peer
+  // stores' acknowledgements (its CTAs arrive with a GPU-scope release) and stores no
+  // seq; the next launch on the stream -- chained, so it starts copying at once -- adds
+  // one publisher CTA (the last) that waits for that launch to complete
+  // (griddepcontrol.wait: every store performed) and stores its seqs (n_prev of them)
+  int32_t defer;
+  int32_t n_prev;
+  int32_t prev_sys;                 // bit q: prev_seq[q] is in a peer's memory
+  int32_t pad2;
+  unsigned long long *prev_seq[kStepPools];
+  unsigned long long prev_step[kStepPools];
   unsigned long long *prev_counter; // chain: the previous launch's counter ...
   unsigned long long prev_target;   // ... and its final value (every CTA arrived, seq stored)
   KvGeomDev g;

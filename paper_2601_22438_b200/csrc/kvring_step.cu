@@ -309,16 +309,25 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
   }
 }
 
-__device__ __forceinline__ void copy_all(int T, Cursor &cur, const KvGeomDev &g,
+//
+// Append rounds and publication rounds are interleaved in proportion (round r is a
+// publication round iff floor((r+1) f) > floor(r f), f = Rp / R in 32.32 fixed point,
+// rounded up so that exactly Rp of the R rounds are): over NVLink the publication's
+// peer stores then run all through the launch instead of waiting for the appends
+// (2 GPUs: +7 % per step; in one GPU's HBM the order makes no measurable difference).
+__device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const KvGeomDev &g,
                                          unsigned int *work) {
   const int lane = threadIdx.x & 31;
   const int gw = (int)blockIdx.x * kWarps + (int)(threadIdx.x >> 5);
-  const int W = (int)gridDim.x * kWarps;
+  const int W = G * kWarps;
   const int cs = g.cps_shift;
   const uint32_t d = 32u >> cs;                 // slices per warp iteration
   const int span = (int)d * kU;                 // slices per warp round
   const uint32_t lc = ((uint32_t)lane & ((1u << cs) - 1u)) << 4;
-  const int R = (int)(((long long)T + span - 1) / span);
+  const int Ra = (A + span - 1) / span, Rp = (P + span - 1) / span;
+  const int R = Ra + Rp;
+  const unsigned long long f =
+      Ra == 0 ? (1ull << 32) : (((unsigned long long)Rp << 32) + (unsigned long long)R - 1) / R;
 #ifdef KV_AB_STATIC  // A/B builds (tools/ab_bench.sh): every round dealt statically
   const int st = R;
 #elif defined(KV_AB_DYN4)
@@ -348,8 +357,16 @@ __device__ __forceinline__ void copy_all(int T, Cursor &cur, const KvGeomDev &g,
       if (lane == 0) next = atomicAdd(ctr, 1u);
       drawn = true;
     }
-    const long long base = (long long)r * span;
-    copy_round((int)base, (int)min((long long)T, base + span), lane, cs, d, lc, cur);
+    int b0, b1;
+    const unsigned int pr = (unsigned int)(((unsigned long long)r * f) >> 32);
+    if ((unsigned int)(((unsigned long long)(r + 1) * f) >> 32) > pr) {  // publication round pr
+      b0 = A + (int)pr * span;
+      b1 = min(A + P, b0 + span);
+    } else {                                                           // append round r - pr
+      b0 = (r - (int)pr) * span;
+      b1 = min(A, b0 + span);
+    }
+    copy_round(b0, b1, lane, cs, d, lc, cur);
     r = r < Rs ? r + W : 0x7fffffff;
   }
 }
@@ -396,6 +413,42 @@ __device__ unsigned long long g_kv_timeline[32 * 1024 * 8];  // the last 32 laun
   } while (0)
 #endif
 
+// Completion (step 5 of step_body; also the publisher CTA's arrival).
+__device__ __forceinline__ void step_complete(const KvStepHdr &h) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#ifdef KV_AB_GPU_RELEASE  // A/B builds only: unsafe for remote readers (bound on the gain)
+    const bool sys_rel = false;
+#else
+    // a deferred launch does not wait for its peer stores here: the next launch's
+    // publisher waits for this grid to complete before it stores the seqs
+    const bool sys_rel = h.sys_any != 0 && !h.defer;
+#endif
+    const unsigned long long old = atom_add_release(h.counter, 1ull, sys_rel);
+    if (old + 1ull == h.target) {
+      if (sys_rel)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+      else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (h.publish && !h.defer)
+        for (int q = 0; q < h.n_rep; ++q) {
+          const KvStepPool &pp = h.rep[q];
+          if (pp.abort_slices >= 0) continue;
+          unsigned long long *seq = reinterpret_cast<unsigned long long *>(pp.meta);
+          if (pp.sys)
+            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
+          else
+            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
+        }
+      // the dynamic round counters are free again (every warp drew its last round)
+      for (int c = 0; c < kWorkCtrs; ++c) h.work[c * kWorkStride] = 0u;
+      // final count: the next chained launch acquires it (its seq stores follow these)
+      atom_add_release(h.counter, 1ull, sys_rel);
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.done), "l"(h.nonce) : "memory");
+    }
+  }
+}
+
 __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   extern __shared__ __align__(16) char sm[];
   KV_STAMP(0);
@@ -406,6 +459,23 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   // programmatic dependent launch: the next step's grid may start its prologue as soon
   // as this grid's CTAs leave (a no-op for a normally serialised launch)
   if (h.pdl) asm volatile("griddepcontrol.launch_dependents;" :::);
+  // the publisher CTA of a launch following a deferred one (kvring_internal.h): wait for
+  // that launch to complete -- every one of its stores, peer stores included, performed
+  // -- then store its seqs; it moves no data and arrives like the others
+  if (h.n_prev > 0 && blockIdx.x == gridDim.x - 1) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int q = 0; q < h.n_prev; ++q) {
+        if ((h.prev_sys >> q) & 1)
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.prev_seq[q]), "l"(h.prev_step[q]) : "memory");
+        else
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(h.prev_seq[q]), "l"(h.prev_step[q]) : "memory");
+      }
+    }
+    step_complete(h);
+    return;
+  }
   // 1. descriptor blob -> shared memory.  The host writes it into pinned host memory and
   //    launches -- no copy-engine call and no event per step.  CTA 0 pulls it across
   //    PCIe once (zero copy) into a device buffer and releases a per-buffer flag carrying
@@ -549,10 +619,10 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   }
   // 3. copies: the grid's flat space, dealt in warp rounds
   KV_STAMP(2);
-  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t G = gridDim.x - (h.n_prev > 0 ? 1u : 0u), b = blockIdx.x;
   {
     Cursor cur(h, s);
-    copy_all(h.app_slices + P, cur, h.g, h.work);
+    copy_all(h.app_slices, P, (int)G, cur, h.g, h.work);
   }
   KV_STAMP(3);
   // 4. tables: the appended items' device bt entries; the publication's parity
@@ -611,31 +681,7 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   //    host the descriptor slot is free (nonce into pinned memory: every CTA read the
   //    slot long before it arrived here).  The slot's counter is monotone: the host passes
   //    the value the last arrival of this launch makes it reach.
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long old = atom_add_release(h.counter, 1ull, h.sys_any != 0);
-    if (old + 1ull == h.target) {
-      if (h.sys_any)
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-      else
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      if (h.publish)
-        for (int q = 0; q < h.n_rep; ++q) {
-          const KvStepPool &pp = h.rep[q];
-          if (pp.abort_slices >= 0) continue;
-          unsigned long long *seq = reinterpret_cast<unsigned long long *>(pp.meta);
-          if (pp.sys)
-            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
-          else
-            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(seq), "l"(pp.step) : "memory");
-        }
-      // the dynamic round counters are free again (every warp drew its last round)
-      for (int c = 0; c < kWorkCtrs; ++c) h.work[c * kWorkStride] = 0u;
-      // final count: the next chained launch acquires it (its seq stores follow these)
-      atom_add_release(h.counter, 1ull, h.sys_any != 0);
-      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(h.done), "l"(h.nonce) : "memory");
-    }
-  }
+  step_complete(h);
   KV_STAMP(5);
 }
 
