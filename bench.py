@@ -940,7 +940,7 @@ def run_bulk(args, rank, world, local_rank, dev, group):
     per_gpu = D / (ms * 1e-3) / 1e9
     if world == 1:
         ach = 2 * D / (ms * 1e-3) / 1e9
-        tr = traffic_ref("bulk_c5")
+        tr = traffic_ref("bulk_c5", "kv_step_kernel")
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(ach / hbm_peak, 4), "peak_source": src_peak,
                 "algorithmic_bytes_per_launch": int(2 * D),

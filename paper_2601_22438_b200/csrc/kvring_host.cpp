@@ -427,6 +427,10 @@ struct kv_pool {
   // allocator (R6, R7)
   IdSet free_blocks, free_slots;
   std::vector<int> q_blocks, q_slots;
+  // begin_step count and, per block, the count when it was last released: a deferred
+  // publication gates stores into blocks freed one step ago (kvring_internal.h)
+  int epoch = 0;
+  std::vector<int> freed_at;
   std::vector<int64_t> slot_req;
   std::vector<int32_t> slot_len, pub_len;
   int slot_hi = 0;  // 1 + highest live slot (slots are taken lowest first): loop bound
@@ -647,6 +651,7 @@ int append_validate(kv_pool *p, const kv_append_args_t &a, long long free_b, lon
 }
 
 void do_begin_step(kv_pool *p) {
+  ++p->epoch;
   for (int b : p->q_blocks) p->free_blocks.insert(b);
   for (int s : p->q_slots) p->free_slots.insert(s);
   p->q_blocks.clear();
@@ -661,7 +666,10 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
       free_rep(p, s);
       p->dropped[s] = 0;
     }
-    for (int b : p->slot_bt[s]) p->q_blocks.push_back(b);
+    for (int b : p->slot_bt[s]) {
+      p->q_blocks.push_back(b);
+      p->freed_at[b] = p->epoch;
+    }
     p->slot_bt[s].clear();
     p->q_slots.push_back(s);
     p->slot_req[s] = -1;
@@ -858,6 +866,7 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
   p->task_segs = std::max(1, 32768 / p->seg_bytes);
   p->cps_shift = __builtin_ctz(p->seg_bytes / 16);
   p->free_blocks.init(p->NB, true);
+  p->freed_at.assign(p->NB, -(1 << 29));
   p->free_slots.init(p->R, true);
   p->slot_req.assign(p->R, -1);
   p->slot_len.assign(p->R, 0);
@@ -1390,7 +1399,16 @@ void step_add_replicate(StepLaunch &S, kv_pool *p, uint64_t step) {
     if (p->slot_req[s] >= 0) {
       const int lo = p->pub_len[s], hi = pub_hi(p, s);
       bytes += (uint64_t)(hi - lo);
-      if (hi > lo) b0 = p->slot_bt[s][lo / B];  // the block of the first dirty token
+      if (hi > lo) {
+        b0 = p->slot_bt[s][lo / B];  // the block of the first dirty token
+        // blocks with no published token that were freed one step ago: the last stored
+        // seq may still list them (only matters when this publication is deferred)
+        for (int j = (lo + B - 1) / B; j <= (hi - 1) / B; ++j)
+          if (p->freed_at[p->slot_bt[s][j]] >= p->epoch - 1) {
+            b0 |= 1 << 30;
+            break;
+          }
+      }
     }
     S.blk0.push_back(b0);
   }
@@ -1618,6 +1636,7 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
   h.hblob = db->hmapped;
   h.gblob = db->dev;
   h.flag = ctx->flags + 16 * slot;        // one 128-B line per slot
+  h.gate = ctx->flags + 16 * slot + 8;    // its second half: the deferred-publication gate
   h.counter = ctx->counters + 16 * slot;
   h.work = ctx->work + 128 * slot;
   h.target = db->arrivals + (unsigned long long)grid;

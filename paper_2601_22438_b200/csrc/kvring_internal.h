@@ -184,10 +184,15 @@ struct alignas(16) KvStepHdr {
   // seq; the next launch on the stream -- chained, so it starts copying at once -- adds
   // one publisher CTA (the last) that waits for that launch to complete
   // (griddepcontrol.wait: every store performed) and stores its seqs (n_prev of them)
+  // R7 under deferral: until the publisher has stored the previous seqs, the last
+  // stored seq may still list blocks freed one step ago -- so this launch's stores into
+  // blocks with no previously published token, and its table writes, wait for `gate`
+  // (= nonce, released by the publisher after its seq stores)
   int32_t defer;
   int32_t n_prev;
   int32_t prev_sys;                 // bit q: prev_seq[q] is in a peer's memory
   int32_t pad2;
+  unsigned long long *gate;
   unsigned long long *prev_seq[kStepPools];
   unsigned long long prev_step[kStepPools];
   unsigned long long *prev_counter; // chain: the previous launch's counter ...

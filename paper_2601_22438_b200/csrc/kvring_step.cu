@@ -138,6 +138,11 @@ __device__ __forceinline__ uint32_t div_small(uint32_t q, uint32_t n, float rn) 
 //           inner = token t < n, outer = combo c: off = block + (c * B + t0 + t) * seg
 // so stepping d slices is pointer += d * stride plus a rare carry; only a piece boundary
 // (or the round's end, or a fault-injection cut) starts a new sub-round with a locate.
+// blk0 word of a publication entry: block id | kBlkGated when one of the entry's blocks
+// with no previously published token was freed one step ago (deferred publication)
+constexpr int kBlkGated = 1 << 30;
+constexpr int kBlkMask = kBlkGated - 1;
+
 struct Cursor {
   const KvStepHdr &h;
   const StepSmem &s;
@@ -150,6 +155,8 @@ struct Cursor {
   int pb = -1;                // end of the piece (flat slice)
   int lim = 0x7fffffff;       // publication cut short by fault injection (flat slice)
   bool in_rep = false;        // idx is a publication entry
+  bool gated = false;         // the piece's block holds no previously published token and
+                              // the entry's new blocks include one freed one step ago
   __device__ Cursor(const KvStepHdr &h_, const StepSmem &s_) : h(h_), s(s_) {}
 
   __device__ __forceinline__ void locate(int x, uint32_t d) {
@@ -164,6 +171,7 @@ struct Cursor {
       }
       idx = a;
       in_rep = false;
+      gated = false;
       const KvAppItem &it = items[a];
       pb = a + 1 < h.n_items ? items[a + 1].off : h.app_slices;
       lim = 0x7fffffff;
@@ -204,12 +212,14 @@ struct Cursor {
       const uint32_t n0 = min(B - t0, phi - plo);
       const uint32_t r = (uint32_t)(xr - s.pref[e]);
       uint32_t j, tok0, rr, pa;
+      gated = true;
       if (r < n0 * SL) {               // the entry's first (possibly partial) block
         j = j0;
         nin = n0;
         tok0 = t0;
         rr = r;
         pa = 0;
+        gated = t0 == 0;
       } else {                         // full blocks, the last one possibly partial
         const uint32_t r2 = r - n0 * SL;
         const uint32_t jj = fdiv(r2, h.div_bs);
@@ -222,7 +232,9 @@ struct Cursor {
       pb = h.app_slices + s.pref[e] + (int)(pa + nin * SL);
       out = div_small(rr, nin, __frcp_rn((float)nin));
       in = rr - out * nin;
-      const int blk = j == j0 ? s.blk0[e] : pp.bt[(size_t)slot * pp.M + j];
+      const int b0w = s.blk0[e];
+      const int blk = j == j0 ? (b0w & kBlkMask) : pp.bt[(size_t)slot * pp.M + j];
+      gated = gated && (b0w & kBlkGated);
       const long long off = (long long)blk * h.g.block_bytes + (long long)tok0 * seg +
                             (long long)in * seg + (long long)out * (B * seg);
       s_in = d_in = seg;
@@ -262,8 +274,20 @@ constexpr int kWorkCtrs = 8;
 constexpr int kBlobBatch = 8;  // descriptor loads in flight per thread
 constexpr int kWorkStride = 16;  // u32 words between counters (64 B)
 
+// Waits (one thread) until the launch's publisher CTA opened the gate (deferred
+// publication, kvring_internal.h); bounded: a trap beats a hang.
+__device__ __forceinline__ void wait_gate(const KvStepHdr &h) {
+  unsigned long long v;
+  for (long long spin = 0;; ++spin) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.gate) : "memory");
+    if (v == h.nonce) break;
+    if (spin > (1ll << 24)) __trap();
+    if (spin > 16) __nanosleep(64);
+  }
+}
+
 __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs, uint32_t d,
-                                           uint32_t lc, Cursor &cur) {
+                                           uint32_t lc, Cursor &cur, bool &gate_shut) {
   {
     int x = base + (lane >> cs);                // this lane's slice
     while (__any_sync(0xffffffffu, x < rend)) {
@@ -289,6 +313,13 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
           cur.in += d;
           cur.carry_src();
         }
+      }
+      // stores into a block that the last stored seq may still list as another
+      // request's wait for the previous publication's seq (deferred publication)
+      if (gate_shut && __any_sync(0xffffffffu, n > 0 && cur.gated)) {
+        if (lane == 0) wait_gate(cur.h);
+        __syncwarp();
+        gate_shut = false;
       }
       char *dq = dp0;
       uint32_t in = in0;
@@ -343,6 +374,7 @@ __device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const
   // latency hides behind them
   unsigned int next = 0;
   bool drawn = false;                           // `next` holds a draw (warp-uniform)
+  bool gate_shut = cur.h.n_prev > 0;            // warp-uniform
   for (int r = gw;;) {
     if (r >= Rs) {                              // static share done: take a drawn round
       if (Rs >= R) break;
@@ -366,7 +398,7 @@ __device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const
       b0 = (r - (int)pr) * span;
       b1 = min(A, b0 + span);
     }
-    copy_round(b0, b1, lane, cs, d, lc, cur);
+    copy_round(b0, b1, lane, cs, d, lc, cur, gate_shut);
     r = r < Rs ? r + W : 0x7fffffff;
   }
 }
@@ -472,6 +504,8 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
         else
           asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(h.prev_seq[q]), "l"(h.prev_step[q]) : "memory");
       }
+      // the seqs are stored (system scope): stores that the old seqs forbade may go
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(h.gate), "l"(h.nonce) : "memory");
     }
     step_complete(h);
     return;
@@ -635,6 +669,10 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
     pp.bt[(size_t)it.slot * pp.M + fdiv((uint32_t)it.p0, h.div_b)] = it.blk;
   }
   if (h.publish) {
+    if (h.n_prev > 0) {  // the tables may be listed by the last stored seq: wait for the newer one
+      if (threadIdx.x == 0) wait_gate(h);
+      __syncthreads();
+    }
     for (int q = 0; q < h.n_rep; ++q) {
       const KvStepPool &pp = h.rep[q];
       if (pp.abort_slices >= 0) continue;  // aborted: nothing of this step is published
@@ -666,7 +704,8 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
         }
         const int sl = a - pp.ent_off;
         const int j = s.lo[a] / B + (gk - s.bpref[a]);
-        mbt[(size_t)sl * pp.M + j] = gk == s.bpref[a] ? s.blk0[a] : pp.bt[(size_t)sl * pp.M + j];
+        mbt[(size_t)sl * pp.M + j] =
+            gk == s.bpref[a] ? (s.blk0[a] & kBlkMask) : pp.bt[(size_t)sl * pp.M + j];
       }
       if (gt == 0) *reinterpret_cast<int32_t *>(pp.meta + 8) = pp.writer_node;
     }
