@@ -144,6 +144,30 @@ int kv_set_successor_shared(kv_pool_t *p, kv_pool_t *holder);
  * count as dropped.  A dead predecessor is unlinked.  Host-only. */
 int kv_drop_replicas(kv_pool_t *holder);
 
+/* Shared capacity across GPUs (NEXT-3 with the holder in another process).  The
+ * holder's process creates a MIRROR of the predecessor: a pool on the HOLDER's
+ * device whose `pool` pointer is the predecessor's pool as mapped into this process
+ * (an NVLink peer address, e.g. from symmetric memory) and whose replica/meta are
+ * scratch.  on = 1 (before the mirror's first append): appends and releases on the
+ * mirror update its tables only (the owner moves the bytes; src_kv may be NULL), so
+ * applying the owner's append calls in the same order keeps identical tables
+ * (allocation is deterministic, reading R6); kv_set_successor_shared(mirror, holder)
+ * then replicates by PULLING the dirty slices from the owner's pool over NVLink into
+ * holder-allocated blocks -- the allocator that must decide them lives here.  The
+ * caller orders the pull after the owner's append of the step (e.g. a host barrier)
+ * and the owner's append of step t+2 after the pull of step t (R7).  kv_fail_stage on
+ * a mirror only marks it dead (the owner poisons its own memory).  KV_ESTATE if the
+ * mirror was already used.  The mirror does not choose block ids: the owner's
+ * allocator also serves the owner's own holder role, so the owner forwards the ids
+ * its append allocated (kv_last_alloc) and the holder queues them
+ * (kv_mirror_blocks) before the mirror's append of the same step (KV_ESTATE if
+ * fewer are queued than the append needs). */
+int kv_pool_set_mirror(kv_pool_t *p, int32_t on);
+int kv_mirror_blocks(kv_pool_t *mirror, int32_t n, const int32_t *block_ids);
+/* Block ids allocated by p's last append, in allocation order (copies min(n, cap));
+ * returns n. */
+int kv_last_alloc(kv_pool_t *p, int32_t *out, int32_t cap);
+
 /* Step boundary: blocks and slots quarantined by the
  * previous step become allocatable. */
 int kv_begin_step(kv_pool_t *p);

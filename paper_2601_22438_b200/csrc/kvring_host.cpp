@@ -122,6 +122,11 @@ class IdSet {
     return hint_ * 64 + b;
   }
   int size() const { return count_; }
+  void erase(int i) {
+    if (!contains(i)) return;
+    words_[i >> 6] &= ~(1ull << (i & 63));
+    --count_;
+  }
 
  private:
   int n_ = 0, count_ = 0, hint_ = 0;
@@ -420,6 +425,12 @@ struct kv_pool {
   int token_bytes = 0, seg_bytes = 0, combos = 0, task_segs = 0, cps_shift = 0;
   // ring link
   int repl_mode = KV_MODE_TOKENS;  // KV_MODE_BLOCKS: completed blocks only (NEXT-2)
+  // mirror of a pool owned by another process (kv_pool_set_mirror): appends update the
+  // tables only, `pool` is the owner's pool through NVLink, the holder pulls from it
+  bool mirror = false;
+  std::vector<int> mirror_q;   // the owner's block ids for the mirror's next appends
+  size_t mirror_qi = 0;
+  std::vector<int> last_alloc; // block ids the last append call allocated, in order
   bool has_succ = false;
   bool succ_sys = true;  // successor memory is not this GPU's HBM (NVLink peer)
   int succ_node = -1, succ_replica_blocks = 0;
@@ -686,6 +697,7 @@ void do_release(kv_pool *p, int n, const int64_t *ids) {
 long long do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx,
                     std::vector<KvAppItem> &items, int32_t &slices) {
   const int B = p->g.block_size;
+  p->last_alloc.clear();
   int row = 0;
   for (int i = 0; i < a.n; ++i) {
     const int64_t r = a.req_ids[i];
@@ -703,7 +715,17 @@ long long do_append(kv_pool *p, const kv_append_args_t &a, int16_t pidx,
     int len = p->slot_len[s];
     int left = a.n_new[i];
     while (left > 0) {
-      if (len % B == 0) p->slot_bt[s].push_back(p->free_blocks.take_min());
+      if (len % B == 0) {
+        int b;
+        if (p->mirror) {  // the owner's choice (its allocator also serves its holder role)
+          b = p->mirror_q[p->mirror_qi++];
+          p->free_blocks.erase(b);
+        } else {
+          b = p->free_blocks.take_min();
+        }
+        p->slot_bt[s].push_back(b);
+        p->last_alloc.push_back(b);
+      }
       const int j = len / B, lo = len % B;
       const int n = std::min(B - lo, left);
       if (p->device >= 0) {
@@ -985,6 +1007,37 @@ KV_API int kv_set_successor_shared(kv_pool_t *p, kv_pool_t *h) {
   std::fill(p->pub_len.begin(), p->pub_len.end(), 0);  // re-seed
   std::fill(p->dropped.begin(), p->dropped.end(), 0);
   return KV_OK;
+}
+
+KV_API int kv_pool_set_mirror(kv_pool_t *p, int32_t on) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  if (p->device < 0) return fail(KV_EINVAL, "a mirror needs a device (the holder's)");
+  if (p->slot_hi > 0 || p->last_step > 0 || p->free_blocks.size() != p->NB)
+    return fail(KV_ESTATE, "mirror a pool before its first append");
+  p->mirror = on != 0;
+  return KV_OK;
+}
+
+KV_API int kv_mirror_blocks(kv_pool_t *p, int32_t n, const int32_t *block_ids) {
+  if (!p || (n > 0 && !block_ids)) return fail(KV_EINVAL, "null argument");
+  if (!p->mirror) return fail(KV_EINVAL, "pool %d is not a mirror", p->node_id);
+  if (p->mirror_qi == p->mirror_q.size()) {
+    p->mirror_q.clear();
+    p->mirror_qi = 0;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (block_ids[i] < 0 || block_ids[i] >= p->NB) return fail(KV_EINVAL, "block id out of range");
+    p->mirror_q.push_back(block_ids[i]);
+  }
+  return KV_OK;
+}
+
+KV_API int kv_last_alloc(kv_pool_t *p, int32_t *out, int32_t cap) {
+  if (!p) return fail(KV_EINVAL, "null pool");
+  const int n = (int)p->last_alloc.size();
+  if (out)
+    for (int i = 0; i < n && i < cap; ++i) out[i] = p->last_alloc[i];
+  return n;
 }
 
 KV_API int kv_drop_replicas(kv_pool_t *h) {
@@ -1469,7 +1522,10 @@ int validate_appends(int n_pools, const kv_append_args_t *args) {
     if (rc) return rc;
     long long rows = 0;
     for (int i = 0; i < args[k].n; ++i) rows += args[k].n_new[i];
-    if (p->device >= 0 && rows > 0 && !args[k].src_kv)
+    if (p->mirror && p->scratch_need > (long long)(p->mirror_q.size() - p->mirror_qi))
+      return fail(KV_ESTATE, "mirror %d: %lld new blocks but %lld owner block ids queued",
+                  p->node_id, p->scratch_need, (long long)(p->mirror_q.size() - p->mirror_qi));
+    if (p->device >= 0 && !p->mirror && rows > 0 && !args[k].src_kv)
       return fail(KV_EINVAL, "null src_kv with tokens to append");
     if (rows * p->combos > (long long)INT32_MAX / 4)
       return fail(KV_EINVAL, "append too large for one launch");
@@ -1486,6 +1542,13 @@ void apply_appends(StepLaunch &S, int n_pools, const kv_append_args_t *args) {
     if (args[k].begin_step) do_begin_step(p);
     do_release(p, args[k].n_release, args[k].release_ids);
     if (p->scratch_need > p->free_blocks.size()) evict_for(p, p->scratch_need);
+    if (p->mirror) {  // the owner moves the bytes: tables only
+      set_geom(S, p);  // the device of withdrawals this append may cause on the holder
+      std::vector<KvAppItem> none;
+      int32_t sl = 0;
+      do_append(p, args[k], 0, none, sl);
+      continue;
+    }
     step_add_append(S, p, args[k]);
   }
   collect_inval(S.inval, S.max_reqs_inval, pools, n_pools);
@@ -1682,7 +1745,13 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
 // than kItemsPerLaunch items, e.g. a 32k-token prefill; the publication rides on the
 // first).
 int step_enqueue(StepLaunch &S, cudaStream_t st) {
-  if (S.empty() || S.device < 0) return KV_OK;
+  if (S.device < 0) return KV_OK;
+  if (S.empty()) {  // nothing to launch (mirror appends only): still withdraw entries
+    if (S.inval.empty()) return KV_OK;
+    DeviceGuard dg(S.device);
+    if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", S.device);
+    return flush_inval(S.inval, S.max_reqs_inval, st);
+  }
   DeviceGuard dg(S.device);
   if (!dg.ok) return fail(KV_ECUDA, "cudaSetDevice(%d) failed", S.device);
   if (!S.inval.empty()) {
@@ -1810,7 +1879,7 @@ KV_API int kv_fail_stage(kv_pool_t *p, void *stream) {
   if (p->dead) return fail(KV_ESTATE, "pool %d already dead", p->node_id);
   p->dead = true;
   p->has_succ = false;
-  if (p->device < 0) return KV_OK;
+  if (p->device < 0 || p->mirror) return KV_OK;  // a mirror's bytes are its owner's
   DeviceGuard dg(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CU(cudaMemsetAsync(p->pool, 0xFF, (size_t)p->NB * p->block_bytes, st));

@@ -28,7 +28,8 @@ EXPORTED = ["kv_abi_version", "kv_append", "kv_append_multi", "kv_begin_step", "
             "kv_replicate_step_multi", "kv_restore", "kv_set_successor", "kv_stats", "kv_sync",
             "kv_unpack", "kv_time_next_launch", "kv_run_steps", "kv_host_profile",
             "kv_plan_targets", "kv_set_mode", "kv_replicate_step_ce",
-            "kv_set_successor_shared", "kv_drop_replicas", "kv_loop_create", "kv_loop_destroy",
+            "kv_set_successor_shared", "kv_drop_replicas", "kv_pool_set_mirror",
+            "kv_mirror_blocks", "kv_last_alloc", "kv_loop_create", "kv_loop_destroy",
             "kv_loop_step", "kv_loop_run", "kv_loop_flush", "kv_launch_log"]
 
 
@@ -136,6 +137,9 @@ def lib() -> ctypes.CDLL:
             "kv_replicate_step_ce": (ctypes.c_int, [_I32, _P, _U64, _P]),
             "kv_set_successor_shared": (ctypes.c_int, [_P, _P]),
             "kv_drop_replicas": (ctypes.c_int, [_P]),
+            "kv_pool_set_mirror": (ctypes.c_int, [_P, _I32]),
+            "kv_mirror_blocks": (ctypes.c_int, [_P, _I32, _P]),
+            "kv_last_alloc": (ctypes.c_int, [_P, _P, _I32]),
             "kv_host_profile": (ctypes.c_int, [_P, _I32, _I32]),
             "kv_plan_targets": (ctypes.c_int, [_I32, _P, _P, _P]),
             "kv_set_mode": (ctypes.c_int, [_P, _I32]),
@@ -333,6 +337,23 @@ def kv_set_successor_shared(p: int, holder: int) -> None:
 
 def kv_drop_replicas(holder: int) -> None:
     _check(lib().kv_drop_replicas(holder))
+
+
+def kv_pool_set_mirror(p: int, on: bool = True) -> None:
+    _check(lib().kv_pool_set_mirror(p, 1 if on else 0))
+
+
+def kv_mirror_blocks(mirror: int, block_ids) -> None:
+    a = _i32(list(block_ids))
+    _check(lib().kv_mirror_blocks(mirror, a.size, _ptr(a)))
+
+
+def kv_last_alloc(p: int) -> list[int]:
+    n = lib().kv_last_alloc(p, None, 0)
+    _check(min(n, 0))
+    out = np.zeros(max(1, n), dtype=np.int32)
+    lib().kv_last_alloc(p, _ptr(out), n)
+    return [int(x) for x in out[:n]]
 
 
 def kv_replicate_step_ce(pools, step: int, stream: int = 0) -> None:

@@ -80,9 +80,13 @@ class RingRuntime:
                  sentinel: int | None = SENTINEL_WORD, dtype_words=torch.int16,
                  mode: int = K.KV_MODE_TOKENS, shared: bool = False):
         self.g = geom
-        # shared capacity (NEXT-3): a successor on this rank keeps the replica in
-        # its own pool (kv_set_successor_shared); the replica regions stay unused
+        # shared capacity (NEXT-3): the successor keeps the replica in its own pool
+        # (kv_set_successor_shared); the replica regions stay unused.  A successor on
+        # another rank PULLS: its rank keeps a mirror of the predecessor (tables only,
+        # pool = the predecessor's pool through NVLink, kv_pool_set_mirror) linked to
+        # the local holder -- the holder's allocator decides the replica blocks
         self.shared = shared
+        self.mirrors: dict[int, tuple[int, torch.Tensor]] = {}
         self.NB, self.R, self.M = num_blocks, max_reqs, max_blocks_per_req
         self.placement = dict(placement)
         self.succ = dict(succ)
@@ -114,12 +118,24 @@ class RingRuntime:
             self.arena = torch.empty(arena_bytes, dtype=torch.uint8, device=self.dev)
             self.symm = None
             self.peer_base = [self.arena.data_ptr()]
+        self.pool_bytes = num_blocks * self.block_bytes
+        self.pool_peer_base = None
+        if world > 1 and shared:   # pools in symmetric memory: a remote holder pulls from them
+            import torch.distributed._symmetric_memory as symm_mem
+            self.pool_arena = symm_mem.empty(self.n_slots * self.pool_bytes, dtype=torch.uint8,
+                                             device=self.dev)
+            self.pool_symm = symm_mem.rendezvous(self.pool_arena, gname)
+            self.pool_peer_base = [int(p) for p in self.pool_symm.buffer_ptrs]
         self.slots: list[NodeSlot] = []
         for k in range(self.n_slots):
             base = k * self.slot_stride
             rep = self.arena[base: base + self.replica_bytes].view(dtype_words).view(self.shape)
             meta = self.arena[base + self.replica_bytes: base + self.slot_stride]
-            pool = torch.empty(self.shape, dtype=dtype_words, device=self.dev)
+            if self.pool_peer_base is not None:
+                pool = self.pool_arena[k * self.pool_bytes:(k + 1) * self.pool_bytes] \
+                    .view(dtype_words).view(self.shape)
+            else:
+                pool = torch.empty(self.shape, dtype=dtype_words, device=self.dev)
             if sentinel is not None:
                 w = sentinel if sentinel < 0x8000 else sentinel - 0x10000
                 pool.fill_(w)
@@ -141,8 +157,16 @@ class RingRuntime:
         for n in sorted(placement):
             if placement[n] == rank:
                 self._create(n, self.slots[self.slot_of_node[n][1]])
+        if self.pool_peer_base is not None:
+            # a mirror of EVERY remote node (every rank receives every owner's block ids),
+            # so a link re-formed after a failure finds its mirror up to date
+            for n in sorted(placement):
+                if placement[n] != rank:
+                    self._create_mirror(n)
         for n in sorted(self.local):
             self._link(n)
+        for n in sorted(self.mirrors):
+            self._link_mirror(n)
 
     # ----------------------------------------------------------------- memory
     def _create(self, node: int, slot: NodeSlot) -> int:
@@ -154,6 +178,22 @@ class RingRuntime:
         slot.node = node
         self.local[node] = slot
         return slot.handle
+
+    def pool_ptr(self, node: int) -> int:
+        r, k = self.slot_of_node[node]
+        return self.pool_peer_base[r] + k * self.pool_bytes
+
+    def _create_mirror(self, node: int) -> None:
+        """Tables-only mirror of remote ``node`` on this rank's device, its pool pointer
+        the node's pool through NVLink (NEXT-3 across GPUs)."""
+        scratch = torch.zeros(self.block_bytes + self.meta_stride, dtype=torch.uint8,
+                              device=self.dev)
+        d = K.kv_pool_desc_t(self.kg, self.NB, self.R, self.M, self.device, node, 1,
+                             self.pool_ptr(node), scratch.data_ptr(),
+                             scratch.data_ptr() + self.block_bytes)
+        h = K.kv_pool_create(d)
+        K.kv_pool_set_mirror(h, True)
+        self.mirrors[node] = (h, scratch)
 
     def replica_ptr(self, node: int) -> int:
         r, k = self.slot_of_node[node]
@@ -169,10 +209,25 @@ class RingRuntime:
             K.kv_set_successor(h, -1, None, 0, None)
         elif self.shared:
             if m not in self.local:
-                raise RuntimeError("shared-capacity links need the successor on this rank")
-            K.kv_set_successor_shared(h, self.local[m].handle)
+                if self.pool_peer_base is None or self.placement.get(m) is None:
+                    raise RuntimeError("shared-capacity links need the successor on this rank")
+                # the holder's rank pulls through its mirror of this node: no link here
+                K.kv_set_successor(h, -1, None, 0, None)
+            else:
+                K.kv_set_successor_shared(h, self.local[m].handle)
         else:
             K.kv_set_successor(h, m, self.replica_ptr(m), self.NB, self.meta_ptr(m))
+
+    def _link_mirror(self, node: int) -> None:
+        """A mirror replicates into a holder on this rank; otherwise it is unlinked."""
+        h = self.mirrors[node][0]
+        m = self.succ.get(node)
+        if node in self.dead:
+            return
+        if m is not None and m in self.local and m not in self.dead:
+            K.kv_set_successor_shared(h, self.local[m].handle)
+        else:
+            K.kv_set_successor(h, -1, None, 0, None)
 
     def handle(self, node: int) -> int:
         return self.local[node].handle
@@ -186,14 +241,21 @@ class RingRuntime:
         if not entries:
             return
         s = self._stream(stream)
-        K.kv_append_multi([dict(e, pool=self.handle(e["node"])) for e in entries], s)
+        K.kv_append_multi([dict(e, pool=self.mirrors[e["node"]][0] if e["node"] in self.mirrors
+                                else self.handle(e["node"])) for e in entries], s)
 
     def replicate_all(self, step: int, nodes: list[int] | None = None, stream=None) -> None:
-        nodes = [n for n in (self.alive_local() if nodes is None else nodes)
-                 if self.succ.get(n) is not None]
-        if nodes:
+        def linked_here(n):   # shared links to a remote holder are pulled by its rank
+            m = self.succ.get(n)
+            return m is not None and (not self.shared or m in self.local)
+        nodes = [n for n in (self.alive_local() if nodes is None else nodes) if linked_here(n)]
+        hs = [self.handle(n) for n in nodes]
+        # mirrors of remote predecessors: the local holder pulls their dirty slices
+        hs += [h for n, (h, _) in sorted(self.mirrors.items())
+               if n not in self.dead and self.succ.get(n) in self.local]
+        if hs:
             fn = K.kv_replicate_step_ce if self.copy_engine else K.kv_replicate_step_multi
-            fn([self.handle(n) for n in nodes], step, self._stream(stream))
+            fn(hs, step, self._stream(stream))
 
     def _stream(self, stream) -> int:
         if stream is None:
@@ -206,11 +268,15 @@ class RingRuntime:
         self.dead.add(node)
         if node in self.local:
             K.kv_fail_stage(self.handle(node), self._stream(stream))
+        if node in self.mirrors:   # marks the mirror dead (its owner poisons the memory)
+            K.kv_fail_stage(self.mirrors[node][0], self._stream(stream))
         for n, m in list(self.succ.items()):
             if m == node:
                 self.succ[n] = None
                 if n in self.local and n not in self.dead:
                     self._link(n)
+                if n in self.mirrors:
+                    self._link_mirror(n)
 
     def new_node(self, node: int, rank: int) -> None:
         """Bind a spare slot on ``rank`` to a fresh logical node id (every rank calls it)."""
@@ -239,6 +305,8 @@ class RingRuntime:
         self.succ[node] = succ
         if node in self.local and node not in self.dead:
             self._link(node)
+        if node in self.mirrors:
+            self._link_mirror(node)
 
     # ---------------------------------------------------------------- readout
     def read_meta(self, node: int) -> dict:
@@ -259,6 +327,9 @@ class RingRuntime:
             if s.handle is not None:
                 K.kv_pool_destroy(s.handle)
                 s.handle = None
+        for n, (h, _) in list(self.mirrors.items()):
+            K.kv_pool_destroy(h)
+        self.mirrors.clear()
 
 
 @dataclass
@@ -326,6 +397,8 @@ class ScheduleDriver:
 
     def append_step(self, t: int, stream=None, sources: dict | None = None,
                     plan: dict | None = None) -> None:
+        if getattr(self.rt, "pool_peer_base", None) is not None:
+            return self._append_step_pulled(t, stream, sources, plan)
         entries = []
         for node, e in (self.plan(t) if plan is None else plan).items():
             if node not in self.rt.local:
@@ -339,6 +412,35 @@ class ScheduleDriver:
                                 req_ids=e["req_ids"], n_new=e["n_new"], src=src))
         self.rt.append_all(entries, stream)
         self._keep = entries   # sources must outlive the async kernel launch
+
+    def _append_step_pulled(self, t, stream, sources, plan):
+        """Shared capacity across ranks (NEXT-3): nodes append in serving order, each
+        owner forwards the block ids its append allocated and a holder's rank applies the
+        same append to its mirror with those ids -- a holder's own append (which may
+        evict its predecessor's replicas) then sees the predecessor's tables of this step
+        exactly as in the one-process protocol."""
+        import torch.distributed as dist
+        rt = self.rt
+        keep = []
+        for node, e in (self.plan(t) if plan is None else plan).items():
+            allocs = None
+            if node in rt.local:
+                if sources is not None and node in sources:
+                    src = sources[node]
+                else:
+                    ids, pos = self.tokens(e["req_ids"], e["n_new"], e["start"])
+                    src = self.content(e["stage"], ids, pos) if ids else None
+                keep.append(src)
+                rt.append_all([dict(node=node, begin_step=1, release=e["release"],
+                                    req_ids=e["req_ids"], n_new=e["n_new"], src=src)], stream)
+                allocs = K.kv_last_alloc(rt.handle(node))
+            obj = [allocs]
+            dist.broadcast_object_list(obj, src=rt.placement[node], group=rt.group)
+            if node in rt.mirrors:
+                K.kv_mirror_blocks(rt.mirrors[node][0], obj[0])
+                rt.append_all([dict(node=node, begin_step=1, release=e["release"],
+                                    req_ids=e["req_ids"], n_new=e["n_new"], src=None)], stream)
+        self._keep = keep
 
     def fail_and_restore(self, t: int, coord: tuple[int, int], stream=None):
         """Fail the node serving ``coord`` after the appends of step t and restore it."""
@@ -445,6 +547,7 @@ class TablesRuntime:
         self.kg = K.geom(geom.layers, geom.kv_heads, geom.head_dim, geom.block_size,
                          geom.elem_bytes)
         self.dead: set[int] = set()
+        self.mirrors: dict = {}   # no cross-rank shared links in tables-only runs
         self.handles: dict[int, int] = {}
         self.local = self.handles
         for n in sorted(placement):

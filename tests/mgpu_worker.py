@@ -38,6 +38,8 @@ def main():
     dist.init_process_group("nccl", device_id=dev, timeout=timedelta(seconds=120))
     if os.environ.get("KV_TRANSPORT") == "r9":
         return r9_main(rank, world, lr, dev)
+    if os.environ.get("KV_TRANSPORT") == "shared":
+        return shared_main(rank, world, lr, dev)
     N, S = world, 4
     cfg = configs.scaled(configs.C1, pipelines=N, num_blocks=96, max_reqs=12,
                          max_blocks_per_req=12, batch_cap=6, n_requests=60, n_steps=30,
@@ -158,6 +160,81 @@ def main():
             if not np.array_equal(got, want):
                 print(f"rank {rank}: remote restore content mismatch for {r}", flush=True)
                 ok = 0
+    okt = torch.tensor([ok], device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    rt.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_PARITY_OK" if int(okt) == 1 else "MGPU_PARITY_FAIL", flush=True)
+    sys.exit(0 if int(okt) == 1 else 1)
+
+
+def shared_main(rank, world, lr, dev):
+    """NEXT-3 across GPUs (reading R17 with the holder on another rank): one 4-stage
+    pipeline, stage s on rank s mod N, so every successor is remote; pools small enough
+    that holders evict and drop replicas.  Each holder's rank keeps a mirror of its
+    predecessor (tables only, pool through NVLink) and PULLS the dirty slices into
+    blocks its own allocator picks.  Stage 1 fails at step 23 and is restored into a
+    fresh pool on its holder's rank.  Every step: whole pools, metadata, tables,
+    evictions, census == oracle on every rank, and every mirror's tables and
+    publication state (pub_len, drops) == the oracle's node."""
+    from kvgen import configs
+    from kvgen.content import CONTENT_SEED
+    from kvgen.cuda import content_tokens_cuda
+    from kvgen.schedule import closed_loop_schedule
+    from oracle.simulate import OracleRing
+    from paper_2601_22438_b200.runtime import RingRuntime, ScheduleDriver
+    from gpu_harness import compare_mirrors, compare_state
+    cfg = configs.scaled(configs.C1, num_blocks=32, max_reqs=12, max_blocks_per_req=12,
+                         batch_cap=5, n_requests=60, n_steps=40, fixed_prompt=None,
+                         pipelines=1, fail_node=(0, 1), fail_step=23)
+    rng = np.random.default_rng(0)
+    sched = [closed_loop_schedule(rng.integers(1, 70, size=cfg.n_requests),
+                                  rng.integers(1, 30, size=cfg.n_requests), cfg.n_steps,
+                                  cfg.batch_cap, pipeline=0)]
+    S = cfg.stages
+    coords = {(0, s): s for s in range(S)}
+    placement = {s: s % world for s in range(S)}
+    succ = {s: (s + 1) % S for s in range(S)}
+    rt = RingRuntime(cfg.geom, cfg.num_blocks, cfg.max_reqs, cfg.max_blocks_per_req, placement,
+                     succ, rank=rank, world=world, device=lr, spares=1, group=dist.group.WORLD,
+                     shared=True)
+    g = cfg.geom
+
+    def content(stage, ids, pos):
+        return content_tokens_cuda(CONTENT_SEED, ids, pos, stage * g.layers, g.layers,
+                                   g.kv_heads, g.head_dim, device=lr)
+
+    drv = ScheduleDriver(rt, sched, coords, content, restore_mode="fresh")
+    oring = OracleRing(cfg, schedules=sched, restore_mode="fresh", shared=True)
+    ok, mirrors_checked = 1, 0
+    try:
+        for t in range(cfg.n_steps):
+            drv.append_step(t)
+            oring.appends(t)
+            if t == cfg.fail_step:
+                drv.fail_and_restore(t, cfg.fail_node)
+                oring.fail_and_restore(t, cfg.fail_node)
+            torch.cuda.synchronize(dev)
+            dist.barrier()       # every owner's appends are in its HBM before a holder pulls
+            if t >= 1:
+                rt.replicate_all(t)
+                oring.replicate(t)
+            torch.cuda.synchronize(dev)
+            dist.barrier()       # pulls complete before an owner reuses freed blocks (R7)
+            compare_state(rt, drv, oring, tag=f"rank {rank} shared step {t}")
+            mirrors_checked += compare_mirrors(rt, drv, oring, tag=f"rank {rank} step {t}")
+            dist.barrier()
+        ev = sum(n.evictions for n in oring.all_nodes())
+        dr = sum(n.drops for n in oring.all_nodes())
+        print(f"shared rank {rank}: {mirrors_checked} mirror checks, oracle evictions {ev}, "
+              f"drops {dr}, mirrors {sorted(rt.mirrors)}", flush=True)
+        if ev == 0 or dr == 0 or mirrors_checked == 0:
+            ok = 0
+    except AssertionError as e:
+        print(f"rank {rank}: {e}", flush=True)
+        ok = 0
     okt = torch.tensor([ok], device=dev)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     rt.destroy()
