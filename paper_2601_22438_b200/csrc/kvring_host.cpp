@@ -232,7 +232,7 @@ struct DeviceCtx {
   // same stream acquires its final count
   cudaStream_t last_stream = nullptr;
   unsigned long long *last_counter = nullptr;
-  unsigned long long last_final = 0;
+  unsigned long long last_final = 0;   // arrival target of the last launch
   // seqs of the last launch if it deferred its publication (kvring_internal.h): the next
   // launch on pend_stream stores them from its publisher CTA
   int n_pend_pub = 0;
@@ -1655,7 +1655,8 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
   const unsigned long long chunks = ((unsigned long long)h.app_slices + rep_slices)
                                     << h.g.cps_shift;
   const int cap = step_resident_ctas(S.device, step_smem_bytes(h));
-  int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + 1023) / 1024));
+  const unsigned long long per = (unsigned long long)step_chunks_per_cta();
+  int grid = (int)std::min<unsigned long long>(cap, std::max(1ull, (chunks + per - 1) / per));
   // a deferred publication of the previous launch: one more CTA stores its seqs
   h.n_prev = 0;
   if (ctx->n_pend_pub > 0) {
@@ -1712,7 +1713,7 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
   }
   ctx->last_stream = st;
   ctx->last_counter = h.counter;
-  ctx->last_final = h.target + 1;
+  ctx->last_final = h.target;             // its arrival target (kvring_internal.h)
   h.done = ctx->done_dev + 8 * slot;      // 64-B apart in pinned memory
   h.nonce = nonce;
   db->used = nonce;

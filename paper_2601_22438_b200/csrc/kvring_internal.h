@@ -196,7 +196,8 @@ struct alignas(16) KvStepHdr {
   unsigned long long *prev_seq[kStepPools];
   unsigned long long prev_step[kStepPools];
   unsigned long long *prev_counter; // chain: the previous launch's counter ...
-  unsigned long long prev_target;   // ... and its final value (every CTA arrived, seq stored)
+  unsigned long long prev_target;   // ... and its arrival target (every CTA arrived: its data
+                                    // is complete; + 1 once its seqs are stored)
   KvGeomDev g;
   KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)
   KvDiv div_b;                      // block size
@@ -209,6 +210,7 @@ struct alignas(16) KvStepHdr {
 // dependent launch (the previous kernel on the stream may still be draining).
 cudaError_t launch_step(const KvStepHdr &h, int grid, cudaStream_t stream, bool pdl);
 int step_smem_bytes(const KvStepHdr &h);
+int step_chunks_per_cta();
 const void *step_kernel_fn();
 int step_resident_ctas(int device, int smem);
 

@@ -462,6 +462,16 @@ __device__ __forceinline__ void step_complete(const KvStepHdr &h) {
         asm volatile("fence.acq_rel.sys;" ::: "memory");
       else
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      // this launch's seqs, and its final count, follow the previous launch's (same
+      // seq locations; the next launch's seqs follow ours through our final count)
+      if (h.chain) {
+        unsigned long long v;
+        for (long long spin = 0;; ++spin) {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.prev_counter) : "memory");
+          if (v > h.prev_target) break;
+          if (spin > (1ll << 24)) __trap();
+        }
+      }
       if (h.publish && !h.defer)
         for (int q = 0; q < h.n_rep; ++q) {
           const KvStepPool &pp = h.rep[q];
@@ -629,9 +639,10 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   // every read below may touch data the previous step's grid wrote (its appends, its
   // device block-table entries, its seq): wait for it.  A chained launch (the previous
   // kernel on the stream is this library's previous step launch, nothing else between)
-  // acquires that launch's final count -- reached once every CTA arrived and its seq
-  // stores were made -- which returns ~2-3 us before griddepcontrol.wait would (that
-  // waits for the whole grid to retire and flush).  No deadlock: a programmatic
+  // acquires that launch's arrival count -- reached once every CTA's data is complete
+  // (each CTA arrives with a release) -- which returns ~3 us before griddepcontrol.wait
+  // would (that waits for the whole grid to retire and flush); only this launch's seq
+  // stores also wait for the previous launch's seqs (its final count, step_complete).  No deadlock: a programmatic
   // dependent grid starts only after every CTA of the previous grid has started.
 #ifdef KV_AB_NOCHAIN  // A/B builds (tools/ab_bench.sh): always griddepcontrol.wait
   if (false) {
@@ -763,6 +774,15 @@ int step_resident_ctas(int device, int smem) {
   cache_smem = smem;
   cache_val = sms * per;
   return cache_val;
+}
+
+// 16-B chunks per CTA the host sizes a launch's grid for (at most every resident CTA).
+int step_chunks_per_cta() {
+#ifdef KV_AB_CHUNKS  // A/B builds (tools/ab_bench.sh)
+  return KV_AB_CHUNKS;
+#else
+  return 1024;
+#endif
 }
 
 int step_smem_bytes(const KvStepHdr &h) {
