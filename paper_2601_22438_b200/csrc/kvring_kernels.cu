@@ -229,36 +229,64 @@ __device__ __noinline__ void publish_pass(const KvTask *__restrict__ tasks, int 
 // CUTLASS's semaphore, so no per-thread fences.  The CTA whose RMW completes a
 // pool's count stores that pool's seq with a release store (last-CTA
 // pattern): readers that acquire seq = t see all of step t.
-template <int SRC, int DST, bool PUB>
+template <int SRC, int DST, bool PUB, bool DYN>
 __device__ __forceinline__ void run_tasks(const KvTask *__restrict__ tasks, int n_tasks,
                                           const KvPoolParams *__restrict__ params,
                                           const KvGeomDev &g, int n_pools) {
   // pass 1: the copies -- identical for every kernel, no publication state live.
-  for (int u = blockIdx.x; u < n_tasks; u += gridDim.x) {
-    const KvTask tk = tasks[u];
-    const KvPoolParams &pp = params[tk.pool];
+  if constexpr (PUB || !DYN) {
+    // the ring-put's publication counts each task on the CTA that copied it (task u on
+    // CTA u mod G): static grid-stride (gather-pack too: measured no faster dynamic)
+    for (int u = blockIdx.x; u < n_tasks; u += gridDim.x) {
+      const KvTask tk = tasks[u];
+      const KvPoolParams &pp = params[tk.pool];
 #ifdef KV_BOUNDS_CHECK
-    const unsigned long long sbytes = pp.src_bytes, dbytes = pp.dst_bytes;
+      const unsigned long long sbytes = pp.src_bytes, dbytes = pp.dst_bytes;
 #else
-    const unsigned long long sbytes = 0, dbytes = 0;
+      const unsigned long long sbytes = 0, dbytes = 0;
 #endif
-    copy_task<SRC, DST>(tk, pp.src, pp.dst, g, sbytes, dbytes);
+      copy_task<SRC, DST>(tk, pp.src, pp.dst, g, sbytes, dbytes);
+    }
+    if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools);
+  } else {
+    // restore: the first task of every CTA static, the rest handed out by a
+    // counter in the launch's staged parameters (zero as staged): SMs do not move bytes
+    // at the same rate, so a static split leaves the slowest CTAs finishing alone.  The
+    // next draw is issued before the current task's copy, so its latency hides.
+    __shared__ int s_next;
+    unsigned int *ctr = reinterpret_cast<unsigned int *>(
+        const_cast<int32_t *>(&params[0].pad0));
+    for (int u = blockIdx.x; u < n_tasks;) {
+      unsigned int nx = 0;
+      if (threadIdx.x == 0) nx = atomicAdd(ctr, 1u);
+      const KvTask tk = tasks[u];
+      const KvPoolParams &pp = params[tk.pool];
+#ifdef KV_BOUNDS_CHECK
+      const unsigned long long sbytes = pp.src_bytes, dbytes = pp.dst_bytes;
+#else
+      const unsigned long long sbytes = 0, dbytes = 0;
+#endif
+      copy_task<SRC, DST>(tk, pp.src, pp.dst, g, sbytes, dbytes);
+      if (threadIdx.x == 0) s_next = (int)gridDim.x + (int)nx;
+      __syncthreads();
+      u = s_next;
+      __syncthreads();  // before thread 0 writes the next draw
+    }
   }
-  if constexpr (PUB) publish_pass(tasks, n_tasks, params, n_pools);
 }
 
 // One named kernel per role (ncu / launch lists show what ran).
-#define KV_KERNEL(NAME, SRC, DST, PUB)                                                   \
+#define KV_KERNEL(NAME, SRC, DST, PUB, DYN)                                              \
   __global__ void __launch_bounds__(kThreads, kMinBlocks)                                \
       NAME(const KvTask *__restrict__ tasks, int n_tasks,                                \
            const KvPoolParams *__restrict__ params, KvGeomDev g, int n_pools) {          \
-    run_tasks<SRC, DST, PUB>(tasks, n_tasks, params, g, n_pools);                        \
+    run_tasks<SRC, DST, PUB, DYN>(tasks, n_tasks, params, g, n_pools);                   \
   }
-KV_KERNEL(kv_restore_remap_kernel, kPaged, kPaged, false)      // a8: replica -> new block ids
-KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false)       // a4: NCCL-variant sender
+KV_KERNEL(kv_restore_remap_kernel, kPaged, kPaged, false, true)   // a8: replica -> new block ids
+KV_KERNEL(kv_gather_pack_kernel, kPaged, kPacked, false, false)   // a4: NCCL-variant sender
 // host-task ring-put: shared-capacity links (replica blocks at holder-allocated ids)
 // and the copy-engine variant's partial blocks + publication
-KV_KERNEL(kv_ring_put_kernel, kPaged, kPaged, true)
+KV_KERNEL(kv_ring_put_kernel, kPaged, kPaged, true, false)
 #undef KV_KERNEL
 
 // Receiver of the NCCL comparison: parameters come from the packed header on
