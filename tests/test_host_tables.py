@@ -328,3 +328,27 @@ def test_decode_loop_argument_errors():
         l2.destroy()
         K.kv_pool_destroy(a)
         K.kv_pool_destroy(b)
+
+
+def test_last_alloc_and_mirror_arguments():
+    """kv_last_alloc lists the block ids the last append allocated, in allocation order
+    (what an owner forwards to a remote holder's mirror, NEXT-3 across GPUs); a mirror
+    needs a device and an unused pool; kv_mirror_blocks only takes a mirror."""
+    cfg = configs.scaled(configs.C1, num_blocks=16, max_reqs=4, max_blocks_per_req=8)
+    h = _pool(cfg, 0)
+    try:
+        K.kv_append(h, [1, 2], [20, 40], None)                  # 2 + 3 blocks, lowest first
+        assert K.kv_last_alloc(h) == [0, 1, 2, 3, 4]
+        assert K.kv_query(h, 1)[1] + K.kv_query(h, 2)[1] == [0, 1, 2, 3, 4]
+        K.kv_append(h, [1, 2], [13, 1], None)                   # 20+13 = 33 -> one more block
+        assert K.kv_last_alloc(h) == [5]
+        K.kv_append(h, [2], [1], None)                          # no new block
+        assert K.kv_last_alloc(h) == []
+        with pytest.raises(K.KvError) as e:
+            K.kv_pool_set_mirror(h, True)                        # tables-only pool: no device
+        assert e.value.code == K.KV_EINVAL
+        with pytest.raises(K.KvError) as e:
+            K.kv_mirror_blocks(h, [1, 2])                        # not a mirror
+        assert e.value.code == K.KV_EINVAL
+    finally:
+        K.kv_pool_destroy(h)
