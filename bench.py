@@ -441,10 +441,15 @@ def run_kvring(args):
     mx, sm = reduce_max_sum([rec["ms"], rec["bytes"], float(rec["launches"])], dev, world)
     ms_max, tot_bytes, tot_launch = mx[0], sm[1], sm[2]
     roof = timed_roofline(rec, N, hbm_peak, peak_src)
-    traffic = traffic_ref("decode_population", "kv_step_kernel")
+    # the committed ncu capture is of this command at N = 1 (ncu replays one process);
+    # at N > 1 the launches differ (peer stores, fewer stages per GPU): not captured
+    traffic = traffic_ref("decode_population", "kv_step_kernel") if N == 1 else None
     roof["traffic"] = traffic["traffic"] if traffic else None
     if traffic:
         roof["traffic_note"] = traffic.get("note")
+    elif N > 1:
+        roof["traffic_note"] = ("no ncu capture at N > 1 (ncu profiles one process; the "
+                                "1-GPU capture's population differs)")
 
     # ---- the same loop, every launch timed alone (events serialise the launches) -------
     inst = timed_loop(args, K, kl, drv, rt, t, comp, content, dev, world, instrument=True)
@@ -1330,13 +1335,21 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
     us = [a.elapsed_time(b) * 1e3 for a, b in evs]
     us_n = [a.elapsed_time(b) * 1e3 for a, b in evn]
     ring.destroy()
-    mx, sm = reduce_max_sum([ms, float(by), wall], dev, world)
-    ms, by, wall = mx[0], sm[1], mx[2]
+    busy_ms = sum(us) * 1e-3          # device time of pack .. unpack, summed over the steps
+    mx, sm = reduce_max_sum([ms, float(by), wall, busy_ms], dev, world)
+    ms, by, wall, busy_ms = mx[0], sm[1], mx[2], mx[3]
     return {"transport": "NCCL 2.28 grouped ncclSend/ncclRecv (libkvnccl): pack, host count "
                          "exchange (gloo, N > 1), send/recv, unpack"
                          + (" -- one rank sending to itself" if world == 1 else ""),
-            "value": round(by / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "steps": n,
-            "ms_per_step": round(ms / n, 4), "wall_ms_per_step": round(wall / n * 1e3, 4),
+            "value": round(by / (busy_ms * 1e-3) / 1e9, 2), "unit": UNIT, "steps": n,
+            "what": "replicated bytes / device time of the replication (CUDA events around "
+                    "pack .. unpack of every step, summed; max over ranks)",
+            "ms_per_step": round(busy_ms / n, 4),
+            "loop": {"value": round(by / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms / n, 4),
+                     "wall_ms_per_step": round(wall / n * 1e3, 4),
+                     "what": "the whole Python loop on the device clock: the per-step host "
+                             "work (append planning in Python, pack bookkeeping, the gloo "
+                             "size exchange) leaves the GPU idle between steps"},
             "step_us": {"median": round(statistics.median(us), 2),
                         "p99": round(float(np.percentile(us, 99)), 2),
                         "what": "pack + count exchange + NCCL group + unpack"},

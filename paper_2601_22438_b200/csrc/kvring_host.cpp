@@ -233,6 +233,11 @@ struct DeviceCtx {
   cudaStream_t last_stream = nullptr;
   unsigned long long *last_counter = nullptr;
   unsigned long long last_final = 0;   // arrival target of the last launch
+  // whether the last launch was chained, and its predecessor's counter / arrival target
+  // (an early-started launch waits for that one before any copy: kvring_internal.h)
+  bool last_chained = false;
+  unsigned long long *last_prev_counter = nullptr;
+  unsigned long long last_prev_final = 0;
   // seqs of the last launch if it deferred its publication (kvring_internal.h): the next
   // launch on pend_stream stores them from its publisher CTA
   int n_pend_pub = 0;
@@ -329,6 +334,33 @@ struct DeviceCtx {
     CU(cudaEventRecord(b->ev, s));
     b->pending = true;
     return KV_OK;
+  }
+  // kv_restore's device scratch for the holder's metadata (kept: a failover must not
+  // cudaMalloc / cudaFree -- cudaFree synchronises the whole device)
+  char *meta_scratch = nullptr;
+  size_t meta_scratch_cap = 0;
+  int reserve_meta_scratch(size_t bytes) {
+    if (meta_scratch_cap >= bytes) return KV_OK;
+    if (meta_scratch) cudaFree(meta_scratch);
+    meta_scratch = nullptr;
+    meta_scratch_cap = 0;
+    CU(cudaMalloc(reinterpret_cast<void **>(&meta_scratch), bytes));
+    meta_scratch_cap = bytes;
+    return KV_OK;
+  }
+  // Setup-time reservation (kv_pool_create): the staging ring the host-task kernels
+  // (restore, ring-put) use and the restore scratch, so their first use on a failover
+  // path does not pin / allocate memory (cudaHostAlloc of the ring costs ~100 ms)
+  int reserve(size_t meta_bytes_needed) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (ring[0].cap < cap_hint) {
+      StageBuf *b = nullptr;
+      int save = next;
+      int rc = acquire(ring, next, cap_hint, true, &b);
+      next = save;
+      if (rc) return rc;
+    }
+    return reserve_meta_scratch(meta_bytes_needed);
   }
 };
 
@@ -912,7 +944,8 @@ KV_API int kv_pool_create(const kv_pool_desc_t *d, kv_pool_t **out) {
     g_launches++;
     p->kernels++;
     CU(cudaDeviceSynchronize());
-    ctx_for(p->device);
+    rc = ctx_for(p->device)->reserve(meta_bytes(p->R, p->M));
+    if (rc) return rc;
   }
   *out = p.release();
   return KV_OK;
@@ -1411,8 +1444,13 @@ void step_add_append(StepLaunch &S, kv_pool *p, const kv_append_args_t &a) {
   pp.R = p->R;
   pp.M = p->M;
   pp.abort_slices = -1;
+  const size_t i0 = S.items.size();
   long long rows = do_append(p, a, (int16_t)q, S.items, S.h.app_slices);
   S.app_bytes += (uint64_t)rows * p->token_bytes;
+  // blocks freed one step ago: the previous launch's publication may still read them
+  // while an early-started launch appends (kItemGated)
+  for (size_t i = i0; i < S.items.size(); ++i)
+    if (p->freed_at[S.items[i].blk] >= p->epoch - 1) S.items[i].blk |= kItemGated;
   if ((a.flags & KV_SRC_HOST) && rows > 0) {
     S.host_src[q] = a.src_kv;
     S.host_src_bytes[q] = (size_t)rows * p->token_bytes;
@@ -1650,6 +1688,7 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
     std::memcpy(b + h.blk0_off, S.blk0.data(), 4 * nent);
   }
   h.pdl = S.pdl ? 1 : 0;
+  h.app_first = h.sys_any ? 0 : 1;  // round order (kvring_step.cu copy_all)
   // grid: enough CTAs for ~1024 16-B chunks each, at most every resident CTA
   const uint64_t rep_slices = with_rep ? S.rep_bytes / (uint64_t)h.g.seg_bytes : 0;
   const unsigned long long chunks = ((unsigned long long)h.app_slices + rep_slices)
@@ -1706,11 +1745,22 @@ int step_launch_one(StepLaunch &S, size_t i0, size_t i1, bool with_rep, bool cha
   h.target = db->arrivals + (unsigned long long)grid;
   db->arrivals = h.target + 1;            // + the final count after the seq stores
   h.chain = 0;
+  h.early = 0;
   if (chain && S.pdl && ctx->last_counter && ctx->last_stream == st) {
     h.chain = 1;
     h.prev_counter = ctx->last_counter;
     h.prev_target = ctx->last_final;
+    // early start (kvring_internal.h) when the launch before the previous one is ours as
+    // well -- not over NVLink, where it measured neutral to -1.5 % (profiles/r02/ab)
+    if (ctx->last_chained && !h.sys_any) {
+      h.early = 1;
+      h.pp_counter = ctx->last_prev_counter;
+      h.pp_target = ctx->last_prev_final;
+    }
   }
+  ctx->last_chained = h.chain != 0;
+  ctx->last_prev_counter = h.prev_counter;
+  ctx->last_prev_final = h.prev_target;
   ctx->last_stream = st;
   ctx->last_counter = h.counter;
   ctx->last_final = h.target;             // its arrival target (kvring_internal.h)
@@ -1915,12 +1965,11 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
   //    device scratch that is read back -- first the 32-B header (shape check), then
   //    the whole region.  Synchronous: restore needs the tables on the host.
   std::vector<char> meta(meta_bytes(R, M));
-  char *scratch = nullptr;
-  CU(cudaMalloc(reinterpret_cast<void **>(&scratch), meta.size()));
-  struct Free {
-    char *p;
-    ~Free() { cudaFree(p); }
-  } free_scratch{scratch};
+  DeviceCtx *ctx = ctx_for(dst->device);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  int rc = ctx->reserve_meta_scratch(meta.size());
+  if (rc) return rc;
+  char *scratch = ctx->meta_scratch;
   uint64_t seq;
   int32_t hdr[4];
   CU(launch_meta_acquire(static_cast<const char *>(holder_meta), scratch, 32, st));
@@ -1989,19 +2038,10 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
                 dst->task_segs);
     }
   }
-  // the device-resident block table of dst (read by the step engine's publications)
+  // 3. one pinned staging buffer: [params][remap tasks][dst's device block table rows]
+  //    -> one H2D; then copy valid slots (local HBM, or NVLink reads when the holder is
+  //    remote).  The device-resident block table is read by the step engine's publications.
   {
-    std::vector<int32_t> rows((size_t)R * M, -1);
-    for (int s = 0; s < dst->slot_hi; ++s)
-      for (size_t j = 0; j < dst->slot_bt[s].size(); ++j) rows[(size_t)s * M + j] = dst->slot_bt[s][j];
-    CU(cudaMemcpyAsync(dst->d_bt, rows.data(), rows.size() * sizeof(int32_t),
-                       cudaMemcpyHostToDevice, st));
-    CU(cudaStreamSynchronize(st));  // `rows` is pageable host memory on the stack
-  }
-  // 3. copy valid slots (local HBM, or NVLink reads when the holder is remote).
-  if (!tasks.empty()) {
-    DeviceCtx *ctx = ctx_for(dst->device);
-    std::lock_guard<std::mutex> lk(ctx->mu);
     KvPoolParams pp;
     std::memset(&pp, 0, sizeof pp);
     pp.src = static_cast<const char *>(holder_replica);
@@ -2009,17 +2049,25 @@ KV_API int kv_restore(kv_pool_t *dst, const void *holder_replica, int32_t holder
     pp.src_bytes = (unsigned long long)holder_replica_blocks * dst->block_bytes;
     pp.dst_bytes = (unsigned long long)dst->NB * dst->block_bytes;
     const size_t pbytes = sizeof pp, tbytes = sizeof(KvTask) * tasks.size();
+    const size_t roff = (pbytes + tbytes + 15) & ~(size_t)15, rbytes = sizeof(int32_t) * (size_t)R * M;
     StageBuf *b = nullptr;
-    int rc = ctx->acquire(ctx->ring, ctx->next, pbytes + tbytes, true, &b);
+    rc = ctx->acquire(ctx->ring, ctx->next, roff + rbytes, true, &b);
     if (rc) return rc;
     std::memcpy(b->host, &pp, pbytes);
-    std::memcpy(b->host + pbytes, tasks.data(), tbytes);
-    CU(cudaMemcpyAsync(b->dev, b->host, pbytes + tbytes, cudaMemcpyHostToDevice, st));
-    CU(timed_launch(kKindRestore, reinterpret_cast<const KvTask *>(b->dev + pbytes),
-                   (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), 1,
-                   dst->geom_dev(), copy_grid(dst->device, (int)tasks.size()), st));
-    g_launches++;
-    dst->kernels++;
+    if (tbytes) std::memcpy(b->host + pbytes, tasks.data(), tbytes);
+    int32_t *rows = reinterpret_cast<int32_t *>(b->host + roff);
+    std::fill(rows, rows + (size_t)R * M, -1);
+    for (int s = 0; s < dst->slot_hi; ++s)
+      for (size_t j = 0; j < dst->slot_bt[s].size(); ++j) rows[(size_t)s * M + j] = dst->slot_bt[s][j];
+    CU(cudaMemcpyAsync(b->dev, b->host, roff + rbytes, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dst->d_bt, b->dev + roff, rbytes, cudaMemcpyDeviceToDevice, st));
+    if (!tasks.empty()) {
+      CU(timed_launch(kKindRestore, reinterpret_cast<const KvTask *>(b->dev + pbytes),
+                     (int)tasks.size(), reinterpret_cast<const KvPoolParams *>(b->dev), 1,
+                     dst->geom_dev(), copy_grid(dst->device, (int)tasks.size()), st));
+      g_launches++;
+      dst->kernels++;
+    }
     rc = ctx->done(b, st);
     if (rc) return rc;
   }

@@ -138,6 +138,11 @@ struct alignas(8) KvAppItem {
   int16_t pool;   // index into KvStepHdr::app
 };
 static_assert(sizeof(KvAppItem) == 24, "KvAppItem must be 24 B");
+// KvAppItem::blk | kItemGated: the block was freed one step ago, so the previous launch's
+// publication may still be reading it -- an early-started launch copies into it only
+// after that launch's arrival count (KvStepHdr::early)
+constexpr int32_t kItemGated = 1 << 30;
+constexpr int32_t kItemBlkMask = kItemGated - 1;
 
 struct alignas(16) KvStepPool {
   const char *src;        // append: dense source; replicate: this pool
@@ -191,13 +196,24 @@ struct alignas(16) KvStepHdr {
   int32_t defer;
   int32_t n_prev;
   int32_t prev_sys;                 // bit q: prev_seq[q] is in a peer's memory
-  int32_t pad2;
+  // early start of a chained launch whose predecessor was chained too: the launch before
+  // the previous one (pp_counter) has arrived before any copy; the append rounds then go
+  // at once -- except items into blocks freed one step ago (kItemGated) -- while the
+  // previous launch drains, and a warp acquires the previous launch's arrival count
+  // (prev_counter) before its first publication round / gated item; every CTA before
+  // its tables (they read and write the device block table the previous launch used)
+  int32_t early;
+  int32_t app_first;                // append rounds before publication rounds (no NVLink
+                                    // successor), else interleaved (kvring_step.cu copy_all)
+  int32_t pad3;
   unsigned long long *gate;
   unsigned long long *prev_seq[kStepPools];
   unsigned long long prev_step[kStepPools];
   unsigned long long *prev_counter; // chain: the previous launch's counter ...
   unsigned long long prev_target;   // ... and its arrival target (every CTA arrived: its data
                                     // is complete; + 1 once its seqs are stored)
+  unsigned long long *pp_counter;   // early: the launch before the previous one ...
+  unsigned long long pp_target;     // ... and its arrival target
   KvGeomDev g;
   KvDiv div_sl;                     // slices per token (layers x 2 x kv_heads)
   KvDiv div_b;                      // block size

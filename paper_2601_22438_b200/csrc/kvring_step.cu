@@ -157,6 +157,7 @@ struct Cursor {
   bool in_rep = false;        // idx is a publication entry
   bool gated = false;         // the piece's block holds no previously published token and
                               // the entry's new blocks include one freed one step ago
+  bool agated = false;        // append item into a block freed one step ago (kItemGated)
   __device__ Cursor(const KvStepHdr &h_, const StepSmem &s_) : h(h_), s(s_) {}
 
   __device__ __forceinline__ void locate(int x, uint32_t d) {
@@ -173,6 +174,7 @@ struct Cursor {
       in_rep = false;
       gated = false;
       const KvAppItem &it = items[a];
+      agated = (it.blk & kItemGated) != 0;
       pb = a + 1 < h.n_items ? items[a + 1].off : h.app_slices;
       lim = 0x7fffffff;
       const uint32_t r = (uint32_t)(x - it.off);
@@ -187,7 +189,7 @@ struct Cursor {
       d_out = seg;
       sp = pp.src + (long long)it.row * h.g.token_bytes + (long long)(in * s_in) +
            (long long)out * s_out;
-      dp = pp.dst + (long long)it.blk * h.g.block_bytes +
+      dp = pp.dst + (long long)(it.blk & kItemBlkMask) * h.g.block_bytes +
            (long long)(it.p0 - j * B) * seg + (long long)(in * d_in) + (long long)out * d_out;
     } else {
       const int xr = x - h.app_slices;
@@ -200,6 +202,7 @@ struct Cursor {
         idx = a;
         in_rep = true;
       }
+      agated = false;
       const int e = idx;
       const int q = rep_pool_of(h, e);
       const KvStepPool &pp = h.rep[q];
@@ -286,8 +289,30 @@ __device__ __forceinline__ void wait_gate(const KvStepHdr &h) {
   }
 }
 
+// Waits (one thread) until a launch's completion counter reached `target` (bounded).
+__device__ __forceinline__ void wait_count(const unsigned long long *c, unsigned long long target) {
+  unsigned long long v;
+  for (long long spin = 0;; ++spin) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+    if (v >= target) break;
+    if (spin > (1ll << 24)) __trap();  // that launch never completed
+    if (spin > 64) __nanosleep(32);
+  }
+}
+
+// A warp of an early-started launch that has not yet seen the previous launch arrive
+// (wait_prev) acquires its arrival count before the loads of a publication round or of an
+// append item into a block freed one step ago.
+__device__ __forceinline__ void warp_wait_prev(const KvStepHdr &h, int lane, bool &wait_prev) {
+  if (lane == 0) wait_count(h.prev_counter, h.prev_target);
+  __syncwarp();
+  wait_prev = false;
+}
+
 __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs, uint32_t d,
-                                           uint32_t lc, Cursor &cur, bool &gate_shut) {
+                                           uint32_t lc, Cursor &cur, bool &gate_shut,
+                                           bool pub_round, bool &wait_prev) {
+  if (wait_prev && pub_round) warp_wait_prev(cur.h, lane, wait_prev);
   {
     int x = base + (lane >> cs);                // this lane's slice
     while (__any_sync(0xffffffffu, x < rend)) {
@@ -302,6 +327,8 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
           n = 0;
         }
       }
+      if (wait_prev && __any_sync(0xffffffffu, n > 0 && cur.agated))
+        warp_wait_prev(cur.h, lane, wait_prev);
       char *const dp0 = cur.dp;
       const uint32_t in0 = cur.in;
       uint4 v[kU];
@@ -341,13 +368,18 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
 }
 
 //
-// Append rounds and publication rounds are interleaved in proportion (round r is a
-// publication round iff floor((r+1) f) > floor(r f), f = Rp / R in 32.32 fixed point,
-// rounded up so that exactly Rp of the R rounds are): over NVLink the publication's
-// peer stores then run all through the launch instead of waiting for the appends
-// (2 GPUs: +7 % per step; in one GPU's HBM the order makes no measurable difference).
+// Round order.  Over NVLink (h.app_first = 0) append rounds and publication rounds are
+// interleaved in proportion (round r is a publication round iff floor((r+1) f) >
+// floor(r f), f = Rp / R in 32.32 fixed point, rounded up so that exactly Rp of the R
+// rounds are): the publication's peer stores then run all through the launch instead of
+// waiting for the appends (2 GPUs: +7 % per step, and 0.68 vs 0.65 of NVLink against
+// appends first with the early start).  In one GPU's HBM (app_first = 1) the append
+// rounds come first: with the early start (wait_prev) the warps that become resident
+// while the previous launch drains take append rounds, which need nothing from it
+// (+1.5 % per step against interleaved, which loses 2 %: its early warps stall on the
+// previous launch's arrival before their publication rounds).
 __device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const KvGeomDev &g,
-                                         unsigned int *work) {
+                                         unsigned int *work, bool wait_prev, bool app_first) {
   const int lane = threadIdx.x & 31;
   const int gw = (int)blockIdx.x * kWarps + (int)(threadIdx.x >> 5);
   const int W = G * kWarps;
@@ -390,15 +422,17 @@ __device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const
       drawn = true;
     }
     int b0, b1;
-    const unsigned int pr = (unsigned int)(((unsigned long long)r * f) >> 32);
-    if ((unsigned int)(((unsigned long long)(r + 1) * f) >> 32) > pr) {  // publication round pr
-      b0 = A + (int)pr * span;
-      b1 = min(A + P, b0 + span);
-    } else {                                                           // append round r - pr
-      b0 = (r - (int)pr) * span;
-      b1 = min(A, b0 + span);
+    bool pub;
+    if (app_first) {                            // append rounds first, then the publication's
+      pub = r >= Ra;
+      b0 = pub ? A + (r - Ra) * span : r * span;
+    } else {
+      const unsigned int pr = (unsigned int)(((unsigned long long)r * f) >> 32);
+      pub = (unsigned int)(((unsigned long long)(r + 1) * f) >> 32) > pr;
+      b0 = pub ? A + (int)pr * span : (r - (int)pr) * span;  // publication round pr / append r - pr
     }
-    copy_round(b0, b1, lane, cs, d, lc, cur, gate_shut);
+    b1 = pub ? min(A + P, b0 + span) : min(A, b0 + span);
+    copy_round(b0, b1, lane, cs, d, lc, cur, gate_shut, pub, wait_prev);
     r = r < Rs ? r + W : 0x7fffffff;
   }
 }
@@ -644,20 +678,25 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   // would (that waits for the whole grid to retire and flush); only this launch's seq
   // stores also wait for the previous launch's seqs (its final count, step_complete).  No deadlock: a programmatic
   // dependent grid starts only after every CTA of the previous grid has started.
-#ifdef KV_AB_NOCHAIN  // A/B builds (tools/ab_bench.sh): always griddepcontrol.wait
-  if (false) {
+  //
+  // Early start (h.early: the previous launch was chained too, so the one before it is
+  // this library's launch as well): only that launch's arrival is awaited here -- the
+  // previous launch may still be copying.  Appends of this step touch neither its
+  // publication's reads (blocks of requests live when it was snapshotted: a block freed
+  // since then is flagged kItemGated and waited for) nor its appends (other tokens /
+  // blocks); so the append rounds start at once and fill the previous grid's tail, and a
+  // warp acquires the previous arrival count only before its first publication round or
+  // gated item (copy_round); every CTA does before its tables.
+#ifdef KV_AB_NOEARLY
+  const bool early = false;
 #else
-  if (h.chain) {
+  const bool early = h.chain && h.early;
 #endif
-    if (threadIdx.x == 0) {
-      unsigned long long v;
-      for (long long spin = 0;; ++spin) {
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.prev_counter) : "memory");
-        if (v >= h.prev_target) break;
-        if (spin > (1ll << 24)) __trap();  // the previous launch never completed
-        if (spin > 64) __nanosleep(32);
-      }
-    }
+  if (early) {
+    if (threadIdx.x == 0) wait_count(h.pp_counter, h.pp_target);
+    __syncthreads();
+  } else if (h.chain) {
+    if (threadIdx.x == 0) wait_count(h.prev_counter, h.prev_target);
     __syncthreads();
   } else if (h.pdl) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -667,17 +706,28 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   const uint32_t G = gridDim.x - (h.n_prev > 0 ? 1u : 0u), b = blockIdx.x;
   {
     Cursor cur(h, s);
-    copy_all(h.app_slices, P, (int)G, cur, h.g, h.work);
+    copy_all(h.app_slices, P, (int)G, cur, h.g, h.work, early, h.app_first != 0);
+  }
+  if (early) {  // the tables below read / write what the previous launch used
+    if (threadIdx.x == 0) wait_count(h.prev_counter, h.prev_target);
+    __syncthreads();
   }
   KV_STAMP(3);
   // 4. tables: the appended items' device bt entries; the publication's parity
   //    (req_id, len) table and the bt entries of the blocks it touched.  Readers trust
   //    none of it before seq = step (written below, after every CTA's release).
+  //    Entries are spread CTA-major (entry i on CTA i mod G): a decode step has a few
+  //    hundred of them, which would otherwise all sit on the first CTAs' threads after
+  //    their copies -- the launch's tail.
+#ifdef KV_AB_TBLPACK  // A/B builds: entries thread-major (the first CTAs take them all)
   const uint32_t gt = b * kThreads + threadIdx.x, stride = G * kThreads;
+#else
+  const uint32_t gt = threadIdx.x * G + b, stride = G * kThreads;
+#endif
   for (uint32_t i = gt; i < (uint32_t)h.n_items; i += stride) {
     const KvAppItem &it = s.items[i];
     const KvStepPool &pp = h.app[it.pool];
-    pp.bt[(size_t)it.slot * pp.M + fdiv((uint32_t)it.p0, h.div_b)] = it.blk;
+    pp.bt[(size_t)it.slot * pp.M + fdiv((uint32_t)it.p0, h.div_b)] = it.blk & kItemBlkMask;
   }
   if (h.publish) {
     if (h.n_prev > 0) {  // the tables may be listed by the last stored seq: wait for the newer one
