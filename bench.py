@@ -1290,6 +1290,9 @@ def run_shared(args, local_rank, dev):
     return out
 
 
+NCCL_WARMUP = 5
+
+
 def run_nccl(args, drv, rt, t0, comp, content, dev, world):
     """The paper's transport (NCCL send/recv, P:8 §3.3) on the same workload, as the
     measured comparison: per step append, then gather-pack, the packed sizes exchanged on
@@ -1317,11 +1320,21 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
            for _ in range(n)]
     evn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(n)]
+    # untimed warm-up steps: NCCL connects a peer pair on its first send/recv (~1 s at
+    # N = 2, which would otherwise sit inside the first timed step)
+    nw = min(NCCL_WARMUP, n - 1)
+    for k in range(nw):
+        tt = t0 + k
+        drv.append_step(tt, stream=comp, sources=srcs[tt], plan=plans[tt])
+        ring.step(tt, comp)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     b0 = {nd: K.kv_stats(rt.handle(nd))["bytes_replicated"] for nd in rt.alive_local()}
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     st.record(comp)
-    for k in range(n):
+    for k in range(nw, n):
         tt = t0 + k
         drv.append_step(tt, stream=comp, sources=srcs[tt], plan=plans[tt])
         evs[k][0].record(comp)
@@ -1332,8 +1345,9 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
     wall = time.perf_counter() - w0
     ms = st.elapsed_time(en)
     by = sum(K.kv_stats(rt.handle(nd))["bytes_replicated"] - b0[nd] for nd in rt.alive_local())
-    us = [a.elapsed_time(b) * 1e3 for a, b in evs]
-    us_n = [a.elapsed_time(b) * 1e3 for a, b in evn]
+    us = [a.elapsed_time(b) * 1e3 for a, b in evs[nw:]]
+    us_n = [a.elapsed_time(b) * 1e3 for a, b in evn[nw:]]
+    n -= nw
     ring.destroy()
     busy_ms = sum(us) * 1e-3          # device time of pack .. unpack, summed over the steps
     mx, sm = reduce_max_sum([ms, float(by), wall, busy_ms], dev, world)
@@ -1342,6 +1356,7 @@ def run_nccl(args, drv, rt, t0, comp, content, dev, world):
                          "exchange (gloo, N > 1), send/recv, unpack"
                          + (" -- one rank sending to itself" if world == 1 else ""),
             "value": round(by / (busy_ms * 1e-3) / 1e9, 2), "unit": UNIT, "steps": n,
+            "warmup_steps": nw,
             "what": "replicated bytes / device time of the replication (CUDA events around "
                     "pack .. unpack of every step, summed; max over ranks)",
             "ms_per_step": round(busy_ms / n, 4),
