@@ -25,6 +25,7 @@
 // blob (items and per-slot tables) is written by the host into pinned memory, pulled
 // across PCIe once by CTA 0 and shared with the other CTAs through device memory and a
 // release/acquire flag -- the per-step host cost is one launch.
+#include <cstdio>
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -34,6 +35,20 @@
 namespace kvring {
 
 namespace {
+
+// A bounded wait that ran out (a launch never completed: a bug, not a slow GPU) traps.
+// Debug builds (-DKV_TRAP_PRINT) say which wait first.
+#ifdef KV_TRAP_PRINT
+#define KV_TRAP(what, a, b)                                                            \
+  do {                                                                                 \
+    printf("kv_step_kernel trap: %s block %d thread %d: %llu vs %llu\n", what,        \
+           (int)blockIdx.x, (int)threadIdx.x, (unsigned long long)(a),                 \
+           (unsigned long long)(b));                                                   \
+    __trap();                                                                          \
+  } while (0)
+#else
+#define KV_TRAP(what, a, b) __trap()
+#endif
 
 constexpr int kThreads = 256;
 // 4 resident 256-thread CTAs per SM (32 warps: the address arithmetic of one warp hides
@@ -284,7 +299,7 @@ __device__ __forceinline__ void wait_gate(const KvStepHdr &h) {
   for (long long spin = 0;; ++spin) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.gate) : "memory");
     if (v == h.nonce) break;
-    if (spin > (1ll << 24)) __trap();
+    if (spin > (1ll << 24)) KV_TRAP("gate", v, h.nonce);
     if (spin > 16) __nanosleep(64);
   }
 }
@@ -295,7 +310,7 @@ __device__ __forceinline__ void wait_count(const unsigned long long *c, unsigned
   for (long long spin = 0;; ++spin) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
     if (v >= target) break;
-    if (spin > (1ll << 24)) __trap();  // that launch never completed
+    if (spin > (1ll << 24)) KV_TRAP("count", v, target);  // that launch never completed
     if (spin > 64) __nanosleep(32);
   }
 }
@@ -378,10 +393,11 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
 // while the previous launch drains take append rounds, which need nothing from it
 // (+1.5 % per step against interleaved, which loses 2 %: its early warps stall on the
 // previous launch's arrival before their publication rounds).
-__device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const KvGeomDev &g,
-                                         unsigned int *work, bool wait_prev, bool app_first) {
+__device__ __forceinline__ void copy_all(int A, int P, int G, int b, Cursor &cur,
+                                         const KvGeomDev &g, unsigned int *work, bool wait_prev,
+                                         bool app_first) {
   const int lane = threadIdx.x & 31;
-  const int gw = (int)blockIdx.x * kWarps + (int)(threadIdx.x >> 5);
+  const int gw = b * kWarps + (int)(threadIdx.x >> 5);
   const int W = G * kWarps;
   const int cs = g.cps_shift;
   const uint32_t d = 32u >> cs;                 // slices per warp iteration
@@ -426,6 +442,11 @@ __device__ __forceinline__ void copy_all(int A, int P, int G, Cursor &cur, const
     if (app_first) {                            // append rounds first, then the publication's
       pub = r >= Ra;
       b0 = pub ? A + (r - Ra) * span : r * span;
+#ifdef KV_AB_PUBFIRST  // A/B builds: over NVLink the publication's rounds first
+    } else if (true) {
+      pub = r < Rp;
+      b0 = pub ? A + r * span : (r - Rp) * span;
+#endif
     } else {
       const unsigned int pr = (unsigned int)(((unsigned long long)r * f) >> 32);
       pub = (unsigned int)(((unsigned long long)(r + 1) * f) >> 32) > pr;
@@ -503,7 +524,7 @@ __device__ __forceinline__ void step_complete(const KvStepHdr &h) {
         for (long long spin = 0;; ++spin) {
           asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.prev_counter) : "memory");
           if (v > h.prev_target) break;
-          if (spin > (1ll << 24)) __trap();
+          if (spin > (1ll << 24)) KV_TRAP("prev final", v, h.prev_target);
         }
       }
       if (h.publish && !h.defer)
@@ -535,10 +556,13 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   // programmatic dependent launch: the next step's grid may start its prologue as soon
   // as this grid's CTAs leave (a no-op for a normally serialised launch)
   if (h.pdl) asm volatile("griddepcontrol.launch_dependents;" :::);
-  // the publisher CTA of a launch following a deferred one (kvring_internal.h): wait for
-  // that launch to complete -- every one of its stores, peer stores included, performed
-  // -- then store its seqs; it moves no data and arrives like the others
-  if (h.n_prev > 0 && blockIdx.x == gridDim.x - 1) {
+  // the publisher CTA of a launch following a deferred one (kvring_internal.h) is CTA 0
+  // (CTA 1 pulls the descriptor): wait for that launch to complete -- every one of its
+  // stores, peer stores included, performed -- then store its seqs and open the gate; it
+  // moves no data and arrives like the others.  CTA 0 is dispatched first, so the copying
+  // CTAs that spin on the gate never hold the slot it needs (as the last CTA it could find
+  // every slot taken by them: a 2-GPU bench trapped in that wait 3 times in 5)
+  if (h.n_prev > 0 && blockIdx.x == 0) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
       asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -555,15 +579,16 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
     return;
   }
   // 1. descriptor blob -> shared memory.  The host writes it into pinned host memory and
-  //    launches -- no copy-engine call and no event per step.  CTA 0 pulls it across
-  //    PCIe once (zero copy) into a device buffer and releases a per-buffer flag carrying
-  //    the launch nonce; every other CTA acquires the flag (bounded wait: a timeout traps)
-  //    and copies the buffer from L2.  (CTA 0 is not waited on by anything it waits for:
-  //    the other CTAs only spin, so it always gets a slot.)
+  //    launches -- no copy-engine call and no event per step.  The first copying CTA (CTA
+  //    0, or CTA 1 behind a publisher CTA) pulls it across PCIe once (zero copy) into a
+  //    device buffer and releases a per-buffer flag carrying the launch nonce; every other
+  //    CTA acquires the flag (bounded wait: a timeout traps) and copies the buffer from
+  //    L2.  (The puller is dispatched before the CTAs that wait for it and waits for none
+  //    of them.)
   {
     const int n16 = h.data_bytes >> 4;
     uint4 *smv = reinterpret_cast<uint4 *>(sm);
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == (h.n_prev > 0 ? 1u : 0u)) {  // the puller: the first copying CTA
       const uint4 *src = reinterpret_cast<const uint4 *>(h.hblob);
       uint4 *dst = reinterpret_cast<uint4 *>(h.gblob);
       // kBlobBatch loads in flight per thread before any store: one PCIe round trip per
@@ -597,7 +622,7 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
         for (long long spin = 0;; ++spin) {
           asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(h.flag) : "memory");
           if (v == h.nonce) break;
-          if (spin > (1ll << 22)) __trap();  // ~1 s: CTA 0 never published the descriptor
+          if (spin > (1ll << 22)) KV_TRAP("blob flag", v, h.nonce);  // CTA 0 never published it
           __nanosleep(64);
         }
       }
@@ -703,10 +728,11 @@ __device__ __forceinline__ void step_body(const KvStepHdr &h) {
   }
   // 3. copies: the grid's flat space, dealt in warp rounds
   KV_STAMP(2);
-  const uint32_t G = gridDim.x - (h.n_prev > 0 ? 1u : 0u), b = blockIdx.x;
+  const uint32_t G = gridDim.x - (h.n_prev > 0 ? 1u : 0u);      // copying CTAs
+  const uint32_t b = blockIdx.x - (h.n_prev > 0 ? 1u : 0u);       // this one's index
   {
     Cursor cur(h, s);
-    copy_all(h.app_slices, P, (int)G, cur, h.g, h.work, early, h.app_first != 0);
+    copy_all(h.app_slices, P, (int)G, (int)b, cur, h.g, h.work, early, h.app_first != 0);
   }
   if (early) {  // the tables below read / write what the previous launch used
     if (threadIdx.x == 0) wait_count(h.prev_counter, h.prev_target);
@@ -804,6 +830,19 @@ extern "C" __attribute__((visibility("default"))) int kv_debug_timeline(unsigned
 }
 #endif
 
+namespace {
+// Function attributes of the step kernel, once per device (they are per context): large
+// launches may carry up to ~200 KiB of descriptors in shared memory.  (The largest
+// shared-memory carveout for every launch measured 4 % slower at 2 GPUs.)
+void step_kernel_attrs(int device) {
+  static unsigned long long done = 0;
+  if (device < 0 || device >= 64 || ((done >> device) & 1ull)) return;
+  cudaFuncSetAttribute(kv_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaGetLastError();
+  done |= 1ull << device;
+}
+}  // namespace
+
 // Resident CTAs of the step kernel on `device` for a launch's shared memory.
 int step_resident_ctas(int device, int smem) {
   static int cache_dev = -1, cache_smem = -1, cache_val = 0;
@@ -811,8 +850,7 @@ int step_resident_ctas(int device, int smem) {
   int sms = 148, per = kMinBlocks;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
     sms = 148;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kv_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  step_kernel_attrs(device);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kv_step_kernel, kThreads, smem) !=
           cudaSuccess || per < 1)
     per = 1;
@@ -839,17 +877,10 @@ int step_smem_bytes(const KvStepHdr &h) {
   return h.data_bytes + 4 * (2 * h.n_ent + 2) + 16;
 }
 
-namespace {
-bool g_attr_set = false;
-}  // namespace
-
 cudaError_t launch_step(const KvStepHdr &h, int grid, cudaStream_t st, bool pdl) {
   const int smem = step_smem_bytes(h);
-  if (!g_attr_set) {
-    // large launches may carry up to ~200 KiB of descriptors in shared memory
-    cudaFuncSetAttribute(kv_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    g_attr_set = true;
-  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) step_kernel_attrs(dev);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
