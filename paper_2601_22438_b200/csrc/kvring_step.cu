@@ -388,7 +388,7 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
 // floor(r f), f = Rp / R in 32.32 fixed point, rounded up so that exactly Rp of the R
 // rounds are): the publication's peer stores then run all through the launch instead of
 // waiting for the appends (2 GPUs: +7 % per step, and 0.68 vs 0.65 of NVLink against
-// appends first with the early start).  In one GPU's HBM (app_first = 1) the append
+// appends first with the early start, 0.66 with the publication's rounds first).  In one GPU's HBM (app_first = 1) the append
 // rounds come first: with the early start (wait_prev) the warps that become resident
 // while the previous launch drains take append rounds, which need nothing from it
 // (+1.5 % per step against interleaved, which loses 2 %: its early warps stall on the
@@ -442,11 +442,6 @@ __device__ __forceinline__ void copy_all(int A, int P, int G, int b, Cursor &cur
     if (app_first) {                            // append rounds first, then the publication's
       pub = r >= Ra;
       b0 = pub ? A + (r - Ra) * span : r * span;
-#ifdef KV_AB_PUBFIRST  // A/B builds: over NVLink the publication's rounds first
-    } else if (true) {
-      pub = r < Rp;
-      b0 = pub ? A + r * span : (r - Rp) * span;
-#endif
     } else {
       const unsigned int pr = (unsigned int)(((unsigned long long)r * f) >> 32);
       pub = (unsigned int)(((unsigned long long)(r + 1) * f) >> 32) > pr;
