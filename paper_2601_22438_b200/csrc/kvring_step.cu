@@ -388,8 +388,9 @@ __device__ __forceinline__ void copy_round(int base, int rend, int lane, int cs,
 // floor(r f), f = Rp / R in 32.32 fixed point, rounded up so that exactly Rp of the R
 // rounds are): the publication's peer stores then run all through the launch instead of
 // waiting for the appends (2 GPUs: +7 % per step, and 0.68 vs 0.65 of NVLink against
-// appends first with the early start, 0.66 with the publication's rounds first).  In one GPU's HBM (app_first = 1) the append
-// rounds come first: with the early start (wait_prev) the warps that become resident
+// appends first with the early start, 0.66 with the publication's rounds first).  In one
+// GPU's HBM (app_first = 1) the append rounds come first: with the early start
+// (wait_prev) the warps that become resident
 // while the previous launch drains take append rounds, which need nothing from it
 // (+1.5 % per step against interleaved, which loses 2 %: its early warps stall on the
 // previous launch's arrival before their publication rounds).
