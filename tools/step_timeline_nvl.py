@@ -83,7 +83,6 @@ def main():
     kl = K.KvLoop()
     kl.run(K.PreparedSteps(steps(0, prelude)), comp.cuda_stream)
     torch.cuda.synchronize(d0)
-    # keep the GPU busy up to the measured launches (no idle clock ramp)
     prep = K.PreparedSteps(steps(prelude, n_steps))
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(d0)

@@ -32,7 +32,7 @@ def main():
     ks = d["kv_step_kernel"]
     old = ks.get("decode_population")
     if old:
-        tag = os.path.basename(old.get("capture", "prev")).replace(".csv", "")
+        tag = os.path.basename(old.get("capture", "prev")).replace(".csv", "").split("_")[-1]
         ks["decode_population_" + tag] = old
     ks["decode_population"] = {
         "what": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
