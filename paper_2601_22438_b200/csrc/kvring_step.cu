@@ -23,8 +23,8 @@
 // Pure data movement, HBM / NVLink bound: no tensor cores.  The per-launch header
 // (pool bases, step, divisors) travels in the kernel parameter space; the descriptor
 // blob (items and per-slot tables) is written by the host into pinned memory, pulled
-// across PCIe once by CTA 0 and shared with the other CTAs through device memory and a
-// release/acquire flag -- the per-step host cost is one launch.
+// across PCIe once by the first copying CTA and shared with the other CTAs through device
+// memory and a release/acquire flag -- the per-step host cost is one launch.
 #include <cstdio>
 #include <cstring>
 
