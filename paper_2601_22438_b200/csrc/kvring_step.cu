@@ -56,7 +56,7 @@ constexpr int kThreads = 256;
 // registers): 128 KB in flight per SM; a decode step's share of a lane (~7 chunks at C2)
 // is one round of loads.
 constexpr int kMinBlocks = 4;
-constexpr int kU = 8;
+constexpr int kU = 8;  // 6: -4 % per step; 10: spills, -33 % (profiles/r02/ab/ku_n1.log)
 constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t x, const KvDiv &d) {
